@@ -1,0 +1,203 @@
+/* rp.h -- C ABI of librp, the B200 (sm_100a) hot path of the rational-program method of
+ * arXiv 1911.02373 (KLARAPTOR: "rational programs" that pick CUDA launch parameters).
+ *
+ * Two halves, following the paper's statement of the problem:
+ *   - compile time, step 2 "Rational function estimation":
+ *     given the profiled points K with measured values V, find g_i = p_i/q_i by linear least
+ *     squares on the linearised system p(x) - V q(x) = 0  ->  rp_fit (and its split form
+ *     rp_minmax / rp_xform_from_box / rp_gram_accumulate / rp_solve_normal for K-sharding);
+ *   - run time, steps 4-5 "Rational program evaluation" and "Selection of optimal values of
+ *     program parameters": for each data tuple D evaluate the rational
+ *     program R over all practically meaningful configurations P in F and take the argmin
+ *     ->  rp_eval_argmin / rp_eval_argmin_batched / rp_plan_*.
+ *
+ * The estimate E is the MWP-CWP program of DESIGN.md Appendix A (PAPER.md:1909-1933 names the
+ * model; its equations are Hong & Kim ISCA'09 Eqs. 1-18, reading R1) fed by l = 3 fitted
+ * metrics (comp, coal, uncoal instructions per thread; reading R2), the occupancy flowchart
+ * (Fig. occupancysimpleflowchart; Eq. (1)) and the grid
+ * rule gx = ceil[N/bx].
+ *
+ * Conventions (all functions):
+ *   - Return an rp_status; on failure rp_last_error() returns a thread-local message.
+ *     Argument checks happen before any launch.  Nothing is written on failure except where
+ *     stated.  Per-D infeasibility is data (idx -1, E +inf), never an error.
+ *   - "device-or-host" pointers may be either: the library inspects them with
+ *     cudaPointerGetAttributes; host inputs are staged through internal device workspace and
+ *     host outputs are copied back before return (the call then synchronises the stream).
+ *     With device pointers everything is stream-ordered and asynchronous unless noted.
+ *   - The caller owns every buffer it passes.  The library owns only internal workspace
+ *     (cached per device, freed at unload) and rp_plan objects (freed by rp_plan_destroy).
+ *   - rp_stream is a cudaStream_t (NULL = the legacy default stream).
+ *   - Every arithmetic step runs in the library's CUDA kernels; there is no CPU fallback.  On a
+ *     machine without a CUDA device every compute entry point returns RP_ERR_CUDA.
+ */
+#ifndef RP_H
+#define RP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RP_ABI_VERSION 1
+#define RP_MAX_VARS 8    /* n = d + p variables (data parameters first, then program ones) */
+#define RP_MAX_METRICS 3 /* l fitted metrics per rational program */
+
+typedef enum {
+  RP_OK = 0,
+  RP_ERR_INVALID_ARG = 1,
+  RP_ERR_CUDA = 2,
+  RP_ERR_DEGENERATE = 3,  /* rank-deficient / non-SPD normal equations */
+  RP_ERR_NO_FEASIBLE = 4, /* reserved */
+  RP_ERR_UNSUPPORTED = 5  /* size or layout outside the compiled limits */
+} rp_status;
+
+typedef void *rp_stream;
+
+/* A monomial basis as an explicit exponent list (the display of
+ * f_b = p_b/q_b; reading R10).  Row j of num_exp is the exponent vector of alpha_j's monomial.
+ * For a fit, den_exp[0] must be the zero vector: its coefficient beta_0 is normalised to 1
+ * (reading R12).  Host pointers, read during the call only.                                  */
+typedef struct {
+  int32_t n_vars, n_num, n_den;
+  const int16_t *num_exp; /* host int16 [n_num][n_vars] */
+  const int16_t *den_exp; /* host int16 [n_den][n_vars] */
+} rp_basis;
+
+/* Variable transform u_k = (x_k - c_k) * 2^-e_k (reading R14; PAPER.md:2601-2611 motivates
+ * it: the monomial system is "essentially a Vandermonde matrix" and "very ill-conditioned").
+ * Coefficients always live in the u-variables.                                             */
+typedef struct {
+  double c[RP_MAX_VARS];
+  int32_t e[RP_MAX_VARS];
+} rp_xform;
+
+/* Hardware parameters H (Ex. ex:cuda PAPER.md:1870-1878; Ex. ex:mwpcwp PAPER.md:1915-1918),
+ * fixed at compile time of the user program (Obs. obs:faisability).
+ * r_max / z_max are per SM (reading R3); z in 4-byte words.                                */
+typedef struct {
+  int32_t n_sm, w_max, b_max, t_max;
+  int64_t r_max, z_max;
+  double freq_hz, mem_bw, load_bytes_per_warp, mem_ld, dd_coal, dd_unc, uncoal_per_mw,
+      issue_cycles;
+} rp_hw;
+
+typedef enum {
+  RP_TEMPLATE_MWPCWP = 0, /* E = DESIGN.md Appendix A, metrics (comp, coal, uncoal)        */
+  RP_TEMPLATE_G1 = 1      /* E = g_1 (the fitted metric itself), same masks               */
+} rp_template;
+
+/* The rational program R (step 3: "the CFG for computing E" plus one
+ * sub-routine per fitted g_i).  Host struct; all pointers host, read during the call.       */
+typedef struct {
+  int32_t d, p;        /* numbers of data / program parameters; n = d + p <= RP_MAX_VARS, p <= 3 */
+  int32_t n_metrics;   /* l; 3 for RP_TEMPLATE_MWPCWP, >= 1 for RP_TEMPLATE_G1              */
+  int32_t e_template;  /* rp_template                                                        */
+  rp_basis basis[RP_MAX_METRICS];
+  const double *coef[RP_MAX_METRICS]; /* host float64 [n_num + n_den]: alpha then beta      */
+  rp_xform xform;
+  rp_hw hw;
+  int32_t regs_per_thread;  /* R: registers per thread of the tuned kernel                 */
+  int32_t grid_map[3];      /* P_k tiles D_{grid_map[k]} (gx = ceil(D/P_k)); -1: dimension 1 */
+  int64_t smem_words_base;  /* Z = smem_words_base + smem_words_per_thread * T (words/block) */
+  int64_t smem_words_per_thread;
+} rp_program;
+
+typedef struct {
+  int32_t rank;      /* n_c - 1 on success                                                  */
+  int32_t status;    /* rp_status of the solve                                              */
+  double resid2;     /* coef^T G coef = sum_r (p(x_r) - V_r q(x_r))^2                        */
+  double min_pivot;  /* smallest pivot of the equilibrated Cholesky factor (squared diag)   */
+  double cond_est;   /* (max pivot / min pivot) of the equilibrated factorisation          */
+} rp_fit_info;
+
+/* ---- library --------------------------------------------------------------------------- */
+int32_t rp_abi_version(void);
+const char *rp_last_error(void);
+/* Number of CUDA devices visible (0 without a GPU).  Never fails.                          */
+int32_t rp_device_count(void);
+
+/* ---- a10: transform -----------------------------------------------------------------------
+ * rp_xform_from_box: host-only helper.  c_k = (lo_k + hi_k)/2; e_k = least integer with
+ * 2^e_k >= max((hi_k - lo_k)/2, 1).  lo, hi host float64 [n]; out host.  INVALID_ARG if
+ * n not in [1, RP_MAX_VARS] or hi < lo.                                                     */
+rp_status rp_xform_from_box(int32_t n, const double *lo, const double *hi, rp_xform *out);
+
+/* rp_minmax: per-column min and max of X (device-or-host float64 [K][n], row-major) into host
+ * lo[n], hi[n].  Synchronises.  INVALID_ARG if K < 1 or n out of range.                     */
+rp_status rp_minmax(const double *X, int64_t K, int32_t n, double *lo, double *hi,
+                    rp_stream s);
+
+/* ---- a11-a12: Gram of the linearised system ---------------------------
+ * G[m][n_c][n_c] (device-or-host float64, overwritten) = A_m^T A_m with, for row r of X,
+ * a_r = [ M(u_r) | -V_m[r] N(u_r) ], M / N the numerator / denominator monomials of `basis`
+ * in basis order (n_c = n_num + n_den), u_r = (X_r - c) 2^-e.  X device-or-host float64
+ * [K][n]; V device-or-host float64 [n_v][K] (n_v >= 1 metrics sharing X).  Rows are split
+ * over CTAs and the per-CTA partial Grams are summed in a fixed order (deterministic).
+ * K = 0 gives G = 0.  UNSUPPORTED if n_c > 256.                                             */
+rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
+                             const rp_basis *basis, const rp_xform *xform, double *G,
+                             rp_stream s);
+
+/* ---- a14: normalise + solve --------------------------------------------
+ * For each of n_v Grams G (device-or-host float64 [n_v][n_c][n_c]): fix beta_0 = 1 (column
+ * n_num) and solve G_ff z = -G_{f,beta0} by Jacobi-equilibrated Cholesky with one step of
+ * iterative refinement (residual in double-double) on one CTA.  coef_out host float64
+ * [n_v][n_c] (u-basis, coef[n_num] == 1).  info host [n_v] (nullable).  Synchronises.
+ * DEGENERATE if a pivot <= 1e-13 (equilibrated) -- coef of that metric is then NaN and the
+ * others are still solved; UNSUPPORTED if n_c > 161.                                       */
+rp_status rp_solve_normal(const double *G, int32_t n_v, const rp_basis *basis, double *coef_out,
+                          rp_fit_info *info, rp_stream s);
+
+/* ---- a10-a14 in one call -------------------------------------------------------------------
+ * Fit n_v metrics sharing the sample points X: transform from the sample box (rp_minmax +
+ * rp_xform_from_box), Gram, solve.  X [K][n], V [n_v][K] device-or-host; coef_out host
+ * [n_v][n_c]; xform_out host; info host [n_v] nullable.  Synchronises.                      */
+rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                 double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream s);
+
+/* ---- a4 alone: fitted metrics at points ----------------------------------------------------
+ * out[i][r] = g_i(X_r) = p_i(u_r)/q_i(u_r) for i < prog->n_metrics (device-or-host float64
+ * [n_metrics][K]); X device-or-host float64 [K][d+p].                                      */
+rp_status rp_eval_metrics(const rp_program *prog, const double *X, int64_t K, double *out,
+                          rp_stream s);
+
+/* ---- a1-a8: sweep + per-D argmin ------------------------------------------------------------
+ * For every D (device-or-host int32 [nD][d]) evaluate E over the configurations F
+ * (device-or-host int32 [nF][p], tuple order = index order), masking P that are not
+ * practically meaningful (T mod 32 != 0, T > t_max, P1 P2 > D1^2, B_active = 0, E not finite
+ * or <= 0), and return the lowest index minimising E: best_idx int32 [nD] (-1 if no P is
+ * feasible), best_E float64 [nD] (+inf if none), second_E float64 [nD] (nullable; the
+ * second-smallest E over the other feasible P, == best_E on an exact tie).  Outputs
+ * device-or-host.  nD = 0 is a no-op.  UNSUPPORTED if nF > 65536 or a basis exceeds the
+ * compiled staging limits.                                   */
+rp_status rp_eval_argmin(const rp_program *prog, const int32_t *D, int64_t nD, const int32_t *F,
+                         int32_t nF, int32_t *best_idx, double *best_E, double *second_E,
+                         rp_stream s);
+
+/* Same for n_prog programs over one D batch and one F (all programs share d and p): outputs
+ * [n_prog][nD].  One launch covers every program.                                           */
+rp_status rp_eval_argmin_batched(const rp_program *progs, int32_t n_prog, const int32_t *D,
+                                 int64_t nD, const int32_t *F, int32_t nF, int32_t *best_idx,
+                                 double *best_E, double *second_E, rp_stream s);
+
+/* ---- plans: a1 once per (programs, F), then many sweeps ------------------------------------
+ * rp_plan_create stages the programs (coefficients, H, resources) to the device and
+ * precomputes the per-configuration table (static mask, B_active, W_active, P-monomials)
+ * and the compaction of statically feasible configurations, on the device.  F
+ * device-or-host.  The plan is bound to the current device.  rp_plan_eval_argmin is
+ * rp_eval_argmin_batched without the setup.  n_static_feasible (nullable) receives the
+ * number of configurations of program 0 that survive the static mask.                      */
+typedef struct rp_plan_s *rp_plan;
+rp_status rp_plan_create(const rp_program *progs, int32_t n_prog, const int32_t *F, int32_t nF,
+                         rp_plan *out, rp_stream s);
+rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_t *best_idx,
+                              double *best_E, double *second_E, rp_stream s);
+rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible);
+rp_status rp_plan_destroy(rp_plan plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RP_H */

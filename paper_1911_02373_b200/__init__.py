@@ -1,0 +1,384 @@
+"""B200 (sm_100a) hot path of the rational-program method of arXiv 1911.02373 (KLARAPTOR).
+
+Thin Python binding over ``librp.so`` (C ABI in ``include/rp.h``): argument marshalling only.
+Every step of the method -- transform, design rows, Gram, solve, occupancy, masks, metric
+evaluation, the MWP-CWP estimate and the argmin -- runs in the library's CUDA kernels.  There is
+no CPU fallback: if ``librp.so`` is missing, importing this package raises, and on a machine
+without a GPU every compute call raises ``RPError`` (RP_ERR_CUDA).
+
+Arrays may be torch tensors (CUDA or CPU) or numpy arrays; CUDA tensors are used in place on
+the current torch stream, host arrays are staged by the library itself (see rp.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librp.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+RP_MAX_VARS = 8
+RP_MAX_METRICS = 3
+STATUS = {0: "RP_OK", 1: "RP_ERR_INVALID_ARG", 2: "RP_ERR_CUDA", 3: "RP_ERR_DEGENERATE",
+          4: "RP_ERR_NO_FEASIBLE", 5: "RP_ERR_UNSUPPORTED"}
+TEMPLATES = {"mwpcwp": 0, "g1": 1}
+
+
+class RPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class rp_basis(C.Structure):
+    _fields_ = [("n_vars", C.c_int32), ("n_num", C.c_int32), ("n_den", C.c_int32),
+                ("num_exp", C.c_void_p), ("den_exp", C.c_void_p)]
+
+
+class rp_xform(C.Structure):
+    _fields_ = [("c", C.c_double * RP_MAX_VARS), ("e", C.c_int32 * RP_MAX_VARS)]
+
+
+class rp_hw(C.Structure):
+    _fields_ = [("n_sm", C.c_int32), ("w_max", C.c_int32), ("b_max", C.c_int32), ("t_max", C.c_int32),
+                ("r_max", C.c_int64), ("z_max", C.c_int64)] + \
+               [(k, C.c_double) for k in ("freq_hz", "mem_bw", "load_bytes_per_warp", "mem_ld", "dd_coal",
+                                          "dd_unc", "uncoal_per_mw", "issue_cycles")]
+
+
+class rp_program(C.Structure):
+    _fields_ = [("d", C.c_int32), ("p", C.c_int32), ("n_metrics", C.c_int32), ("e_template", C.c_int32),
+                ("basis", rp_basis * RP_MAX_METRICS), ("coef", C.c_void_p * RP_MAX_METRICS),
+                ("xform", rp_xform), ("hw", rp_hw), ("regs_per_thread", C.c_int32),
+                ("grid_map", C.c_int32 * 3), ("smem_words_base", C.c_int64),
+                ("smem_words_per_thread", C.c_int64)]
+
+
+class rp_fit_info(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("status", C.c_int32), ("resid2", C.c_double),
+                ("min_pivot", C.c_double), ("cond_est", C.c_double)]
+
+
+_vp, _i32, _i64 = C.c_void_p, C.c_int32, C.c_int64
+_lib.rp_abi_version.restype = _i32
+_lib.rp_last_error.restype = C.c_char_p
+_lib.rp_device_count.restype = _i32
+_SIGS = {
+    "rp_xform_from_box": [_i32, _vp, _vp, C.POINTER(rp_xform)],
+    "rp_minmax": [_vp, _i64, _i32, _vp, _vp, _vp],
+    "rp_gram_accumulate": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
+    "rp_solve_normal": [_vp, _i32, C.POINTER(rp_basis), _vp, _vp, _vp],
+    "rp_fit": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, C.POINTER(rp_xform), _vp, _vp],
+    "rp_eval_metrics": [C.POINTER(rp_program), _vp, _i64, _vp, _vp],
+    "rp_eval_argmin": [C.POINTER(rp_program), _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
+    "rp_eval_argmin_batched": [_vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
+    "rp_plan_create": [_vp, _i32, _vp, _i32, C.POINTER(_vp), _vp],
+    "rp_plan_eval_argmin": [_vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "rp_plan_static_feasible": [_vp, _i32, C.POINTER(_i32)],
+    "rp_plan_destroy": [_vp],
+}
+for _name, _args in _SIGS.items():
+    getattr(_lib, _name).argtypes = _args
+    getattr(_lib, _name).restype = C.c_int
+
+EXPORTED = ["rp_abi_version", "rp_last_error", "rp_device_count"] + list(_SIGS)
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise RPError(status, _lib.rp_last_error().decode(errors="replace"))
+
+
+def abi_version() -> int:
+    return int(_lib.rp_abi_version())
+
+
+def device_count() -> int:
+    return int(_lib.rp_device_count())
+
+
+# --------------------------------------------------------------------------------------------
+# array marshalling
+# --------------------------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(a) -> int:
+    """Raw data pointer of a contiguous torch tensor or numpy array."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _stream_of(*arrays):
+    torch = _torch()
+    for a in arrays:
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            return C.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+    return C.c_void_p(0)
+
+
+def _contig(a, dtype):
+    """Contiguous array of `dtype` (torch stays torch, on its device; else numpy)."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int16: torch.int16}[dtype]
+        return a.to(dtype=tdt).contiguous()
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _empty_like_family(ref, shape, dtype):
+    torch = _torch()
+    if isinstance(ref, torch.Tensor):
+        tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        return torch.empty(shape, dtype=tdt, device=ref.device)
+    return np.empty(shape, dtype=dtype)
+
+
+# --------------------------------------------------------------------------------------------
+# transform, basis
+# --------------------------------------------------------------------------------------------
+
+def xform_from_box(lo, hi):
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    hi = np.ascontiguousarray(hi, dtype=np.float64)
+    out = rp_xform()
+    _check(_lib.rp_xform_from_box(len(lo), _ptr(lo), _ptr(hi), C.byref(out)))
+    n = len(lo)
+    return np.array(out.c[:n]), np.array(out.e[:n], dtype=np.int32)
+
+
+def _xform_struct(c, e) -> rp_xform:
+    x = rp_xform()
+    for k in range(len(c)):
+        x.c[k] = float(c[k])
+        x.e[k] = int(e[k])
+    return x
+
+
+class Basis:
+    """Numerator / denominator exponent lists (held alive for the C struct)."""
+
+    def __init__(self, num_exp, den_exp):
+        self.num = np.ascontiguousarray(num_exp, dtype=np.int16)
+        self.den = np.ascontiguousarray(den_exp, dtype=np.int16)
+        assert self.num.ndim == 2 and self.den.ndim == 2 and self.num.shape[1] == self.den.shape[1]
+        self.c = rp_basis(self.num.shape[1], len(self.num), len(self.den), _ptr(self.num), _ptr(self.den))
+
+    @property
+    def n_c(self) -> int:
+        return len(self.num) + len(self.den)
+
+
+# --------------------------------------------------------------------------------------------
+# programs
+# --------------------------------------------------------------------------------------------
+
+class Program:
+    """An ``rp_program`` built from a program description with the attributes of
+    ``synth.ProgramSpec`` (d, p, num_exp, den_exp, coef, hw, R, Z0, Z1, grid_map, template and
+    either box_lo/box_hi -- transform derived by the library -- or xform_c/xform_e)."""
+
+    def __init__(self, spec):
+        self.spec = spec
+        self._keep = []
+        pr = rp_program()
+        pr.d, pr.p = spec.d, spec.p
+        pr.n_metrics = len(spec.coef)
+        pr.e_template = TEMPLATES[spec.template]
+        for i in range(pr.n_metrics):
+            b = Basis(spec.num_exp[i], spec.den_exp[i])
+            cf = np.ascontiguousarray(spec.coef[i], dtype=np.float64)
+            assert cf.size == b.n_c
+            self._keep += [b, cf]
+            pr.basis[i] = b.c
+            pr.coef[i] = _ptr(cf)
+        if getattr(spec, "xform_c", None) is not None:
+            c, e = spec.xform_c, spec.xform_e
+        else:
+            c, e = xform_from_box(spec.box_lo, spec.box_hi)
+        pr.xform = _xform_struct(c, e)
+        self.xform = (np.asarray(c, dtype=np.float64), np.asarray(e, dtype=np.int32))
+        hw = spec.hw
+        pr.hw = rp_hw(**{k: hw[k] for k, _ in rp_hw._fields_})
+        pr.regs_per_thread = int(spec.R)
+        for k in range(3):
+            pr.grid_map[k] = int(spec.grid_map[k]) if k < len(spec.grid_map) else -1
+        pr.smem_words_base = int(spec.Z0)
+        pr.smem_words_per_thread = int(spec.Z1)
+        self.c = pr
+
+    @property
+    def d(self):
+        return self.c.d
+
+    @property
+    def p(self):
+        return self.c.p
+
+    @property
+    def n_metrics(self):
+        return self.c.n_metrics
+
+
+def _programs(progs):
+    progs = [p if isinstance(p, Program) else Program(p) for p in progs]
+    arr = (rp_program * len(progs))(*[p.c for p in progs])
+    return progs, arr
+
+
+# --------------------------------------------------------------------------------------------
+# sweep
+# --------------------------------------------------------------------------------------------
+
+def eval_argmin_batched(progs, D, F, second: bool = True, out=None):
+    """Per-D argmin of E over F for each program: (idx int32 [n_prog][nD], E float64
+    [n_prog][nD], second float64 [n_prog][nD] or None)."""
+    progs, arr = _programs(progs)
+    d, p = progs[0].d, progs[0].p
+    D = _contig(D, np.int32)
+    F = _contig(F, np.int32)
+    nD = D.shape[0] if D.ndim > 1 else len(D) // d
+    nF = F.shape[0] if F.ndim > 1 else len(F) // p
+    shape = (len(progs), nD)
+    if out is None:
+        out = (_empty_like_family(D, shape, np.int32), _empty_like_family(D, shape, np.float64),
+               _empty_like_family(D, shape, np.float64) if second else None)
+    idx, E, S = out
+    s = _stream_of(D, F, idx)
+    _check(_lib.rp_eval_argmin_batched(C.cast(arr, _vp), len(progs), _ptr(D), nD, _ptr(F), nF, _ptr(idx),
+                                       _ptr(E), _ptr(S) if S is not None else None, s))
+    return idx, E, S
+
+
+def eval_argmin(prog, D, F, second: bool = True):
+    idx, E, S = eval_argmin_batched([prog], D, F, second)
+    return idx[0], E[0], (S[0] if S is not None else None)
+
+
+class Plan:
+    """a1 once per (programs, F) -- static mask, occupancy, P-monomials, compaction on the
+    device -- then many sweeps over D batches."""
+
+    def __init__(self, progs, F, device=None):
+        self.progs, arr = _programs(progs)
+        self.d, self.p = self.progs[0].d, self.progs[0].p
+        F = _contig(F, np.int32)
+        self.nF = F.shape[0] if F.ndim > 1 else len(F) // self.p
+        self.handle = C.c_void_p()
+        s = _stream_of(F)
+        _check(_lib.rp_plan_create(C.cast(arr, _vp), len(self.progs), _ptr(F), self.nF, C.byref(self.handle), s))
+
+    def static_feasible(self, prog: int = 0) -> int:
+        v = C.c_int32()
+        _check(_lib.rp_plan_static_feasible(self.handle, prog, C.byref(v)))
+        return int(v.value)
+
+    def eval(self, D, out=None, second: bool = True):
+        D = _contig(D, np.int32)
+        nD = D.shape[0] if D.ndim > 1 else len(D) // self.d
+        shape = (len(self.progs), nD)
+        if out is None:
+            out = (_empty_like_family(D, shape, np.int32), _empty_like_family(D, shape, np.float64),
+                   _empty_like_family(D, shape, np.float64) if second else None)
+        idx, E, S = out
+        s = _stream_of(D, idx)
+        _check(_lib.rp_plan_eval_argmin(self.handle, _ptr(D), nD, _ptr(idx), _ptr(E),
+                                        _ptr(S) if S is not None else None, s))
+        return idx, E, S
+
+    def close(self):
+        if self.handle:
+            _lib.rp_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def eval_metrics(prog, X):
+    """g_i at the rows of X: float64 [n_metrics][K]."""
+    prog = prog if isinstance(prog, Program) else Program(prog)
+    X = _contig(X, np.float64)
+    K = X.shape[0]
+    out = _empty_like_family(X, (prog.n_metrics, K), np.float64)
+    _check(_lib.rp_eval_metrics(C.byref(prog.c), _ptr(X), K, _ptr(out), _stream_of(X, out)))
+    return out
+
+
+# --------------------------------------------------------------------------------------------
+# fit
+# --------------------------------------------------------------------------------------------
+
+def minmax(X):
+    X = _contig(X, np.float64)
+    K, n = X.shape
+    lo = np.zeros(n)
+    hi = np.zeros(n)
+    _check(_lib.rp_minmax(_ptr(X), K, n, _ptr(lo), _ptr(hi), _stream_of(X)))
+    return lo, hi
+
+
+def gram(X, V, num_exp, den_exp, c, e, out=None):
+    """G [n_v][n_c][n_c] of the linearised system for n_v metrics V [n_v][K] sharing X."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    xf = _xform_struct(c, e)
+    G = out if out is not None else _empty_like_family(X, (n_v, b.n_c, b.n_c), np.float64)
+    _check(_lib.rp_gram_accumulate(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), C.byref(xf), _ptr(G), _stream_of(X, V, G)))
+    return G
+
+
+def _infos(infos):
+    return [dict(rank=i.rank, status=i.status, resid2=i.resid2, min_pivot=i.min_pivot, cond_est=i.cond_est)
+            for i in infos]
+
+
+def solve_normal(G, num_exp, den_exp, raise_on_degenerate: bool = True):
+    b = Basis(num_exp, den_exp)
+    G = _contig(G, np.float64)
+    n_v = G.shape[0] if G.ndim == 3 else 1
+    coef = np.zeros((n_v, b.n_c))
+    infos = (rp_fit_info * n_v)()
+    st = _lib.rp_solve_normal(_ptr(G), n_v, C.byref(b.c), _ptr(coef), C.cast(infos, _vp), _stream_of(G))
+    if st != 0 and (st != 3 or raise_on_degenerate):
+        _check(st)
+    return coef, _infos(infos)
+
+
+def fit(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
+    """rp_fit: transform from the sample box, Gram, beta_0 = 1 solve, for n_v metrics sharing
+    X.  Returns (coef float64 [n_v][n_c] in the u-basis, (c, e), infos)."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    coef = np.zeros((n_v, b.n_c))
+    xf = rp_xform()
+    infos = (rp_fit_info * n_v)()
+    st = _lib.rp_fit(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), _ptr(coef), C.byref(xf), C.cast(infos, _vp),
+                     _stream_of(X, V))
+    if st != 0 and (st != 3 or raise_on_degenerate):
+        _check(st)
+    n = b.num.shape[1]
+    return coef, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)

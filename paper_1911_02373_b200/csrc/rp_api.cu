@@ -1,0 +1,666 @@
+// rp_api.cu -- the C ABI of librp (include/rp.h): argument checks, host/device staging,
+// program marshalling, plans.  All arithmetic of the method happens in the kernels of
+// rp_sweep.cu, rp_gram.cu and rp_solve.cu.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "rp_internal.cuh"
+
+namespace rp {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+rp_status cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+  set_error("CUDA error %d (%s) in %s at %s:%d", (int)e, cudaGetErrorString(e), what, file, line);
+  cudaGetLastError();
+  return RP_ERR_CUDA;
+}
+
+static bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static rp_status ensure_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device available (librp has no CPU fallback)");
+    return RP_ERR_CUDA;
+  }
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  return RP_OK;
+}
+
+// Stream-ordered temporary device buffer (cudaMallocAsync pool).
+struct Tmp {
+  void *p = nullptr;
+  cudaStream_t s = nullptr;
+  ~Tmp() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  cudaError_t alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+  }
+};
+
+// Input that may be host or device: returns a device pointer (staging host data on `s`).
+template <class T>
+static rp_status stage_in(const T *src, size_t count, Tmp &tmp, const T **out, cudaStream_t s) {
+  if (count == 0 || is_device_ptr(src)) {
+    *out = src;
+    return RP_OK;
+  }
+  RP_CUDA(tmp.alloc(count * sizeof(T), s));
+  RP_CUDA(cudaMemcpyAsync(tmp.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  *out = (const T *)tmp.p;
+  return RP_OK;
+}
+// Output that may be host or device: returns a device pointer; `host` is set if a copy back
+// (and a synchronisation) is needed.
+template <class T>
+static rp_status stage_out(T *dst, size_t count, Tmp &tmp, T **out, bool *host, cudaStream_t s) {
+  *host = false;
+  if (!dst || count == 0 || is_device_ptr(dst)) {
+    *out = dst;
+    return RP_OK;
+  }
+  RP_CUDA(tmp.alloc(count * sizeof(T), s));
+  *out = (T *)tmp.p;
+  *host = true;
+  return RP_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// program marshalling (layout only)
+// ---------------------------------------------------------------------------------------------
+static rp_status check_basis(const rp_basis &b, int n, const char *what, bool fit) {
+  RP_REQUIRE(b.n_vars == n, RP_ERR_INVALID_ARG, "%s: basis n_vars %d != %d", what, b.n_vars, n);
+  RP_REQUIRE(b.n_num >= 1 && b.n_den >= 1, RP_ERR_INVALID_ARG, "%s: empty numerator/denominator basis", what);
+  RP_REQUIRE(b.num_exp && b.den_exp, RP_ERR_INVALID_ARG, "%s: null exponent table", what);
+  for (int j = 0; j < b.n_num * n; ++j)
+    RP_REQUIRE(b.num_exp[j] >= 0 && b.num_exp[j] <= 64, RP_ERR_INVALID_ARG, "%s: exponent out of [0,64]", what);
+  for (int j = 0; j < b.n_den * n; ++j)
+    RP_REQUIRE(b.den_exp[j] >= 0 && b.den_exp[j] <= 64, RP_ERR_INVALID_ARG, "%s: exponent out of [0,64]", what);
+  if (fit)
+    for (int k = 0; k < n; ++k)
+      RP_REQUIRE(b.den_exp[k] == 0, RP_ERR_UNSUPPORTED,
+                 "%s: den_exp[0] must be the zero vector (beta_0 = 1 normalisation)", what);
+  return RP_OK;
+}
+
+rp_status compile_program(const rp_program *prog, DevProg *o) {
+  RP_REQUIRE(prog, RP_ERR_INVALID_ARG, "null program");
+  const int d = prog->d, p = prog->p, n = d + p, nm = prog->n_metrics;
+  RP_REQUIRE(d >= 1 && p >= 1 && p <= 3 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG,
+             "program: need d >= 1, 1 <= p <= 3, d + p <= %d (got d=%d p=%d)", RP_MAX_VARS, d, p);
+  RP_REQUIRE(nm >= 1 && nm <= RP_MAX_METRICS, RP_ERR_INVALID_ARG, "program: n_metrics %d", nm);
+  RP_REQUIRE(prog->e_template == RP_TEMPLATE_MWPCWP || prog->e_template == RP_TEMPLATE_G1,
+             RP_ERR_INVALID_ARG, "program: unknown template %d", prog->e_template);
+  RP_REQUIRE(prog->e_template != RP_TEMPLATE_MWPCWP || nm == 3, RP_ERR_INVALID_ARG,
+             "program: the MWP-CWP template needs 3 metrics (comp, coal, uncoal)");
+  const rp_hw &h = prog->hw;
+  RP_REQUIRE(h.n_sm >= 1 && h.w_max >= 1 && h.b_max >= 1 && h.t_max >= 1 && h.r_max >= 1 && h.z_max >= 1,
+             RP_ERR_INVALID_ARG, "program: hardware limits must be >= 1");
+  RP_REQUIRE(prog->regs_per_thread >= 0 && prog->smem_words_base >= 0 && prog->smem_words_per_thread >= 0,
+             RP_ERR_INVALID_ARG, "program: negative resource usage");
+  for (int k = 0; k < 3; ++k)
+    RP_REQUIRE(prog->grid_map[k] >= -1 && prog->grid_map[k] < d, RP_ERR_INVALID_ARG,
+               "program: grid_map[%d] = %d out of range", k, prog->grid_map[k]);
+  for (int k = 0; k < n; ++k)
+    RP_REQUIRE(prog->xform.e[k] > -1000 && prog->xform.e[k] < 1000, RP_ERR_INVALID_ARG, "program: xform exponent");
+
+  memset(o, 0, sizeof *o);
+  o->d = d;
+  o->p = p;
+  o->nm = nm;
+  o->tmpl = prog->e_template;
+  o->npoly = 2 * nm;
+  for (int k = 0; k < 3; ++k) o->grid_map[k] = prog->grid_map[k];
+  o->n_sm = h.n_sm;
+  o->w_max = h.w_max;
+  o->b_max = h.b_max;
+  o->t_max = h.t_max;
+  o->r_max = h.r_max;
+  o->z_max = h.z_max;
+  o->R = prog->regs_per_thread;
+  o->Z0 = prog->smem_words_base;
+  o->Z1 = prog->smem_words_per_thread;
+  o->freq = h.freq_hz;
+  o->mem_bw = h.mem_bw;
+  o->lbpw = h.load_bytes_per_warp;
+  o->mem_ld = h.mem_ld;
+  o->dd_coal = h.dd_coal;
+  o->dd_unc = h.dd_unc;
+  o->U = h.uncoal_per_mw;
+  o->issue = h.issue_cycles;
+  for (int k = 0; k < n; ++k) {
+    o->xc[k] = prog->xform.c[k];
+    o->xe[k] = prog->xform.e[k];
+  }
+  struct Term {
+    int k;
+    std::vector<int> eD, eP;
+    double c;
+  };
+  std::vector<Term> terms;
+  for (int i = 0; i < nm; ++i) {
+    rp_status st = check_basis(prog->basis[i], n, "program", false);
+    if (st != RP_OK) return st;
+    const rp_basis &b = prog->basis[i];
+    RP_REQUIRE(prog->coef[i], RP_ERR_INVALID_ARG, "program: null coef[%d]", i);
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int cnt = h2 ? b.n_den : b.n_num;
+      const int16_t *ex = h2 ? b.den_exp : b.num_exp;
+      for (int j = 0; j < cnt; ++j) {
+        Term t;
+        t.k = 2 * i + h2;
+        t.eD.assign(ex + j * n, ex + j * n + d);
+        t.eP.assign(ex + j * n + d, ex + j * n + n);
+        t.c = prog->coef[i][(h2 ? b.n_num : 0) + j];
+        terms.push_back(t);
+      }
+    }
+  }
+  auto graded_less = [](const std::vector<int> &a, const std::vector<int> &b) {
+    int sa = 0, sb = 0;
+    for (int v : a) sa += v;
+    for (int v : b) sb += v;
+    return sa != sb ? sa < sb : a < b;
+  };
+  std::vector<std::vector<int>> PE, DE;
+  for (auto &t : terms) {
+    PE.push_back(t.eP);
+    DE.push_back(t.eD);
+  }
+  std::sort(PE.begin(), PE.end(), graded_less);
+  PE.erase(std::unique(PE.begin(), PE.end()), PE.end());
+  std::sort(DE.begin(), DE.end(), graded_less);
+  DE.erase(std::unique(DE.begin(), DE.end()), DE.end());
+  RP_REQUIRE((int)PE.size() <= kMaxPE, RP_ERR_UNSUPPORTED,
+             "program: %d distinct program-part monomials > %d", (int)PE.size(), kMaxPE);
+  RP_REQUIRE((int)DE.size() <= kMaxDE, RP_ERR_UNSUPPORTED,
+             "program: %d distinct data-part monomials > %d", (int)DE.size(), kMaxDE);
+  RP_REQUIRE((int)terms.size() <= kMaxTerms, RP_ERR_UNSUPPORTED, "program: %d terms > %d",
+             (int)terms.size(), kMaxTerms);
+  o->nPE = (int)PE.size();
+  o->nDE = (int)DE.size();
+  o->nterm = (int)terms.size();
+  for (int a = 0; a < o->nPE; ++a)
+    for (int k = 0; k < p; ++k) o->pe_exp[a][k] = (int8_t)PE[a][k];
+  for (int a = 0; a < o->nDE; ++a)
+    for (int k = 0; k < d; ++k) o->de_exp[a][k] = (int8_t)DE[a][k];
+  // rows r = k * nPE + pe; terms grouped by row keeping basis order within a row
+  const int nrows = o->npoly * o->nPE;
+  std::vector<std::vector<std::pair<int, double>>> rows(nrows);
+  for (auto &t : terms) {
+    const int pe = (int)(std::lower_bound(PE.begin(), PE.end(), t.eP, graded_less) - PE.begin());
+    const int de = (int)(std::lower_bound(DE.begin(), DE.end(), t.eD, graded_less) - DE.begin());
+    rows[t.k * o->nPE + pe].push_back({de, t.c});
+  }
+  int pos = 0;
+  for (int r = 0; r < nrows; ++r) {
+    o->row_start[r] = (int16_t)pos;
+    for (auto &e : rows[r]) {
+      o->term_de[pos] = (int16_t)e.first;
+      o->term_coef[pos] = e.second;
+      ++pos;
+    }
+  }
+  o->row_start[nrows] = (int16_t)pos;
+  return RP_OK;
+}
+
+static int npe_pad_for(int nPE) {
+  const int opts[] = {4, 8, 16, 20, 24, 36};
+  for (int v : opts)
+    if (nPE <= v) return v;
+  return -1;
+}
+
+static rp_status build_gram_basis(const rp_basis *basis, const rp_xform *xf, GramBasis *gb) {
+  RP_REQUIRE(basis, RP_ERR_INVALID_ARG, "null basis");
+  const int n = basis->n_vars;
+  RP_REQUIRE(n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "basis: n_vars %d", n);
+  rp_status st = check_basis(*basis, n, "fit", true);
+  if (st != RP_OK) return st;
+  const int nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc <= 176, RP_ERR_UNSUPPORTED, "fit: n_c = %d > 176 columns", nc);
+  memset(gb, 0, sizeof *gb);
+  gb->n = n;
+  gb->n_num = basis->n_num;
+  gb->n_den = basis->n_den;
+  gb->nc = nc;
+  int maxdeg = 0;
+  for (int j = 0; j < nc; ++j)
+    for (int k = 0; k < n; ++k) {
+      const int e = j < basis->n_num ? basis->num_exp[j * n + k] : basis->den_exp[(j - basis->n_num) * n + k];
+      gb->exp[j][k] = (int8_t)e;
+      maxdeg = std::max(maxdeg, e);
+    }
+  gb->maxdeg = maxdeg;
+  if (xf)
+    for (int k = 0; k < n; ++k) {
+      gb->xc[k] = xf->c[k];
+      gb->xe[k] = xf->e[k];
+    }
+  return RP_OK;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+// =============================================================================================
+// plans
+// =============================================================================================
+struct rp_plan_s {
+  int device = 0;
+  int n_prog = 0, nF = 0, d = 0, p = 0, npe_pad = 0;
+  DevProg *d_progs = nullptr;
+  int32_t *buf_i = nullptr;
+  double *buf_d = nullptr;
+  CfgTable tab{};
+  cudaStream_t stream = nullptr;
+  bool async_free = false;
+};
+
+static void plan_free(rp_plan pl) {
+  if (!pl) return;
+  if (pl->async_free) {
+    if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
+    if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
+    if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
+  } else {
+    cudaStreamSynchronize(pl->stream);
+    if (pl->d_progs) cudaFree(pl->d_progs);
+    if (pl->buf_i) cudaFree(pl->buf_i);
+    if (pl->buf_d) cudaFree(pl->buf_d);
+  }
+  delete pl;
+}
+
+static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int32_t *F, int32_t nF,
+                             rp_plan *out, cudaStream_t s, bool async_free) {
+  RP_REQUIRE(out, RP_ERR_INVALID_ARG, "null plan out");
+  *out = nullptr;
+  RP_REQUIRE(progs && n_prog >= 1 && n_prog <= 65535, RP_ERR_INVALID_ARG, "n_prog %d", n_prog);
+  RP_REQUIRE(F && nF >= 1 && nF <= 65536, RP_ERR_UNSUPPORTED, "nF = %d outside [1, 65536]", nF);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  std::vector<DevProg> hp(n_prog);
+  int npe_max = 0;
+  for (int g = 0; g < n_prog; ++g) {
+    st = compile_program(&progs[g], &hp[g]);
+    if (st != RP_OK) return st;
+    RP_REQUIRE(progs[g].d == progs[0].d && progs[g].p == progs[0].p, RP_ERR_INVALID_ARG,
+               "batched programs must share d and p");
+    npe_max = std::max(npe_max, hp[g].nPE);
+  }
+  const int npe_pad = npe_pad_for(npe_max);
+  RP_REQUIRE(npe_pad > 0, RP_ERR_UNSUPPORTED, "too many program-part monomials");
+  rp_plan pl = new rp_plan_s;
+  pl->n_prog = n_prog;
+  pl->nF = nF;
+  pl->d = progs[0].d;
+  pl->p = progs[0].p;
+  pl->npe_pad = npe_pad;
+  pl->stream = s;
+  pl->async_free = async_free;
+  cudaGetDevice(&pl->device);
+  auto fail = [&](cudaError_t e, const char *w) {
+    rp_status r = cuda_fail(e, w, __FILE__, __LINE__);
+    plan_free(pl);
+    return r;
+  };
+  cudaError_t e;
+  const size_t ni = (size_t)n_prog * nF * 6 + n_prog;  // orig, P[3], B, W, nFc
+  const size_t nd = (size_t)n_prog * npe_pad * nF;
+  if (async_free) {
+    if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMallocAsync((void **)&pl->buf_i, ni * 4, s)) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMallocAsync((void **)&pl->buf_d, nd * 8, s)) != cudaSuccess) return fail(e, "alloc");
+  } else {
+    if ((e = cudaMalloc((void **)&pl->d_progs, sizeof(DevProg) * n_prog)) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc((void **)&pl->buf_i, ni * 4)) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc((void **)&pl->buf_d, nd * 8)) != cudaSuccess) return fail(e, "alloc");
+  }
+  pl->tab.orig = pl->buf_i;
+  pl->tab.P = pl->buf_i + (size_t)n_prog * nF;
+  pl->tab.B = pl->tab.P + (size_t)n_prog * 3 * nF;
+  pl->tab.W = pl->tab.B + (size_t)n_prog * nF;
+  pl->tab.nFc = pl->tab.W + (size_t)n_prog * nF;
+  pl->tab.mP = pl->buf_d;
+  // the DevProg blob is staged through pinned-free pageable memory: copy synchronously w.r.t.
+  // the host buffer lifetime (cudaMemcpyAsync from pageable memory returns after staging)
+  if ((e = cudaMemcpyAsync(pl->d_progs, hp.data(), sizeof(DevProg) * n_prog, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return fail(e, "H2D program");
+  Tmp tF;
+  const int32_t *dF = nullptr;
+  st = stage_in(F, (size_t)nF * pl->p, tF, &dF, s);
+  if (st != RP_OK) {
+    plan_free(pl);
+    return st;
+  }
+  if ((e = launch_plan_configs(pl->d_progs, n_prog, dF, nF, npe_pad, pl->tab, s)) != cudaSuccess)
+    return fail(e, "k_plan_configs");
+  *out = pl;
+  return RP_OK;
+}
+
+static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *best_idx,
+                           double *best_E, double *second_E, cudaStream_t s) {
+  RP_REQUIRE(pl, RP_ERR_INVALID_ARG, "null plan");
+  RP_REQUIRE(nD >= 0, RP_ERR_INVALID_ARG, "nD < 0");
+  if (nD == 0) return RP_OK;
+  RP_REQUIRE(D && best_idx && best_E, RP_ERR_INVALID_ARG, "null D / outputs");
+  RP_REQUIRE((nD + 7) / 8 <= 0x7fffffffll, RP_ERR_UNSUPPORTED, "nD too large");
+  pl->stream = s;
+  Tmp tD, ti, tb, ts;
+  const int32_t *dD;
+  rp_status st = stage_in(D, (size_t)nD * pl->d, tD, &dD, s);
+  if (st != RP_OK) return st;
+  const size_t no = (size_t)pl->n_prog * nD;
+  int32_t *di;
+  double *db, *ds;
+  bool hi, hb, hs;
+  if ((st = stage_out(best_idx, no, ti, &di, &hi, s)) != RP_OK) return st;
+  if ((st = stage_out(best_E, no, tb, &db, &hb, s)) != RP_OK) return st;
+  if ((st = stage_out(second_E, no, ts, &ds, &hs, s)) != RP_OK) return st;
+  RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->tab, pl->nF, pl->npe_pad, pl->d, dD, nD, di, db, ds, s));
+  if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, no * 4, cudaMemcpyDeviceToHost, s));
+  if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, no * 8, cudaMemcpyDeviceToHost, s));
+  if (hs) RP_CUDA(cudaMemcpyAsync(second_E, ds, no * 8, cudaMemcpyDeviceToHost, s));
+  if (hi || hb || hs) RP_CUDA(cudaStreamSynchronize(s));
+  return RP_OK;
+}
+
+// =============================================================================================
+// ABI
+// =============================================================================================
+extern "C" {
+
+int32_t rp_abi_version(void) { return RP_ABI_VERSION; }
+const char *rp_last_error(void) { return g_err; }
+int32_t rp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+rp_status rp_xform_from_box(int32_t n, const double *lo, const double *hi, rp_xform *out) {
+  RP_REQUIRE(n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "n = %d", n);
+  RP_REQUIRE(lo && hi && out, RP_ERR_INVALID_ARG, "null argument");
+  for (int k = 0; k < n; ++k) RP_REQUIRE(lo[k] <= hi[k], RP_ERR_INVALID_ARG, "hi < lo at %d", k);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  double hlohi[2 * RP_MAX_VARS], hout[2 * RP_MAX_VARS];
+  for (int k = 0; k < n; ++k) {
+    hlohi[2 * k] = lo[k];
+    hlohi[2 * k + 1] = hi[k];
+  }
+  Tmp t;
+  RP_CUDA(t.alloc(4 * RP_MAX_VARS * sizeof(double), nullptr));
+  double *d = (double *)t.p;
+  RP_CUDA(cudaMemcpyAsync(d, hlohi, 2 * n * sizeof(double), cudaMemcpyHostToDevice, nullptr));
+  RP_CUDA(launch_xform(d, n, d + 2 * RP_MAX_VARS, nullptr));
+  RP_CUDA(cudaMemcpyAsync(hout, d + 2 * RP_MAX_VARS, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, nullptr));
+  RP_CUDA(cudaStreamSynchronize(nullptr));
+  memset(out, 0, sizeof *out);
+  for (int k = 0; k < n; ++k) {
+    out->c[k] = hout[2 * k];
+    out->e[k] = (int32_t)hout[2 * k + 1];
+  }
+  return RP_OK;
+}
+
+rp_status rp_minmax(const double *X, int64_t K, int32_t n, double *lo, double *hi, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(X && lo && hi, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 1 && n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "K = %lld, n = %d", (long long)K, n);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  Tmp tX, tw;
+  const double *dX;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  const int nblk = minmax_blocks(K);
+  RP_CUDA(tw.alloc(((size_t)nblk * n * 2 + 2 * RP_MAX_VARS) * sizeof(double), s));
+  double *part = (double *)tw.p, *res = part + (size_t)nblk * n * 2;
+  RP_CUDA(launch_minmax(dX, K, n, part, nblk, res, s));
+  double h[2 * RP_MAX_VARS];
+  RP_CUDA(cudaMemcpyAsync(h, res, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < n; ++k) {
+    lo[k] = h[2 * k];
+    hi[k] = h[2 * k + 1];
+  }
+  return RP_OK;
+}
+
+rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
+                             const rp_basis *basis, const rp_xform *xform, double *G, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(G && basis && xform, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 0 && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "K = %lld, n_v = %d", (long long)K, n_v);
+  RP_REQUIRE(K == 0 || (X && V), RP_ERR_INVALID_ARG, "null X / V");
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, xform, &gb)) != RP_OK) return st;
+  const int nc = gb.nc, n = gb.n;
+  Tmp tX, tV, tG, tb, tp;
+  const double *dX = nullptr, *dV = nullptr;
+  double *dG;
+  bool hG;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  if ((st = stage_out(G, (size_t)n_v * nc * nc, tG, &dG, &hG, s)) != RP_OK) return st;
+  if (K == 0) {
+    RP_CUDA(cudaMemsetAsync(dG, 0, (size_t)n_v * nc * nc * 8, s));
+  } else {
+    RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+    RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+    const size_t pe = gram_partial_elems(gb, n_v, K, num_sms());
+    RP_CUDA(tp.alloc(pe * 8, s));
+    RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, K, n_v, dG, (double *)tp.p, pe, s));
+  }
+  // (host sources of H2D copies from pageable memory are consumed before cudaMemcpyAsync
+  // returns, so stack-resident staging data needs no synchronisation)
+  if (hG) {
+    RP_CUDA(cudaMemcpyAsync(G, dG, (size_t)n_v * nc * nc * 8, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+  return RP_OK;
+}
+
+static rp_status solve_impl(const double *dG, int32_t n_v, int nc, int beta0, double *coef_out,
+                            rp_fit_info *info, cudaStream_t s) {
+  Tmp tc;
+  RP_CUDA(tc.alloc((size_t)n_v * (nc + 5) * 8, s));
+  double *dc = (double *)tc.p, *di = dc + (size_t)n_v * nc;
+  RP_CUDA(launch_solve(dG, n_v, nc, beta0, dc, di, s));
+  std::vector<double> hinfo((size_t)n_v * 5);
+  RP_CUDA(cudaMemcpyAsync(coef_out, dc, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaMemcpyAsync(hinfo.data(), di, (size_t)n_v * 5 * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  rp_status worst = RP_OK;
+  for (int v = 0; v < n_v; ++v) {
+    const int stv = (int)hinfo[v * 5];
+    if (info) {
+      info[v].status = stv;
+      info[v].rank = (int32_t)hinfo[v * 5 + 1];
+      info[v].resid2 = hinfo[v * 5 + 2];
+      info[v].min_pivot = hinfo[v * 5 + 3];
+      info[v].cond_est = hinfo[v * 5 + 4];
+    }
+    if (stv != 0) worst = (rp_status)stv;
+  }
+  if (worst != RP_OK) set_error("normal equations are degenerate (non-SPD or pivot <= 1e-13)");
+  return worst;
+}
+
+rp_status rp_solve_normal(const double *G, int32_t n_v, const rp_basis *basis, double *coef_out,
+                          rp_fit_info *info, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(G && basis && coef_out, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "n_v = %d", n_v);
+  rp_status st = check_basis(*basis, basis->n_vars, "solve", true);
+  if (st != RP_OK) return st;
+  const int nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc >= 2 && nc <= 161, RP_ERR_UNSUPPORTED, "solve: n_c = %d outside [2, 161]", nc);
+  if ((st = ensure_device()) != RP_OK) return st;
+  Tmp tG;
+  const double *dG;
+  if ((st = stage_in(G, (size_t)n_v * nc * nc, tG, &dG, s)) != RP_OK) return st;
+  return solve_impl(dG, n_v, nc, basis->n_num, coef_out, info, s);
+}
+
+rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                 double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(X && V && basis && coef_out, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 1 && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "K = %lld, n_v = %d", (long long)K, n_v);
+  rp_status st = check_basis(*basis, basis->n_vars, "fit", true);
+  if (st != RP_OK) return st;
+  const int n = basis->n_vars, nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc <= 161, RP_ERR_UNSUPPORTED, "fit: n_c = %d > 161", nc);
+  if ((st = ensure_device()) != RP_OK) return st;
+  Tmp tX, tV, tw, tG, tb, tp;
+  const double *dX, *dV;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  // a10 on the device: min / max, then the transform
+  const int nblk = minmax_blocks(K);
+  RP_CUDA(tw.alloc(((size_t)nblk * n * 2 + 4 * RP_MAX_VARS) * sizeof(double), s));
+  double *part = (double *)tw.p, *lohi = part + (size_t)nblk * n * 2, *xf = lohi + 2 * RP_MAX_VARS;
+  RP_CUDA(launch_minmax(dX, K, n, part, nblk, lohi, s));
+  RP_CUDA(launch_xform(lohi, n, xf, s));
+  double hxf[2 * RP_MAX_VARS];
+  RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  rp_xform xform;
+  memset(&xform, 0, sizeof xform);
+  for (int k = 0; k < n; ++k) {
+    xform.c[k] = hxf[2 * k];
+    xform.e[k] = (int32_t)hxf[2 * k + 1];
+  }
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, &xform, &gb)) != RP_OK) return st;
+  RP_CUDA(tG.alloc((size_t)n_v * nc * nc * 8, s));
+  RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+  RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+  const size_t pe = gram_partial_elems(gb, n_v, K, num_sms());
+  RP_CUDA(tp.alloc(pe * 8, s));
+  RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, K, n_v, (double *)tG.p, (double *)tp.p, pe, s));
+  if (xform_out) *xform_out = xform;
+  return solve_impl((const double *)tG.p, n_v, nc, basis->n_num, coef_out, info, s);
+}
+
+rp_status rp_eval_metrics(const rp_program *prog, const double *X, int64_t K, double *out, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(prog && out && (X || K == 0) && K >= 0, RP_ERR_INVALID_ARG, "bad argument");
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  DevProg hp;
+  if ((st = compile_program(prog, &hp)) != RP_OK) return st;
+  if (K == 0) return RP_OK;
+  const int n = prog->d + prog->p;
+  Tmp tX, to, tp;
+  const double *dX;
+  double *dout;
+  bool ho;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_out(out, (size_t)K * prog->n_metrics, to, &dout, &ho, s)) != RP_OK) return st;
+  RP_CUDA(tp.alloc(sizeof(DevProg), s));
+  RP_CUDA(cudaMemcpyAsync(tp.p, &hp, sizeof hp, cudaMemcpyHostToDevice, s));
+  RP_CUDA(launch_eval_metrics((const DevProg *)tp.p, prog->n_metrics, dX, K, dout, s));
+  if (ho) {
+    RP_CUDA(cudaMemcpyAsync(out, dout, (size_t)K * prog->n_metrics * 8, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+  return RP_OK;
+}
+
+rp_status rp_plan_create(const rp_program *progs, int32_t n_prog, const int32_t *F, int32_t nF,
+                         rp_plan *out, rp_stream sv) {
+  rp_status st = plan_create(progs, n_prog, F, nF, out, (cudaStream_t)sv, false);
+  if (st == RP_OK) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)sv);
+    if (e != cudaSuccess) {
+      plan_free(*out);
+      *out = nullptr;
+      return cuda_fail(e, "plan create", __FILE__, __LINE__);
+    }
+  }
+  return st;
+}
+
+rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_t *best_idx,
+                              double *best_E, double *second_E, rp_stream sv) {
+  return plan_eval(plan, D, nD, best_idx, best_E, second_E, (cudaStream_t)sv);
+}
+
+rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible) {
+  RP_REQUIRE(plan && n_static_feasible && prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "bad argument");
+  int32_t v = 0;
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  RP_CUDA(cudaMemcpy(&v, plan->tab.nFc + prog, 4, cudaMemcpyDeviceToHost));
+  *n_static_feasible = v;
+  return RP_OK;
+}
+
+rp_status rp_plan_destroy(rp_plan plan) {
+  plan_free(plan);
+  return RP_OK;
+}
+
+rp_status rp_eval_argmin_batched(const rp_program *progs, int32_t n_prog, const int32_t *D, int64_t nD,
+                                 const int32_t *F, int32_t nF, int32_t *best_idx, double *best_E,
+                                 double *second_E, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(nD >= 0, RP_ERR_INVALID_ARG, "nD < 0");
+  rp_plan pl = nullptr;
+  rp_status st = plan_create(progs, n_prog, F, nF, &pl, s, true);
+  if (st != RP_OK) return st;
+  st = plan_eval(pl, D, nD, best_idx, best_E, second_E, s);
+  plan_free(pl);  // stream-ordered frees
+  return st;
+}
+
+rp_status rp_eval_argmin(const rp_program *prog, const int32_t *D, int64_t nD, const int32_t *F,
+                         int32_t nF, int32_t *best_idx, double *best_E, double *second_E, rp_stream s) {
+  return rp_eval_argmin_batched(prog, 1, D, nD, F, nF, best_idx, best_E, second_E, s);
+}
+
+}  // extern "C"

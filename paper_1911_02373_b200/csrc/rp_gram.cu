@@ -1,0 +1,441 @@
+// rp_gram.cu -- the compile-time least-squares fit's dense part, and small helpers.
+//
+// the coefficients alpha, beta of g = p/q are estimated by "linear least
+// squares" on an "over-determined system of linear equations" whose rows are built "from the
+// evaluation of monomial terms, resulting in essentially a Vandermonde matrix"
+// (PAPER.md:2601-2603).  Row r of the linearised system p(x) - V q(x) = 0 is
+// a_r = [M(u_r) | -V_r N(u_r)]; the normal equations need G = A^T A = sum_r a_r a_r^T.
+//
+// k_gram: one CTA per SM, 8 warps.  Each CTA owns a contiguous slab of rows, builds RT = 64
+// design rows at a time in shared memory (never in HBM) and accumulates the upper-triangular
+// 8x8 tiles of G with FP64 tensor-core mma.sync.m8n8k4 (SASS DMMA.8x8x4).  X / V tiles arrive
+// in shared memory through the bulk-copy (TMA) engine: cp.async.bulk + mbarrier, double
+// buffered, so the next slab streams in while the current one is multiplied.  Accuracy: the
+// register accumulators are flushed into a shared-memory accumulator every kChunk rows
+// (two-level summation), the per-CTA partials are summed in a fixed order by k_gram_reduce.
+#include <cstdio>
+
+#include "rp_internal.cuh"
+
+namespace rp {
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ============================================================================================
+// minmax (a10): per-column min / max of X [K][n]
+// ============================================================================================
+__global__ void k_minmax_part(const double *X, int64_t K, int n, double *part) {
+  __shared__ double smin[32][kMaxVars], smax[32][kMaxVars];
+  double lo[kMaxVars], hi[kMaxVars];
+  for (int k = 0; k < kMaxVars; ++k) {
+    lo[k] = __longlong_as_double(0x7ff0000000000000ll);
+    hi[k] = -lo[k];
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < K;
+       r += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < n; ++k) {
+      const double x = X[r * n + k];
+      lo[k] = fmin(lo[k], x);
+      hi[k] = fmax(hi[k], x);
+    }
+  for (int k = 0; k < n; ++k)
+    for (int o = 16; o >= 1; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      smin[wid][k] = lo[k];
+      smax[wid][k] = hi[k];
+    }
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int k = threadIdx.x;
+    double a = smin[0][k], b = smax[0][k];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmin(a, smin[w][k]);
+      b = fmax(b, smax[w][k]);
+    }
+    part[((int64_t)blockIdx.x * n + k) * 2 + 0] = a;
+    part[((int64_t)blockIdx.x * n + k) * 2 + 1] = b;
+  }
+}
+
+__global__ void k_minmax_final(const double *part, int nblk, int n, double *out) {
+  const int k = threadIdx.x;
+  if (k >= n) return;
+  double a = part[k * 2], b = part[k * 2 + 1];
+  for (int i = 1; i < nblk; ++i) {
+    a = fmin(a, part[((int64_t)i * n + k) * 2]);
+    b = fmax(b, part[((int64_t)i * n + k) * 2 + 1]);
+  }
+  out[k * 2] = a;
+  out[k * 2 + 1] = b;
+}
+
+// a10: c_k = (lo_k + hi_k) / 2, e_k = least integer with 2^e_k >= max((hi_k - lo_k) / 2, 1)
+// (reading R14).  lohi [n][2] -> out [n][2] = (c_k, (double)e_k).
+__global__ void k_xform(const double *lohi, int n, double *out) {
+  const int k = threadIdx.x;
+  if (k >= n) return;
+  const double lo = lohi[2 * k], hi = lohi[2 * k + 1];
+  double h = (hi - lo) * 0.5;
+  if (!(h >= 1.0)) h = 1.0;
+  int e = 0;
+  while (ldexp(1.0, e) < h) ++e;
+  out[2 * k] = (lo + hi) * 0.5;
+  out[2 * k + 1] = (double)e;
+}
+
+cudaError_t launch_xform(const double *d_lohi, int n, double *d_out, cudaStream_t s) {
+  k_xform<<<1, 32, 0, s>>>(d_lohi, n, d_out);
+  return cudaGetLastError();
+}
+
+int minmax_blocks(int64_t K) {
+  int64_t b = (K + 255) / 256;
+  int64_t cap = 4LL * num_sms();
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int nblk,
+                          double *d_out, cudaStream_t s) {
+  k_minmax_part<<<nblk, 256, 0, s>>>(X, K, n, d_part);
+  k_minmax_final<<<1, 32, 0, s>>>(d_part, nblk, n, d_out);
+  return cudaGetLastError();
+}
+
+// ============================================================================================
+// eval_metrics (a4 alone): out[i][r] = p_i(u_r) / q_i(u_r)
+// ============================================================================================
+__global__ void k_eval_metrics(const DevProg *pgp, int nm, const double *X, int64_t K,
+                               double *out) {
+  const DevProg &pg = *pgp;
+  const int n = pg.d + pg.p;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < K;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double u[kMaxVars];
+    for (int k = 0; k < n; ++k) u[k] = (X[r * n + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+    double mD[kMaxDE];
+    for (int de = 0; de < pg.nDE; ++de) {
+      double m = 1.0;
+      for (int k = 0; k < pg.d; ++k)
+        for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u[k];
+      mD[de] = m;
+    }
+    for (int i = 0; i < nm; ++i) {
+      double pq[2];
+      for (int h = 0; h < 2; ++h) {
+        const int k = 2 * i + h;
+        double acc = 0.0;
+        for (int pe = 0; pe < pg.nPE; ++pe) {
+          const int row = k * pg.nPE + pe;
+          double c = 0.0;
+          for (int j = pg.row_start[row]; j < pg.row_start[row + 1]; ++j)
+            c = fma(pg.term_coef[j], mD[pg.term_de[j]], c);
+          double m = 1.0;
+          for (int kk = 0; kk < pg.p; ++kk)
+            for (int e = 0; e < pg.pe_exp[pe][kk]; ++e) m *= u[pg.d + kk];
+          acc = fma(c, m, acc);
+        }
+        pq[h] = acc;
+      }
+      out[(int64_t)i * K + r] = pq[0] / pq[1];
+    }
+  }
+}
+
+cudaError_t launch_eval_metrics(const DevProg *d_prog, int nm, const double *X, int64_t K,
+                                double *out, cudaStream_t s) {
+  if (K == 0) return cudaSuccess;
+  int64_t b = (K + 127) / 128;
+  int cap = 8 * num_sms();
+  k_eval_metrics<<<(int)(b > cap ? cap : b), 128, 0, s>>>(d_prog, nm, X, K, out);
+  return cudaGetLastError();
+}
+
+// ============================================================================================
+// Gram (a11 + a12)
+// ============================================================================================
+constexpr int kGramWarps = 8;
+constexpr int kGramThreads = kGramWarps * 32;
+constexpr int kRT = 64;             // design rows per smem tile (16 k-steps of 4)
+constexpr int kMaxTilesPerWarp = 32;
+constexpr int kTilesPerGroup = kGramWarps * kMaxTilesPerWarp;  // 256 upper tiles per CTA pass
+constexpr int kChunkTiles = 8;      // flush register accumulators every 8 tiles (512 rows)
+
+__host__ __device__ inline int gram_stride(int nb) {  // smem row stride (doubles), = 4 mod 16
+  int s = nb * 8;
+  while (s % 16 != 4) ++s;
+  return s;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP), completes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct GramArgs {
+  const GramBasis *basis;
+  const double *X;
+  const double *V;  // [n_v][K]
+  int64_t K;
+  int n_v;
+  int nb, ntiles, stride;
+  double *part;     // [n_v][gridDim.y][gridDim.x][ntiles_in_group * 64] (tile-major)
+};
+
+// Shared memory layout (dynamic): sA [kRT][stride] | sAcc [kTilesPerGroup][64] |
+// sX[2][kRT * 8] | sV[2][kRT] | sU[kRT * 8] | bars[2]
+__global__ void __launch_bounds__(kGramThreads, 1) k_gram(GramArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const GramBasis &B = *a.basis;
+  const int n = B.n, nc = B.nc, n_num = B.n_num;
+  const int stride = a.stride;
+  double *sA = (double *)smem_raw;
+  double *sAcc = sA + kRT * stride;
+  double *sX = sAcc + kTilesPerGroup * 64;
+  double *sV = sX + 2 * kRT * kMaxVars;
+  double *sU = sV + 2 * kRT;
+  uint64_t *bars = (uint64_t *)(sU + kRT * kMaxVars);
+
+  const int metric = blockIdx.z;
+  const int group = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double *V = a.V + (int64_t)metric * a.K;
+
+  // contiguous slab of rows for this CTA
+  // (slab boundaries rounded to even rows so bulk copies of V stay 16-byte aligned)
+  const int64_t r_begin = (a.K * blockIdx.x / gridDim.x) & ~1ll;
+  const int64_t r_end =
+      (blockIdx.x + 1 == gridDim.x) ? a.K : ((a.K * (blockIdx.x + 1) / gridDim.x) & ~1ll);
+
+  // tiles of this warp: group tiles t_g = group * 256 + w + 8 * t, upper-triangular (bi <= bj)
+  int toff[kMaxTilesPerWarp];  // (8*bi) | (8*bj) << 16, or -1
+  {
+    // enumerate upper tiles row-major: tile id -> (bi, bj)
+#pragma unroll
+    for (int t = 0; t < kMaxTilesPerWarp; ++t) {
+      int id = group * kTilesPerGroup + wid + kGramWarps * t;
+      toff[t] = -1;
+      if (id < a.ntiles) {
+        int bi = 0, rem = id;
+        while (rem >= a.nb - bi) {
+          rem -= a.nb - bi;
+          ++bi;
+        }
+        const int bj = bi + rem;
+        toff[t] = (8 * bi) | ((8 * bj) << 16);
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < kTilesPerGroup * 64; i += blockDim.x) sAcc[i] = 0.0;
+  // zero the pad columns of sA once (columns nc .. stride-1 stay zero)
+  for (int i = threadIdx.x; i < kRT * stride; i += blockDim.x) sA[i] = 0.0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t nrows = r_end - r_begin;
+  const int64_t ntile_rows = (nrows + kRT - 1) / kRT;
+  // producer: one elected thread issues the bulk copies of X / V row tiles
+  auto issue = [&](int64_t tr, int buf) {
+    const int64_t r0 = r_begin + tr * kRT;
+    const int64_t rows = (r_end - r0) < kRT ? (r_end - r0) : kRT;
+    const unsigned bx = (unsigned)(rows * n * sizeof(double));
+    const unsigned bv = (unsigned)(rows * sizeof(double));
+    mbar_expect_tx(&bars[buf], bx + bv);
+    bulk_g2s(sX + buf * kRT * kMaxVars, a.X + r0 * n, bx, &bars[buf]);
+    bulk_g2s(sV + buf * kRT, V + r0, bv, &bars[buf]);
+  };
+  // bulk copies need 16-byte aligned sources and sizes: use them when the slab allows it
+  const bool bulk_ok = ((((uintptr_t)(a.X + r_begin * n)) & 15) == 0) &&
+                       ((((uintptr_t)(V + r_begin)) & 15) == 0) && ((kRT * n) % 2 == 0) &&
+                       (nrows % 2 == 0);
+  if (bulk_ok && threadIdx.x == 0 && ntile_rows > 0) issue(0, 0);
+
+  double acc[kMaxTilesPerWarp][2];
+#pragma unroll
+  for (int t = 0; t < kMaxTilesPerWarp; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+  for (int64_t tr = 0; tr < ntile_rows; ++tr) {
+    const int buf = (int)(tr & 1);
+    const int64_t r0 = r_begin + tr * kRT;
+    const int rows = (int)((r_end - r0) < kRT ? (r_end - r0) : kRT);
+    const double *tX;
+    const double *tV;
+    if (bulk_ok) {
+      if (threadIdx.x == 0 && tr + 1 < ntile_rows) issue(tr + 1, buf ^ 1);
+      mbar_wait(&bars[buf], (unsigned)((tr >> 1) & 1));
+      tX = sX + buf * kRT * kMaxVars;
+      tV = sV + buf * kRT;
+    } else {
+      tX = a.X + r0 * n;  // generic path: plain loads
+      tV = V + r0;
+    }
+    // a10: u = (x - c) 2^-e for the tile's rows
+    for (int i = threadIdx.x; i < kRT * n; i += blockDim.x) {
+      const int r = i / n, k = i % n;
+      sU[i] = r < rows ? (tX[r * n + k] - B.xc[k]) * ldexp(1.0, -B.xe[k]) : 0.0;
+    }
+    __syncthreads();
+    // a11: design rows [M(u) | -V N(u)] into sA (rows >= `rows` are zero: no contribution)
+    for (int i = threadIdx.x; i < kRT * nc; i += blockDim.x) {
+      const int r = i / nc, j = i % nc;
+      double m = 0.0;
+      if (r < rows) {
+        m = 1.0;
+        for (int k = 0; k < n; ++k) {
+          const double u = sU[r * n + k];
+          for (int e = 0; e < B.exp[j][k]; ++e) m *= u;
+        }
+        if (j >= n_num) m *= -tV[r];
+      }
+      sA[r * stride + j] = m;
+    }
+    __syncthreads();
+    // a12: G_tile += A_bi^T A_bj over the 16 k-steps of this row tile
+#pragma unroll 1
+    for (int ks = 0; ks < kRT / 4; ++ks) {
+      const double *row = sA + (ks * 4 + (lane & 3)) * stride + (lane >> 2);
+#pragma unroll
+      for (int t = 0; t < kMaxTilesPerWarp; ++t) {
+        if (toff[t] >= 0) {
+          const double av = row[toff[t] & 0xffff];
+          const double bv = row[toff[t] >> 16];
+          dmma_8x8x4(acc[t][0], acc[t][1], av, bv);
+        }
+      }
+    }
+    // two-level accumulation: flush registers every kChunkTiles row tiles
+    if (((tr + 1) % kChunkTiles) == 0 || tr + 1 == ntile_rows) {
+#pragma unroll
+      for (int t = 0; t < kMaxTilesPerWarp; ++t) {
+        if (toff[t] >= 0) {
+          double *dst = sAcc + (wid + kGramWarps * t) * 64 + lane * 2;
+          dst[0] += acc[t][0];
+          dst[1] += acc[t][1];
+          acc[t][0] = acc[t][1] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write this CTA's partial tiles (tile-major, 64 doubles per tile in fragment order)
+  const int64_t groups = gridDim.y;
+  double *out = a.part + (((int64_t)metric * groups + group) * gridDim.x + blockIdx.x) *
+                             (int64_t)kTilesPerGroup * 64;
+  for (int i = threadIdx.x; i < kTilesPerGroup * 64; i += blockDim.x) out[i] = sAcc[i];
+}
+
+// Fixed-order sum of the per-CTA partials, scattered into the symmetric G.
+__global__ void k_gram_reduce(const double *part, int nblk, int groups, int nb, int ntiles,
+                              int nc, double *G) {
+  const int metric = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)ntiles * 64;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(i / 64), e = (int)(i % 64);
+    const int group = tile / kTilesPerGroup, tig = tile % kTilesPerGroup;
+    // tig = wid + 8 * t within the group; element e = lane * 2 + v
+    const int lane = e >> 1, v = e & 1;
+    // tile id -> (bi, bj)
+    int bi = 0, rem = tile;
+    while (rem >= nb - bi) {
+      rem -= nb - bi;
+      ++bi;
+    }
+    const int bj = bi + rem;
+    const int row = 8 * bi + (lane >> 2), col = 8 * bj + 2 * (lane & 3) + v;
+    const double *src = part + ((int64_t)metric * groups + group) * nblk * (int64_t)kTilesPerGroup * 64 +
+                         (int64_t)tig * 64 + e;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += src[(int64_t)b * kTilesPerGroup * 64];
+    if (row < nc && col < nc) {
+      double *Gm = G + (int64_t)metric * nc * nc;
+      Gm[(int64_t)row * nc + col] = s;
+      Gm[(int64_t)col * nc + row] = s;
+    }
+  }
+}
+
+static int gram_grid_x(int64_t K) {
+  int64_t want = (K + kRT - 1) / kRT;
+  int64_t cap = num_sms();
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm) {
+  (void)nsm;
+  const int nb = (h.nc + 7) / 8;
+  const int ntiles = nb * (nb + 1) / 2;
+  const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
+  return (size_t)n_v * groups * gram_grid_x(K) * kTilesPerGroup * 64;
+}
+
+cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const double *X,
+                        const double *V, int64_t K, int n_v, double *G, double *d_part,
+                        size_t part_elems, cudaStream_t s) {
+  const int nb = (h.nc + 7) / 8;
+  const int ntiles = nb * (nb + 1) / 2;
+  const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
+  const int gx = gram_grid_x(K);
+  if (gram_partial_elems(h, n_v, K, 0) > part_elems) return cudaErrorInvalidValue;
+  const int stride = gram_stride(nb);
+  GramArgs a{d_basis, X, V, K, n_v, nb, ntiles, stride, d_part};
+  const size_t smem = (size_t)kRT * stride * 8 + (size_t)kTilesPerGroup * 64 * 8 +
+                      2 * kRT * kMaxVars * 8 + 2 * kRT * 8 + kRT * kMaxVars * 8 + 16;
+  cudaError_t e = cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gram<<<dim3(gx, groups, n_v), kGramThreads, smem, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int rb = (int)((ntiles * 64 + 255) / 256);
+  k_gram_reduce<<<dim3(rb, n_v), 256, 0, s>>>(d_part, gx, groups, nb, ntiles, h.nc, G);
+  return cudaGetLastError();
+}
+
+}  // namespace rp

@@ -1,0 +1,101 @@
+// rp_internal.cuh -- internal types shared by librp's translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rp.h"
+
+namespace rp {
+
+// ---- errors ---------------------------------------------------------------------------------
+void set_error(const char *fmt, ...);
+rp_status cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define RP_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) return rp::cuda_fail(e_, #call, __FILE__, __LINE__);    \
+  } while (0)
+#define RP_REQUIRE(cond, status, ...)   \
+  do {                                  \
+    if (!(cond)) {                      \
+      rp::set_error(__VA_ARGS__);       \
+      return (status);                  \
+    }                                   \
+  } while (0)
+
+// ---- compiled program (device layout) --------------------------------------------------------
+// The l numerators / denominators ("polys", k = 2i for p_i, 2i+1 for q_i) are split into
+// data and program parts of each monomial: m_e(u) = m_{eD}(u_D) * m_{eP}(u_P).  For every
+// poly k and every distinct program-part exponent pe, the data polynomial
+//   C_{k,pe}(D) = sum_{terms with eP = pe} coef * m_{eD}(u_D)
+// is staged once per D (a2), so that p_k(D,P) = sum_pe C_{k,pe}(D) * m_pe(u_P) (a4).
+constexpr int kMaxVars = RP_MAX_VARS;
+constexpr int kMaxMetrics = RP_MAX_METRICS;
+constexpr int kMaxPolys = 2 * RP_MAX_METRICS;
+constexpr int kMaxPE = 36;     // distinct program-part exponents (degree 4 in 3 vars = 35)
+constexpr int kMaxDE = 64;     // distinct data-part exponents
+constexpr int kMaxTerms = 1536;
+constexpr int kMaxRows = kMaxPolys * kMaxPE;
+
+struct DevProg {
+  int32_t d, p, nm, tmpl, npoly, nPE, nDE, nterm;
+  int32_t grid_map[3];
+  int32_t n_sm, w_max, b_max, t_max;
+  int64_t r_max, z_max, R, Z0, Z1;
+  double freq, mem_bw, lbpw, mem_ld, dd_coal, dd_unc, U, issue;
+  double xc[kMaxVars];
+  int32_t xe[kMaxVars];
+  int8_t de_exp[kMaxDE][kMaxVars];  // data-part exponents (first d entries used)
+  int8_t pe_exp[kMaxPE][3];         // program-part exponents
+  int16_t row_start[kMaxRows + 1];  // terms of row (k * nPE + pe) are [row_start[r], row_start[r+1])
+  int16_t term_de[kMaxTerms];
+  double term_coef[kMaxTerms];
+};
+
+// Per-configuration table of a plan (SoA over the statically feasible, compacted configs in
+// ascending original index; program g at offset g * nF).
+struct CfgTable {
+  int32_t *orig;   // [n_prog][nF]
+  int32_t *P;      // [n_prog][3][nF]
+  int32_t *B;      // [n_prog][nF]  B_active
+  int32_t *W;      // [n_prog][nF]  W_active
+  double *mP;      // [n_prog][npe_pad][nF]  program-part monomials (0 for pe >= nPE)
+  int32_t *nFc;    // [n_prog]
+};
+
+// Host-side marshalling of an rp_program into DevProg (layout only: splitting exponent vectors,
+// sorting terms, copying coefficients; no arithmetic on values).
+rp_status compile_program(const rp_program *prog, DevProg *out);
+
+// ---- launchers (defined in the kernel TUs) ----------------------------------------------------
+cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_t *d_F, int nF,
+                                int npe_pad, CfgTable tab, cudaStream_t s);
+cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, CfgTable tab, int nF, int npe_pad,
+                         int d, const int32_t *d_D, int64_t nD, int32_t *idx, double *bestE,
+                         double *secondE, cudaStream_t s);
+cudaError_t launch_eval_metrics(const DevProg *d_prog, int nm, const double *X, int64_t K,
+                                double *out, cudaStream_t s);
+cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int nblk,
+                          double *d_out, cudaStream_t s);
+int minmax_blocks(int64_t K);
+cudaError_t launch_xform(const double *d_lohi, int n, double *d_out, cudaStream_t s);
+
+struct GramBasis {  // exponents of the n_c design columns (numerator then denominator)
+  int32_t n, n_num, n_den, nc, maxdeg;
+  int8_t exp[256][kMaxVars];
+  double xc[kMaxVars];
+  int32_t xe[kMaxVars];
+};
+cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, const double *X,
+                        const double *V, int64_t K, int n_v, double *G, double *d_part,
+                        size_t part_elems, cudaStream_t s);
+size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_sms);
+
+cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *coef_out,
+                         double *info_out, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace rp

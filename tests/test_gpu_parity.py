@@ -1,0 +1,200 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): argmin config index bit-exact wherever the oracle's
+(second - best)/best margin exceeds 1e-9; E within 1e-12 relative; fitted coefficients within
+1e-9 relative (inf-norm, after beta_0 = 1); Gram entries within
+1e-12 * sqrt(G_ii G_jj).  Near ties (margin <= 1e-9) must pick a config inside the oracle's
+epsilon-tie set (reading R20).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1911_02373_b200 as rp  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def check_sweep(idx, E, S, ref, spec=None, D=None, F=None, tag=""):
+    idx = np.asarray(idx.cpu() if hasattr(idx, "cpu") else idx)
+    E = np.asarray(E.cpu() if hasattr(E, "cpu") else E)
+    feas = ref["idx"] >= 0
+    assert np.array_equal(idx < 0, ~feas), tag
+    assert np.all(np.isinf(E[~feas])), tag
+    b = ref["best"][feas]
+    rel = np.abs(E[feas] - b) / b
+    assert rel.max(initial=0) <= 1e-12, (tag, rel.max())
+    margin = (ref["second"] - ref["best"]) / ref["best"]
+    strict = feas & (margin > 1e-9)
+    assert np.array_equal(idx[strict], ref["idx"][strict]), tag
+    # near ties: the GPU winner's oracle E must be within the tie margin of the best
+    for i in np.nonzero(feas & ~(margin > 1e-9))[0]:
+        if idx[i] != ref["idx"][i]:
+            tr = oracle.eval_pair(spec, D[i], F[idx[i]])
+            assert tr["feasible"] and abs(float(tr["E"]) - ref["best"][i]) <= 1e-9 * ref["best"][i], (tag, i)
+    if S is not None:
+        S = np.asarray(S.cpu() if hasattr(S, "cpu") else S)
+        fin = np.isfinite(ref["second"])
+        assert np.array_equal(np.isfinite(S), fin), tag
+        r2 = np.abs(S[fin] - ref["second"][fin]) / ref["second"][fin]
+        assert r2.max(initial=0) <= 1e-12, (tag, r2.max())
+    return int(strict.sum()), int(feas.sum())
+
+
+def test_sweep_tiny():
+    case = synth.tiny_sweep()
+    spec = case.programs[0]
+    D = np.concatenate([synth.random_D_edge_cases(1), case.D])
+    ref = oracle.sweep(spec, D, case.F)
+    idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(case.F))
+    check_sweep(idx, E, S, ref, spec, D, case.F, "tiny")
+
+
+def test_sweep_tiny_host_pointers():
+    """The same call with host (numpy) buffers: the library stages them itself."""
+    case = synth.tiny_sweep()
+    spec = case.programs[0]
+    ref = oracle.sweep(spec, case.D, case.F)
+    idx, E, S = rp.eval_argmin(spec, case.D, case.F)
+    assert isinstance(idx, np.ndarray)
+    check_sweep(idx, E, S, ref, spec, case.D, case.F, "tiny-host")
+
+
+def test_sweep_g1_template_all_tie():
+    """SPEC.md:492 example through the GPU: E = N^2/(bx*by), N = 64 -> lowest T=1024 index."""
+    from helpers import ratfunc_program
+    F = synth.F_pow2_2d()
+    spec = ratfunc_program(synth.HW_GTX1080TI, [[2, 0, 0]], [[0, 1, 1]], [1.0, 1.0], d=1, p=2, R=16)
+    D = np.array([[64], [8], [1000]], dtype=np.int32)
+    ref = oracle.sweep(spec, D, F)
+    idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F))
+    assert np.array_equal(idx.cpu().numpy(), ref["idx"])
+    assert np.array_equal(E.cpu().numpy(), ref["best"])
+
+
+@pytest.mark.parametrize("which", ["polybench", "multikernel"])
+def test_sweep_batched(which):
+    case = synth.polybench_sweep() if which == "polybench" else synth.multikernel_sweep()
+    D = np.concatenate([synth.random_D_edge_cases(1), case.D])
+    idx, E, S = rp.eval_argmin_batched(case.programs, _cuda(D), _cuda(case.F))
+    for g, spec in enumerate(case.programs):
+        ref = oracle.sweep(spec, D, case.F)
+        check_sweep(idx[g], E[g], S[g], ref, spec, D, case.F, f"{which}[{g}]")
+
+
+def test_sweep_large_full_size_sampled():
+    """The bench's launch configuration: all 10^6 D x 1,024 F on the GPU (through a plan, as
+    bench.py does), compared on the oracle's subsample (every 100th D + first/last 100)."""
+    case = synth.large_sweep()
+    spec = case.programs[0]
+    plan = rp.Plan([spec], _cuda(case.F))
+    assert plan.static_feasible() == 464
+    idx, E, S = plan.eval(_cuda(case.D))
+    sub = synth.large_subsample_index(len(case.D))
+    ref = oracle.sweep(spec, case.D[sub], case.F)
+    strict, feas = check_sweep(idx[0][sub], E[0][sub], S[0][sub], ref, spec, case.D[sub], case.F, "large")
+    assert feas == len(sub) and strict >= 0.99 * feas
+    c = ref["counters"]
+    assert c["case1"] > 0 and c["case2"] > 0 and c["case3"] > 0
+
+
+def test_eval_metrics():
+    fc = synth.fitheavy(K=5000)
+    spec = fc.truths[0]
+    got = rp.eval_metrics(spec, _cuda(fc.X)).cpu().numpy()
+    want = np.asarray(oracle.program_metrics(spec, fc.X), dtype=np.float64)
+    assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-13
+
+
+def _fit_parity(fc, sigma_noise=None, gram_check=True):
+    truth = fc.truths[0]
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(truth, fc.X)])
+    if fc.noise is not None:
+        V = V * fc.noise
+    coef, (c, e), infos = rp.fit(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp)
+    worst = 0.0
+    for i in range(len(V)):
+        r = oracle.fit(fc.X, V[i], fc.num_exp, fc.den_exp, nthreads=8)
+        assert np.array_equal(r["c"], c) and np.array_equal(r["e"], e)
+        want = np.asarray(r["coef"], dtype=np.float64)
+        err = np.max(np.abs(coef[i] - want)) / np.max(np.abs(want))
+        worst = max(worst, err)
+        assert err <= 1e-9, (fc.name, i, err, infos[i])
+        if gram_check:
+            G = rp.gram(_cuda(fc.X), _cuda(V[i:i + 1]), fc.num_exp, fc.den_exp, c, e)[0].cpu().numpy()
+            Go = np.asarray(r["G"], dtype=np.float64)
+            dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go)))
+            assert np.max(np.abs(G - Go) / dg) <= 1e-12, (fc.name, i)
+    return worst
+
+
+def test_fit_tiny_box():
+    _fit_parity(synth.tiny_fit_box())
+    _fit_parity(synth.tiny_fit_box(sigma=0.01))
+
+
+def test_fit_polybench_box():
+    _fit_parity(synth.polybench_fit_box(sigma=0.01))
+
+
+def test_fit_fitheavy_full_size():
+    """The north star's 10^6-row Gram fit (noise-free and 1% noise, 3 metrics, 140 columns)."""
+    _fit_parity(synth.fitheavy(), gram_check=False)
+    _fit_parity(synth.fitheavy(sigma=0.01), gram_check=True)
+
+
+def test_fit_host_pointers_and_gram_edge_cases():
+    fc = synth.tiny_fit_box()
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(fc.truths[0], fc.X)])
+    coef_h, xf_h, _ = rp.fit(fc.X, V, fc.num_exp, fc.den_exp)  # host buffers
+    coef_d, xf_d, _ = rp.fit(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp)
+    assert np.array_equal(coef_h, coef_d)
+    c, e = xf_d
+    # K = 0: G = 0; ragged K (not a multiple of the 64-row tile, odd)
+    G0 = rp.gram(np.zeros((0, 3)), np.zeros((1, 0)), fc.num_exp, fc.den_exp, c, e)
+    assert np.all(G0 == 0)
+    for K in (1, 3, 63, 65, 127):
+        X = fc.X[:K]
+        Gk = rp.gram(_cuda(X), _cuda(V[:1, :K]), fc.num_exp, fc.den_exp, c, e)[0].cpu().numpy()
+        Go = np.asarray(oracle.gram(X, V[0, :K], fc.num_exp, fc.den_exp, c, e), dtype=np.float64)
+        dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
+        assert np.max(np.abs(Gk - Go) / dg) <= 1e-13, K
+
+
+def test_fit_degenerate():
+    X = np.ones((10, 1))
+    V = np.full((1, 10), 3.0)
+    b = np.array([[0], [1]], dtype=np.int16)
+    with pytest.raises(rp.RPError) as ei:
+        rp.fit(_cuda(X), _cuda(V), b, b)
+    assert ei.value.status == 3
+
+
+def test_end_to_end_fit_then_sweep():
+    """fitheavy noise-free fit (GPU) -> large sweep (GPU) vs the same chain on the oracle, on a
+    subsample; the fitted program recovers the truth to ~1e-13 so both agree."""
+    import copy
+    fc = synth.fitheavy(K=200_000)
+    truth = fc.truths[0]
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(truth, fc.X)])
+    coef, (c, e), _ = rp.fit(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp)
+    fitted = copy.deepcopy(truth)
+    fitted.coef = [coef[i] for i in range(3)]
+    fitted.xform_c, fitted.xform_e = list(c), list(e)
+    D = synth.large_D(2000)
+    F = synth.F_large()
+    idx, E, S = rp.eval_argmin(fitted, _cuda(D), _cuda(F))
+    ref = oracle.sweep(fitted, D, F)
+    check_sweep(idx, E, S, ref, fitted, D, F, "e2e")

@@ -1,0 +1,56 @@
+"""CPU-side checks of the boundary: librp.so loads, exports every symbol include/rp.h declares,
+and (without a GPU) fails loudly instead of falling back to the CPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rp.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:rp_status|int32_t|const char \*)\s*(rp_\w+)\s*\(", src, re.M)))
+
+
+def test_header_symbols_exported():
+    import paper_1911_02373_b200 as rp
+    names = _declared()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(rp.lib(), n), n
+    assert sorted(rp.EXPORTED) == names
+    assert rp.abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    """ctypes mirrors of rp.h structs have the C sizes (x86-64 ABI)."""
+    import ctypes as C
+    import paper_1911_02373_b200 as rp
+    assert C.sizeof(rp.rp_basis) == 4 * 3 + 4 + 8 * 2
+    assert C.sizeof(rp.rp_xform) == 8 * 8 + 4 * 8
+    assert C.sizeof(rp.rp_hw) == 4 * 4 + 8 * 2 + 8 * 8
+    assert C.sizeof(rp.rp_fit_info) == 4 * 2 + 8 * 3
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    import paper_1911_02373_b200 as rp
+    import synth
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    assert rp.device_count() == 0
+    case = synth.tiny_sweep()
+    with pytest.raises(rp.RPError) as ei:
+        rp.eval_argmin(case.programs[0], case.D, case.F)
+    assert ei.value.status == 2
+    with pytest.raises(rp.RPError):
+        rp.fit(np.ones((4, 1)), np.ones((1, 4)), [[0], [1]], [[0], [1]])
+
+
+def test_invalid_arguments_rejected_before_launch():
+    import paper_1911_02373_b200 as rp
+    with pytest.raises(rp.RPError) as ei:
+        rp.xform_from_box([2.0], [1.0])  # hi < lo
+    assert ei.value.status == 1
