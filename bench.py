@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the rational-program hot path (arXiv 1911.02373) on B200.
+
+One step = the whole hot path over one batch of synthetic input:
+  fit   -- rp_fit of the 3 metrics (comp, coal, uncoal) on the `fitheavy` sample set
+           (K = 10^6 noisy points in (D1, D2, bx, by), total degree <= 4 -> 140 Gram columns);
+  sweep -- the fitted rational program (MWP-CWP estimate E) over the `large` grid
+           (10^6 data tuples x 1,024 configurations, ~10^9 (D,P) pairs) with per-D argmin.
+N > 1 (torchrun): K rows and D tuples are split across ranks (strong scaling); the partial Grams
+are all-reduced and the per-D winners all-gathered over NCCL.
+
+value = nD * nF / (device time of one step, max over ranks)  [RP evals/s, fit included];
+fit_rows_per_s and sweep_evals_per_s break the step down.  Prints ONE JSON line on rank 0.
+
+`--impl reference` times the CPU oracle (oracle/, x87 long double) as it stands on the host
+cores, each step a bounded 1/200 sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import copy
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "RP evals/s over (D,P) grid incl. per-D argmin at 1/2/4/8 B200; fit rows/s"
+UNIT = "evals/s"
+SAMPLE_DIV = 200  # CPU oracle sample: 1/200 of the step (5,000 D x 1,024 F and 5,000 rows x 3 metrics)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+FLOP_PER_PAIR = 220  # a4 183 + a6 1 + a7 36 (division = 1 flop)
+FLOP_PER_D = 860     # a2 staging: 6 polys x 70 terms x 2 + data monomials
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def workload_inputs(nD=1_000_000, K=1_000_000):
+    """Seeded host inputs: fitheavy X + noise multipliers, large D, F, the truth program."""
+    fc = synth.fitheavy(sigma=0.01, K=K)
+    return dict(X=fc.X, noise=fc.noise, num=fc.num_exp, den=fc.den_exp, truth=fc.truths[0],
+                D=synth.large_D(nD), F=synth.F_large())
+
+
+def evaluated_pairs(D, F, t_max=1024):
+    """Number of (D,P) pairs the sweep evaluates: statically feasible P (warp rule, T <= T_max;
+    B_active > 0 holds for every such T at R = 40, Z = 0) that pass P1 P2 <= D1^2."""
+    T = F[:, 0].astype(np.int64) * F[:, 1]
+    ok = (T % 32 == 0) & (T <= t_max)
+    p12 = np.sort(T[ok])
+    d1sq = D[:, 0].astype(np.int64) ** 2
+    return int(np.searchsorted(p12, d1sq, side="right").sum())
+
+
+# ------------------------------------------------------------------------------------------
+# clocks
+# ------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/rp_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[1].isdigit():
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------
+
+def oracle_step(inp, part: int, cores: int):
+    """The oracle's whole path on a 1/SAMPLE_DIV slice (slice `part`): fit of the 3 metrics on
+    K/200 rows, then the sweep of the fitted program over nD/200 tuples x all of F."""
+    import oracle
+    K = len(inp["X"]) // SAMPLE_DIV
+    nd = len(inp["D"]) // SAMPLE_DIV
+    X = inp["X"][part * K:(part + 1) * K]
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(inp["truth"], X)])
+    V *= inp["noise"][:, part * K:(part + 1) * K]
+    D = inp["D"][part * nd:(part + 1) * nd]
+    t0 = time.perf_counter()
+    prog = copy.deepcopy(inp["truth"])
+    coefs = []
+    for i in range(3):
+        r = oracle.fit(X, V[i], inp["num"], inp["den"], nthreads=cores)
+        coefs.append(np.asarray(r["coef"], dtype=np.float64))
+    prog.coef = coefs
+    prog.xform_c, prog.xform_e = list(r["c"]), list(r["e"])
+    oracle.sweep(prog, D, inp["F"], nthreads=cores)
+    dt = time.perf_counter() - t0
+    return nd * len(inp["F"]) / dt, dt
+
+
+def cpu_info():
+    cores = len(os.sched_getaffinity(0))
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return  # rank 0 alone runs and prints it
+    inp = workload_inputs()
+    cores, model = cpu_info()
+    for w in range(args.warmup):
+        oracle_step(inp, w % SAMPLE_DIV, cores)
+    vals, dts = [], []
+    for s in range(args.steps):
+        v, dt = oracle_step(inp, (args.warmup + s) % SAMPLE_DIV, cores)
+        vals.append(v)
+        dts.append(dt)
+    value = len(inp["F"]) * (len(inp["D"]) // SAMPLE_DIV) * len(dts) / sum(dts)
+    sample = (f"1/{SAMPLE_DIV} of the step per step: fit of 3 metrics on {len(inp['X']) // SAMPLE_DIV} rows + "
+              f"sweep of {len(inp['D']) // SAMPLE_DIV} D x {len(inp['F'])} F (consecutive slices)")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "long double (x87)",
+           "data": "synthetic (seeded)", "config": {"workload": "large+fitheavy", "nD": len(inp["D"]),
+                                                   "nF": len(inp["F"]), "K": len(inp["X"]), "n_metrics": 3,
+                                                   "n_c": 140, "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                            "cpu": model},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nD", type=int, default=1_000_000)
+    ap.add_argument("--K", type=int, default=1_000_000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1911_02373_b200 as rp
+    from paper_1911_02373_b200 import dist as rdist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    inp = workload_inputs(args.nD, args.K)
+    F_dev = torch.from_numpy(inp["F"]).to(dev)
+    # metric values V of the sample set: the truth evaluated by the product (rp_eval_metrics),
+    # times the seeded 1% noise multipliers -- input synthesis, outside the timed region
+    X_all = torch.from_numpy(inp["X"]).to(dev)
+    V_all = rp.eval_metrics(inp["truth"], X_all) * torch.from_numpy(inp["noise"]).to(dev)
+    klo, khi = rdist.shard_bounds(len(inp["X"]), world, rank)
+    dlo, dhi = rdist.shard_bounds(len(inp["D"]), world, rank)
+    X_dev = X_all[klo:khi].contiguous()
+    V_dev = V_all[:, klo:khi].contiguous()
+    D_dev = torch.from_numpy(inp["D"][dlo:dhi]).to(dev)
+    del X_all
+    nD, nF, K = len(inp["D"]), len(inp["F"]), len(inp["X"])
+    ops = rdist.LibOps()
+    idx_out = torch.empty((1, dhi - dlo), dtype=torch.int32, device=dev)
+    E_out = torch.empty((1, dhi - dlo), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def fitted_program(coef, c, e):
+        prog = copy.deepcopy(inp["truth"])
+        prog.coef = [np.asarray(coef[i]) for i in range(3)]
+        prog.xform_c, prog.xform_e = list(c), list(e)
+        return prog
+
+    def step(ev=None, X=X_dev, V=V_dev, D=D_dev, out=(idx_out, E_out), F=F_dev):
+        if world == 1:
+            coef, (c, e), _ = rp.fit(X, V, inp["num"], inp["den"], raise_on_degenerate=False)
+        else:
+            coef, (c, e), _ = rdist.sharded_fit(X, V, inp["num"], inp["den"], ops, n_vars=4)
+        if ev is not None:
+            ev[0].record(stream)
+        plan = rp.Plan([fitted_program(coef, c, e)], F)
+        if ev is not None:
+            ev[1].record(stream)
+        idx, E, _ = plan.eval(D, out=(out[0], out[1], None), second=False)
+        if ev is not None:
+            ev[2].record(stream)
+        if world > 1:
+            idx, E = rdist.gather_winners(idx, E, nD)
+        plan.close()
+        return idx, E
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    times, t_fit, t_sweep_k, t_plan = [], [], [], []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 (126 MB) flushed between timed steps
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        a.record(stream)
+        step(ev)
+        b.record(stream)
+        barrier()
+        times.append(a.elapsed_time(b))
+        t_fit.append(a.elapsed_time(ev[0]))
+        t_sweep_k.append(ev[1].elapsed_time(ev[2]))
+        t_plan.append(ev[0].elapsed_time(ev[1]))
+    clocks = sampler.stop() if sampler else None
+    step_ms = sum(times) / len(times)
+    fit_ms = sum(t_fit) / len(t_fit)
+    sweep_ms = sum(t_sweep_k) / len(t_sweep_k)
+    if world > 1:
+        t = torch.tensor([step_ms, fit_ms, sweep_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        step_ms, fit_ms, sweep_ms = t.tolist()
+
+    # ---- secondary kernel: the Gram (timed alone after the timed region) ----------------------
+    c0, e0 = rp.xform_from_box(*rp.minmax(X_dev))
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    G = rp.gram(X_dev, V_dev, inp["num"], inp["den"], c0, e0)
+    torch.cuda.synchronize()
+    g0.record(stream)
+    for _ in range(3):
+        rp.gram(X_dev, V_dev, inp["num"], inp["den"], c0, e0, out=G)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gram_ms = g0.elapsed_time(g1) / 3
+
+    # ---- e2e: the same step through the C ABI with pinned host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(inp["X"][klo:khi]).pin_memory().numpy()
+        Vh = V_dev.cpu().pin_memory().numpy()
+        Dh = torch.from_numpy(inp["D"][dlo:dhi]).pin_memory().numpy()
+        Fh = torch.from_numpy(inp["F"]).pin_memory().numpy()
+        oi = torch.empty((1, dhi - dlo), dtype=torch.int32).pin_memory().numpy()
+        oE = torch.empty((1, dhi - dlo), dtype=torch.float64).pin_memory().numpy()
+        for _ in range(2):
+            step(X=Xh, V=Vh, D=Dh, out=(oi, oE), F=Fh)
+        e_times = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            idx, E = step(X=Xh, V=Vh, D=Dh, out=(oi, oE), F=Fh)
+            if world > 1:
+                idx, E = idx.cpu(), E.cpu()  # gathered winners back to the host
+            b.record(stream)
+            barrier()
+            e_times.append(a.elapsed_time(b))
+        e_ms = sum(e_times) / len(e_times)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_ms = t.item()
+        h2d = Xh.nbytes + Vh.nbytes + Dh.nbytes + Fh.nbytes
+        d2h = oi.nbytes + oE.nbytes + 3 * 140 * 8 + (nD * 12 if world > 1 else 0)
+        e2e = {"value": nD * nF / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "rp_fit + rp_plan_create + rp_plan_eval_argmin with pinned host buffers (library-staged copies)"}
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (k_sweep) ----------------------------------------------
+    pairs_eval = evaluated_pairs(inp["D"][dlo:dhi], inp["F"])
+    flop_launch = pairs_eval * FLOP_PER_PAIR + (dhi - dlo) * FLOP_PER_D
+    achieved = flop_launch / (sweep_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "sweep_ncu_latest.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_sweep", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DESIGN.md 'Peaks'); "
+                               "measured DFMA microbenchmark 34.1 TF/s (profiles/r01_fp64_microbench.jsonl)",
+                "flop_per_launch": flop_launch, "evaluated_pairs": pairs_eval, "ms_per_launch": sweep_ms}
+    gram_flop = (khi - klo) * 3 * 140 * 141  # upper triangle incl. diagonal, multiply+add, 3 metrics
+    gram_ach = gram_flop / (gram_ms * 1e-3) / 1e12
+    roofline_fit = {"bound": "tensor", "kernel": "k_gram (DMMA.8x8x4)", "achieved": gram_ach,
+                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gram_ach / FP64_PEAK_TFLOPS,
+                    "ms_per_call": gram_ms, "peak_source": "FP64 tensor = FP64 FMA rate on B200 "
+                                                           "(measured DMMA 36.9 TF/s)"}
+
+    cpu_baseline = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores, model = cpu_info()
+        v, dt = oracle_step(inp, 0, cores)
+        cpu_baseline = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
+                        "seconds": dt, "sample": f"1/{SAMPLE_DIV} of the step: fit of 3 metrics on "
+                                               f"{K // SAMPLE_DIV} rows + sweep of {nD // SAMPLE_DIV} D x {nF} F"}
+
+    launches_per_step = 8  # fit: minmax x2, xform, gram, gram_reduce, solve; sweep: plan_configs, sweep
+    out = {"metric": METRIC, "value": nD * nF / (step_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded: class-F truths, box-sampled K with 1% noise, log-uniform D)",
+           "config": {"workload": "large+fitheavy", "nD": nD, "nF": nF, "K": K, "n_metrics": 3, "n_c": 140,
+                      "parallelism": f"dp{world}: D and K rows sharded, Gram all_reduce, winners all_gather",
+                      "l2": "flushed between timed steps (256 MiB write); inputs 64 MB"},
+           "fit_rows_per_s": K / (fit_ms * 1e-3), "fit_ms": fit_ms,
+           "sweep_evals_per_s": nD * nF / (sweep_ms * 1e-3), "sweep_kernel_ms": sweep_ms,
+           "plan_ms": sum(t_plan) / len(t_plan),
+           "evaluated_pairs_per_s": (pairs_eval if world == 1 else evaluated_pairs(inp["D"], inp["F"])) / (sweep_ms * 1e-3),
+           "roofline": roofline, "roofline_fit": roofline_fit, "cpu_baseline": cpu_baseline, "e2e": e2e,
+           "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

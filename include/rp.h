@@ -119,9 +119,11 @@ const char *rp_last_error(void);
 int32_t rp_device_count(void);
 
 /* ---- a10: transform -----------------------------------------------------------------------
- * rp_xform_from_box: host-only helper.  c_k = (lo_k + hi_k)/2; e_k = least integer with
- * 2^e_k >= max((hi_k - lo_k)/2, 1).  lo, hi host float64 [n]; out host.  INVALID_ARG if
- * n not in [1, RP_MAX_VARS] or hi < lo.                                                     */
+ * rp_xform_from_box: c_k = (lo_k + hi_k)/2; e_k = least integer with 2^e_k >=
+ * max((hi_k - lo_k)/2, 1), computed by a one-thread kernel on the legacy default stream
+ * (synchronises).  lo, hi host float64 [n]; out host.  INVALID_ARG if n not in
+ * [1, RP_MAX_VARS] or hi < lo.  rp_fit computes the same transform on the device without a
+ * host round trip of the box.                                                               */
 rp_status rp_xform_from_box(int32_t n, const double *lo, const double *hi, rp_xform *out);
 
 /* rp_minmax: per-column min and max of X (device-or-host float64 [K][n], row-major) into host
@@ -135,7 +137,7 @@ rp_status rp_minmax(const double *X, int64_t K, int32_t n, double *lo, double *h
  * in basis order (n_c = n_num + n_den), u_r = (X_r - c) 2^-e.  X device-or-host float64
  * [K][n]; V device-or-host float64 [n_v][K] (n_v >= 1 metrics sharing X).  Rows are split
  * over CTAs and the per-CTA partial Grams are summed in a fixed order (deterministic).
- * K = 0 gives G = 0.  UNSUPPORTED if n_c > 256.                                             */
+ * K = 0 gives G = 0.  UNSUPPORTED if n_c > 176 (shared-memory tile of the DMMA kernel).                                             */
 rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
                              const rp_basis *basis, const rp_xform *xform, double *G,
                              rp_stream s);
@@ -187,8 +189,11 @@ rp_status rp_eval_argmin_batched(const rp_program *progs, int32_t n_prog, const 
  * precomputes the per-configuration table (static mask, B_active, W_active, P-monomials)
  * and the compaction of statically feasible configurations, on the device.  F
  * device-or-host.  The plan is bound to the current device.  rp_plan_eval_argmin is
- * rp_eval_argmin_batched without the setup.  n_static_feasible (nullable) receives the
- * number of configurations of program 0 that survive the static mask.                      */
+ * rp_eval_argmin_batched without the setup.  rp_plan_static_feasible returns the number of
+ * configurations of program `prog` that survive the static mask (synchronises).  Plan memory
+ * comes from the stream-ordered pool; rp_plan_destroy frees it in order on the stream of the
+ * last rp_plan_eval_argmin (or of the creation): if the plan was used on several streams,
+ * synchronise them before destroying it.  rp_plan_create synchronises its stream.            */
 typedef struct rp_plan_s *rp_plan;
 rp_status rp_plan_create(const rp_program *progs, int32_t n_prog, const int32_t *F, int32_t nF,
                          rp_plan *out, rp_stream s);

@@ -285,26 +285,21 @@ using namespace rp;
 struct rp_plan_s {
   int device = 0;
   int n_prog = 0, nF = 0, d = 0, p = 0, npe_pad = 0;
+  bool mwp = true;
+  int nde_max = 1, n_sm_max = 1;
   DevProg *d_progs = nullptr;
   int32_t *buf_i = nullptr;
   double *buf_d = nullptr;
   CfgTable tab{};
   cudaStream_t stream = nullptr;
-  bool async_free = false;
 };
 
 static void plan_free(rp_plan pl) {
   if (!pl) return;
-  if (pl->async_free) {
-    if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
-    if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
-    if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
-  } else {
-    cudaStreamSynchronize(pl->stream);
-    if (pl->d_progs) cudaFree(pl->d_progs);
-    if (pl->buf_i) cudaFree(pl->buf_i);
-    if (pl->buf_d) cudaFree(pl->buf_d);
-  }
+  // stream-ordered frees on the stream the plan was last used on (rp.h: rp_plan_destroy)
+  if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
+  if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
+  if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
   delete pl;
 }
 
@@ -321,8 +316,9 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   for (int g = 0; g < n_prog; ++g) {
     st = compile_program(&progs[g], &hp[g]);
     if (st != RP_OK) return st;
-    RP_REQUIRE(progs[g].d == progs[0].d && progs[g].p == progs[0].p, RP_ERR_INVALID_ARG,
-               "batched programs must share d and p");
+    RP_REQUIRE(progs[g].d == progs[0].d && progs[g].p == progs[0].p &&
+                   progs[g].e_template == progs[0].e_template,
+               RP_ERR_INVALID_ARG, "batched programs must share d, p and the E template");
     npe_max = std::max(npe_max, hp[g].nPE);
   }
   const int npe_pad = npe_pad_for(npe_max);
@@ -334,31 +330,34 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   pl->p = progs[0].p;
   pl->npe_pad = npe_pad;
   pl->stream = s;
-  pl->async_free = async_free;
+  (void)async_free;
   cudaGetDevice(&pl->device);
   auto fail = [&](cudaError_t e, const char *w) {
     rp_status r = cuda_fail(e, w, __FILE__, __LINE__);
     plan_free(pl);
     return r;
   };
+  pl->mwp = progs[0].e_template == RP_TEMPLATE_MWPCWP;
   cudaError_t e;
-  const size_t ni = (size_t)n_prog * nF * 6 + n_prog;  // orig, P[3], B, W, nFc
-  const size_t nd = (size_t)n_prog * npe_pad * nF;
-  if (async_free) {
-    if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
-    if ((e = cudaMallocAsync((void **)&pl->buf_i, ni * 4, s)) != cudaSuccess) return fail(e, "alloc");
-    if ((e = cudaMallocAsync((void **)&pl->buf_d, nd * 8, s)) != cudaSuccess) return fail(e, "alloc");
-  } else {
-    if ((e = cudaMalloc((void **)&pl->d_progs, sizeof(DevProg) * n_prog)) != cudaSuccess) return fail(e, "alloc");
-    if ((e = cudaMalloc((void **)&pl->buf_i, ni * 4)) != cudaSuccess) return fail(e, "alloc");
-    if ((e = cudaMalloc((void **)&pl->buf_d, nd * 8)) != cudaSuccess) return fail(e, "alloc");
+  const int nFp = (nF + 7) & ~7;
+  for (int g = 0; g < n_prog; ++g) {
+    pl->nde_max = std::max(pl->nde_max, hp[g].nDE);
+    pl->n_sm_max = std::max(pl->n_sm_max, hp[g].n_sm);
   }
-  pl->tab.orig = pl->buf_i;
-  pl->tab.P = pl->buf_i + (size_t)n_prog * nF;
-  pl->tab.B = pl->tab.P + (size_t)n_prog * 3 * nF;
-  pl->tab.W = pl->tab.B + (size_t)n_prog * nF;
-  pl->tab.nFc = pl->tab.W + (size_t)n_prog * nF;
+  const size_t nrec = (size_t)n_prog * nFp;                               // CfgRec (64 B)
+  const size_t nd = (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab;  // mP, rSM
+  // stream-ordered pool allocations (a synchronous cudaMalloc/cudaFree per plan costs ms)
+  if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
+  if ((e = cudaMallocAsync((void **)&pl->buf_i, nrec * sizeof(CfgRec) + n_prog * 4 + 16, s)) != cudaSuccess) return fail(e, "alloc");
+  if ((e = cudaMallocAsync((void **)&pl->buf_d, nd * 8, s)) != cudaSuccess) return fail(e, "alloc");
+  // zero padding entries: padded configurations read as m_pe = 0 by the DMMA tiles
+  if ((e = cudaMemsetAsync(pl->buf_i, 0, nrec * sizeof(CfgRec) + n_prog * 4 + 16, s)) != cudaSuccess) return fail(e, "memset");
+  if ((e = cudaMemsetAsync(pl->buf_d, 0, nd * 8, s)) != cudaSuccess) return fail(e, "memset");
+  pl->tab.nFp = nFp;
+  pl->tab.rec = reinterpret_cast<CfgRec *>(pl->buf_i);
+  pl->tab.nFc = reinterpret_cast<int32_t *>(pl->tab.rec + nrec);
   pl->tab.mP = pl->buf_d;
+  pl->tab.rSM = pl->buf_d + (size_t)n_prog * nFp * npe_pad;
   // the DevProg blob is staged through pinned-free pageable memory: copy synchronously w.r.t.
   // the host buffer lifetime (cudaMemcpyAsync from pageable memory returns after staging)
   if ((e = cudaMemcpyAsync(pl->d_progs, hp.data(), sizeof(DevProg) * n_prog, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -395,7 +394,8 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
   if ((st = stage_out(best_idx, no, ti, &di, &hi, s)) != RP_OK) return st;
   if ((st = stage_out(best_E, no, tb, &db, &hb, s)) != RP_OK) return st;
   if ((st = stage_out(second_E, no, ts, &ds, &hs, s)) != RP_OK) return st;
-  RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->tab, pl->nF, pl->npe_pad, pl->d, dD, nD, di, db, ds, s));
+  RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->mwp, pl->tab, pl->npe_pad, pl->nde_max, pl->n_sm_max,
+                       pl->d, dD, nD, di, db, ds, s));
   if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, no * 4, cudaMemcpyDeviceToHost, s));
   if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, no * 8, cudaMemcpyDeviceToHost, s));
   if (hs) RP_CUDA(cudaMemcpyAsync(second_E, ds, no * 8, cudaMemcpyDeviceToHost, s));

@@ -55,15 +55,24 @@ struct DevProg {
 };
 
 // Per-configuration table of a plan (SoA over the statically feasible, compacted configs in
-// ascending original index; program g at offset g * nF).
+// ascending original index; program g at offset g * nFp, nFp = nF rounded up to 8 so that
+// config octets of the DMMA tiles never straddle programs).
+struct CfgRec {      // one statically feasible configuration, 64 B (4 x 16-byte loads)
+  int32_t orig, P0, P1, P2;  // original index in F, block dims (1 for k >= p)
+  float rP0, rP1, rP2, pad;  // 1/P_k in fp32 (estimate for the exact integer ceil)
+  double W, rB;              // W_active, 1/B_active
+  double rW, pad2;           // 1/W_active
+};
+static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
+
 struct CfgTable {
-  int32_t *orig;   // [n_prog][nF]
-  int32_t *P;      // [n_prog][3][nF]
-  int32_t *B;      // [n_prog][nF]  B_active
-  int32_t *W;      // [n_prog][nF]  W_active
-  double *mP;      // [n_prog][npe_pad][nF]  program-part monomials (0 for pe >= nPE)
+  int32_t nFp;     // padded stride (multiple of 8)
+  CfgRec *rec;     // [n_prog][nFp]
+  double *mP;      // [n_prog][npe_pad][nFp]  program-part monomials (0 for pe >= nPE or pad)
+  double *rSM;     // [n_prog][kRSMTab]  1/k for SM_act = k (k <= n_sm)
   int32_t *nFc;    // [n_prog]
 };
+constexpr int kRSMTab = 1024;  // n_sm <= 1023 uses the table
 
 // Host-side marshalling of an rp_program into DevProg (layout only: splitting exponent vectors,
 // sorting terms, copying coefficients; no arithmetic on values).
@@ -72,9 +81,9 @@ rp_status compile_program(const rp_program *prog, DevProg *out);
 // ---- launchers (defined in the kernel TUs) ----------------------------------------------------
 cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_t *d_F, int nF,
                                 int npe_pad, CfgTable tab, cudaStream_t s);
-cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, CfgTable tab, int nF, int npe_pad,
-                         int d, const int32_t *d_D, int64_t nD, int32_t *idx, double *bestE,
-                         double *secondE, cudaStream_t s);
+cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
+                         int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
+                         int32_t *idx, double *bestE, double *secondE, cudaStream_t s);
 cudaError_t launch_eval_metrics(const DevProg *d_prog, int nm, const double *X, int64_t K,
                                 double *out, cudaStream_t s);
 cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int nblk,

@@ -1,19 +1,21 @@
 // rp_sweep.cu -- the runtime sweep of the rational program R over (D, P) with per-D argmin.
 //
 // PAPER.md:2259-2305 (steps 4 and 5): for the runtime data parameters D and "all practically
-// meaningful values of P from the set F, we compute an estimate of E using R", then an
-// exhaustive search picks the optimum.  Here one CTA owns a tile of TD data tuples and sweeps
-// every statically feasible configuration of F for them; one thread owns one configuration at
-// a time (its program-part monomials live in registers) and walks the TD tuples, whose staged
-// data polynomials C_{k,pe}(D) are broadcast from shared memory.  The argmin key is the exact
-// lexicographic (E, original config index), so exact ties go to the lowest index (reading R15).
+// meaningful values of P from the set F, we compute an estimate of E using R", then "an
+// exhaustive search is feasible" picks the optimum.
 //
 // Kernels:
-//   k_plan_configs -- a1 + a5: per configuration T, the static mask (warp rule, T <= T_max,
-//                     B_active > 0), B_active (occupancy flowchart), W_active (Eq. (1)) and the
-//                     program-part monomials; compaction of the feasible ones in index order.
-//   k_sweep        -- a2 (stage C(D)), a3 (P1 P2 <= D1^2), a4 (g_i), a6 (grid), a7 (E),
-//                     a8 (argmin + second best), for a tile of D x all feasible configs.
+//   k_plan_configs -- a1 + a5, once per (program, F): per configuration T, the static mask
+//                     (warp rule, T <= T_max, B_active > 0), B_active (occupancy flowchart),
+//                     W_active (Eq. (1)), the program-part monomials m_pe(u_P) and a few
+//                     reciprocals; compaction of the feasible configurations in index order.
+//   k_sweep        -- a2 (stage the data polynomials C_{k,pe}(D) of a tile of 32 tuples in
+//                     shared memory), a4 (the contraction p_k(D,P) = sum_pe C_{k,pe}(D) m_pe(P)
+//                     on the FP64 tensor pipe: DMMA.8x8x4, A = C of 8 tuples, B = m of 8
+//                     configurations, so each lane ends up with all 2l polynomials of 2 (D,P)
+//                     pairs), a3 (P1 P2 <= D1^2), a6 (grid), a7 (E in common-denominator form,
+//                     4-5 Newton reciprocals instead of ~11 divisions), a8 (argmin on the exact
+//                     key (E, original index) + runner-up, lane -> quad -> warp -> CTA).
 #include <cstdio>
 
 #include "rp_internal.cuh"
@@ -24,11 +26,11 @@ namespace rp {
 __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_t Z,
                                                     const DevProg &pg) {
   const int64_t Bm = pg.b_max, W32 = 32 * (int64_t)pg.w_max, Rm = pg.r_max, Zm = pg.z_max;
-  if (T * Bm <= W32 && R * T * Bm <= Rm && Z * Bm <= Zm) return Bm;             // no limit
-  if (W32 <= T * Bm && W32 * R <= Rm && W32 * Z <= Zm * T) return W32 / T;       // warps
+  if (T * Bm <= W32 && R * T * Bm <= Rm && Z * Bm <= Zm) return Bm;                   // none
+  if (W32 <= T * Bm && W32 * R <= Rm && W32 * Z <= Zm * T) return W32 / T;             // warps
   if (Rm <= R * T * Bm && Rm <= R * W32 && Rm * Z <= R * T * Zm) return Rm / (R * T);  // regs
-  if (Zm <= Bm * Z && Zm * T <= W32 * Z && Zm * R * T <= Z * Rm) return Zm / Z;   // smem
-  return 0;                                                                       // failure
+  if (Zm <= Bm * Z && Zm * T <= W32 * Z && Zm * R * T <= Z * Rm) return Zm / Z;         // smem
+  return 0;                                                                             // fail
 }
 
 // ---- a1 + a5 + P-monomials, compaction in index order --------------------------------------
@@ -36,6 +38,7 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
                                                        int nF, int npe_pad, CfgTable tab) {
   const int g = blockIdx.x;
   const DevProg &pg = progs[g];
+  const int nFp = tab.nFp;
   __shared__ int warp_tot[32];
   __shared__ int base;
   if (threadIdx.x == 0) base = 0;
@@ -48,17 +51,22 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     int64_t T = 1, B = 0, W = 0;
     if (c < nF) {
       for (int k = 0; k < pg.p; ++k) Pk[k] = F[(int64_t)c * pg.p + k];
-      for (int k = 0; k < pg.p; ++k) T *= Pk[k];
-      ok = (T % 32 == 0) && (T <= pg.t_max) && (T > 0);
+      bool pos = true;
+      for (int k = 0; k < pg.p; ++k) {
+        T *= Pk[k];
+        pos = pos && Pk[k] >= 1;
+      }
+      // "a multiple of the warp size (32)" and "bounded over by the maximum number of threads
+      // per block"
+      ok = pos && (T % 32 == 0) && (T <= pg.t_max);
       if (ok) {
         const int64_t Z = pg.Z0 + pg.Z1 * T;
         B = occupancy_blocks(T, pg.R, Z, pg);
-        ok = B > 0;
+        ok = B > 0;        // B_active = 0: "Failure to Launch"
         W = (B * T) / 32;  // Eq. (1)
         if (W > pg.w_max) W = pg.w_max;
       }
     }
-    // block-wide exclusive scan of ok (index order preserved)
     const unsigned ball = __ballot_sync(0xffffffffu, ok);
     const int pre = __popc(ball & ((1u << lane) - 1u));
     if (lane == 0) warp_tot[wid] = __popc(ball);
@@ -75,11 +83,21 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     __syncthreads();
     const int pos = base + warp_tot[wid] + pre;
     if (ok) {
-      const int64_t off = (int64_t)g * nF;
-      tab.orig[off + pos] = c;
-      for (int k = 0; k < 3; ++k) tab.P[(int64_t)g * 3 * nF + (int64_t)k * nF + pos] = Pk[k];
-      tab.B[off + pos] = (int32_t)B;
-      tab.W[off + pos] = (int32_t)W;
+      const int64_t off = (int64_t)g * nFp;
+      CfgRec r;
+      r.orig = c;
+      r.P0 = Pk[0];
+      r.P1 = Pk[1];
+      r.P2 = Pk[2];
+      r.rP0 = 1.0f / (float)Pk[0];
+      r.rP1 = 1.0f / (float)Pk[1];
+      r.rP2 = 1.0f / (float)Pk[2];
+      r.pad = 0.0f;
+      r.W = (double)W;
+      r.rB = 1.0 / (double)B;
+      r.rW = 1.0 / (double)W;
+      r.pad2 = 0.0;
+      tab.rec[off + pos] = r;
       double u[3];
       for (int k = 0; k < pg.p; ++k)
         u[k] = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
@@ -90,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
           for (int k = 0; k < pg.p; ++k)
             for (int t = 0; t < pg.pe_exp[pe][k]; ++t) m *= u[k];
         }
-        tab.mP[(int64_t)g * npe_pad * nF + (int64_t)pe * nF + pos] = m;
+        tab.mP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + pos] = m;
       }
     }
     __syncthreads();
@@ -98,6 +116,9 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     __syncthreads();
   }
   if (threadIdx.x == 0) tab.nFc[g] = base;
+  // 1/k for SM_act = k (line 15 of Appendix A); correctly rounded, computed once per plan
+  for (int k = threadIdx.x; k < kRSMTab; k += blockDim.x)
+    tab.rSM[(int64_t)g * kRSMTab + k] = k > 0 ? 1.0 / (double)k : 0.0;
 }
 
 cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_t *d_F, int nF,
@@ -108,9 +129,9 @@ cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_
 
 // ---- argmin state: exact lexicographic (E, index) with the runner-up E ----------------------
 struct Best {
-  double e;    // best E (+inf: none)
-  int32_t i;   // its original config index (INT_MAX: none)
-  double s;    // second-smallest E among the others
+  double e;   // best E (+inf: none)
+  int32_t i;  // its original config index (INT_MAX: none)
+  double s;   // second-smallest E among the others
 };
 __device__ __forceinline__ bool key_less(double e1, int32_t i1, double e2, int32_t i2) {
   return e1 < e2 || (e1 == e2 && i1 < i2);
@@ -118,9 +139,13 @@ __device__ __forceinline__ bool key_less(double e1, int32_t i1, double e2, int32
 __device__ __forceinline__ Best merge(const Best &a, const Best &b) {
   Best r;
   if (key_less(a.e, a.i, b.e, b.i)) {
-    r.e = a.e; r.i = a.i; r.s = fmin(a.s, b.e);
+    r.e = a.e;
+    r.i = a.i;
+    r.s = fmin(a.s, b.e);
   } else {
-    r.e = b.e; r.i = b.i; r.s = fmin(b.s, a.e);
+    r.e = b.e;
+    r.i = b.i;
+    r.s = fmin(b.s, a.e);
   }
   return r;
 }
@@ -132,45 +157,42 @@ __device__ __forceinline__ Best shfl_xor(const Best &a, int m) {
   return r;
 }
 
-// ---- a7: the MWP-CWP estimate (DESIGN.md Appendix A = Hong & Kim ISCA'09 Eqs. 1-18) --------
-__device__ __forceinline__ double mwpcwp_E(double g1, double g2, double g3, double Wact,
-                                           double Bact, double SMact, double blocks,
-                                           const DevProg &pg) {
-  const double Mem = g2 + g3;
-  const double Tot = g1 + g2 + g3;
-  const double W_unc = g3 / Mem;
-  const double W_coal = g2 / Mem;
-  const double L_unc = pg.mem_ld + (pg.U - 1.0) * pg.dd_unc;
-  const double L_coal = pg.mem_ld;
-  const double Mem_L = L_unc * W_unc + L_coal * W_coal;
-  const double Dep = pg.dd_unc * pg.U * W_unc + pg.dd_coal * W_coal;
-  const double MWP_nb = Mem_L / Dep;
-  const double BWpw = pg.freq * pg.lbpw / Mem_L;
-  const double MWP_bw = pg.mem_bw / (BWpw * SMact);
-  double MWP = MWP_nb;
-  if (MWP_bw < MWP) MWP = MWP_bw;
-  if (Wact < MWP) MWP = Wact;
-  const double Comp_c = pg.issue * Tot;
-  const double Mem_c = L_unc * g3 + L_coal * g2;
-  const double CWP_full = (Mem_c + Comp_c) / Comp_c;
-  const double CWP = CWP_full < Wact ? CWP_full : Wact;
-  const double Rep = blocks / (Bact * SMact);
-  double E;
-  if (MWP == Wact && CWP == Wact)
-    E = (Mem_c + Comp_c + Comp_c / Mem * (MWP - 1.0)) * Rep;
-  else if (CWP >= MWP || Comp_c > Mem_c)
-    E = (Mem_c * Wact / MWP + Comp_c / Mem * (MWP - 1.0)) * Rep;
-  else
-    E = (Mem_L + Comp_c * Wact) * Rep;
-  return E;
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 1/x: MUFU.RCP64H seed + two Newton steps (relative error ~1 ulp; 0 and +-inf give NaN,
+// which the final finiteness test masks, as the literal program's x/0 would).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// exact ceil(D / P) for D, P >= 1: fp32 estimate (|error| < 1 for D < 2^24) + integer correction
+__device__ __forceinline__ int64_t ceil_div(int32_t D, int32_t P, float rP) {
+  if (D < (1 << 24)) {
+    int q = __float2int_rz(__int2float_rn(D) * rP);
+    int r = D - q * P;
+    q = r < 0 ? q - 1 : (r >= P ? q + 1 : q);
+    r = D - q * P;
+    return (int64_t)q + (r > 0);
+  }
+  return ((int64_t)D + P - 1) / P;
 }
 
 // ---- the sweep ------------------------------------------------------------------------------
 struct SweepArgs {
   const DevProg *progs;
   CfgTable tab;
-  int nF;
+  int npe_pad;
   int d;
+  int nde_max;  // max nDE over the programs (shared-memory layout)
   const int32_t *D;
   int64_t nD;
   int32_t *idx;
@@ -178,190 +200,246 @@ struct SweepArgs {
   double *secondE;
 };
 
-constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = 4;
+constexpr int kSweepThreads = 32 * kSweepWarps;
+constexpr int kTD = 8 * kSweepWarps;  // tuples per CTA: one octet (the DMMA M side) per warp
 
-template <int NPE, int TD>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
+template <int NPOLY, int NPE>
+__host__ __device__ constexpr int c_stride() {  // per-tuple stride of sC in doubles, = 4 mod 16
+  int s = NPOLY * NPE;
+  while (s % 16 != 4) ++s;
+  return s;
+}
+
+template <int NPOLY, int NPE>
+size_t sweep_smem_bytes(int nde_max, int n_sm) {
+  const int rsm = (n_sm + 2) & ~1;
+  return sizeof(double) * ((size_t)kTD * c_stride<NPOLY, NPE>() + (size_t)kTD * nde_max + rsm) +
+         sizeof(int32_t) * kTD * kMaxVars;
+}
+
+// E for one (D, P) pair from its 2l polynomial values (Appendix A in
+// common-denominator form g_i = a_i / Q; every division is a Newton reciprocal).  Straight-line
+// code: masked pairs are carried to the end and returned as +inf.
+struct EConst {
+  double Lunc, Lcoal, DdU, ddc, issue, Kbw;
+};
+__device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, double q2, double p3,
+                                           double q3, double W, double rW, double Rep,
+                                           double rSM, const EConst &k) {
+  const double q23 = q2 * q3, q13 = q1 * q3, q12 = q1 * q2;
+  const double Q = q1 * q23;
+  const double a1 = p1 * q23, a2 = p2 * q13, a3 = p3 * q12;  // g_i = a_i / Q
+  const double s23 = a2 + a3;                                 // Mem Q          (line 5)
+  const double s = a1 + s23;                                  // Tot Q          (line 5)
+  const double mc = fma(k.Lunc, a3, k.Lcoal * a2);            // Mem_c Q        (line 13)
+  const double dn = fma(k.DdU, a3, k.ddc * a2);               // Dep Mem Q      (lines 6, 9)
+  const double cc = k.issue * s;                              // Comp_c Q       (line 13)
+  const double rQ = frcp(Q), r23 = frcp(s23);
+  const double Mem_c = mc * rQ, Comp_c = cc * rQ;
+  const double MWP_nb = mc * frcp(dn);         // line 10: Mem_L / Dep
+  const double MWP_bw = k.Kbw * mc * r23 * rSM;  // line 11: Mem_BW / (BW_per_warp SM_act)
+  const double CWPf = 1.0 + mc * frcp(cc);     // line 14: (Mem_c + Comp_c) / Comp_c
+  double mwp = MWP_nb;                         // line 12
+  mwp = MWP_bw < mwp ? MWP_bw : mwp;
+  mwp = W < mwp ? W : mwp;
+  const double cwp = CWPf < W ? CWPf : W;  // line 14
+  const double cpm = cc * r23;             // Comp_c / Mem
+  const double tail = cpm * (mwp - 1.0);
+  const double rm = (mwp == W) ? rW : frcp(mwp);
+  const double E1 = Mem_c + Comp_c + tail;         // line 16
+  const double E2 = Mem_c * W * rm + tail;         // line 17
+  const double E3 = mc * r23 + Comp_c * W;         // line 18 (Mem_L = Mem_c / Mem)
+  const bool c1 = (mwp == W) && (cwp == W);
+  const bool c2 = (cwp >= mwp) || (Comp_c > Mem_c);
+  return (c1 ? E1 : (c2 ? E2 : E3)) * Rep;
+}
+
+template <int NPE, bool MWP, bool SECOND>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+  constexpr int NPOLY = MWP ? 6 : 2;
+  constexpr int KS = NPE / 4;
+  constexpr int CS = c_stride<NPOLY, NPE>();
+  constexpr double kInf = __builtin_huge_val();
   const int g = blockIdx.y;
   const DevProg &pg = a.progs[g];
   const int d = a.d;
-  const int nPE = pg.nPE, nDE = pg.nDE, npoly = pg.npoly, nm = pg.nm;
-  const int64_t d0 = (int64_t)blockIdx.x * TD;
+  const int64_t d0 = (int64_t)blockIdx.x * kTD;
+  const int tmax = (int)((a.nD - d0) < kTD ? (a.nD - d0) : kTD);
+  const int nde = a.nde_max;
+  const int n_sm = pg.n_sm;
 
-  // dynamic shared memory (sweep_smem_bytes<NPE, TD>())
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto sC = reinterpret_cast<double(*)[kMaxPolys][NPE]>(smem_raw);
-  auto sMD = reinterpret_cast<double(*)[kMaxDE]>(smem_raw + sizeof(double) * TD * kMaxPolys * NPE);
-  auto sBe = reinterpret_cast<double(*)[kSweepThreads]>(&sMD[TD][0]);
-  auto sBs = reinterpret_cast<double(*)[kSweepThreads]>(&sBe[TD][0]);
-  auto sRed = reinterpret_cast<Best(*)[kSweepThreads / 32]>(&sBs[TD][0]);
-  auto sBi = reinterpret_cast<int32_t(*)[kSweepThreads]>(&sRed[TD][0]);
-  auto sD = reinterpret_cast<int32_t(*)[kMaxVars]>(&sBi[TD][0]);
+  extern __shared__ __align__(16) double smem[];
+  double *sC = smem;                   // [kTD][CS]
+  double *sMD = sC + kTD * CS;         // [kTD][nde]
+  double *sRSM = sMD + kTD * nde;      // [n_sm + 1]
+  int32_t *sDv = reinterpret_cast<int32_t *>(sRSM + ((n_sm + 2) & ~1));  // [kTD][kMaxVars]
 
-  // a2: load the D tile (tuples past nD are replaced by D = 1, and their results dropped)
-  for (int i = threadIdx.x; i < TD * d; i += blockDim.x) {
+  // ---- a2: stage the tile (D values, data monomials, data polynomials) --------------------------
+  const int nDE = pg.nDE, nPE = pg.nPE, npoly = pg.npoly;
+  for (int i = threadIdx.x; i < kTD * d; i += blockDim.x) {
     const int t = i / d, k = i % d;
-    sD[t][k] = (d0 + t < a.nD) ? a.D[(d0 + t) * d + k] : 1;
+    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[(d0 + t) * d + k] : 1;
   }
+  const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
+  const bool rsm_tab = n_sm < kRSMTab;
+  if (rsm_tab)
+    for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) sRSM[i] = gRSM[i];
   __syncthreads();
-  // a2: data-part monomials m_de(u_D), u = (D - c) 2^-e
-  for (int i = threadIdx.x; i < TD * nDE; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kTD * nDE; i += blockDim.x) {
     const int t = i / nDE, de = i % nDE;
     double m = 1.0;
     for (int k = 0; k < d; ++k) {
-      const double u = ((double)sD[t][k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+      const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
       for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
     }
-    sMD[t][de] = m;
+    sMD[t * nde + de] = m;
   }
   __syncthreads();
-  // a2: staged data polynomials C_{k,pe}(D) (zero padding for k >= npoly or pe >= nPE)
-  for (int i = threadIdx.x; i < TD * kMaxPolys * NPE; i += blockDim.x) {
-    const int t = i / (kMaxPolys * NPE), r = i % (kMaxPolys * NPE);
+  for (int i = threadIdx.x; i < kTD * NPOLY * NPE; i += blockDim.x) {
+    const int t = i / (NPOLY * NPE), r = i % (NPOLY * NPE);
     const int k = r / NPE, pe = r % NPE;
     double acc = 0.0;
     if (k < npoly && pe < nPE) {
       const int row = k * nPE + pe;
       for (int j = pg.row_start[row]; j < pg.row_start[row + 1]; ++j)
-        acc = fma(pg.term_coef[j], sMD[t][pg.term_de[j]], acc);
+        acc = fma(pg.term_coef[j], sMD[t * nde + pg.term_de[j]], acc);
     }
-    sC[t][k][pe] = acc;
+    sC[t * CS + k * NPE + pe] = acc;
   }
   __syncthreads();
 
-  // running argmin state of (tuple t, thread): shared memory, updated in place
-  for (int t = 0; t < TD; ++t) {
-    sBe[t][threadIdx.x] = __longlong_as_double(0x7ff0000000000000ll);
-    sBs[t][threadIdx.x] = __longlong_as_double(0x7ff0000000000000ll);
-    sBi[t][threadIdx.x] = 0x7fffffff;
-  }
-  const int nFc = a.tab.nFc[g];
-  const int64_t off = (int64_t)g * a.nF;
-  const int dmap0 = pg.grid_map[0], dmap1 = pg.grid_map[1], dmap2 = pg.grid_map[2];
-  const int p = pg.p;
-  const double n_sm = (double)pg.n_sm;
-  const int tmax = (int)((a.nD - d0) < TD ? (a.nD - d0) : TD);
+  // ---- per-program constants of Appendix A, folded once ----------------------------------------
+  EConst kc;
+  kc.Lunc = pg.mem_ld + (pg.U - 1.0) * pg.dd_unc;  // line 7
+  kc.Lcoal = pg.mem_ld;
+  kc.DdU = pg.dd_unc * pg.U;  // line 9
+  kc.ddc = pg.dd_coal;
+  kc.issue = pg.issue;                         // line 13
+  kc.Kbw = pg.mem_bw / (pg.freq * pg.lbpw);    // line 11: Mem_BW / (Freq LoadBytesPerWarp)
+  const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
+            map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
+  const bool two = pg.p >= 2;
+  const double rNSM = 1.0 / (double)n_sm;
 
-  for (int c = threadIdx.x; c < nFc; c += blockDim.x) {
-    const int32_t orig = a.tab.orig[off + c];
-    const int32_t P0 = a.tab.P[off * 3 + c];
-    const int32_t P1 = a.tab.P[off * 3 + a.nF + c];
-    const int32_t P2 = a.tab.P[off * 3 + 2 * a.nF + c];
-    const double Bact = (double)a.tab.B[off + c];
-    const double Wact = (double)a.tab.W[off + c];
-    double mP[NPE];
-#pragma unroll
-    for (int pe = 0; pe < NPE; ++pe) mP[pe] = a.tab.mP[off * NPE + (int64_t)pe * a.nF + c];
-    const int64_t P01 = (int64_t)P0 * (p >= 2 ? P1 : 1);
-
-#pragma unroll 1
-    for (int t = 0; t < tmax; ++t) {
-      // a3: "P1 P2 <= D1^2 is meaningful"
-      const int64_t D1 = sD[t][0];
-      if (P01 > D1 * D1) continue;
-      // a6: grid gx = ceil(D/bx), ...; SM_act = min(#blocks, n_SM)
-      int64_t blocks = 1;
-      if (dmap0 >= 0) blocks *= (sD[t][dmap0] + P0 - 1) / P0;
-      if (p >= 2 && dmap1 >= 0) blocks *= (sD[t][dmap1] + P1 - 1) / P1;
-      if (p >= 3 && dmap2 >= 0) blocks *= (sD[t][dmap2] + P2 - 1) / P2;
-      const double dblocks = (double)blocks;
-      const double SMact = fmin(dblocks, n_sm);
-      // a4: g_i = p_i / q_i with p_k = sum_pe C_{k,pe}(D) m_pe(P)
-      double gv[kMaxMetrics];
-#pragma unroll
-      for (int i = 0; i < kMaxMetrics; ++i) {
-        double pn = 0.0, qd = 0.0;
-        if (i < nm) {
-#pragma unroll
-          for (int pe = 0; pe < NPE; ++pe) {
-            pn = fma(sC[t][2 * i][pe], mP[pe], pn);
-            qd = fma(sC[t][2 * i + 1][pe], mP[pe], qd);
-          }
-        }
-        gv[i] = pn / qd;
-      }
-      // a7
-      double E;
-      if (pg.tmpl == RP_TEMPLATE_G1)
-        E = gv[0];
-      else
-        E = mwpcwp_E(gv[0], gv[1], gv[2], Wact, Bact, SMact, dblocks, pg);
-      if (!(E > 0.0 && E < __longlong_as_double(0x7ff0000000000000ll))) continue;  // R17
-      // a8: running argmin (exact key (E, original index); configs arrive in index order)
-      const double be = sBe[t][threadIdx.x];
-      if (E < be) {
-        sBs[t][threadIdx.x] = be;
-        sBe[t][threadIdx.x] = E;
-        sBi[t][threadIdx.x] = orig;
-      } else if (E < sBs[t][threadIdx.x]) {
-        sBs[t][threadIdx.x] = E;
-      }
-    }
-  }
-
-  // a8: warp then block reduction of the TD states
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int t = 0; t < TD; ++t) {
-    Best b;
-    b.e = sBe[t][threadIdx.x];
-    b.i = sBi[t][threadIdx.x];
-    b.s = sBs[t][threadIdx.x];
+  const int nFc = a.tab.nFc[g];
+  const int nFp = a.tab.nFp;
+  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
+  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
+
+  // this warp's octet of tuples: row lane/4 of the DMMA tiles
+  const int t = wid * 8 + (lane >> 2);
+  const bool tok = t < tmax;
+  const int32_t *Dt = sDv + t * kMaxVars;
+  const int64_t D1 = Dt[0];
+  const int64_t D1sq = D1 * D1;
+  const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1,
+                Dc = map2 >= 0 ? Dt[map2] : 1;
+  const double *arow = sC + t * CS + (lane & 3);
+
+  Best st;
+  st.e = kInf;
+  st.i = 0x7fffffff;
+  st.s = kInf;
+
+  const int nOctF = (nFc + 7) >> 3;
+  if (wid * 8 < tmax) {
+    for (int oc = 0; oc < nOctF; ++oc) {
+      // B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
+      double bfr[KS];
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) b = merge(b, shfl_xor(b, m));
-    if (lane == 0) sRed[t][wid] = b;
-  }
-  __syncthreads();
-  if (threadIdx.x < TD) {
-    const int t = threadIdx.x;
-    const int64_t di = d0 + t;
-    if (di < a.nD) {
-      Best b = sRed[t][0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = merge(b, sRed[t][w]);
-      const int64_t o = (int64_t)g * a.nD + di;
-      const bool none = !(b.e < __longlong_as_double(0x7ff0000000000000ll));
-      a.idx[o] = none ? -1 : b.i;
-      a.bestE[o] = b.e;
-      if (a.secondE) a.secondE[o] = b.s;
+      for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
+      // a4: p_k(D_t, P_c) for the octet of tuples x the octet of configurations
+      double acc[NPOLY][2];
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) {
+        acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) dmma(acc[k][0], acc[k][1], arow[k * NPE + ks * 4], bfr[ks]);
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int c = oc * 8 + 2 * (lane & 3) + v;  // output column 2 (lane % 4) + v
+        const CfgRec *cr = rec + (c < nFc ? c : 0);
+        const int4 ip = __ldg(reinterpret_cast<const int4 *>(cr));
+        const float4 fp = __ldg(reinterpret_cast<const float4 *>(cr) + 1);
+        // a3: "P1 P2 <= D1^2 is meaningful"
+        const int64_t P01 = (int64_t)ip.y * (two ? ip.z : 1);
+        const bool ok = tok && c < nFc && P01 <= D1sq;
+        double E;
+        if (MWP) {
+          const double2 wb = __ldg(reinterpret_cast<const double2 *>(cr) + 2);  // (W, 1/B) at byte 32
+          const double rW = __ldg(reinterpret_cast<const double *>(cr) + 6);
+          // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
+          int64_t blocks = 1;
+          if (map0 >= 0) blocks *= ceil_div(Da, ip.y, fp.x);
+          if (map1 >= 0) blocks *= ceil_div(Db, ip.z, fp.y);
+          if (map2 >= 0) blocks *= ceil_div(Dc, ip.w, fp.z);
+          const int64_t smact = blocks < n_sm ? blocks : n_sm;
+          const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
+          const double Rep = (double)blocks * wb.y * rSM;  // line 15: #Blocks / (B_act SM_act)
+          E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], wb.x, rW,
+                       Rep, rSM, kc);
+        } else {
+          E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
+        }
+        // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
+        E = (ok && E > 0.0 && E < kInf) ? E : kInf;
+        // a8: configurations arrive in ascending original index: strict < keeps the lowest
+        const bool better = E < st.e;
+        if (SECOND) st.s = better ? st.e : fmin(st.s, E);
+        st.i = better ? ip.x : st.i;
+        st.e = better ? E : st.e;
+      }
     }
   }
-}
-
-template <int NPE, int TD>
-constexpr size_t sweep_smem_bytes() {
-  return sizeof(double) * TD * kMaxPolys * NPE + sizeof(double) * TD * kMaxDE +
-         2 * sizeof(double) * TD * kSweepThreads + sizeof(Best) * TD * (kSweepThreads / 32) +
-         sizeof(int32_t) * TD * kSweepThreads + sizeof(int32_t) * TD * kMaxVars;
-}
-
-template <int NPE>
-static cudaError_t launch_npe(const SweepArgs &a, int n_prog, cudaStream_t s) {
-  constexpr int TD = 8;
-  constexpr size_t smem = sweep_smem_bytes<NPE, TD>();
-  const int64_t tiles = (a.nD + TD - 1) / TD;
-  if (tiles > 0x7fffffffll) return cudaErrorInvalidValue;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sweep<NPE, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
+  st = merge(st, shfl_xor(st, 1));
+  st = merge(st, shfl_xor(st, 2));
+  if ((lane & 3) == 0 && tok) {
+    const int64_t o = (int64_t)g * a.nD + d0 + t;
+    a.idx[o] = (st.e < kInf) ? st.i : -1;
+    a.bestE[o] = st.e;
+    if (SECOND) a.secondE[o] = st.s;
   }
-  dim3 grid((unsigned)tiles, (unsigned)n_prog);
-  k_sweep<NPE, TD><<<grid, kSweepThreads, smem, s>>>(a);
+}
+
+template <int NPE, bool MWP, bool SECOND>
+static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
+  const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_max, n_sm_max);
+  const int64_t tiles = (a.nD + kTD - 1) / kTD;
+  if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_sweep<NPE, MWP, SECOND>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_sweep<NPE, MWP, SECOND><<<dim3((unsigned)tiles, (unsigned)n_prog), kSweepThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, CfgTable tab, int nF, int npe_pad,
-                         int d, const int32_t *d_D, int64_t nD, int32_t *idx, double *bestE,
-                         double *secondE, cudaStream_t s) {
+template <int NPE>
+static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm_max, cudaStream_t s) {
+  const bool second = a.secondE != nullptr;
+  if (mwp)
+    return second ? launch3<NPE, true, true>(a, n_prog, n_sm_max, s)
+                  : launch3<NPE, true, false>(a, n_prog, n_sm_max, s);
+  return second ? launch3<NPE, false, true>(a, n_prog, n_sm_max, s)
+                : launch3<NPE, false, false>(a, n_prog, n_sm_max, s);
+}
+
+cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
+                         int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
+                         int32_t *idx, double *bestE, double *secondE, cudaStream_t s) {
   if (nD == 0) return cudaSuccess;
-  SweepArgs a{d_progs, tab, nF, d, d_D, nD, idx, bestE, secondE};
+  if (n_sm_max >= kRSMTab) n_sm_max = 0;  // no table: 1/SM_act computed directly
+  SweepArgs a{d_progs, tab, npe_pad, d, nde_max < 1 ? 1 : nde_max, d_D, nD, idx, bestE, secondE};
   switch (npe_pad) {
-    case 4: return launch_npe<4>(a, n_prog, s);
-    case 8: return launch_npe<8>(a, n_prog, s);
-    case 16: return launch_npe<16>(a, n_prog, s);
-    case 20: return launch_npe<20>(a, n_prog, s);
-    case 24: return launch_npe<24>(a, n_prog, s);
-    case 36: return launch_npe<36>(a, n_prog, s);
+    case 4: return launch_npe<4>(a, n_prog, mwp, n_sm_max, s);
+    case 8: return launch_npe<8>(a, n_prog, mwp, n_sm_max, s);
+    case 16: return launch_npe<16>(a, n_prog, mwp, n_sm_max, s);
+    case 20: return launch_npe<20>(a, n_prog, mwp, n_sm_max, s);
+    case 24: return launch_npe<24>(a, n_prog, mwp, n_sm_max, s);
+    case 36: return launch_npe<36>(a, n_prog, mwp, n_sm_max, s);
     default: return cudaErrorInvalidValue;
   }
 }
