@@ -267,6 +267,15 @@ static rp_status build_gram_basis(const rp_basis *basis, const rp_xform *xf, Gra
       maxdeg = std::max(maxdeg, e);
     }
   gb->maxdeg = maxdeg;
+  // the fused weighted-Gram path needs identical numerator / denominator exponent lists
+  bool same = basis->n_num == basis->n_den && maxdeg <= 15;
+  for (int j = 0; same && j < basis->n_num * n; ++j) same = basis->num_exp[j] == basis->den_exp[j];
+  gb->fused = same ? 1 : 0;
+  for (int j = 0; j < basis->n_num; ++j) {
+    uint32_t w = 0;
+    for (int k = 0; k < n; ++k) w |= (uint32_t)(basis->num_exp[j * n + k] & 15) << (4 * k);
+    gb->pexp[j] = w;
+  }
   if (xf)
     for (int k = 0; k < n; ++k) {
       gb->xc[k] = xf->c[k];

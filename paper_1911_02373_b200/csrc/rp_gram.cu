@@ -401,6 +401,287 @@ __global__ void k_gram_reduce(const double *part, int nblk, int groups, int nb, 
   }
 }
 
+// ============================================================================================
+// Fused weighted Gram (numerator basis == denominator basis; every BASELINE config)
+//
+// With N = M the linearised rows a = [M | -V_i M] of the n_v metrics sharing X give
+//   G_i = [[ M^T M , -M^T diag(V_i) M ], [ . , M^T diag(V_i^2) M ]],
+// so 1 + 2 n_v symmetric m x m blocks replace n_v full (2m)^2 Grams.  With X_0 = M and
+// X_{1+i} = V_i M (staged in shared memory), the blocks are X_0^T X_0, X_0^T X_{1+i} and
+// X_{1+i}^T X_{1+i}; their upper-triangular 8x8 tiles are accumulated with DMMA.8x8x4.  Tiles
+// are ordered by A-row group so the slots of one warp mostly share their A fragment.
+// ============================================================================================
+constexpr int kFW = 16;          // warps per CTA
+constexpr int kFRT = 64;         // design rows per shared-memory tile (16 k-steps)
+constexpr int kFlushTiles = 16;  // add register accumulators into the partial every 1024 rows
+
+__host__ __device__ constexpr int fstride(int m8) {  // = 4 mod 16 (conflict-free fragments)
+  int s = m8;
+  while (s % 16 != 4) ++s;
+  return s;
+}
+
+template <int NB, int NV>
+struct FL {
+  static constexpr int M8 = 8 * NB;
+  static constexpr int T = NB * (NB + 1) / 2;  // upper tiles of one m x m block
+  static constexpr int NP = 1 + 2 * NV;        // blocks: (0,0), (0,1+i), (1+i,1+i)
+  static constexpr int NT = NP * T;
+  static constexpr int SLOTS = (NT + kFW - 1) / kFW;
+  static constexpr int NX = 1 + NV;
+  static constexpr int S = fstride(M8);
+};
+
+// packed compile-time operand offsets (doubles) of a slot: A | B << 16, or kNoTile
+constexpr uint32_t kNoTile = 0xffffffffu;
+
+// tile id (A-row-group order) -> X arrays (pa, pb), block pair index and 8-blocks (bi <= bj)
+template <int NB, int NV>
+__host__ __device__ constexpr void fused_tile(int id, int &pa, int &pb, int &pair, int &bi, int &bj) {
+  for (int a = 0; a <= NV; ++a)
+    for (int i = 0; i < NB; ++i) {
+      const int cnt = (a == 0 ? NV + 1 : 1) * (NB - i);
+      if (id < cnt) {
+        pa = a;
+        bi = i;
+        if (a == 0) {
+          pb = id / (NB - i);
+          bj = i + id % (NB - i);
+          pair = pb;  // (0,0) -> 0, (0,1+v) -> 1+v
+        } else {
+          pb = a;
+          bj = i + id;
+          pair = 1 + NV + (a - 1);
+        }
+        return;
+      }
+      id -= cnt;
+    }
+  pa = pb = pair = bi = bj = -1;
+}
+
+__host__ __device__ constexpr int upper_index(int NB, int bi, int bj) {
+  return bi * NB - bi * (bi - 1) / 2 + (bj - bi);
+}
+
+template <int NB, int NV>
+__host__ __device__ constexpr uint32_t fused_slot_off(int wid, int j, int S, int RT) {
+  const int NT = (1 + 2 * NV) * NB * (NB + 1) / 2;
+  const int id = wid * ((NT + 15) / 16) + j;
+  if (id >= NT) return kNoTile;
+  int pa = 0, pb = 0, pair = 0, bi = 0, bj = 0;
+  fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
+  return (uint32_t)(pa * RT * S + 8 * bi) | ((uint32_t)(pb * RT * S + 8 * bj) << 16);
+}
+
+// The MMA phase of one warp over the k-steps of a row tile: every operand offset is a
+// compile-time constant (template on the warp id), so fragment loads are immediate-offset LDS
+// and slots sharing an A fragment reuse the loaded value.
+template <int NB, int NV, int WID, int SLOTS, int S, int RT>
+__device__ __forceinline__ void fused_mma_warp(const double *sX, int lane, double (&acc)[SLOTS][2]) {
+#pragma unroll 2
+  for (int ks = 0; ks < RT / 4; ++ks) {
+    const double *row = sX + (ks * 4 + (lane & 3)) * S + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const uint32_t off = fused_slot_off<NB, NV>(WID, j, S, RT);
+      if (off != kNoTile) dmma_8x8x4(acc[j][0], acc[j][1], row[off & 0xffffu], row[off >> 16]);
+    }
+  }
+}
+
+struct FusedArgs {
+  const GramBasis *basis;
+  const double *X;
+  const double *V;  // [NV][K]
+  int64_t K;
+  double *part;     // [gridDim.x][NT][64]  canonical (pair, upper tile) order
+};
+
+template <int NB, int NV>
+__global__ void __launch_bounds__(kFW * 32, 1) k_gram_fused(FusedArgs a) {
+  using L = FL<NB, NV>;
+  extern __shared__ __align__(16) double fsm[];
+  const GramBasis &B = *a.basis;
+  const int n = B.n, m = B.n_num, pw = B.maxdeg + 1;
+  double *sX = fsm;                          // [NX][kFRT][S]
+  double *sU = sX + L::NX * kFRT * L::S;     // [kFRT][n]
+  double *sPow = sU + kFRT * kMaxVars;       // [kFRT][n][pw]
+  double *sV = sPow + kFRT * n * pw;         // [NV][kFRT]
+  uint32_t *sExp = reinterpret_cast<uint32_t *>(sV + NV * kFRT);  // [M8]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+  const int64_t r_begin = a.K * blockIdx.x / gridDim.x;
+  const int64_t r_end = a.K * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ntr = (r_end - r_begin + kFRT - 1) / kFRT;
+
+  for (int i = threadIdx.x; i < L::NX * kFRT * L::S; i += blockDim.x) sX[i] = 0.0;  // pads
+  for (int j = threadIdx.x; j < m; j += blockDim.x) sExp[j] = B.pexp[j];
+
+  double acc[L::SLOTS][2];
+#pragma unroll
+  for (int j = 0; j < L::SLOTS; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double *part = a.part + (int64_t)blockIdx.x * L::NT * 64;
+  bool first = true;
+  __syncthreads();
+
+  for (int64_t tr = 0; tr < ntr; ++tr) {
+    const int64_t r0 = r_begin + tr * kFRT;
+    const int rows = (int)((r_end - r0) < kFRT ? (r_end - r0) : kFRT);
+    // a10: u = (x - c) 2^-e; the metric values of the tile
+    for (int i = threadIdx.x; i < kFRT * n; i += blockDim.x) {
+      const int r = i / n, k = i % n;
+      sU[r * kMaxVars + k] = r < rows ? (a.X[(r0 + r) * n + k] - B.xc[k]) * ldexp(1.0, -B.xe[k]) : 0.0;
+    }
+    for (int i = threadIdx.x; i < NV * kFRT; i += blockDim.x) {
+      const int v = i / kFRT, r = i % kFRT;
+      sV[i] = r < rows ? a.V[(int64_t)v * a.K + r0 + r] : 0.0;
+    }
+    __syncthreads();
+    // powers u^e, e <= maxdeg, by repeated multiplication
+    for (int i = threadIdx.x; i < kFRT * n; i += blockDim.x) {
+      const int r = i / n, k = i % n;
+      const double u = sU[r * kMaxVars + k];
+      double p = r < rows ? 1.0 : 0.0;  // rows past the slab: all-zero design row
+      double *dst = sPow + (r * n + k) * pw;
+      for (int e = 0; e < pw; ++e) {
+        dst[e] = p;
+        p *= u;
+      }
+    }
+    __syncthreads();
+    // a11: X_0 = M(u) and X_{1+v} = V_v M(u) (the design row is [X_0 | -X_{1+v}])
+    for (int i = threadIdx.x; i < kFRT * m; i += blockDim.x) {
+      const int r = i / m, j = i % m;
+      const uint32_t w = sExp[j];
+      const double *pr = sPow + r * n * pw;
+      double prod = pr[w & 15];
+      for (int k = 1; k < n; ++k) prod *= pr[k * pw + ((w >> (4 * k)) & 15)];
+      sX[r * L::S + j] = prod;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sX[(1 + v) * kFRT * L::S + r * L::S + j] = sV[v * kFRT + r] * prod;
+    }
+    __syncthreads();
+    // a12: the upper tiles of the 1 + 2 NV blocks (per-warp compile-time tile lists)
+    switch (wid) {
+#define RP_W(w) \
+  case w: fused_mma_warp<NB, NV, w, L::SLOTS, L::S, kFRT>(sX, lane, acc); break;
+      RP_W(0) RP_W(1) RP_W(2) RP_W(3) RP_W(4) RP_W(5) RP_W(6) RP_W(7)
+      RP_W(8) RP_W(9) RP_W(10) RP_W(11) RP_W(12) RP_W(13) RP_W(14) RP_W(15)
+#undef RP_W
+    }
+    __syncthreads();
+    if (((tr + 1) % kFlushTiles) == 0 || tr + 1 == ntr) {
+#pragma unroll
+      for (int j = 0; j < L::SLOTS; ++j) {
+        const int id = wid * L::SLOTS + j;
+        if (id < L::NT) {
+          int pa, pb, pair, bi, bj;
+          fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
+          double *dst = part + (int64_t)(pair * L::T + upper_index(NB, bi, bj)) * 64 + lane * 2;
+          if (first) {
+            dst[0] = acc[j][0];
+            dst[1] = acc[j][1];
+          } else {
+            dst[0] += acc[j][0];
+            dst[1] += acc[j][1];
+          }
+          acc[j][0] = acc[j][1] = 0.0;
+        }
+      }
+      first = false;
+    }
+  }
+  if (ntr == 0)  // empty slab: zero partial
+    for (int i = threadIdx.x; i < L::NT * 64; i += blockDim.x) part[i] = 0.0;
+}
+
+// G_v (v < n_v) assembled from the block partials, summed over CTAs in fixed order.
+__global__ void k_gram_fused_reduce(const double *part, int nblk, int NB, int NV, int m, double *G) {
+  const int T = NB * (NB + 1) / 2, NT = (1 + 2 * NV) * T, nc = 2 * m;
+  const int64_t total = (int64_t)NV * nc * nc;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(idx / ((int64_t)nc * nc));
+    const int rc = (int)(idx % ((int64_t)nc * nc));
+    const int row = rc / nc, col = rc % nc;
+    const int qa = row >= m, qb = col >= m;
+    int x = row - qa * m, y = col - qb * m;
+    const int pair = (!qa && !qb) ? 0 : (qa != qb ? 1 + v : 1 + NV + v);
+    const double sign = (qa != qb) ? -1.0 : 1.0;
+    if (x / 8 > y / 8) {  // symmetric block: use the transposed element of the upper tile
+      const int t = x;
+      x = y;
+      y = t;
+    }
+    const int bi = x / 8, bj = y / 8, mr = x % 8, nn = y % 8;
+    const int can = pair * T + upper_index(NB, bi, bj);
+    const int e = (mr * 4 + nn / 2) * 2 + (nn & 1);
+    const double *src = part + (int64_t)can * 64 + e;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += src[(int64_t)b * NT * 64];
+    G[idx] = sign * s;
+  }
+}
+
+template <int NB, int NV>
+static size_t fused_smem(int n, int pw) {
+  using L = FL<NB, NV>;
+  return sizeof(double) * ((size_t)L::NX * kFRT * L::S + kFRT * kMaxVars + (size_t)kFRT * n * pw + NV * kFRT) +
+         sizeof(uint32_t) * L::M8;
+}
+
+static int fused_grid_x(int64_t K) {
+  int64_t want = (K + kFRT - 1) / kFRT;
+  int64_t cap = num_sms();
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+template <int NB, int NV>
+static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, const double *X,
+                                  const double *V, int64_t K, double *G, double *d_part,
+                                  size_t part_elems, cudaStream_t s) {
+  using L = FL<NB, NV>;
+  const int gx = fused_grid_x(K);
+  if ((size_t)gx * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
+  const size_t smem = fused_smem<NB, NV>(h.n, h.maxdeg + 1);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_gram_fused<NB, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  FusedArgs fa{d_basis, X, V, K, d_part};
+  k_gram_fused<NB, NV><<<gx, kFW * 32, smem, s>>>(fa);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int64_t total = (int64_t)NV * 4 * h.n_num * h.n_num;
+  const int rb = (int)((total + 255) / 256);
+  k_gram_fused_reduce<<<rb, 256, 0, s>>>(d_part, gx, NB, NV, h.n_num, G);
+  return cudaGetLastError();
+}
+
+// which (NB, NV) pairs are compiled for the fused path
+static bool fused_supported(const GramBasis &h, int n_v) {
+  if (!h.fused || h.n > kMaxVars || h.maxdeg > 15) return false;
+  const int nb = (h.n_num + 7) / 8;
+  return (n_v == 1 || n_v == 3) && (nb == 2 || nb == 5 || nb == 9);
+}
+
+static size_t fused_partial_elems(const GramBasis &h, int n_v, int64_t K) {
+  const int nb = (h.n_num + 7) / 8;
+  const int NT = (1 + 2 * n_v) * nb * (nb + 1) / 2;
+  return (size_t)fused_grid_x(K) * NT * 64;
+}
+
+static cudaError_t launch_fused(const GramBasis *d_basis, const GramBasis &h, const double *X,
+                                const double *V, int64_t K, int n_v, double *G, double *d_part,
+                                size_t part_elems, cudaStream_t s) {
+  const int nb = (h.n_num + 7) / 8;
+#define RP_FUSED_CASE(NB_, NV_) \
+  if (nb == NB_ && n_v == NV_) return launch_fused_t<NB_, NV_>(d_basis, h, X, V, K, G, d_part, part_elems, s);
+  RP_FUSED_CASE(2, 1) RP_FUSED_CASE(2, 3) RP_FUSED_CASE(5, 1) RP_FUSED_CASE(5, 3)
+  RP_FUSED_CASE(9, 1) RP_FUSED_CASE(9, 3)
+#undef RP_FUSED_CASE
+  return cudaErrorInvalidValue;
+}
+
 static int gram_grid_x(int64_t K) {
   int64_t want = (K + kRT - 1) / kRT;
   int64_t cap = num_sms();
@@ -409,6 +690,7 @@ static int gram_grid_x(int64_t K) {
 
 size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm) {
   (void)nsm;
+  if (fused_supported(h, n_v)) return fused_partial_elems(h, n_v, K);
   const int nb = (h.nc + 7) / 8;
   const int ntiles = nb * (nb + 1) / 2;
   const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
@@ -418,6 +700,7 @@ size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm) {
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const double *X,
                         const double *V, int64_t K, int n_v, double *G, double *d_part,
                         size_t part_elems, cudaStream_t s) {
+  if (fused_supported(h, n_v)) return launch_fused(d_basis, h, X, V, K, n_v, G, d_part, part_elems, s);
   const int nb = (h.nc + 7) / 8;
   const int ntiles = nb * (nb + 1) / 2;
   const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;

@@ -96,6 +96,10 @@ struct GramBasis {  // exponents of the n_c design columns (numerator then denom
   int8_t exp[256][kMaxVars];
   double xc[kMaxVars];
   int32_t xe[kMaxVars];
+  // fused path (numerator basis == denominator basis): the m = n_num monomials with their
+  // exponents packed 4 bits per variable
+  int32_t fused;
+  uint32_t pexp[256];
 };
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, const double *X,
                         const double *V, int64_t K, int n_v, double *G, double *d_part,
