@@ -82,7 +82,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.gpu), "-lms", "100"], stdout=open(self.path, "w"),
+                                          "-i", str(self.gpu), "-lms", "20"], stdout=open(self.path, "w"),
                                          stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -185,7 +185,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -266,6 +266,10 @@ def main():
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
+        time.sleep(0.5)  # nvidia-smi up before the timed region
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
     times, t_fit, t_sweep_k, t_plan = [], [], [], []
     for _ in range(args.steps):
         flush.zero_()  # L2 (126 MB) flushed between timed steps
@@ -356,7 +360,9 @@ def main():
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DESIGN.md 'Peaks'); "
                                "measured DFMA microbenchmark 34.1 TF/s (profiles/r01_fp64_microbench.jsonl)",
                 "flop_per_launch": flop_launch, "evaluated_pairs": pairs_eval, "ms_per_launch": sweep_ms}
-    gram_flop = (khi - klo) * 3 * 140 * 141  # upper triangle incl. diagonal, multiply+add, 3 metrics
+    # fused algorithm: 1 + 2*3 symmetric 70x70 blocks per row,
+    # 70*71/2 unique multiply-adds each
+    gram_flop = (khi - klo) * (1 + 2 * 3) * 70 * 71
     gram_ach = gram_flop / (gram_ms * 1e-3) / 1e12
     roofline_fit = {"bound": "tensor", "kernel": "k_gram (DMMA.8x8x4)", "achieved": gram_ach,
                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gram_ach / FP64_PEAK_TFLOPS,
