@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librp.so")
+# RP_LIBRP overrides the in-tree library (developer knob for A/B builds of the same sources)
+LIB_PATH = os.environ.get("RP_LIBRP") or os.path.join(_HERE, "librp.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(there is no CPU fallback)")

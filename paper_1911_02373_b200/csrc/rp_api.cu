@@ -353,20 +353,26 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
     pl->nde_max = std::max(pl->nde_max, hp[g].nDE);
     pl->n_sm_max = std::max(pl->n_sm_max, hp[g].n_sm);
   }
+  const int nde_pad = std::max(4, (pl->nde_max + 3) & ~3);
   const size_t nrec = (size_t)n_prog * nFp;                               // CfgRec (64 B)
-  const size_t nd = (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab;  // mP, rSM
+  const size_t ncm = (size_t)n_prog * kMaxPolys * npe_pad * nde_pad;      // Cmat
+  const size_t nd = 2 * (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab + ncm;  // mP x2, rSM, Cmat
   // stream-ordered pool allocations (a synchronous cudaMalloc/cudaFree per plan costs ms)
   if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
-  if ((e = cudaMallocAsync((void **)&pl->buf_i, nrec * sizeof(CfgRec) + n_prog * 4 + 16, s)) != cudaSuccess) return fail(e, "alloc");
+  if ((e = cudaMallocAsync((void **)&pl->buf_i, 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16, s)) != cudaSuccess) return fail(e, "alloc");
   if ((e = cudaMallocAsync((void **)&pl->buf_d, nd * 8, s)) != cudaSuccess) return fail(e, "alloc");
   // zero padding entries: padded configurations read as m_pe = 0 by the DMMA tiles
-  if ((e = cudaMemsetAsync(pl->buf_i, 0, nrec * sizeof(CfgRec) + n_prog * 4 + 16, s)) != cudaSuccess) return fail(e, "memset");
+  if ((e = cudaMemsetAsync(pl->buf_i, 0, 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16, s)) != cudaSuccess) return fail(e, "memset");
   if ((e = cudaMemsetAsync(pl->buf_d, 0, nd * 8, s)) != cudaSuccess) return fail(e, "memset");
   pl->tab.nFp = nFp;
   pl->tab.rec = reinterpret_cast<CfgRec *>(pl->buf_i);
-  pl->tab.nFc = reinterpret_cast<int32_t *>(pl->tab.rec + nrec);
+  pl->tab.srec = pl->tab.rec + nrec;
+  pl->tab.nFc = reinterpret_cast<int32_t *>(pl->tab.srec + nrec);
   pl->tab.mP = pl->buf_d;
-  pl->tab.rSM = pl->buf_d + (size_t)n_prog * nFp * npe_pad;
+  pl->tab.smP = pl->buf_d + (size_t)n_prog * nFp * npe_pad;
+  pl->tab.rSM = pl->tab.smP + (size_t)n_prog * nFp * npe_pad;
+  pl->tab.Cmat = pl->tab.rSM + (size_t)n_prog * kRSMTab;
+  pl->tab.nde_pad = nde_pad;
   // the DevProg blob is staged through pinned-free pageable memory: copy synchronously w.r.t.
   // the host buffer lifetime (cudaMemcpyAsync from pageable memory returns after staging)
   if ((e = cudaMemcpyAsync(pl->d_progs, hp.data(), sizeof(DevProg) * n_prog, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -644,7 +650,7 @@ rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_
   RP_REQUIRE(plan && n_static_feasible && prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "bad argument");
   int32_t v = 0;
   RP_CUDA(cudaStreamSynchronize(plan->stream));
-  RP_CUDA(cudaMemcpy(&v, plan->tab.nFc + prog, 4, cudaMemcpyDeviceToHost));
+  RP_CUDA(cudaMemcpy(&v, plan->tab.nFc + 2 * prog, 4, cudaMemcpyDeviceToHost));
   *n_static_feasible = v;
   return RP_OK;
 }

@@ -58,19 +58,26 @@ struct DevProg {
 // ascending original index; program g at offset g * nFp, nFp = nF rounded up to 8 so that
 // config octets of the DMMA tiles never straddle programs).
 struct CfgRec {      // one statically feasible configuration, 64 B (4 x 16-byte loads)
-  int32_t orig, P0, P1, P2;  // original index in F, block dims (1 for k >= p)
-  float rP0, rP1, rP2, pad;  // 1/P_k in fp32 (estimate for the exact integer ceil)
-  double W, rB;              // W_active, 1/B_active
-  double rW, pad2;           // 1/W_active
+  int64_t P01;               // P_1 P_2 (P_1 if p = 1), for the D rule P_1 P_2 <= D_1^2
+  int32_t orig, Pm1_0;       // original index in F; P_0 - 1
+  int32_t Pm1_1, Pm1_2;      // P_k - 1 (0 for k >= p)
+  uint32_t M0, M1, M2;       // ceil(n / P_k) = (n + P_k - 1) * M_k >> s_k  (exact, n < 2^31)
+  uint32_t s012;             // s_k in bits 8k..8k+7
+  double W, rB, rW;          // W_active, 1/B_active, 1/W_active
 };
 static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
 
 struct CfgTable {
   int32_t nFp;     // padded stride (multiple of 8)
-  CfgRec *rec;     // [n_prog][nFp]
+  CfgRec *rec;     // [n_prog][nFp]  sorted by (P1 P2, original index)
+  CfgRec *srec;    // [n_prog][nFp]  scratch: compacted in index order
+  double *smP;     // [n_prog][npe_pad][nFp]  scratch
   double *mP;      // [n_prog][npe_pad][nFp]  program-part monomials (0 for pe >= nPE or pad)
   double *rSM;     // [n_prog][kRSMTab]  1/k for SM_act = k (k <= n_sm)
-  int32_t *nFc;    // [n_prog]
+  double *Cmat;    // [n_prog][6 * npe_pad][nde_pad]  dense coefficient matrix of the staging:
+                   // row k * npe_pad + pe, column de: coef of m_de(u_D) m_pe(u_P) in poly k
+  int32_t nde_pad; // data-part monomials padded to a multiple of 4 (the DMMA K step)
+  int32_t *nFc;    // [n_prog][2]: number of feasible configurations, sorted flag
 };
 constexpr int kRSMTab = 1024;  // n_sm <= 1023 uses the table
 

@@ -22,6 +22,8 @@
 
 namespace rp {
 
+constexpr int kSortMaxPlan = 8192;  // plans with more feasible configurations keep index order
+
 // ---- a5: occupancy, Fig. occupancysimpleflowchart, 64-bit integers ----
 __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_t Z,
                                                     const DevProg &pg) {
@@ -85,19 +87,29 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     if (ok) {
       const int64_t off = (int64_t)g * nFp;
       CfgRec r;
+      r.P01 = (int64_t)Pk[0] * (pg.p >= 2 ? Pk[1] : 1);
       r.orig = c;
-      r.P0 = Pk[0];
-      r.P1 = Pk[1];
-      r.P2 = Pk[2];
-      r.rP0 = 1.0f / (float)Pk[0];
-      r.rP1 = 1.0f / (float)Pk[1];
-      r.rP2 = 1.0f / (float)Pk[2];
-      r.pad = 0.0f;
+      r.Pm1_0 = Pk[0] - 1;
+      r.Pm1_1 = Pk[1] - 1;
+      r.Pm1_2 = Pk[2] - 1;
+      // division by the invariant P: M = ceil(2^s / P), s = 31 + ceil(log2 P) gives
+      // floor(n / P) = (n * M) >> s exactly for 0 <= n < 2^31 (error (M P - 2^s) n / (P 2^s) < 1/P)
+      uint32_t Ms[3], ss[3];
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t P = (uint32_t)Pk[k];
+        uint32_t l = 0;
+        while ((1ull << l) < P) ++l;
+        ss[k] = 31 + l;
+        Ms[k] = (uint32_t)(((1ull << ss[k]) + P - 1) / P);
+      }
+      r.M0 = Ms[0];
+      r.M1 = Ms[1];
+      r.M2 = Ms[2];
+      r.s012 = ss[0] | (ss[1] << 8) | (ss[2] << 16);
       r.W = (double)W;
       r.rB = 1.0 / (double)B;
       r.rW = 1.0 / (double)W;
-      r.pad2 = 0.0;
-      tab.rec[off + pos] = r;
+      tab.srec[off + pos] = r;
       double u[3];
       for (int k = 0; k < pg.p; ++k)
         u[k] = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
@@ -108,14 +120,46 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
           for (int k = 0; k < pg.p; ++k)
             for (int t = 0; t < pg.pe_exp[pe][k]; ++t) m *= u[k];
         }
-        tab.mP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + pos] = m;
+        tab.smP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + pos] = m;
       }
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) base = pos + ok;
     __syncthreads();
   }
-  if (threadIdx.x == 0) tab.nFc[g] = base;
+  __syncthreads();
+  const int nFc = base;
+  // order the feasible configurations by (P1 P2, original index) so a warp can stop at the
+  // first octet whose smallest P1 P2 exceeds every D1^2 of its tuples (a3); rank sort, O(n^2)
+  // per plan, skipped above kSortMax (then index order and no early exit)
+  const bool sorted = nFc <= kSortMaxPlan;
+  for (int i = threadIdx.x; i < nFc; i += blockDim.x) {
+    const CfgRec ri = tab.srec[(int64_t)g * nFp + i];
+    int rank = i;
+    if (sorted) {
+      rank = 0;
+      for (int j = 0; j < nFc; ++j) {
+        const int64_t pj = tab.srec[(int64_t)g * nFp + j].P01;
+        rank += (pj < ri.P01) || (pj == ri.P01 && j < i);
+      }
+    }
+    tab.rec[(int64_t)g * nFp + rank] = ri;
+    for (int pe = 0; pe < npe_pad; ++pe)
+      tab.mP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + rank] =
+          tab.smP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + i];
+  }
+  if (threadIdx.x == 0) {
+    tab.nFc[2 * g] = nFc;
+    tab.nFc[2 * g + 1] = sorted ? 1 : 0;
+  }
+  // dense staging matrix: Cmat[k * npe_pad + pe][de] = coefficient of m_de(u_D) m_pe(u_P) in
+  // polynomial k (zero elsewhere; the buffer is zeroed at plan creation)
+  double *Cm = tab.Cmat + (int64_t)g * kMaxPolys * npe_pad * tab.nde_pad;
+  for (int r = threadIdx.x; r < pg.npoly * pg.nPE; r += blockDim.x) {
+    const int k = r / pg.nPE, pe = r % pg.nPE;
+    for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
+      Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
+  }
   // 1/k for SM_act = k (line 15 of Appendix A); correctly rounded, computed once per plan
   for (int k = threadIdx.x; k < kRSMTab; k += blockDim.x)
     tab.rSM[(int64_t)g * kRSMTab + k] = k > 0 ? 1.0 / (double)k : 0.0;
@@ -174,16 +218,11 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, e, r);
 }
 
-// exact ceil(D / P) for D, P >= 1: fp32 estimate (|error| < 1 for D < 2^24) + integer correction
-__device__ __forceinline__ int64_t ceil_div(int32_t D, int32_t P, float rP) {
-  if (D < (1 << 24)) {
-    int q = __float2int_rz(__int2float_rn(D) * rP);
-    int r = D - q * P;
-    q = r < 0 ? q - 1 : (r >= P ? q + 1 : q);
-    r = D - q * P;
-    return (int64_t)q + (r > 0);
-  }
-  return ((int64_t)D + P - 1) / P;
+// exact ceil(D / P) = floor((D + P - 1) / P) for 1 <= D + P - 1 < 2^31 via the per-config
+// multiply-shift (M, s) of k_plan_configs
+__device__ __forceinline__ int64_t ceil_div_magic(int32_t D, int32_t Pm1, uint32_t M, uint32_t s) {
+  const uint64_t n = (uint64_t)(uint32_t)(D + Pm1);
+  return (int64_t)((n * (uint64_t)M) >> s);
 }
 
 // ---- the sweep ------------------------------------------------------------------------------
@@ -192,7 +231,7 @@ struct SweepArgs {
   CfgTable tab;
   int npe_pad;
   int d;
-  int nde_max;  // max nDE over the programs (shared-memory layout)
+  int nde_stride;  // row stride of the data-monomial tile in shared memory (= 4 mod 16)
   const int32_t *D;
   int64_t nD;
   int32_t *idx;
@@ -200,6 +239,9 @@ struct SweepArgs {
   double *secondE;
 };
 
+#ifndef RP_SWEEP_MINB
+#define RP_SWEEP_MINB 4
+#endif
 constexpr int kSweepWarps = 4;
 constexpr int kSweepThreads = 32 * kSweepWarps;
 constexpr int kTD = 8 * kSweepWarps;  // tuples per CTA: one octet (the DMMA M side) per warp
@@ -211,10 +253,16 @@ __host__ __device__ constexpr int c_stride() {  // per-tuple stride of sC in dou
   return s;
 }
 
+static int md_stride(int nde_pad) {  // = 4 mod 16: conflict-free B fragments
+  int s = nde_pad;
+  while (s % 16 != 4) ++s;
+  return s;
+}
+
 template <int NPOLY, int NPE>
-size_t sweep_smem_bytes(int nde_max, int n_sm) {
+size_t sweep_smem_bytes(int nde_stride, int n_sm) {
   const int rsm = (n_sm + 2) & ~1;
-  return sizeof(double) * ((size_t)kTD * c_stride<NPOLY, NPE>() + (size_t)kTD * nde_max + rsm) +
+  return sizeof(double) * ((size_t)kTD * c_stride<NPOLY, NPE>() + (size_t)kTD * nde_stride + rsm) +
          sizeof(int32_t) * kTD * kMaxVars;
 }
 
@@ -222,11 +270,11 @@ size_t sweep_smem_bytes(int nde_max, int n_sm) {
 // common-denominator form g_i = a_i / Q; every division is a Newton reciprocal).  Straight-line
 // code: masked pairs are carried to the end and returned as +inf.
 struct EConst {
-  double Lunc, Lcoal, DdU, ddc, issue, Kbw;
+  double Lunc, Lcoal, DdU, ddc, issue, Kbw, rKbw;
 };
 __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, double q2, double p3,
-                                           double q3, double W, double rW, double Rep,
-                                           double rSM, const EConst &k) {
+                                           double q3, double W, double Rep, double rSM,
+                                           double SMact, const EConst &k) {
   const double q23 = q2 * q3, q13 = q1 * q3, q12 = q1 * q2;
   const double Q = q1 * q23;
   const double a1 = p1 * q23, a2 = p2 * q13, a3 = p3 * q12;  // g_i = a_i / Q
@@ -246,9 +294,11 @@ __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, doub
   const double cwp = CWPf < W ? CWPf : W;  // line 14
   const double cpm = cc * r23;             // Comp_c / Mem
   const double tail = cpm * (mwp - 1.0);
-  const double rm = (mwp == W) ? rW : frcp(mwp);
+  // Mem_c W / MWP for each operand of the min: W / W = 1; Mem_c / MWP_nb = Dep Mem = dn / Q;
+  // Mem_c / MWP_bw = Mem SM_act / K_bw = s23 SM_act / (Q K_bw)
+  const double mcw = (mwp == W) ? Mem_c : W * rQ * ((mwp == MWP_nb) ? dn : s23 * SMact * k.rKbw);
   const double E1 = Mem_c + Comp_c + tail;         // line 16
-  const double E2 = Mem_c * W * rm + tail;         // line 17
+  const double E2 = mcw + tail;                    // line 17
   const double E3 = mc * r23 + Comp_c * W;         // line 18 (Mem_L = Mem_c / Mem)
   const bool c1 = (mwp == W) && (cwp == W);
   const bool c2 = (cwp >= mwp) || (Comp_c > Mem_c);
@@ -256,7 +306,7 @@ __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, doub
 }
 
 template <int NPE, bool MWP, bool SECOND>
-__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArgs a) {
   constexpr int NPOLY = MWP ? 6 : 2;
   constexpr int KS = NPE / 4;
   constexpr int CS = c_stride<NPOLY, NPE>();
@@ -266,7 +316,7 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
   const int d = a.d;
   const int64_t d0 = (int64_t)blockIdx.x * kTD;
   const int tmax = (int)((a.nD - d0) < kTD ? (a.nD - d0) : kTD);
-  const int nde = a.nde_max;
+  const int nde = a.nde_stride;
   const int n_sm = pg.n_sm;
 
   extern __shared__ __align__(16) double smem[];
@@ -276,7 +326,7 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
   int32_t *sDv = reinterpret_cast<int32_t *>(sRSM + ((n_sm + 2) & ~1));  // [kTD][kMaxVars]
 
   // ---- a2: stage the tile (D values, data monomials, data polynomials) --------------------------
-  const int nDE = pg.nDE, nPE = pg.nPE, npoly = pg.npoly;
+  const int nDE = pg.nDE, ndp = a.tab.nde_pad;
   for (int i = threadIdx.x; i < kTD * d; i += blockDim.x) {
     const int t = i / d, k = i % d;
     sDv[t * kMaxVars + k] = (t < tmax) ? a.D[(d0 + t) * d + k] : 1;
@@ -286,26 +336,40 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
   if (rsm_tab)
     for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) sRSM[i] = gRSM[i];
   __syncthreads();
-  for (int i = threadIdx.x; i < kTD * nDE; i += blockDim.x) {
-    const int t = i / nDE, de = i % nDE;
-    double m = 1.0;
-    for (int k = 0; k < d; ++k) {
-      const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
-      for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
+  // data monomials m_de(u_D), u = (D - c) 2^-e, zero for the padding de >= nDE
+  for (int i = threadIdx.x; i < kTD * ndp; i += blockDim.x) {
+    const int t = i / ndp, de = i % ndp;
+    double m = 0.0;
+    if (de < nDE) {
+      m = 1.0;
+      for (int k = 0; k < d; ++k) {
+        const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+        for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
+      }
     }
     sMD[t * nde + de] = m;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kTD * NPOLY * NPE; i += blockDim.x) {
-    const int t = i / (NPOLY * NPE), r = i % (NPOLY * NPE);
-    const int k = r / NPE, pe = r % NPE;
-    double acc = 0.0;
-    if (k < npoly && pe < nPE) {
-      const int row = k * nPE + pe;
-      for (int j = pg.row_start[row]; j < pg.row_start[row + 1]; ++j)
-        acc = fma(pg.term_coef[j], sMD[t * nde + pg.term_de[j]], acc);
+  // staged data polynomials C[t][k NPE + pe] = sum_de Cmat[k NPE + pe][de] m_de(t): a
+  // (NPOLY NPE x ndp) x (ndp x 32) product on DMMA.8x8x4 (A from the plan's dense matrix,
+  // B = the monomials of the tile); output tiles (8 rows x 8 tuples) spread over the warps
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
+    constexpr int MT = NPOLY * NPE / 8;  // 8-row tiles of the staging matrix
+    constexpr int NT = kTD / 8;          // 8-tuple tiles
+    for (int tile = wid; tile < MT * NT; tile += kSweepWarps) {
+      const int mt = tile / NT, nt = tile % NT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < ndp / 4; ++ks) {
+        const double av = __ldg(Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3));
+        const double bv = sMD[(nt * 8 + (lane >> 2)) * nde + ks * 4 + (lane & 3)];
+        dmma(c0, c1, av, bv);
+      }
+      const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
+      sC[t * CS + row] = c0;
+      sC[(t + 1) * CS + row] = c1;
     }
-    sC[t * CS + k * NPE + pe] = acc;
   }
   __syncthreads();
 
@@ -317,13 +381,15 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
   kc.ddc = pg.dd_coal;
   kc.issue = pg.issue;                         // line 13
   kc.Kbw = pg.mem_bw / (pg.freq * pg.lbpw);    // line 11: Mem_BW / (Freq LoadBytesPerWarp)
+  kc.rKbw = (pg.freq * pg.lbpw) / pg.mem_bw;
   const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
             map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
   const bool two = pg.p >= 2;
   const double rNSM = 1.0 / (double)n_sm;
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nFc = a.tab.nFc[g];
+  const int nFc = a.tab.nFc[2 * g];
+  const bool sorted = a.tab.nFc[2 * g + 1] != 0;
   const int nFp = a.tab.nFp;
   const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
   const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
@@ -343,9 +409,17 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
   st.i = 0x7fffffff;
   st.s = kInf;
 
+  // the largest D1^2 among the warp's tuples (a3 early exit over configurations sorted by P1 P2)
+  int64_t maxD1sq = tok ? D1sq : 0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const int64_t x = __shfl_xor_sync(0xffffffffu, maxD1sq, o);
+    maxD1sq = x > maxD1sq ? x : maxD1sq;
+  }
   const int nOctF = (nFc + 7) >> 3;
   if (wid * 8 < tmax) {
     for (int oc = 0; oc < nOctF; ++oc) {
+      if (sorted && __ldg(&rec[oc * 8].P01) > maxD1sq) break;  // every later pair fails a3
       // B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
       double bfr[KS];
 #pragma unroll
@@ -360,36 +434,40 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
       }
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int c = oc * 8 + 2 * (lane & 3) + v;  // output column 2 (lane % 4) + v
-        const CfgRec *cr = rec + (c < nFc ? c : 0);
-        const int4 ip = __ldg(reinterpret_cast<const int4 *>(cr));
-        const float4 fp = __ldg(reinterpret_cast<const float4 *>(cr) + 1);
+        // output column 2 (lane % 4) + v; padded configurations (c >= nFc) have zero records
+        // and zero monomials, so their E is NaN and they are masked below
+        const CfgRec *cr = rec + oc * 8 + 2 * (lane & 3) + v;
+        const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));      // P01 | orig, Pm1_0
+        const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);             // Pm1_1, Pm1_2, M0, M1
+        const int32_t orig = (int32_t)(h0.y & 0xffffffff);
         // a3: "P1 P2 <= D1^2 is meaningful"
-        const int64_t P01 = (int64_t)ip.y * (two ? ip.z : 1);
-        const bool ok = tok && c < nFc && P01 <= D1sq;
+        const bool ok = tok && h0.x <= D1sq;
         double E;
         if (MWP) {
-          const double2 wb = __ldg(reinterpret_cast<const double2 *>(cr) + 2);  // (W, 1/B) at byte 32
-          const double rW = __ldg(reinterpret_cast<const double *>(cr) + 6);
+          const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);           // M2, s012, W
+          const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);     // rB, rW
+          const int32_t Pm1_0 = (int32_t)(h0.y >> 32);
+          const uint32_t s012 = (uint32_t)h2.y;
+          const double W = __hiloint2double(h2.w, h2.z);
           // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
           int64_t blocks = 1;
-          if (map0 >= 0) blocks *= ceil_div(Da, ip.y, fp.x);
-          if (map1 >= 0) blocks *= ceil_div(Db, ip.z, fp.y);
-          if (map2 >= 0) blocks *= ceil_div(Dc, ip.w, fp.z);
+          if (map0 >= 0) blocks *= ceil_div_magic(Da, Pm1_0, (uint32_t)h1.z, s012 & 255);
+          if (map1 >= 0) blocks *= ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255);
+          if (map2 >= 0) blocks *= ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
           const int64_t smact = blocks < n_sm ? blocks : n_sm;
           const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
-          const double Rep = (double)blocks * wb.y * rSM;  // line 15: #Blocks / (B_act SM_act)
-          E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], wb.x, rW,
-                       Rep, rSM, kc);
+          const double Rep = (double)blocks * h3.x * rSM;  // line 15: #Blocks / (B_act SM_act)
+          E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
+                       rSM, (double)smact, kc);
         } else {
           E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
         }
         // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
         E = (ok && E > 0.0 && E < kInf) ? E : kInf;
-        // a8: configurations arrive in ascending original index: strict < keeps the lowest
-        const bool better = E < st.e;
+        // a8: exact lexicographic key (E, original index): ties go to the lowest index
+        const bool better = E < st.e || (E == st.e && orig < st.i);
         if (SECOND) st.s = better ? st.e : fmin(st.s, E);
-        st.i = better ? ip.x : st.i;
+        st.i = better ? orig : st.i;
         st.e = better ? E : st.e;
       }
     }
@@ -407,7 +485,7 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
 
 template <int NPE, bool MWP, bool SECOND>
 static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
-  const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_max, n_sm_max);
+  const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_stride, n_sm_max);
   const int64_t tiles = (a.nD + kTD - 1) / kTD;
   if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_sweep<NPE, MWP, SECOND>,
@@ -432,7 +510,8 @@ cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable 
                          int32_t *idx, double *bestE, double *secondE, cudaStream_t s) {
   if (nD == 0) return cudaSuccess;
   if (n_sm_max >= kRSMTab) n_sm_max = 0;  // no table: 1/SM_act computed directly
-  SweepArgs a{d_progs, tab, npe_pad, d, nde_max < 1 ? 1 : nde_max, d_D, nD, idx, bestE, secondE};
+  (void)nde_max;
+  SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE};
   switch (npe_pad) {
     case 4: return launch_npe<4>(a, n_prog, mwp, n_sm_max, s);
     case 8: return launch_npe<8>(a, n_prog, mwp, n_sm_max, s);
