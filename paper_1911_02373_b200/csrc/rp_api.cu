@@ -581,25 +581,28 @@ rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const
   double *part = (double *)tw.p, *lohi = part + (size_t)nblk * n * 2, *xf = lohi + 2 * RP_MAX_VARS;
   RP_CUDA(launch_minmax(dX, K, n, part, nblk, lohi, s));
   RP_CUDA(launch_xform(lohi, n, xf, s));
-  double hxf[2 * RP_MAX_VARS];
-  RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  RP_CUDA(cudaStreamSynchronize(s));
-  rp_xform xform;
-  memset(&xform, 0, sizeof xform);
-  for (int k = 0; k < n; ++k) {
-    xform.c[k] = hxf[2 * k];
-    xform.e[k] = (int32_t)hxf[2 * k + 1];
-  }
+  // the Gram reads the transform from the device copy of the basis: no host round trip
   GramBasis gb;
-  if ((st = build_gram_basis(basis, &xform, &gb)) != RP_OK) return st;
+  if ((st = build_gram_basis(basis, nullptr, &gb)) != RP_OK) return st;
   RP_CUDA(tG.alloc((size_t)n_v * nc * nc * 8, s));
   RP_CUDA(tb.alloc(sizeof(GramBasis), s));
   RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+  RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
   const size_t pe = gram_partial_elems(gb, n_v, K, num_sms());
   RP_CUDA(tp.alloc(pe * 8, s));
   RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, K, n_v, (double *)tG.p, (double *)tp.p, pe, s));
-  if (xform_out) *xform_out = xform;
-  return solve_impl((const double *)tG.p, n_v, nc, basis->n_num, coef_out, info, s);
+  rp_status sst = solve_impl((const double *)tG.p, n_v, nc, basis->n_num, coef_out, info, s);  // synchronises
+  double hxf[2 * RP_MAX_VARS];
+  RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  if (xform_out) {
+    memset(xform_out, 0, sizeof *xform_out);
+    for (int k = 0; k < n; ++k) {
+      xform_out->c[k] = hxf[2 * k];
+      xform_out->e[k] = (int32_t)hxf[2 * k + 1];
+    }
+  }
+  return sst;
 }
 
 rp_status rp_eval_metrics(const rp_program *prog, const double *X, int64_t K, double *out, rp_stream sv) {

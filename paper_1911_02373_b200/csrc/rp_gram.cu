@@ -102,6 +102,19 @@ cudaError_t launch_xform(const double *d_lohi, int n, double *d_out, cudaStream_
   return cudaGetLastError();
 }
 
+// the transform of k_xform copied into the device-side GramBasis (c_k, e_k)
+__global__ void k_xform_to_basis(const double *xf, int n, GramBasis *gb) {
+  const int k = threadIdx.x;
+  if (k >= n) return;
+  gb->xc[k] = xf[2 * k];
+  gb->xe[k] = (int32_t)xf[2 * k + 1];
+}
+
+cudaError_t launch_xform_to_basis(const double *d_xf, int n, GramBasis *d_gb, cudaStream_t s) {
+  k_xform_to_basis<<<1, 32, 0, s>>>(d_xf, n, d_gb);
+  return cudaGetLastError();
+}
+
 int minmax_blocks(int64_t K) {
   int64_t b = (K + 255) / 256;
   int64_t cap = 4LL * num_sms();

@@ -97,6 +97,8 @@ cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int
                           double *d_out, cudaStream_t s);
 int minmax_blocks(int64_t K);
 cudaError_t launch_xform(const double *d_lohi, int n, double *d_out, cudaStream_t s);
+struct GramBasis;
+cudaError_t launch_xform_to_basis(const double *d_xf, int n, GramBasis *d_gb, cudaStream_t s);
 
 struct GramBasis {  // exponents of the n_c design columns (numerator then denominator)
   int32_t n, n_num, n_den, nc, maxdeg;

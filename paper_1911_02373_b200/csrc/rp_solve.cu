@@ -32,21 +32,38 @@ __device__ __forceinline__ void dd_fma(double &hi, double &lo, double a, double 
   lo += pe;
 }
 
-// x <- (L L^T)^{-1} x, L lower triangular in sL (stride ld); y is scratch.
-__device__ void chol_solve(const double *sL, int ld, int m, double *x) {
-  for (int j = 0; j < m; ++j) {  // forward: L y = x
-    if (threadIdx.x == 0) x[j] /= sL[j * ld + j];
-    __syncthreads();
-    const double xj = x[j];
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) x[i] -= sL[i * ld + j] * xj;
-    __syncthreads();
+// x <- (L L^T)^{-1} x, L lower triangular in sL (stride ld), rd[j] = 1 / L_jj.  One warp does
+// both triangular solves (warp-synchronous steps instead of block-wide barriers).
+__device__ void chol_solve(const double *sL, const double *rd, int ld, int m, double *x) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int j = 0; j < m; ++j) {  // forward: L y = x
+      const double xj = x[j] * rd[j];
+      __syncwarp();
+      if (lane == 0) x[j] = xj;
+      for (int i = j + 1 + lane; i < m; i += 32) x[i] -= sL[i * ld + j] * xj;
+      __syncwarp();
+    }
+    for (int j = m - 1; j >= 0; --j) {  // backward: L^T z = y
+      const double xj = x[j] * rd[j];
+      __syncwarp();
+      if (lane == 0) x[j] = xj;
+      for (int i = lane; i < j; i += 32) x[i] -= sL[j * ld + i] * xj;
+      __syncwarp();
+    }
   }
-  for (int j = m - 1; j >= 0; --j) {  // backward: L^T z = y
-    if (threadIdx.x == 0) x[j] /= sL[j * ld + j];
-    __syncthreads();
-    const double xj = x[j];
-    for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] -= sL[j * ld + i] * xj;
-    __syncthreads();
+  __syncthreads();
+}
+
+// double-double sum of a warp's (hi, lo) pairs (fixed butterfly order)
+__device__ __forceinline__ void dd_warp_sum(double &hi, double &lo) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    dd_add(hi, lo, h2);
+    lo += l2;
   }
 }
 
@@ -59,6 +76,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
   double *b0 = dsc + m;       // -G_{f,beta0}
   double *x = b0 + m;         // work vector
   double *z = x + m;          // solution, unequilibrated
+  double *rd = z + m;         // 1 / L_jj
   __shared__ int s_status;
   __shared__ double s_pmin, s_pmax;
   const double *Gm = G + (int64_t)blockIdx.x * nc * nc;
@@ -86,24 +104,47 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
     sL[i * ld + j] *= dsc[i] * dsc[j];
   }
   __syncthreads();
-  // Cholesky, lower triangle
-  for (int k = 0; k < m; ++k) {
-    if (threadIdx.x == 0) {
-      const double piv = sL[k * ld + k];
-      if (!(piv > 1e-13)) s_status = RP_ERR_DEGENERATE;
-      s_pmin = fmin(s_pmin, piv);
-      s_pmax = fmax(s_pmax, piv);
-      sL[k * ld + k] = sqrt(fmax(piv, 1e-300));
+  // Cholesky, lower triangle, blocked right-looking: an 8-column panel is factorised by warp 0
+  // (warp-synchronous), then every warp applies the rank-8 update to its rows of the trailing
+  // matrix (2 block barriers per panel)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int kb = 0; kb < m; kb += 8) {
+    const int nb = (m - kb) < 8 ? (m - kb) : 8;
+    if (wid == 0 && s_status == 0) {
+      for (int c = kb; c < kb + nb; ++c) {
+        const double piv = sL[c * ld + c];
+        if (lane == 0) {
+          if (!(piv > 1e-13)) s_status = RP_ERR_DEGENERATE;
+          s_pmin = fmin(s_pmin, piv);
+          s_pmax = fmax(s_pmax, piv);
+        }
+        const double lcc = sqrt(fmax(piv, 1e-300));
+        const double rlcc = 1.0 / lcc;
+        __syncwarp();
+        if (lane == 0) sL[c * ld + c] = lcc;
+        for (int i = c + 1 + lane; i < m; i += 32) sL[i * ld + c] *= rlcc;
+        __syncwarp();
+        for (int j = c + 1; j < kb + nb; ++j) {
+          const double ljc = sL[j * ld + c];
+          for (int i = j + lane; i < m; i += 32) sL[i * ld + j] -= sL[i * ld + c] * ljc;
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
     if (s_status != 0) break;
-    const double lkk = sL[k * ld + k];
-    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) sL[i * ld + k] /= lkk;
-    __syncthreads();
-    const int w = m - k - 1;
-    for (int t = threadIdx.x; t < w * w; t += blockDim.x) {
-      const int i = k + 1 + t / w, j = k + 1 + t % w;
-      if (j <= i) sL[i * ld + j] -= sL[i * ld + k] * sL[j * ld + k];
+    const int j0 = kb + nb;
+    for (int i = j0 + wid; i < m; i += nw) {
+      double li[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) li[c] = c < nb ? sL[i * ld + kb + c] : 0.0;
+      for (int j = j0 + lane; j <= i; j += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < nb) acc = fma(li[c], sL[j * ld + kb + c], acc);
+        sL[i * ld + j] -= acc;
+      }
     }
     __syncthreads();
   }
@@ -121,59 +162,68 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
     }
     return;
   }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) rd[i] = 1.0 / sL[i * ld + i];
   // solve
   for (int i = threadIdx.x; i < m; i += blockDim.x) x[i] = dsc[i] * b0[i];
-  __syncthreads();
-  chol_solve(sL, ld, m, x);
+  chol_solve(sL, rd, ld, m, x);
   for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] = dsc[i] * x[i];
   __syncthreads();
-  // one refinement step: r = b0 - G_ff z in double-double from the original Gram
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    double hi = b0[i], lo = 0.0;
+  // one refinement step: r = b0 - G_ff z in double-double from the original Gram (a warp per
+  // row, lanes over columns: coalesced reads of G)
+  for (int i = wid; i < m; i += nw) {
     const double *Gi = Gm + (int64_t)col(i) * nc;
-    for (int j = 0; j < m; ++j) dd_fma(hi, lo, -Gi[col(j)], z[j]);
-    x[i] = dsc[i] * (hi + lo);
+    double hi = 0.0, lo = 0.0;
+    for (int j = lane; j < m; j += 32) dd_fma(hi, lo, -Gi[col(j)], z[j]);
+    dd_warp_sum(hi, lo);
+    if (lane == 0) {
+      dd_add(hi, lo, b0[i]);
+      x[i] = dsc[i] * (hi + lo);
+    }
   }
-  __syncthreads();
-  chol_solve(sL, ld, m, x);
+  chol_solve(sL, rd, ld, m, x);
   for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] += dsc[i] * x[i];
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) cf[col(i)] = z[i];
   if (threadIdx.x == 0) cf[beta0] = 1.0;
-  __syncthreads();
-  // resid2 = coef^T G coef (double-double), from the original Gram
-  if (threadIdx.x < 32) {
-    double hi = 0.0, lo = 0.0;
-    for (int i = threadIdx.x; i < nc; i += 32) {
+  // resid2 = coef^T G coef (double-double): a warp per row, then the warp partials in order
+  __shared__ double s_rh[32], s_rl[32];
+  {
+    double wh = 0.0, wl = 0.0;
+    for (int i = wid; i < nc; i += nw) {
       const double ci = (i == beta0) ? 1.0 : z[i < beta0 ? i : i - 1];
       double rh = 0.0, rl = 0.0;
-      for (int j = 0; j < nc; ++j) {
+      for (int j = lane; j < nc; j += 32) {
         const double cj = (j == beta0) ? 1.0 : z[j < beta0 ? j : j - 1];
         dd_fma(rh, rl, Gm[(int64_t)i * nc + j], cj);
       }
-      dd_fma(hi, lo, ci, rh);
-      dd_fma(hi, lo, ci, rl);
+      dd_warp_sum(rh, rl);
+      dd_fma(wh, wl, ci, rh);
+      dd_fma(wh, wl, ci, rl);
     }
-    for (int o = 16; o >= 1; o >>= 1) {
-      const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-      const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
-      dd_add(hi, lo, h2);
-      lo += l2;
+    if (lane == 0) {
+      s_rh[wid] = wh;
+      s_rl[wid] = wl;
     }
-    if (threadIdx.x == 0) {
-      inf[0] = 0;
-      inf[1] = (double)m;
-      inf[2] = hi + lo;
-      inf[3] = s_pmin;
-      inf[4] = s_pmax / s_pmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double hi = 0.0, lo = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      dd_add(hi, lo, s_rh[w]);
+      lo += s_rl[w];
     }
+    inf[0] = 0;
+    inf[1] = (double)m;
+    inf[2] = hi + lo;
+    inf[3] = s_pmin;
+    inf[4] = s_pmax / s_pmin;
   }
 }
 
 cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *coef_out,
                          double *info_out, cudaStream_t s) {
   const int m = nc - 1;
-  const size_t smem = ((size_t)m * (m + 1) + 4 * (size_t)m) * sizeof(double);
+  const size_t smem = ((size_t)m * (m + 1) + 5 * (size_t)m) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

@@ -384,7 +384,6 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   kc.rKbw = (pg.freq * pg.lbpw) / pg.mem_bw;
   const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
             map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
-  const bool two = pg.p >= 2;
   const double rNSM = 1.0 / (double)n_sm;
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -424,13 +423,15 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       double bfr[KS];
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
-      // a4: p_k(D_t, P_c) for the octet of tuples x the octet of configurations
+      // a4: p_k(D_t, P_c) for the octet of tuples x the octet of configurations (k-step major:
+      // the NPOLY accumulation chains are independent, so consecutive DMMAs do not wait)
       double acc[NPOLY][2];
 #pragma unroll
-      for (int k = 0; k < NPOLY; ++k) {
-        acc[k][0] = acc[k][1] = 0.0;
+      for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) dmma(acc[k][0], acc[k][1], arow[k * NPE + ks * 4], bfr[ks]);
+      for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], arow[k * NPE + ks * 4], bfr[ks]);
       }
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
