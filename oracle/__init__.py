@@ -77,6 +77,8 @@ def lib():
             L.orc_eval_pair.argtypes = [C.POINTER(_Program), vp, vp, C.POINTER(_Trace)]
             L.orc_eval_pair.restype = i
             L.orc_sweep.argtypes = [C.POINTER(_Program), vp, ll, vp, i, vp, vp, vp, vp, vp, vp, i]
+            L.orc_decide.argtypes = [C.POINTER(_Program), vp, vp, i, d, vp, vp, vp]
+            L.orc_decide.restype = i
             L.orc_design_row.argtypes = [i, i, i, vp, vp, vp, vp, vp, d, vp]
             L.orc_gram.argtypes = [vp, vp, ll, i, i, i, vp, vp, vp, vp, vp, i]
             L.orc_solve.argtypes = [vp, i, i, vp, vp, vp]
@@ -207,6 +209,19 @@ def sweep(spec, D, F, nthreads: int = 0) -> dict:
                     _p(margin), _p(cnt), nthreads)
     return dict(idx=idx, best=best, second=second, kappa=kappa, margin=margin,
                 counters={k: int(cnt[i]) for i, k in enumerate(COUNTER_NAMES)})
+
+
+def decide(spec, D, F, margin: float = 0.0) -> dict:
+    """One runtime decision for the data tuple D: chosen index (-1 if none), its E, the six
+    launch integers (gx, gy, gz, bx, by, bz) and the margin-boundary gap (diagnostic)."""
+    h = _ProgramHolder(spec)
+    Da = np.ascontiguousarray(D, dtype=np.int32).ravel()
+    Fa = np.ascontiguousarray(F, dtype=np.int32).reshape(-1, spec.p)
+    E = np.zeros(1)
+    six = np.zeros(6, dtype=np.int32)
+    gap = np.zeros(1)
+    j = lib().orc_decide(C.byref(h.pr), _p(Da), _p(Fa), len(Fa), float(margin), _p(E), _p(six), _p(gap))
+    return dict(idx=int(j), E=float(E[0]), launch=tuple(int(v) for v in six), boundary=float(gap[0]))
 
 
 def eval_ratfunc(num_exp, den_exp, coef, c, e, X):

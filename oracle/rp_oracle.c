@@ -316,6 +316,64 @@ void orc_sweep(const orc_program *pr, const int *D, long long nD, const int *F, 
 }
 
 /* ------------------------------------------------------------------------------------------
+ * f2 -- one runtime decision: "there may be several configurations which, up to some margin,
+ * optimize E.  Then, a secondary performance metric or some heuristic ... may be used to
+ * refine the choice"; returns the six launch integers of the IO function
+ * "(gx, gy, gz, bx, by, bz)".  Secondary metric: occupancy W_active /
+ * W_max, then larger bx, smaller by, smaller bz (reading R28).
+ * ---------------------------------------------------------------------------------------- */
+int orc_decide(const orc_program *pr, const int *D, const int *F, int nF, double margin,
+               double *E_out, int *out6, double *boundary) {
+  ld best = INFINITY;
+  int bi = -1;
+  orc_trace *tr = (orc_trace *)malloc(sizeof(orc_trace) * (nF > 0 ? nF : 1));
+  for (int j = 0; j < nF; ++j) {
+    orc_eval_pair(pr, D, F + (long)j * pr->p, &tr[j]);
+    if (tr[j].feasible && tr[j].E < best) {
+      best = tr[j].E;
+      bi = j;
+    }
+  }
+  int choice = bi;
+  ld bgap = INFINITY;
+  if (bi >= 0 && margin > 0) {
+    const ld lim = best * (1.0L + (ld)margin);
+    for (int j = 0; j < nF; ++j) {
+      if (!tr[j].feasible) continue;
+      ld gap = fabsl(tr[j].E - lim) / best;
+      if (gap < bgap) bgap = gap;
+      if (!(tr[j].E <= lim)) continue;
+      const int *Pj = F + (long)j * pr->p, *Pc = F + (long)choice * pr->p;
+      int Pj1 = pr->p >= 2 ? Pj[1] : 1, Pc1 = pr->p >= 2 ? Pc[1] : 1;
+      int Pj2 = pr->p >= 3 ? Pj[2] : 1, Pc2 = pr->p >= 3 ? Pc[2] : 1;
+      int better;
+      if (tr[j].W_active != tr[choice].W_active) better = tr[j].W_active > tr[choice].W_active;
+      else if (Pj[0] != Pc[0]) better = Pj[0] > Pc[0];
+      else if (Pj1 != Pc1) better = Pj1 < Pc1;
+      else if (Pj2 != Pc2) better = Pj2 < Pc2;
+      else better = j < choice;
+      if (better) choice = j;
+    }
+  }
+  for (int k = 0; k < 6; ++k) out6[k] = 0;
+  if (choice >= 0) {
+    const int *Pc = F + (long)choice * pr->p;
+    for (int k = 0; k < 3; ++k) {
+      const int Pk = k < pr->p ? Pc[k] : 1;
+      const int j = k < pr->p ? pr->grid_map[k] : -1;
+      out6[k] = j >= 0 ? (int)(((long long)D[j] + Pk - 1) / Pk) : 1; /* gx = ceil[N/bx] */
+      out6[3 + k] = Pk;
+    }
+    *E_out = (double)tr[choice].E;
+  } else {
+    *E_out = INFINITY;
+  }
+  if (boundary) *boundary = (double)bgap;
+  free(tr);
+  return choice;
+}
+
+/* ------------------------------------------------------------------------------------------
  * a11 -- one row of the linearised system p(x) - V q(x) = 0: a = [M(u) | -V N(u)]
  * ("over-determined system of linear equations"; draft PAPER.md:2590-2598
  * "the sample matrix for the denominator polynomial appended to the sample matrix for the

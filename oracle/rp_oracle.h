@@ -85,6 +85,15 @@ void orc_sweep(const orc_program *prog, const int *D, long long nD, const int *F
                int *idx, double *best, double *second, double *kappa, double *margin,
                long long *counters, int nthreads);
 
+/* ---- f2: runtime decision (PAPER.md:2292-2305 step 5, 2490-2491 the six launch integers) --
+ * margin == 0: the argmin of orc_sweep.  margin > 0: among the candidates with
+ * E <= best (1 + margin) pick the one with the larger W_active (occupancy), then larger P1,
+ * smaller P2, smaller P3, lower index (SPEC.md:489's secondary metric; reading R28).
+ * out6 = (gx, gy, gz, bx, by, bz) of the choice (grid rule), zeros if none;
+ * boundary = min over candidates of |E - best (1 + margin)| / best (diagnostic).              */
+int orc_decide(const orc_program *prog, const int *D, const int *F, int nF, double margin,
+               double *E_out, int *out6, double *boundary);
+
 /* ---- a11..a14: least-squares fit ------------------------------------------------------- */
 void orc_design_row(int n, int n_num, int n_den, const short *num_exp, const short *den_exp,
                     const double *xc, const int *xe, const double *x, double v, long double *row);

@@ -36,7 +36,8 @@ def check_sweep(idx, E, S, ref, spec=None, D=None, F=None, tag=""):
     b = ref["best"][feas]
     rel = np.abs(E[feas] - b) / b
     assert rel.max(initial=0) <= 1e-12, (tag, rel.max())
-    margin = (ref["second"] - ref["best"]) / ref["best"]
+    with np.errstate(invalid="ignore"):
+        margin = (ref["second"] - ref["best"]) / ref["best"]
     strict = feas & (margin > 1e-9)
     assert np.array_equal(idx[strict], ref["idx"][strict]), tag
     # near ties: the GPU winner's oracle E must be within the tie margin of the best
@@ -198,3 +199,68 @@ def test_end_to_end_fit_then_sweep():
     idx, E, S = rp.eval_argmin(fitted, _cuda(D), _cuda(F))
     ref = oracle.sweep(fitted, D, F)
     check_sweep(idx, E, S, ref, fitted, D, F, "e2e")
+
+
+def test_determinism_bitwise():
+    """Same inputs, same launch configuration -> bit-identical outputs (no atomics in the
+    sweep's argmin, fixed-order Gram partial sums)."""
+    case = synth.polybench_sweep(nD=3000)
+    D, F = _cuda(case.D), _cuda(case.F)
+    a = rp.eval_argmin_batched(case.programs, D, F)
+    b = rp.eval_argmin_batched(case.programs, D, F)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    fc = synth.fitheavy(K=50_000)
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(fc.truths[0], fc.X)])
+    c, e = oracle.xform_from_box(*oracle.minmax(fc.X))
+    G1 = rp.gram(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp, c, e)
+    G2 = rp.gram(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp, c, e)
+    assert torch.equal(G1, G2)
+
+
+def test_sweep_without_second_and_single_tuple():
+    case = synth.large_sweep(nD=1)
+    spec = case.programs[0]
+    D = synth.large_D(4001)[3990:]
+    ref = oracle.sweep(spec, D, case.F)
+    idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(case.F), second=False)
+    assert S is None
+    check_sweep(idx, E, None, ref, spec, D, case.F, "no-second")
+    idx1, E1, _ = rp.eval_argmin(spec, _cuda(D[:1]), _cuda(case.F))
+    assert idx1.item() == idx[0].item() and E1.item() == E[0].item()
+
+
+def test_sweep_one_dimensional_blocks():
+    """p = 1 (1-D thread blocks): the D rule is P1 <= D1^2, grid gx = ceil(N / bx)."""
+    n = 2
+    basis = synth.basis_total_degree(n, 3)
+    g = synth.rng("tests", "p1")
+    coefs = [synth.classf_coefficients(g, basis, s) for s in synth.METRIC_SCALES]
+    spec = synth.ProgramSpec(d=1, p=1, num_exp=[basis] * 3, den_exp=[basis] * 3, coef=coefs,
+                             hw=dict(synth.HW_GTX1080TI), R=32, Z0=0, Z1=0, grid_map=(0, -1, -1),
+                             box_lo=[2, 1], box_hi=[4096, 1024])
+    F = np.array([[b] for b in (1, 16, 32, 48, 64, 96, 128, 256, 512, 768, 1024)], dtype=np.int32)
+    D = np.array([[2], [4], [5], [6], [10], [31], [32], [100], [1000], [4096]], dtype=np.int32)
+    ref = oracle.sweep(spec, D, F)
+    idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F))
+    check_sweep(idx, E, S, ref, spec, D, F, "p=1")
+
+
+def test_sweep_batch_of_mixed_bases():
+    """Programs of different degree (different staged shapes) in one batched launch."""
+    base = synth.polybench_sweep(nD=500)
+    p2 = synth.classf_program("mixed", 1, 3, 2, *synth.POLY_BOX, hw=synth.HW_GTX1080TI, R=64, Z0=1024, Z1=1,
+                              grid_map=(0, 0, -1))
+    progs = [base.programs[0], p2, base.programs[3]]
+    idx, E, S = rp.eval_argmin_batched(progs, _cuda(base.D), _cuda(base.F))
+    for g, spec in enumerate(progs):
+        ref = oracle.sweep(spec, base.D, base.F)
+        check_sweep(idx[g], E[g], S[g], ref, spec, base.D, base.F, f"mixed[{g}]")
+
+
+def test_unsupported_sizes_rejected():
+    b = synth.basis_total_degree(4, 5)  # 126 monomials -> n_c = 252 > 176
+    X = np.ones((10, 4))
+    with pytest.raises(rp.RPError) as ei:
+        rp.gram(_cuda(X), _cuda(np.ones((1, 10))), b, b, [0.0] * 4, [0] * 4)
+    assert ei.value.status == 5
