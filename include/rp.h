@@ -202,6 +202,39 @@ rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_
 rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible);
 rp_status rp_plan_destroy(rp_plan plan);
 
+/* ---- f2: runtime decision service ----------------------------------------------------------
+ * One decision per data tuple, as the paper's driver program makes before every kernel launch
+ * (PAPER.md:2094-2099): evaluate R over F, take the optimum (step 5) and
+ * return the six launch integers "(gx, gy, gz, bx, by, bz)" of the IO function
+ * (the paper's text has a "gx, gx" typo).  "There may be several
+ * configurations which, up to some margin, optimize E.  Then, a secondary performance metric
+ * ... may be used to refine the choice": with margin > 0 every candidate with
+ * E <= E_best (1 + margin) ties, and the tie goes to the larger W_active (occupancy, Eq. (1)),
+ * then the larger P1, the smaller P2, the smaller P3, the lower index (reading
+ * R28).  margin == 0 returns exactly the argmin of rp_plan_eval_argmin (lowest index on exact
+ * ties).  One CTA per tuple; nFc <= 8192 statically feasible configurations.
+ * D device-or-host int32 [n][d]; out device-or-host [n].                                      */
+typedef struct {
+  int32_t idx;          /* chosen configuration (index in F); -1 if none is feasible          */
+  int32_t from_history; /* 1 if served by the runtime history                                  */
+  double E;             /* its estimate (+inf if none)                                         */
+  int32_t launch[6];    /* gx, gy, gz, bx, by, bz (grid rule gx = ceil(D/P), 1 for unmapped
+                           dimensions); zeros if none                                          */
+  int32_t pad[2];
+} rp_decision;
+
+rp_status rp_plan_decide(rp_plan plan, int32_t prog, const int32_t *D, int64_t n, double margin,
+                         rp_decision *out, rp_stream s);
+
+/* Runtime history ("maintaining a runtime history to instantly provide results for future kernel
+ * launches"): a device-resident open-addressing hash table D -> decision,
+ * owned by the plan, 2^log2_capacity slots (4..24), for one program of the plan and one
+ * margin; rp_plan_decide then probes it first and inserts its fresh decisions (a full table
+ * keeps serving hits and computes the rest).  Enabling twice clears it.                       */
+rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capacity, double margin);
+rp_status rp_plan_history_stats(rp_plan plan, int64_t *hits, int64_t *misses, int64_t *entries);
+rp_status rp_plan_history_clear(rp_plan plan, rp_stream s);
+
 #ifdef __cplusplus
 }
 #endif

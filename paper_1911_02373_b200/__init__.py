@@ -61,6 +61,16 @@ class rp_program(C.Structure):
                 ("smem_words_per_thread", C.c_int64)]
 
 
+class rp_decision(C.Structure):
+    _fields_ = [("idx", C.c_int32), ("from_history", C.c_int32), ("E", C.c_double),
+                ("launch", C.c_int32 * 6), ("pad", C.c_int32 * 2)]
+
+
+DECISION_DTYPE = np.dtype([("idx", np.int32), ("from_history", np.int32), ("E", np.float64),
+                           ("launch", np.int32, (6,)), ("pad", np.int32, (2,))])
+assert DECISION_DTYPE.itemsize == C.sizeof(rp_decision) == 48
+
+
 class rp_fit_info(C.Structure):
     _fields_ = [("rank", C.c_int32), ("status", C.c_int32), ("resid2", C.c_double),
                 ("min_pivot", C.c_double), ("cond_est", C.c_double)]
@@ -83,6 +93,10 @@ _SIGS = {
     "rp_plan_eval_argmin": [_vp, _vp, _i64, _vp, _vp, _vp, _vp],
     "rp_plan_static_feasible": [_vp, _i32, C.POINTER(_i32)],
     "rp_plan_destroy": [_vp],
+    "rp_plan_decide": [_vp, _i32, _vp, _i64, C.c_double, _vp, _vp],
+    "rp_plan_history_enable": [_vp, _i32, _i32, C.c_double],
+    "rp_plan_history_stats": [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)],
+    "rp_plan_history_clear": [_vp, _vp],
 }
 for _name, _args in _SIGS.items():
     getattr(_lib, _name).argtypes = _args
@@ -301,6 +315,33 @@ class Plan:
                                         _ptr(S) if S is not None else None, s))
         return idx, E, S
 
+    # ---- f2: runtime decisions -------------------------------------------------------------
+    def decide(self, D, prog: int = 0, margin: float = 0.0, out=None):
+        """One decision per data tuple (rp_plan_decide): a numpy structured array of
+        DECISION_DTYPE (idx, from_history, E, launch = (gx, gy, gz, bx, by, bz)) for host D,
+        or a uint8 device tensor [n][48] for device D / out."""
+        D = _contig(D, np.int32)
+        n = D.shape[0] if D.ndim > 1 else len(D) // self.d
+        if out is None:
+            torch = _torch()
+            if isinstance(D, torch.Tensor) and D.is_cuda:
+                out = torch.empty((n, 48), dtype=torch.uint8, device=D.device)
+            else:
+                out = np.zeros(n, dtype=DECISION_DTYPE)
+        _check(_lib.rp_plan_decide(self.handle, prog, _ptr(D), n, float(margin), _ptr(out), _stream_of(D, out)))
+        return out
+
+    def enable_history(self, prog: int = 0, log2_capacity: int = 16, margin: float = 0.0):
+        _check(_lib.rp_plan_history_enable(self.handle, prog, log2_capacity, float(margin)))
+
+    def history_stats(self) -> dict:
+        h, m, e = _i64(), _i64(), _i64()
+        _check(_lib.rp_plan_history_stats(self.handle, C.byref(h), C.byref(m), C.byref(e)))
+        return {"hits": h.value, "misses": m.value, "entries": e.value}
+
+    def clear_history(self):
+        _check(_lib.rp_plan_history_clear(self.handle, C.c_void_p(0)))
+
     def close(self):
         if self.handle:
             _lib.rp_plan_destroy(self.handle)
@@ -383,3 +424,57 @@ def fit(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
         _check(st)
     n = b.num.shape[1]
     return coef, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)
+
+
+def decisions_from_device(out) -> np.ndarray:
+    """A uint8 [n][48] device tensor of rp_decision records as a DECISION_DTYPE array."""
+    return np.frombuffer(out.cpu().numpy().tobytes(), dtype=DECISION_DTYPE)
+
+
+class DecisionService:
+    """The single-launch latency path of NEXT row f2: one rp_plan_decide on pre-allocated device
+    buffers, captured with the pinned host <-> device copies in one CUDA graph, replayed per
+    kernel launch of the user's program (the rational program runs
+    "immediately preceding the launch of a kernel")."""
+
+    def __init__(self, plan: "Plan", prog: int = 0, margin: float = 0.0, history_log2: int | None = 16,
+                 host_memo: int = 1 << 16):
+        torch = _torch()
+        self.plan, self.prog, self.margin = plan, prog, margin
+        self.memo = {} if host_memo else None
+        self.memo_cap = host_memo
+        if history_log2:
+            plan.enable_history(prog, history_log2, margin)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.D_host = torch.zeros((1, plan.d), dtype=torch.int32).pin_memory()
+        self.out_host = torch.zeros((1, 48), dtype=torch.uint8).pin_memory()
+        self.D_dev = torch.zeros((1, plan.d), dtype=torch.int32, device=dev)
+        self.out_dev = torch.zeros((1, 48), dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.Stream(dev)
+        # warm up (kernel attributes, modules) outside the capture
+        with torch.cuda.stream(self.stream):
+            plan.decide(self.D_dev, prog, margin, out=self.out_dev)
+        self.stream.synchronize()
+        if history_log2:
+            plan.clear_history()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream, capture_error_mode="thread_local"):
+            self.D_dev.copy_(self.D_host, non_blocking=True)
+            plan.decide(self.D_dev, prog, margin, out=self.out_dev)
+            self.out_host.copy_(self.out_dev, non_blocking=True)
+        self.stream.synchronize()
+
+    def __call__(self, D) -> np.void:
+        torch = _torch()
+        key = tuple(int(v) for v in np.asarray(D).ravel()[: self.plan.d])
+        hit = self.memo.get(key) if self.memo is not None else None
+        if hit is not None:  # host memo in front of the device history: no GPU round trip
+            return hit
+        self.D_host.numpy()[0, :] = key
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+        self.stream.synchronize()
+        r = np.frombuffer(self.out_host.numpy().tobytes(), dtype=DECISION_DTYPE)[0].copy()
+        if self.memo is not None and len(self.memo) < self.memo_cap:
+            self.memo[key] = r
+        return r

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "rp_internal.cuh"
+#include "rp_decide.cuh"
 
 namespace rp {
 
@@ -301,6 +302,7 @@ struct rp_plan_s {
   double *buf_d = nullptr;
   CfgTable tab{};
   cudaStream_t stream = nullptr;
+  HistTable hist;
 };
 
 static void plan_free(rp_plan pl) {
@@ -309,6 +311,11 @@ static void plan_free(rp_plan pl) {
   if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
   if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
   if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
+  if (pl->hist.slots) {
+    cudaStreamSynchronize(pl->stream);
+    cudaFree(pl->hist.slots);
+    cudaFree(pl->hist.counters);
+  }
   delete pl;
 }
 
@@ -655,6 +662,80 @@ rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_
   RP_CUDA(cudaStreamSynchronize(plan->stream));
   RP_CUDA(cudaMemcpy(&v, plan->tab.nFc + 2 * prog, 4, cudaMemcpyDeviceToHost));
   *n_static_feasible = v;
+  return RP_OK;
+}
+
+rp_status rp_plan_decide(rp_plan plan, int32_t prog, const int32_t *D, int64_t n, double margin,
+                         rp_decision *out, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
+  RP_REQUIRE(prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "prog %d out of range", prog);
+  RP_REQUIRE(n >= 0 && margin >= 0.0, RP_ERR_INVALID_ARG, "n < 0 or margin < 0 / NaN");
+  RP_REQUIRE(plan->nF <= kDecideMaxF, RP_ERR_UNSUPPORTED, "decide: nF = %d > %d", plan->nF, kDecideMaxF);
+  if (plan->hist.enabled)
+    RP_REQUIRE(plan->hist.prog == prog && plan->hist.margin == margin, RP_ERR_INVALID_ARG,
+               "the runtime history was enabled for program %d, margin %g", plan->hist.prog, plan->hist.margin);
+  if (n == 0) return RP_OK;
+  RP_REQUIRE(D && out, RP_ERR_INVALID_ARG, "null D / out");
+  plan->stream = s;
+  Tmp tD, to;
+  const int32_t *dD;
+  rp_decision *dout;
+  bool ho;
+  rp_status st = stage_in(D, (size_t)n * plan->d, tD, &dD, s);
+  if (st != RP_OK) return st;
+  if ((st = stage_out(out, (size_t)n, to, &dout, &ho, s)) != RP_OK) return st;
+  DecideArgs a{plan->d_progs, plan->tab, plan->npe_pad, prog, dD, n, margin, dout, plan->hist};
+  RP_CUDA(launch_decide(a, plan->mwp, s));
+  if (ho) {
+    RP_CUDA(cudaMemcpyAsync(out, dout, (size_t)n * sizeof(rp_decision), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+  return RP_OK;
+}
+
+rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capacity, double margin) {
+  RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
+  RP_REQUIRE(prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "prog %d out of range", prog);
+  RP_REQUIRE(log2_capacity >= 4 && log2_capacity <= 24 && margin >= 0.0, RP_ERR_INVALID_ARG,
+             "log2_capacity in [4, 24], margin >= 0");
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  if (plan->hist.slots) {
+    cudaFree(plan->hist.slots);
+    cudaFree(plan->hist.counters);
+    plan->hist = HistTable();
+  }
+  const size_t cap = (size_t)1 << log2_capacity;
+  RP_CUDA(cudaMalloc((void **)&plan->hist.slots, cap * sizeof(HistSlot)));
+  RP_CUDA(cudaMalloc((void **)&plan->hist.counters, 3 * sizeof(unsigned long long)));
+  RP_CUDA(cudaMemset(plan->hist.slots, 0, cap * sizeof(HistSlot)));
+  RP_CUDA(cudaMemset(plan->hist.counters, 0, 3 * sizeof(unsigned long long)));
+  plan->hist.mask = (uint32_t)(cap - 1);
+  plan->hist.enabled = 1;
+  plan->hist.prog = prog;
+  plan->hist.margin = margin;
+  return RP_OK;
+}
+
+rp_status rp_plan_history_stats(rp_plan plan, int64_t *hits, int64_t *misses, int64_t *entries) {
+  RP_REQUIRE(plan && hits && misses && entries, RP_ERR_INVALID_ARG, "null argument");
+  *hits = *misses = *entries = 0;
+  if (!plan->hist.enabled) return RP_OK;
+  unsigned long long c[3];
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  RP_CUDA(cudaMemcpy(c, plan->hist.counters, sizeof c, cudaMemcpyDeviceToHost));
+  *hits = (int64_t)c[0];
+  *misses = (int64_t)c[1];
+  *entries = (int64_t)c[2];
+  return RP_OK;
+}
+
+rp_status rp_plan_history_clear(rp_plan plan, rp_stream sv) {
+  RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
+  if (!plan->hist.enabled) return RP_OK;
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_CUDA(cudaMemsetAsync(plan->hist.slots, 0, ((size_t)plan->hist.mask + 1) * sizeof(HistSlot), s));
+  RP_CUDA(cudaMemsetAsync(plan->hist.counters, 0, 3 * sizeof(unsigned long long), s));
   return RP_OK;
 }
 

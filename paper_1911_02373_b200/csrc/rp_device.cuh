@@ -1,0 +1,114 @@
+// rp_device.cuh -- device helpers shared by the sweep and the decision kernels.
+#pragma once
+
+#include "rp_internal.cuh"
+
+namespace rp {
+
+// ---- argmin state: exact lexicographic (E, index) with the runner-up E ----------------------
+struct Best {
+  double e;   // best E (+inf: none)
+  int32_t i;  // its original config index (INT_MAX: none)
+  double s;   // second-smallest E among the others
+};
+__device__ __forceinline__ bool key_less(double e1, int32_t i1, double e2, int32_t i2) {
+  return e1 < e2 || (e1 == e2 && i1 < i2);
+}
+__device__ __forceinline__ Best merge(const Best &a, const Best &b) {
+  Best r;
+  if (key_less(a.e, a.i, b.e, b.i)) {
+    r.e = a.e;
+    r.i = a.i;
+    r.s = fmin(a.s, b.e);
+  } else {
+    r.e = b.e;
+    r.i = b.i;
+    r.s = fmin(b.s, a.e);
+  }
+  return r;
+}
+__device__ __forceinline__ Best shfl_xor(const Best &a, int m) {
+  Best r;
+  r.e = __shfl_xor_sync(0xffffffffu, a.e, m);
+  r.i = __shfl_xor_sync(0xffffffffu, a.i, m);
+  r.s = __shfl_xor_sync(0xffffffffu, a.s, m);
+  return r;
+}
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 1/x: MUFU.RCP64H seed + two Newton steps (relative error ~1 ulp; 0 and +-inf give NaN,
+// which the final finiteness test masks, as the literal program's x/0 would).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// exact ceil(D / P) = floor((D + P - 1) / P) for 1 <= D + P - 1 < 2^31 via the per-config
+// multiply-shift (M, s) of k_plan_configs
+__device__ __forceinline__ int64_t ceil_div_magic(int32_t D, int32_t Pm1, uint32_t M, uint32_t s) {
+  const uint64_t n = (uint64_t)(uint32_t)(D + Pm1);
+  return (int64_t)((n * (uint64_t)M) >> s);
+}
+
+// E for one (D, P) pair from its 2l polynomial values (Appendix A in
+// common-denominator form g_i = a_i / Q; every division is a Newton reciprocal).  Straight-line
+// code: masked pairs are carried to the end and returned as +inf.
+struct EConst {
+  double Lunc, Lcoal, DdU, ddc, issue, Kbw, rKbw;
+};
+// per-program constants of Appendix A, folded once (lines 7, 9, 11, 13)
+__device__ __forceinline__ EConst make_econst(const DevProg &pg) {
+  EConst kc;
+  kc.Lunc = pg.mem_ld + (pg.U - 1.0) * pg.dd_unc;  // line 7
+  kc.Lcoal = pg.mem_ld;
+  kc.DdU = pg.dd_unc * pg.U;  // line 9
+  kc.ddc = pg.dd_coal;
+  kc.issue = pg.issue;                       // line 13
+  kc.Kbw = pg.mem_bw / (pg.freq * pg.lbpw);  // line 11: Mem_BW / (Freq LoadBytesPerWarp)
+  kc.rKbw = (pg.freq * pg.lbpw) / pg.mem_bw;
+  return kc;
+}
+
+__device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, double q2, double p3,
+                                           double q3, double W, double Rep, double rSM,
+                                           double SMact, const EConst &k) {
+  const double q23 = q2 * q3, q13 = q1 * q3, q12 = q1 * q2;
+  const double Q = q1 * q23;
+  const double a1 = p1 * q23, a2 = p2 * q13, a3 = p3 * q12;  // g_i = a_i / Q
+  const double s23 = a2 + a3;                                 // Mem Q          (line 5)
+  const double s = a1 + s23;                                  // Tot Q          (line 5)
+  const double mc = fma(k.Lunc, a3, k.Lcoal * a2);            // Mem_c Q        (line 13)
+  const double dn = fma(k.DdU, a3, k.ddc * a2);               // Dep Mem Q      (lines 6, 9)
+  const double cc = k.issue * s;                              // Comp_c Q       (line 13)
+  const double rQ = frcp(Q), r23 = frcp(s23);
+  const double Mem_c = mc * rQ, Comp_c = cc * rQ;
+  const double MWP_nb = mc * frcp(dn);         // line 10: Mem_L / Dep
+  const double MWP_bw = k.Kbw * mc * r23 * rSM;  // line 11: Mem_BW / (BW_per_warp SM_act)
+  const double CWPf = 1.0 + mc * frcp(cc);     // line 14: (Mem_c + Comp_c) / Comp_c
+  double mwp = MWP_nb;                         // line 12
+  mwp = MWP_bw < mwp ? MWP_bw : mwp;
+  mwp = W < mwp ? W : mwp;
+  const double cwp = CWPf < W ? CWPf : W;  // line 14
+  const double cpm = cc * r23;             // Comp_c / Mem
+  const double tail = cpm * (mwp - 1.0);
+  // Mem_c W / MWP for each operand of the min: W / W = 1; Mem_c / MWP_nb = Dep Mem = dn / Q;
+  // Mem_c / MWP_bw = Mem SM_act / K_bw = s23 SM_act / (Q K_bw)
+  const double mcw = (mwp == W) ? Mem_c : W * rQ * ((mwp == MWP_nb) ? dn : s23 * SMact * k.rKbw);
+  const double E1 = Mem_c + Comp_c + tail;         // line 16
+  const double E2 = mcw + tail;                    // line 17
+  const double E3 = mc * r23 + Comp_c * W;         // line 18 (Mem_L = Mem_c / Mem)
+  const bool c1 = (mwp == W) && (cwp == W);
+  const bool c2 = (cwp >= mwp) || (Comp_c > Mem_c);
+  return (c1 ? E1 : (c2 ? E2 : E3)) * Rep;
+}
+
+}  // namespace rp

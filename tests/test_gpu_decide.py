@@ -1,0 +1,110 @@
+"""Parity of the runtime decision service (NEXT row f2, rp_plan_decide) with the oracle's
+orc_decide, and the runtime history."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1911_02373_b200 as rp  # noqa: E402
+from helpers import golden, ratfunc_program  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def test_spec_decision_example_on_gpu():
+    ex, grid_ex = golden("spec_worked.json")["decision"]
+    F = synth.F_pow2_2d()
+    spec = ratfunc_program(synth.HW_GTX1080TI, [[2, 0, 0]], [[0, 1, 1]], [1.0, 1.0], d=1, p=2, R=16)
+    plan = rp.Plan([spec], _cuda(F))
+    r = plan.decide(np.array([[ex["N"]]], dtype=np.int32), margin=1e-9)[0]
+    assert tuple(F[r["idx"]]) == tuple(ex["block"]) and tuple(r["launch"]) == tuple(ex["launch"])
+    assert r["E"] == 4.0 and r["from_history"] == 0
+    plan1 = rp.Plan([spec], _cuda(np.array([grid_ex["block"]], dtype=np.int32)))
+    r = plan1.decide(np.array([[grid_ex["N"]]], dtype=np.int32))[0]
+    assert tuple(r["launch"][:3]) == tuple(grid_ex["grid"])
+
+
+@pytest.mark.parametrize("which", ["tiny", "polybench", "multikernel"])
+def test_decide_parity(which):
+    case = {"tiny": synth.tiny_sweep, "polybench": lambda: synth.polybench_sweep(nD=150),
+            "multikernel": lambda: synth.multikernel_sweep(nD=60)}[which]()
+    D = np.concatenate([synth.random_D_edge_cases(1), case.D])
+    plan = rp.Plan(case.programs, _cuda(case.F))
+    checked = 0
+    for g, spec in enumerate(case.programs[:4]):
+        ref_sweep = oracle.sweep(spec, D, case.F)
+        for margin in (0.0, 0.05, 1e300):
+            got = plan.decide(D, prog=g, margin=margin)
+            for i, d in enumerate(D):
+                ref = oracle.decide(spec, d, case.F, margin=margin)
+                if ref["idx"] < 0:
+                    assert got[i]["idx"] == -1 and np.isinf(got[i]["E"]) and tuple(got[i]["launch"]) == (0,) * 6
+                    continue
+                if margin == 0.0:
+                    gap = (ref_sweep["second"][i] - ref_sweep["best"][i]) / ref_sweep["best"][i]
+                    if not gap > 1e-9:
+                        continue  # near tie (reading R20)
+                elif not ref["boundary"] > 1e-10:
+                    continue  # a candidate within rounding of the margin boundary (reading R28)
+                assert got[i]["idx"] == ref["idx"], (which, g, margin, i)
+                assert tuple(got[i]["launch"]) == ref["launch"]
+                assert abs(got[i]["E"] - ref["E"]) <= 1e-12 * ref["E"]
+                checked += 1
+    assert checked > 0.9 * len(D) * min(4, len(case.programs)) * 3 * 0.6
+
+
+def test_decide_matches_sweep_at_margin_zero():
+    case = synth.large_sweep(nD=1)
+    D = synth.large_D(3000)
+    plan = rp.Plan(case.programs, _cuda(case.F))
+    idx, E, S = plan.eval(_cuda(D))
+    dec = rp.decisions_from_device(plan.decide(_cuda(D)))
+    idx, E, S = idx[0].cpu().numpy(), E[0].cpu().numpy(), S[0].cpu().numpy()
+    strict = (S - E) / E > 1e-9
+    assert np.array_equal(dec["idx"][strict], idx[strict])
+    assert np.max(np.abs(dec["E"][strict] - E[strict]) / E[strict]) <= 1e-13
+
+
+def test_runtime_history():
+    case = synth.polybench_sweep(nD=64)
+    D = np.concatenate([case.D, case.D[:16]])  # 16 repeated tuples in the batch
+    plan = rp.Plan(case.programs, _cuda(case.F))
+    fresh = plan.decide(D, prog=2, margin=0.02)
+    plan.enable_history(prog=2, log2_capacity=10, margin=0.02)
+    first = plan.decide(D, prog=2, margin=0.02)
+    st = plan.history_stats()
+    assert st["hits"] + st["misses"] == len(D) and st["entries"] == len(np.unique(case.D))
+    again = plan.decide(D, prog=2, margin=0.02)
+    assert np.all(again["from_history"] == 1)
+    for f in ("idx", "E", "launch"):
+        assert np.array_equal(again[f], first[f]) and np.array_equal(first[f], fresh[f])
+    assert plan.history_stats()["hits"] == st["hits"] + len(D)
+    with pytest.raises(rp.RPError):
+        plan.decide(D, prog=1, margin=0.02)  # the history belongs to program 2
+    plan.clear_history()
+    assert plan.history_stats() == {"hits": 0, "misses": 0, "entries": 0}
+    assert np.all(plan.decide(D[:5], prog=2, margin=0.02)["from_history"] == 0)
+
+
+def test_decision_service_graph():
+    case = synth.polybench_sweep(nD=40)
+    plan = rp.Plan(case.programs[:1], _cuda(case.F))
+    ref = plan.decide(case.D, prog=0, margin=0.01)
+    svc = rp.DecisionService(plan, prog=0, margin=0.01, history_log2=12)
+    for i in range(len(case.D)):
+        r = svc(case.D[i])
+        assert r["idx"] == ref[i]["idx"] and r["E"] == ref[i]["E"]
+        assert tuple(r["launch"]) == tuple(ref[i]["launch"])
+    r = svc(case.D[3])
+    assert r["from_history"] == 1 and r["idx"] == ref[3]["idx"]
