@@ -83,6 +83,8 @@ def lib():
             L.orc_gram.argtypes = [vp, vp, ll, i, i, i, vp, vp, vp, vp, vp, i]
             L.orc_solve.argtypes = [vp, i, i, vp, vp, vp]
             L.orc_solve.restype = i
+            L.orc_fit_sk.argtypes = [vp, vp, ll, i, i, i, vp, vp, i, vp, vp, vp, i]
+            L.orc_fit_sk.restype = i
             _LIB = L
         return _LIB
 
@@ -299,3 +301,18 @@ def fit(X, V, num_exp, den_exp, nthreads: int = 1, xform=None):
     s = solve(G, len(num_exp))
     s.update(c=c, e=e, G=G)
     return s
+
+
+def fit_sk(X, V, num_exp, den_exp, iters: int = 3, nthreads: int = 1):
+    """Sanathanan-Koerner refit (NEXT row f4): `iters` weighted solves, weights 1/q_prev(x)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    K, n = X.shape
+    ne = np.ascontiguousarray(num_exp, dtype=np.int16)
+    de = np.ascontiguousarray(den_exp, dtype=np.int16)
+    coef = np.zeros(len(ne) + len(de), dtype=LD)
+    c = np.zeros(n)
+    e = np.zeros(n, dtype=np.int32)
+    st = lib().orc_fit_sk(_p(X), _p(V), K, n, len(ne), len(de), _p(ne), _p(de), iters, _p(coef), _p(c), _p(e),
+                          nthreads)
+    return dict(coef=coef, c=c, e=e, status=int(st))

@@ -494,3 +494,50 @@ int orc_solve(const long double *G, int nc, int beta0, long double *coef, long d
   free(col);
   return status;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * f4 -- Sanathanan-Koerner iteration (reading R29): the linearised residual p - V q of
+ * PAPER.md:2578-2584 weighs each row by q(x_r); dividing by the previous q_{t-1}(x_r) makes the
+ * minimised quantity approach sum_r (p/q - V)^2, the error of the fitted value itself.
+ * ---------------------------------------------------------------------------------------- */
+int orc_fit_sk(const double *X, const double *V, long long K, int n, int n_num, int n_den,
+               const short *num_exp, const short *den_exp, int iters, long double *coef,
+               double *c, int *e, int nthreads) {
+  const int nc = n_num + n_den;
+  double lo[ORC_MAX_VARS], hi[ORC_MAX_VARS];
+  orc_minmax(X, K, n, lo, hi);
+  orc_xform_from_box(n, lo, hi, c, e);
+  ld *G = (ld *)calloc((size_t)nc * nc, sizeof(ld));
+  ld *row = (ld *)malloc(sizeof(ld) * nc);
+  ld *s = (ld *)malloc(sizeof(ld) * (K > 0 ? K : 1));
+  int status = 0;
+  for (int t = 0; t < iters; ++t) {
+    if (t == 0) {
+      orc_gram(X, V, K, n, n_num, n_den, num_exp, den_exp, c, e, G, nthreads);
+    } else {
+      /* s_r = 1 / q_{t-1}(x_r) with the previous coefficients (denominator block) */
+      ld u[ORC_MAX_VARS];
+      for (long long r = 0; r < K; ++r) {
+        for (int k = 0; k < n; ++k) u[k] = to_u(X[r * n + k], c[k], e[k]);
+        ld q = 0;
+        for (int j = 0; j < n_den; ++j) q += coef[n_num + j] * monomial(den_exp + (long)j * n, n, u);
+        s[r] = 1.0L / q;
+      }
+      memset(G, 0, sizeof(ld) * (size_t)nc * nc);
+      for (long long r = 0; r < K; ++r) {
+        orc_design_row(n, n_num, n_den, num_exp, den_exp, c, e, X + r * n, V[r], row);
+        for (int i = 0; i < nc; ++i) row[i] *= s[r];
+        for (int i = 0; i < nc; ++i)
+          for (int j = i; j < nc; ++j) G[(size_t)i * nc + j] += row[i] * row[j];
+      }
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < i; ++j) G[(size_t)i * nc + j] = G[(size_t)j * nc + i];
+    }
+    status = orc_solve(G, nc, n_num, coef, NULL, NULL);
+    if (status != 0) break;
+  }
+  free(G);
+  free(row);
+  free(s);
+  return status;
+}

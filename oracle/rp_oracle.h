@@ -107,6 +107,15 @@ void orc_gram(const double *X, const double *V, long long K, int n, int n_num, i
 int orc_solve(const long double *G, int n_c, int beta0, long double *coef, long double *resid2,
               long double *min_pivot);
 
+/* ---- f4: Sanathanan-Koerner reweighted refit ----------------------------------------------
+ * iters >= 1 solves; solve 1 is orc_gram + orc_solve; solve t > 1 weights row r by
+ * s_r = 1 / q_{t-1}(x_r) (q of the previous solve, long double), i.e. minimises
+ * sum_r ((p(x_r) - V_r q(x_r)) / q_{t-1}(x_r))^2 (reading R29).  The transform comes from the
+ * sample box.  Returns the status of the last solve; coef[n_c], c[n], e[n] out.             */
+int orc_fit_sk(const double *X, const double *V, long long K, int n, int n_num, int n_den,
+               const short *num_exp, const short *den_exp, int iters, long double *coef,
+               double *c, int *e, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif
