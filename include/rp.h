@@ -159,6 +159,20 @@ rp_status rp_solve_normal(const double *G, int32_t n_v, const rp_basis *basis, d
 rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
                  double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream s);
 
+/* ---- f4: Sanathanan-Koerner reweighted refit ---------------------------------------------------
+ * The linearised rows p(x) - V q(x) of PAPER.md:2578-2584 weigh each sample by q(x), which biases
+ * noisy fits.  rp_gram_accumulate_weighted is rp_gram_accumulate with every
+ * design row of metric m scaled by S[m][r] (device-or-host float64 [n_v][K]); rp_fit_sk runs
+ * `iters` solves: the first is rp_fit, each later one refits with S[m][r] = 1 / q_m(x_r) of the
+ * previous solution (reading R29), i.e. minimises sum_r ((p - V q) / q_prev)^2 -> sum (p/q - V)^2.
+ * Same layouts, ownership and errors as rp_gram_accumulate / rp_fit.                          */
+rp_status rp_gram_accumulate_weighted(const double *X, const double *V, const double *S, int64_t K,
+                                      int32_t n_v, const rp_basis *basis, const rp_xform *xform,
+                                      double *G, rp_stream s);
+rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                    int32_t iters, double *coef_out, rp_xform *xform_out, rp_fit_info *info,
+                    rp_stream s);
+
 /* ---- a4 alone: fitted metrics at points ----------------------------------------------------
  * out[i][r] = g_i(X_r) = p_i(u_r)/q_i(u_r) for i < prog->n_metrics (device-or-host float64
  * [n_metrics][K]); X device-or-host float64 [K][d+p].                                      */

@@ -86,6 +86,8 @@ _SIGS = {
     "rp_gram_accumulate": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
     "rp_solve_normal": [_vp, _i32, C.POINTER(rp_basis), _vp, _vp, _vp],
     "rp_fit": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, C.POINTER(rp_xform), _vp, _vp],
+    "rp_gram_accumulate_weighted": [_vp, _vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
+    "rp_fit_sk": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _i32, _vp, C.POINTER(rp_xform), _vp, _vp],
     "rp_eval_metrics": [C.POINTER(rp_program), _vp, _i64, _vp, _vp],
     "rp_eval_argmin": [C.POINTER(rp_program), _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
     "rp_eval_argmin_batched": [_vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
@@ -388,6 +390,39 @@ def gram(X, V, num_exp, den_exp, c, e, out=None):
     G = out if out is not None else _empty_like_family(X, (n_v, b.n_c, b.n_c), np.float64)
     _check(_lib.rp_gram_accumulate(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), C.byref(xf), _ptr(G), _stream_of(X, V, G)))
     return G
+
+
+def gram_weighted(X, V, S, num_exp, den_exp, c, e, out=None):
+    """rp_gram_accumulate_weighted: every design row of metric m scaled by S[m][r]."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    S = _contig(S, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    xf = _xform_struct(c, e)
+    G = out if out is not None else _empty_like_family(X, (n_v, b.n_c, b.n_c), np.float64)
+    _check(_lib.rp_gram_accumulate_weighted(_ptr(X), _ptr(V), _ptr(S), K, n_v, C.byref(b.c), C.byref(xf), _ptr(G),
+                                            _stream_of(X, V, G)))
+    return G
+
+
+def fit_sk(X, V, num_exp, den_exp, iters: int = 3, raise_on_degenerate: bool = True):
+    """rp_fit_sk: Sanathanan-Koerner refit (NEXT row f4); returns like fit()."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    coef = np.zeros((n_v, b.n_c))
+    xf = rp_xform()
+    infos = (rp_fit_info * n_v)()
+    st = _lib.rp_fit_sk(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), iters, _ptr(coef), C.byref(xf), C.cast(infos, _vp),
+                        _stream_of(X, V))
+    if st != 0 and (st != 3 or raise_on_degenerate):
+        _check(st)
+    n = b.num.shape[1]
+    return coef, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)
 
 
 def _infos(infos):

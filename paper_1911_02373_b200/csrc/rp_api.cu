@@ -490,9 +490,8 @@ rp_status rp_minmax(const double *X, int64_t K, int32_t n, double *lo, double *h
   return RP_OK;
 }
 
-rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
-                             const rp_basis *basis, const rp_xform *xform, double *G, rp_stream sv) {
-  cudaStream_t s = (cudaStream_t)sv;
+static rp_status gram_impl(const double *X, const double *V, const double *S, int64_t K, int32_t n_v,
+                           const rp_basis *basis, const rp_xform *xform, double *G, cudaStream_t s) {
   RP_REQUIRE(G && basis && xform, RP_ERR_INVALID_ARG, "null argument");
   RP_REQUIRE(K >= 0 && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "K = %lld, n_v = %d", (long long)K, n_v);
   RP_REQUIRE(K == 0 || (X && V), RP_ERR_INVALID_ARG, "null X / V");
@@ -507,15 +506,18 @@ rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_
   bool hG;
   if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
   if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  Tmp tS;
+  const double *dS = nullptr;
+  if (S && (st = stage_in(S, (size_t)K * n_v, tS, &dS, s)) != RP_OK) return st;
   if ((st = stage_out(G, (size_t)n_v * nc * nc, tG, &dG, &hG, s)) != RP_OK) return st;
   if (K == 0) {
     RP_CUDA(cudaMemsetAsync(dG, 0, (size_t)n_v * nc * nc * 8, s));
   } else {
     RP_CUDA(tb.alloc(sizeof(GramBasis), s));
     RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
-    const size_t pe = gram_partial_elems(gb, n_v, K, num_sms());
+    const size_t pe = gram_partial_elems(gb, n_v, K, num_sms(), dS != nullptr);
     RP_CUDA(tp.alloc(pe * 8, s));
-    RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, K, n_v, dG, (double *)tp.p, pe, s));
+    RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, dS, K, n_v, dG, (double *)tp.p, pe, s));
   }
   // (host sources of H2D copies from pageable memory are consumed before cudaMemcpyAsync
   // returns, so stack-resident staging data needs no synchronisation)
@@ -524,6 +526,18 @@ rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_
     RP_CUDA(cudaStreamSynchronize(s));
   }
   return RP_OK;
+}
+
+rp_status rp_gram_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
+                             const rp_basis *basis, const rp_xform *xform, double *G, rp_stream sv) {
+  return gram_impl(X, V, nullptr, K, n_v, basis, xform, G, (cudaStream_t)sv);
+}
+
+rp_status rp_gram_accumulate_weighted(const double *X, const double *V, const double *S, int64_t K,
+                                      int32_t n_v, const rp_basis *basis, const rp_xform *xform,
+                                      double *G, rp_stream sv) {
+  RP_REQUIRE(S || K == 0, RP_ERR_INVALID_ARG, "null row scales");
+  return gram_impl(X, V, S, K, n_v, basis, xform, G, (cudaStream_t)sv);
 }
 
 static rp_status solve_impl(const double *dG, int32_t n_v, int nc, int beta0, double *coef_out,
@@ -595,9 +609,9 @@ rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const
   RP_CUDA(tb.alloc(sizeof(GramBasis), s));
   RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
   RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
-  const size_t pe = gram_partial_elems(gb, n_v, K, num_sms());
+  const size_t pe = gram_partial_elems(gb, n_v, K, num_sms(), false);
   RP_CUDA(tp.alloc(pe * 8, s));
-  RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, K, n_v, (double *)tG.p, (double *)tp.p, pe, s));
+  RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, nullptr, K, n_v, (double *)tG.p, (double *)tp.p, pe, s));
   rp_status sst = solve_impl((const double *)tG.p, n_v, nc, basis->n_num, coef_out, info, s);  // synchronises
   double hxf[2 * RP_MAX_VARS];
   RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -610,6 +624,73 @@ rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const
     }
   }
   return sst;
+}
+
+rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                    int32_t iters, double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(X && V && basis && coef_out, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 1 && n_v >= 1 && n_v <= 64 && iters >= 1 && iters <= 64, RP_ERR_INVALID_ARG,
+             "K = %lld, n_v = %d, iters = %d", (long long)K, n_v, iters);
+  rp_status st = check_basis(*basis, basis->n_vars, "fit", true);
+  if (st != RP_OK) return st;
+  const int n = basis->n_vars, nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc <= 161, RP_ERR_UNSUPPORTED, "fit: n_c = %d > 161", nc);
+  if ((st = ensure_device()) != RP_OK) return st;
+  Tmp tX, tV, tw, tG, tb, tp, tS, tc;
+  const double *dX, *dV;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  const int nblk = minmax_blocks(K);
+  RP_CUDA(tw.alloc(((size_t)nblk * n * 2 + 4 * RP_MAX_VARS) * sizeof(double), s));
+  double *part = (double *)tw.p, *lohi = part + (size_t)nblk * n * 2, *xf = lohi + 2 * RP_MAX_VARS;
+  RP_CUDA(launch_minmax(dX, K, n, part, nblk, lohi, s));
+  RP_CUDA(launch_xform(lohi, n, xf, s));
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, nullptr, &gb)) != RP_OK) return st;
+  RP_CUDA(tG.alloc((size_t)n_v * nc * nc * 8, s));
+  RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+  RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+  RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
+  const size_t pe = std::max(gram_partial_elems(gb, n_v, K, num_sms(), false),
+                             gram_partial_elems(gb, n_v, K, num_sms(), true));
+  RP_CUDA(tp.alloc(pe * 8, s));
+  RP_CUDA(tS.alloc((size_t)n_v * K * 8, s));
+  RP_CUDA(tc.alloc((size_t)n_v * (nc + 5) * 8, s));
+  double *dc = (double *)tc.p, *di = dc + (size_t)n_v * nc;
+  for (int t = 0; t < iters; ++t) {
+    if (t > 0) RP_CUDA(launch_den_weights((const GramBasis *)tb.p, dX, K, n_v, dc, (double *)tS.p, s));
+    RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, dX, dV, t > 0 ? (const double *)tS.p : nullptr, K, n_v,
+                        (double *)tG.p, (double *)tp.p, pe, s));
+    RP_CUDA(launch_solve((const double *)tG.p, n_v, nc, basis->n_num, dc, di, s));
+  }
+  std::vector<double> hinfo((size_t)n_v * 5);
+  double hxf[2 * RP_MAX_VARS];
+  RP_CUDA(cudaMemcpyAsync(coef_out, dc, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaMemcpyAsync(hinfo.data(), di, (size_t)n_v * 5 * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  if (xform_out) {
+    memset(xform_out, 0, sizeof *xform_out);
+    for (int k = 0; k < n; ++k) {
+      xform_out->c[k] = hxf[2 * k];
+      xform_out->e[k] = (int32_t)hxf[2 * k + 1];
+    }
+  }
+  rp_status worst = RP_OK;
+  for (int v = 0; v < n_v; ++v) {
+    const int stv = (int)hinfo[v * 5];
+    if (info) {
+      info[v].status = stv;
+      info[v].rank = (int32_t)hinfo[v * 5 + 1];
+      info[v].resid2 = hinfo[v * 5 + 2];
+      info[v].min_pivot = hinfo[v * 5 + 3];
+      info[v].cond_est = hinfo[v * 5 + 4];
+    }
+    if (stv != 0) worst = (rp_status)stv;
+  }
+  if (worst != RP_OK) set_error("weighted normal equations are degenerate");
+  return worst;
 }
 
 rp_status rp_eval_metrics(const rp_program *prog, const double *X, int64_t K, double *out, rp_stream sv) {

@@ -232,6 +232,7 @@ struct GramArgs {
   const GramBasis *basis;
   const double *X;
   const double *V;  // [n_v][K]
+  const double *S;  // [n_v][K] row scales or null
   int64_t K;
   int n_v;
   int nb, ntiles, stride;
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_gram(GramArgs a) {
           for (int e = 0; e < B.exp[j][k]; ++e) m *= u;
         }
         if (j >= n_num) m *= -tV[r];
+        if (a.S) m *= a.S[(int64_t)metric * a.K + r0 + r];
       }
       sA[r * stride + j] = m;
     }
@@ -507,6 +509,7 @@ struct FusedArgs {
   const GramBasis *basis;
   const double *X;
   const double *V;  // [NV][K]
+  const double *S;  // [K] row scales (NV = 1, weighted refit) or null
   int64_t K;
   double *part;     // [gridDim.x][NT][64]  canonical (pair, upper tile) order
 };
@@ -521,7 +524,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_gram_fused(FusedArgs a) {
   double *sU = sX + L::NX * kFRT * L::S;     // [kFRT][n]
   double *sPow = sU + kFRT * kMaxVars;       // [kFRT][n][pw]
   double *sV = sPow + kFRT * n * pw;         // [NV][kFRT]
-  uint32_t *sExp = reinterpret_cast<uint32_t *>(sV + NV * kFRT);  // [M8]
+  double *sS = sV + NV * kFRT;                                     // [kFRT]
+  uint32_t *sExp = reinterpret_cast<uint32_t *>(sS + kFRT);       // [M8]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   const int64_t r_begin = a.K * blockIdx.x / gridDim.x;
@@ -550,12 +554,15 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_gram_fused(FusedArgs a) {
       const int v = i / kFRT, r = i % kFRT;
       sV[i] = r < rows ? a.V[(int64_t)v * a.K + r0 + r] : 0.0;
     }
+    if (a.S)  // weighted rows (f4): the power table of row r starts at s_r instead of 1
+      for (int r = threadIdx.x; r < kFRT; r += blockDim.x) sS[r] = r < rows ? a.S[r0 + r] : 0.0;
     __syncthreads();
     // powers u^e, e <= maxdeg, by repeated multiplication
     for (int i = threadIdx.x; i < kFRT * n; i += blockDim.x) {
       const int r = i / n, k = i % n;
       const double u = sU[r * kMaxVars + k];
       double p = r < rows ? 1.0 : 0.0;  // rows past the slab: all-zero design row
+      if (a.S && k == 0) p = sS[r];      // the row scale enters through variable 0's powers
       double *dst = sPow + (r * n + k) * pw;
       for (int e = 0; e < pw; ++e) {
         dst[e] = p;
@@ -640,7 +647,8 @@ __global__ void k_gram_fused_reduce(const double *part, int nblk, int NB, int NV
 template <int NB, int NV>
 static size_t fused_smem(int n, int pw) {
   using L = FL<NB, NV>;
-  return sizeof(double) * ((size_t)L::NX * kFRT * L::S + kFRT * kMaxVars + (size_t)kFRT * n * pw + NV * kFRT) +
+  return sizeof(double) * ((size_t)L::NX * kFRT * L::S + kFRT * kMaxVars + (size_t)kFRT * n * pw + NV * kFRT +
+                            kFRT) +
          sizeof(uint32_t) * L::M8;
 }
 
@@ -652,8 +660,8 @@ static int fused_grid_x(int64_t K) {
 
 template <int NB, int NV>
 static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, const double *X,
-                                  const double *V, int64_t K, double *G, double *d_part,
-                                  size_t part_elems, cudaStream_t s) {
+                                  const double *V, const double *S, int64_t K, double *G,
+                                  double *d_part, size_t part_elems, cudaStream_t s) {
   using L = FL<NB, NV>;
   const int gx = fused_grid_x(K);
   if ((size_t)gx * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
@@ -661,7 +669,7 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_gram_fused<NB, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  FusedArgs fa{d_basis, X, V, K, d_part};
+  FusedArgs fa{d_basis, X, V, S, K, d_part};
   k_gram_fused<NB, NV><<<gx, kFW * 32, smem, s>>>(fa);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t total = (int64_t)NV * 4 * h.n_num * h.n_num;
@@ -684,11 +692,12 @@ static size_t fused_partial_elems(const GramBasis &h, int n_v, int64_t K) {
 }
 
 static cudaError_t launch_fused(const GramBasis *d_basis, const GramBasis &h, const double *X,
-                                const double *V, int64_t K, int n_v, double *G, double *d_part,
-                                size_t part_elems, cudaStream_t s) {
+                                const double *V, const double *S, int64_t K, int n_v, double *G,
+                                double *d_part, size_t part_elems, cudaStream_t s) {
   const int nb = (h.n_num + 7) / 8;
-#define RP_FUSED_CASE(NB_, NV_) \
-  if (nb == NB_ && n_v == NV_) return launch_fused_t<NB_, NV_>(d_basis, h, X, V, K, G, d_part, part_elems, s);
+#define RP_FUSED_CASE(NB_, NV_)                                                                \
+  if (nb == NB_ && n_v == NV_)                                                               \
+    return launch_fused_t<NB_, NV_>(d_basis, h, X, V, S, K, G, d_part, part_elems, s);
   RP_FUSED_CASE(2, 1) RP_FUSED_CASE(2, 3) RP_FUSED_CASE(5, 1) RP_FUSED_CASE(5, 3)
   RP_FUSED_CASE(9, 1) RP_FUSED_CASE(9, 3)
 #undef RP_FUSED_CASE
@@ -701,9 +710,10 @@ static int gram_grid_x(int64_t K) {
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
-size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm) {
+size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm, bool weighted) {
   (void)nsm;
-  if (fused_supported(h, n_v)) return fused_partial_elems(h, n_v, K);
+  if (weighted && fused_supported(h, 1)) return fused_partial_elems(h, 1, K);
+  if (!weighted && fused_supported(h, n_v)) return fused_partial_elems(h, n_v, K);
   const int nb = (h.nc + 7) / 8;
   const int ntiles = nb * (nb + 1) / 2;
   const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
@@ -711,16 +721,24 @@ size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm) {
 }
 
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const double *X,
-                        const double *V, int64_t K, int n_v, double *G, double *d_part,
-                        size_t part_elems, cudaStream_t s) {
-  if (fused_supported(h, n_v)) return launch_fused(d_basis, h, X, V, K, n_v, G, d_part, part_elems, s);
+                        const double *V, const double *S, int64_t K, int n_v, double *G,
+                        double *d_part, size_t part_elems, cudaStream_t s) {
+  if (S && fused_supported(h, 1)) {  // weighted rows: one fused launch per metric
+    for (int v = 0; v < n_v; ++v) {
+      cudaError_t e = launch_fused(d_basis, h, X, V + (int64_t)v * K, S + (int64_t)v * K, K, 1,
+                                   G + (int64_t)v * h.nc * h.nc, d_part, part_elems, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  if (!S && fused_supported(h, n_v)) return launch_fused(d_basis, h, X, V, nullptr, K, n_v, G, d_part, part_elems, s);
   const int nb = (h.nc + 7) / 8;
   const int ntiles = nb * (nb + 1) / 2;
   const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
   const int gx = gram_grid_x(K);
-  if (gram_partial_elems(h, n_v, K, 0) > part_elems) return cudaErrorInvalidValue;
+  if (gram_partial_elems(h, n_v, K, 0, false) > part_elems) return cudaErrorInvalidValue;
   const int stride = gram_stride(nb);
-  GramArgs a{d_basis, X, V, K, n_v, nb, ntiles, stride, d_part};
+  GramArgs a{d_basis, X, V, S, K, n_v, nb, ntiles, stride, d_part};
   const size_t smem = (size_t)kRT * stride * 8 + (size_t)kTilesPerGroup * 64 * 8 +
                       2 * kRT * kMaxVars * 8 + 2 * kRT * 8 + kRT * kMaxVars * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -731,6 +749,42 @@ cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const doub
   if (e != cudaSuccess) return e;
   const int rb = (int)((ntiles * 64 + 255) / 256);
   k_gram_reduce<<<dim3(rb, n_v), 256, 0, s>>>(d_part, gx, groups, nb, ntiles, h.nc, G);
+  return cudaGetLastError();
+}
+
+}  // namespace rp
+
+namespace rp {
+
+// f4: S[v][r] = 1 / q_v(x_r), q_v the denominator of metric v with device coefficients coef
+// [n_v][n_c] in the u-basis of the device GramBasis (repeated multiplication per monomial)
+__global__ void k_den_weights(const GramBasis *gb, const double *X, int64_t K, int n_v,
+                              const double *coef, double *S) {
+  const GramBasis &B = *gb;
+  const int n = B.n, n_num = B.n_num, n_den = B.n_den, nc = B.nc;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < K;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double u[kMaxVars];
+    for (int k = 0; k < n; ++k) u[k] = (X[r * n + k] - B.xc[k]) * ldexp(1.0, -B.xe[k]);
+    for (int v = 0; v < n_v; ++v) {
+      double q = 0.0;
+      for (int j = 0; j < n_den; ++j) {
+        double m = 1.0;
+        for (int k = 0; k < n; ++k)
+          for (int e = 0; e < B.exp[n_num + j][k]; ++e) m *= u[k];
+        q = fma(coef[(int64_t)v * nc + n_num + j], m, q);
+      }
+      S[(int64_t)v * K + r] = 1.0 / q;
+    }
+  }
+}
+
+cudaError_t launch_den_weights(const GramBasis *d_basis, const double *X, int64_t K, int n_v,
+                               const double *d_coef, double *S, cudaStream_t s) {
+  if (K == 0) return cudaSuccess;
+  int64_t b = (K + 255) / 256;
+  const int cap = 8 * num_sms();
+  k_den_weights<<<(int)(b > cap ? cap : b), 256, 0, s>>>(d_basis, X, K, n_v, d_coef, S);
   return cudaGetLastError();
 }
 

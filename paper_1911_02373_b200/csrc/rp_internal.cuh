@@ -111,9 +111,11 @@ struct GramBasis {  // exponents of the n_c design columns (numerator then denom
   uint32_t pexp[256];
 };
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, const double *X,
-                        const double *V, int64_t K, int n_v, double *G, double *d_part,
-                        size_t part_elems, cudaStream_t s);
-size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_sms);
+                        const double *V, const double *S, int64_t K, int n_v, double *G,
+                        double *d_part, size_t part_elems, cudaStream_t s);
+size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_sms, bool weighted);
+cudaError_t launch_den_weights(const GramBasis *d_basis, const double *X, int64_t K, int n_v,
+                               const double *d_coef, double *S, cudaStream_t s);
 
 cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *coef_out,
                          double *info_out, cudaStream_t s);

@@ -101,10 +101,15 @@ def test_decision_service_graph():
     case = synth.polybench_sweep(nD=40)
     plan = rp.Plan(case.programs[:1], _cuda(case.F))
     ref = plan.decide(case.D, prog=0, margin=0.01)
-    svc = rp.DecisionService(plan, prog=0, margin=0.01, history_log2=12)
-    for i in range(len(case.D)):
-        r = svc(case.D[i])
-        assert r["idx"] == ref[i]["idx"] and r["E"] == ref[i]["E"]
-        assert tuple(r["launch"]) == tuple(ref[i]["launch"])
-    r = svc(case.D[3])
-    assert r["from_history"] == 1 and r["idx"] == ref[3]["idx"]
+    for memo in (0, 1 << 10):
+        svc = rp.DecisionService(plan, prog=0, margin=0.01, history_log2=12, host_memo=memo)
+        for i in range(len(case.D)):
+            r = svc(case.D[i])
+            assert r["idx"] == ref[i]["idx"] and r["E"] == ref[i]["E"]
+            assert tuple(r["launch"]) == tuple(ref[i]["launch"])
+        r = svc(case.D[3])
+        assert r["idx"] == ref[3]["idx"]
+        if memo == 0:
+            assert r["from_history"] == 1  # served by the device history
+        else:
+            assert len(svc.memo) == len(np.unique(case.D))  # served by the host memo
