@@ -377,7 +377,9 @@ def main():
                         "seconds": dt, "sample": f"1/{SAMPLE_DIV} of the step: fit of 3 metrics on "
                                                f"{K // SAMPLE_DIV} rows + sweep of {nD // SAMPLE_DIV} D x {nF} F"}
 
-    launches_per_step = 8  # fit: minmax x2, xform, gram, gram_reduce, solve; sweep: plan_configs, sweep
+    # fit: minmax x2, xform, xform_to_basis, gram_fused, gram_fused_reduce, solve (7);
+    # sweep: plan_configs, bucket count / scan / scatter, sweep (5)
+    launches_per_step = 12
     out = {"metric": METRIC, "value": nD * nF / (step_ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64",

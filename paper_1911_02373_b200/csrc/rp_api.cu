@@ -297,6 +297,7 @@ struct rp_plan_s {
   int n_prog = 0, nF = 0, d = 0, p = 0, npe_pad = 0;
   bool mwp = true;
   int nde_max = 1, n_sm_max = 1;
+  int kb = 1;  // D1 bucket bound: kb^2 > max T_max >= P1 P2 of any feasible configuration
   DevProg *d_progs = nullptr;
   int32_t *buf_i = nullptr;
   double *buf_d = nullptr;
@@ -359,6 +360,9 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   for (int g = 0; g < n_prog; ++g) {
     pl->nde_max = std::max(pl->nde_max, hp[g].nDE);
     pl->n_sm_max = std::max(pl->n_sm_max, hp[g].n_sm);
+    int kb = 1;
+    while ((int64_t)kb * kb <= (int64_t)hp[g].t_max) ++kb;
+    pl->kb = std::max(pl->kb, kb);
   }
   const int nde_pad = std::max(4, (pl->nde_max + 3) & ~3);
   const size_t nrec = (size_t)n_prog * nFp;                               // CfgRec (64 B)
@@ -416,8 +420,19 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
   if ((st = stage_out(best_idx, no, ti, &di, &hi, s)) != RP_OK) return st;
   if ((st = stage_out(best_E, no, tb, &db, &hb, s)) != RP_OK) return st;
   if ((st = stage_out(second_E, no, ts, &ds, &hs, s)) != RP_OK) return st;
+  // group tuples by D1 (only D1 < kb, kb^2 > T_max >= P1 P2, can fail the D rule) so whole
+  // configuration octets are skipped by the sweep's early exit; pays off on large batches
+  Tmp tperm;
+  const int32_t *perm = nullptr;
+  if (nD >= 4096 && nD <= 0x7fffffffll && pl->kb < 255) {
+    const int kb = pl->kb;
+    RP_CUDA(tperm.alloc((size_t)nD * 4 + (size_t)(kb + 1) * 4 + 16, s));
+    int32_t *p = (int32_t *)tperm.p;
+    RP_CUDA(launch_bucket_perm(dD, nD, pl->d, kb, (unsigned *)(p + nD), p, s));
+    perm = p;
+  }
   RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->mwp, pl->tab, pl->npe_pad, pl->nde_max, pl->n_sm_max,
-                       pl->d, dD, nD, di, db, ds, s));
+                       pl->d, dD, nD, di, db, ds, perm, s));
   if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, no * 4, cudaMemcpyDeviceToHost, s));
   if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, no * 8, cudaMemcpyDeviceToHost, s));
   if (hs) RP_CUDA(cudaMemcpyAsync(second_E, ds, no * 8, cudaMemcpyDeviceToHost, s));

@@ -90,7 +90,10 @@ cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_
                                 int npe_pad, CfgTable tab, cudaStream_t s);
 cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
                          int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
-                         int32_t *idx, double *bestE, double *secondE, cudaStream_t s);
+                         int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
+                         cudaStream_t s);
+cudaError_t launch_bucket_perm(const int32_t *d_D, int64_t nD, int d, int kb, unsigned *d_hist,
+                               int32_t *d_perm, cudaStream_t s);
 cudaError_t launch_eval_metrics(const DevProg *d_prog, int nm, const double *X, int64_t K,
                                 double *out, cudaStream_t s);
 cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int nblk,

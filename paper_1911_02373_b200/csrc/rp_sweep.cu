@@ -171,6 +171,70 @@ cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_
   return cudaGetLastError();
 }
 
+// ---- tuple grouping by D1 (a3 early exit) ------------------------------------------------------
+// Only tuples with D1 < kb (kb^2 > the largest P1 P2 of the plan) can fail the D rule, so a
+// counting sort on min(D1, kb) groups them by D1 in front; everything else keeps one bucket.
+// Which tile computes a tuple does not change its result (rows of the DMMA tiles are
+// independent), so outputs are bit-identical to the identity order.
+constexpr int kBucketMax = 256;  // kb + 1 <= kBucketMax (t_max <= 65025)
+
+__global__ void k_bucket_count(const int32_t *D, int64_t nD, int d, int kb, unsigned *hist) {
+  __shared__ unsigned sh[kBucketMax];
+  for (int b = threadIdx.x; b <= kb; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nD; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d1 = D[i * d];
+    atomicAdd(&sh[d1 < kb ? (d1 < 0 ? 0 : d1) : kb], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= kb; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+__global__ void k_bucket_scan(unsigned *hist, int kb) {  // exclusive scan of kb+1 counters, 1 thread
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b <= kb; ++b) {
+      const unsigned c = hist[b];
+      hist[b] = run;
+      run += c;
+    }
+  }
+}
+// each block claims one contiguous range per bucket for the tuples of its grid-stride pass
+__global__ void k_bucket_scatter(const int32_t *D, int64_t nD, int d, int kb, unsigned *pos, int32_t *perm) {
+  __shared__ unsigned sh[kBucketMax], base[kBucketMax];
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < nD; c0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int b = threadIdx.x; b <= kb; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const int64_t i = c0 + threadIdx.x;
+    int bk = -1;
+    unsigned local = 0;
+    if (i < nD) {
+      const int32_t d1 = D[i * d];
+      bk = d1 < kb ? (d1 < 0 ? 0 : d1) : kb;
+      local = atomicAdd(&sh[bk], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b <= kb; b += blockDim.x) base[b] = sh[b] ? atomicAdd(&pos[b], sh[b]) : 0;
+    __syncthreads();
+    if (bk >= 0) perm[base[bk] + local] = (int32_t)i;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_bucket_perm(const int32_t *d_D, int64_t nD, int d, int kb, unsigned *d_hist,
+                               int32_t *d_perm, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_hist, 0, sizeof(unsigned) * (kb + 1), s);
+  if (e != cudaSuccess) return e;
+  int64_t b = (nD + 255) / 256;
+  const int cap = 4 * num_sms();
+  const int grid = (int)(b > cap ? cap : (b < 1 ? 1 : b));
+  k_bucket_count<<<grid, 256, 0, s>>>(d_D, nD, d, kb, d_hist);
+  k_bucket_scan<<<1, 32, 0, s>>>(d_hist, kb);
+  k_bucket_scatter<<<grid, 256, 0, s>>>(d_D, nD, d, kb, d_hist, d_perm);
+  return cudaGetLastError();
+}
+
 // ---- the sweep ------------------------------------------------------------------------------
 struct SweepArgs {
   const DevProg *progs;
@@ -183,6 +247,7 @@ struct SweepArgs {
   int32_t *idx;
   double *bestE;
   double *secondE;
+  const int32_t *perm;  // tuple order of the tiles (grouped by D1), or null: identity
 };
 
 #ifndef RP_SWEEP_MINB
@@ -236,7 +301,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   const int nDE = pg.nDE, ndp = a.tab.nde_pad;
   for (int i = threadIdx.x; i < kTD * d; i += blockDim.x) {
     const int t = i / d, k = i % d;
-    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[(d0 + t) * d + k] : 1;
+    const int64_t src = (t < tmax) ? (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t) : 0;
+    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[src * d + k] : 1;
   }
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
   const bool rsm_tab = n_sm < kRSMTab;
@@ -377,7 +443,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   st = merge(st, shfl_xor(st, 1));
   st = merge(st, shfl_xor(st, 2));
   if ((lane & 3) == 0 && tok) {
-    const int64_t o = (int64_t)g * a.nD + d0 + t;
+    const int64_t o = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t);
     a.idx[o] = (st.e < kInf) ? st.i : -1;
     a.bestE[o] = st.e;
     if (SECOND) a.secondE[o] = st.s;
@@ -408,11 +474,12 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
 
 cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
                          int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
-                         int32_t *idx, double *bestE, double *secondE, cudaStream_t s) {
+                         int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
+                         cudaStream_t s) {
   if (nD == 0) return cudaSuccess;
   if (n_sm_max >= kRSMTab) n_sm_max = 0;  // no table: 1/SM_act computed directly
   (void)nde_max;
-  SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE};
+  SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE, perm};
   switch (npe_pad) {
     case 4: return launch_npe<4>(a, n_prog, mwp, n_sm_max, s);
     case 8: return launch_npe<8>(a, n_prog, mwp, n_sm_max, s);
