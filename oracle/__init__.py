@@ -85,6 +85,8 @@ def lib():
             L.orc_solve.restype = i
             L.orc_fit_sk.argtypes = [vp, vp, ll, i, i, i, vp, vp, i, vp, vp, vp, i]
             L.orc_fit_sk.restype = i
+            L.orc_fit_svd.argtypes = [vp, vp, ll, i, i, i, vp, vp, vp, vp, vp, vp]
+            L.orc_fit_svd.restype = i
             _LIB = L
         return _LIB
 
@@ -316,3 +318,20 @@ def fit_sk(X, V, num_exp, den_exp, iters: int = 3, nthreads: int = 1):
     st = lib().orc_fit_sk(_p(X), _p(V), K, n, len(ne), len(de), _p(ne), _p(de), iters, _p(coef), _p(c), _p(e),
                           nthreads)
     return dict(coef=coef, c=c, e=e, status=int(st))
+
+
+def fit_svd(X, V, num_exp, den_exp):
+    """Homogeneous least squares by one-sided Jacobi SVD (NEXT row f1): the right singular vector
+    of the smallest singular value, beta_0 = 1.  Returns coef, ascending sigma, (c, e)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    K, n = X.shape
+    ne = np.ascontiguousarray(num_exp, dtype=np.int16)
+    de = np.ascontiguousarray(den_exp, dtype=np.int16)
+    nc = len(ne) + len(de)
+    coef = np.zeros(nc, dtype=LD)
+    sigma = np.zeros(nc, dtype=LD)
+    c = np.zeros(n)
+    e = np.zeros(n, dtype=np.int32)
+    st = lib().orc_fit_svd(_p(X), _p(V), K, n, len(ne), len(de), _p(ne), _p(de), _p(coef), _p(sigma), _p(c), _p(e))
+    return dict(coef=coef, sigma=sigma, c=c, e=e, status=int(st))

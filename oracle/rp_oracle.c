@@ -541,3 +541,87 @@ int orc_fit_sk(const double *X, const double *V, long long K, int n, int n_num, 
   free(s);
   return status;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * f1 -- "we use the computationally more intensive yet more numerically stable method of
+ * singular value decomposition" on "a system of homogeneous equations"
+ * (draft): min ||A c|| over ||c|| = 1 is the right singular vector of the
+ * smallest singular value.  One-sided Jacobi (Hestenes): rotate column pairs of A until they are
+ * orthogonal; the rotations accumulate into V, the column norms are the singular values.
+ * ---------------------------------------------------------------------------------------- */
+int orc_fit_svd(const double *X, const double *V, long long K, int n, int n_num, int n_den,
+                const short *num_exp, const short *den_exp, long double *coef, long double *sigma,
+                double *c, int *e) {
+  const int nc = n_num + n_den;
+  double lo[ORC_MAX_VARS], hi[ORC_MAX_VARS];
+  orc_minmax(X, K, n, lo, hi);
+  orc_xform_from_box(n, lo, hi, c, e);
+  ld *A = (ld *)malloc(sizeof(ld) * (size_t)K * nc); /* column-major: A[j * K + r] */
+  ld *row = (ld *)malloc(sizeof(ld) * nc);
+  for (long long r = 0; r < K; ++r) {
+    orc_design_row(n, n_num, n_den, num_exp, den_exp, c, e, X + r * n, V[r], row);
+    for (int j = 0; j < nc; ++j) A[(size_t)j * K + r] = row[j];
+  }
+  ld *W = (ld *)calloc((size_t)nc * nc, sizeof(ld)); /* V of the SVD, column-major */
+  for (int j = 0; j < nc; ++j) W[(size_t)j * nc + j] = 1.0L;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int i = 0; i < nc - 1; ++i)
+      for (int j = i + 1; j < nc; ++j) {
+        ld *ai = A + (size_t)i * K, *aj = A + (size_t)j * K;
+        ld al = 0, be = 0, ga = 0;
+        for (long long r = 0; r < K; ++r) {
+          al += ai[r] * ai[r];
+          be += aj[r] * aj[r];
+          ga += ai[r] * aj[r];
+        }
+        if (ga == 0 || fabsl(ga) <= 1e-18L * sqrtl(al * be)) continue;
+        rotated = 1;
+        const ld zeta = (be - al) / (2 * ga);
+        const ld t = (zeta >= 0 ? 1.0L : -1.0L) / (fabsl(zeta) + sqrtl(1 + zeta * zeta));
+        const ld cs = 1 / sqrtl(1 + t * t), sn = cs * t;
+        for (long long r = 0; r < K; ++r) {
+          const ld x = ai[r], y = aj[r];
+          ai[r] = cs * x - sn * y;
+          aj[r] = sn * x + cs * y;
+        }
+        ld *wi = W + (size_t)i * nc, *wj = W + (size_t)j * nc;
+        for (int r = 0; r < nc; ++r) {
+          const ld x = wi[r], y = wj[r];
+          wi[r] = cs * x - sn * y;
+          wj[r] = sn * x + cs * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  /* singular values = column norms; pick the smallest */
+  int jmin = 0;
+  ld smin = INFINITY;
+  for (int j = 0; j < nc; ++j) {
+    ld s2 = 0;
+    for (long long r = 0; r < K; ++r) s2 += A[(size_t)j * K + r] * A[(size_t)j * K + r];
+    sigma[j] = sqrtl(s2);
+    if (sigma[j] < smin) {
+      smin = sigma[j];
+      jmin = j;
+    }
+  }
+  /* ascending order of sigma (insertion sort, nc <= a few hundred) */
+  for (int a = 1; a < nc; ++a) {
+    ld v = sigma[a];
+    int b = a - 1;
+    while (b >= 0 && sigma[b] > v) {
+      sigma[b + 1] = sigma[b];
+      --b;
+    }
+    sigma[b + 1] = v;
+  }
+  int status = 0;
+  const ld b0 = W[(size_t)jmin * nc + n_num];
+  if (!(fabsl(b0) > 1e-300L)) status = 3;
+  for (int r = 0; r < nc; ++r) coef[r] = status ? NAN : W[(size_t)jmin * nc + r] / b0;
+  free(A);
+  free(row);
+  free(W);
+  return status;
+}
