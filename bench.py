@@ -114,12 +114,12 @@ class ClockSampler:
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ------------------------------------------------------------------------------------------
 
-def oracle_step(inp, part: int, cores: int):
-    """The oracle's whole path on a 1/SAMPLE_DIV slice (slice `part`): fit of the 3 metrics on
-    K/200 rows, then the sweep of the fitted program over nD/200 tuples x all of F."""
+def oracle_step(inp, part: int, cores: int, div: int = SAMPLE_DIV):
+    """The oracle's whole path on a 1/div slice (slice `part`): fit of the 3 metrics on
+    K/div rows, then the sweep of the fitted program over nD/div tuples x all of F."""
     import oracle
-    K = len(inp["X"]) // SAMPLE_DIV
-    nd = len(inp["D"]) // SAMPLE_DIV
+    K = len(inp["X"]) // div
+    nd = len(inp["D"]) // div
     X = inp["X"][part * K:(part + 1) * K]
     V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(inp["truth"], X)])
     V *= inp["noise"][:, part * K:(part + 1) * K]
@@ -372,10 +372,13 @@ def main():
     cpu_baseline = None
     if world == 1 and not args.no_cpu_baseline:
         cores, model = cpu_info()
-        v, dt = oracle_step(inp, 0, cores)
+        # size the sample for ~12 s of oracle work: probe on 1/SAMPLE_DIV, then rescale
+        _, dt0 = oracle_step(inp, 0, cores)
+        div = max(2, min(SAMPLE_DIV, int(SAMPLE_DIV * dt0 / 12.0)))
+        v, dt = oracle_step(inp, 1, cores, div)
         cpu_baseline = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
-                        "seconds": dt, "sample": f"1/{SAMPLE_DIV} of the step: fit of 3 metrics on "
-                                               f"{K // SAMPLE_DIV} rows + sweep of {nD // SAMPLE_DIV} D x {nF} F"}
+                        "seconds": dt, "sample": f"1/{div} of the step (second slice): fit of 3 metrics on "
+                                               f"{K // div} rows + sweep of {nD // div} D x {nF} F"}
 
     # fit: minmax x2, xform, xform_to_basis, gram_fused, gram_fused_reduce, solve (7);
     # sweep: plan_configs, bucket count / scan / scatter, sweep (5)

@@ -71,16 +71,42 @@ __global__ void k_minmax_part(const double *X, int64_t K, int n, double *part) {
   }
 }
 
+// one CTA: every thread folds a strided subset of the partials (independent loads, not one
+// dependent chain over nblk), then warp shuffles and a shared-memory pass
 __global__ void k_minmax_final(const double *part, int nblk, int n, double *out) {
-  const int k = threadIdx.x;
-  if (k >= n) return;
-  double a = part[k * 2], b = part[k * 2 + 1];
-  for (int i = 1; i < nblk; ++i) {
-    a = fmin(a, part[((int64_t)i * n + k) * 2]);
-    b = fmax(b, part[((int64_t)i * n + k) * 2 + 1]);
+  __shared__ double smin[8][kMaxVars], smax[8][kMaxVars];
+  double lo[kMaxVars], hi[kMaxVars];
+  for (int k = 0; k < kMaxVars; ++k) {
+    lo[k] = __longlong_as_double(0x7ff0000000000000ll);
+    hi[k] = -lo[k];
   }
-  out[k * 2] = a;
-  out[k * 2 + 1] = b;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x)
+    for (int k = 0; k < n; ++k) {
+      lo[k] = fmin(lo[k], part[((int64_t)i * n + k) * 2]);
+      hi[k] = fmax(hi[k], part[((int64_t)i * n + k) * 2 + 1]);
+    }
+  for (int k = 0; k < n; ++k)
+    for (int o = 16; o >= 1; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      smin[wid][k] = lo[k];
+      smax[wid][k] = hi[k];
+    }
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int k = threadIdx.x;
+    double a = smin[0][k], b = smax[0][k];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmin(a, smin[w][k]);
+      b = fmax(b, smax[w][k]);
+    }
+    out[k * 2] = a;
+    out[k * 2 + 1] = b;
+  }
 }
 
 // a10: c_k = (lo_k + hi_k) / 2, e_k = least integer with 2^e_k >= max((hi_k - lo_k) / 2, 1)
@@ -124,7 +150,7 @@ int minmax_blocks(int64_t K) {
 cudaError_t launch_minmax(const double *X, int64_t K, int n, double *d_part, int nblk,
                           double *d_out, cudaStream_t s) {
   k_minmax_part<<<nblk, 256, 0, s>>>(X, K, n, d_part);
-  k_minmax_final<<<1, 32, 0, s>>>(d_part, nblk, n, d_out);
+  k_minmax_final<<<1, 256, 0, s>>>(d_part, nblk, n, d_out);
   return cudaGetLastError();
 }
 
