@@ -173,6 +173,34 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
                     int32_t iters, double *coef_out, rp_xform *xform_out, rp_fit_info *info,
                     rp_stream s);
 
+/* ---- f1: the homogeneous system by singular value decomposition ------------------------------
+ * "we use the computationally more intensive yet more numerically stable method of singular
+ * value decomposition" on the homogeneous system p(x) - V q(x) = 0 (draft
+ * footnote PAPER.md:2595-2598): coef = the right singular vector of the smallest singular value
+ * of A_m = [M(u_r) | -V_m[r] N(u_r)] (rows as in rp_gram_accumulate), scaled so that beta_0 = 1
+ * (reading R12).  A is never formed in memory: a Householder TSQR builds R (A = QR) from design
+ * rows generated on chip, and a one-sided Jacobi SVD of R (2-CTA cluster per metric) gives the
+ * right singular vectors.  Deterministic (fixed merge tree).
+ *
+ * rp_fit_svd: transform from the sample box as rp_fit, then TSQR + SVD.  X [K][n], V [n_v][K]
+ *   device-or-host; coef_out host [n_v][n_c]; sigma_out host [n_v][n_c] ascending singular values
+ *   (nullable); xform_out host (nullable); info host [n_v] (nullable) with rank = #{sigma >
+ *   1e-13 sigma_max}, resid2 = ||A coef||^2, min_pivot = sigma_min, cond_est = sigma_max /
+ *   sigma_min.  Synchronises.  DEGENERATE if beta_0 of that singular vector is 0 (coef NaN;
+ *   other metrics still solved); UNSUPPORTED if n_c outside [2, 144].
+ * rp_tsqr_accumulate: the split form for K-sharding -- R_m of this rank's rows under an agreed
+ *   transform: R device-or-host float64 [n_v][n_c][n_c], row-major upper triangular (zeros
+ *   below the diagonal; A_m^T A_m = R_m^T R_m).  K = 0 gives R = 0.
+ * rp_svd_rows: TSQR + SVD of dense rows (device-or-host float64 [n_v][n_rows][n_c]), e.g. the
+ *   ranks' stacked factors [R_0; R_1; ...]; outputs as rp_fit_svd.                          */
+rp_status rp_fit_svd(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                     double *coef_out, double *sigma_out, rp_xform *xform_out, rp_fit_info *info,
+                     rp_stream s);
+rp_status rp_tsqr_accumulate(const double *X, const double *V, int64_t K, int32_t n_v,
+                             const rp_basis *basis, const rp_xform *xform, double *R, rp_stream s);
+rp_status rp_svd_rows(const double *rows, int64_t n_rows, int32_t n_v, const rp_basis *basis,
+                      double *coef_out, double *sigma_out, rp_fit_info *info, rp_stream s);
+
 /* ---- a4 alone: fitted metrics at points ----------------------------------------------------
  * out[i][r] = g_i(X_r) = p_i(u_r)/q_i(u_r) for i < prog->n_metrics (device-or-host float64
  * [n_metrics][K]); X device-or-host float64 [K][d+p].                                      */

@@ -87,6 +87,8 @@ def lib():
             L.orc_fit_sk.restype = i
             L.orc_fit_svd.argtypes = [vp, vp, ll, i, i, i, vp, vp, vp, vp, vp, vp]
             L.orc_fit_svd.restype = i
+            L.orc_svd_rows.argtypes = [vp, ll, i, i, vp, vp]
+            L.orc_svd_rows.restype = i
             _LIB = L
         return _LIB
 
@@ -335,3 +337,14 @@ def fit_svd(X, V, num_exp, den_exp):
     e = np.zeros(n, dtype=np.int32)
     st = lib().orc_fit_svd(_p(X), _p(V), K, n, len(ne), len(de), _p(ne), _p(de), _p(coef), _p(sigma), _p(c), _p(e))
     return dict(coef=coef, sigma=sigma, c=c, e=e, status=int(st))
+
+
+def svd_rows(rows, n_num: int):
+    """The oracle's Jacobi SVD of an explicit matrix rows [K][n_c] (e.g. stacked design rows of
+    several shards): coef with beta_0 = 1 and ascending sigma (NEXT row f1)."""
+    rows = np.ascontiguousarray(rows, dtype=LD)
+    K, nc = rows.shape
+    coef = np.zeros(nc, dtype=LD)
+    sigma = np.zeros(nc, dtype=LD)
+    st = lib().orc_svd_rows(_p(rows), K, nc, n_num, _p(coef), _p(sigma))
+    return dict(coef=coef, sigma=sigma, status=int(st))

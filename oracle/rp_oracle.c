@@ -549,19 +549,14 @@ int orc_fit_sk(const double *X, const double *V, long long K, int n, int n_num, 
  * smallest singular value.  One-sided Jacobi (Hestenes): rotate column pairs of A until they are
  * orthogonal; the rotations accumulate into V, the column norms are the singular values.
  * ---------------------------------------------------------------------------------------- */
-int orc_fit_svd(const double *X, const double *V, long long K, int n, int n_num, int n_den,
-                const short *num_exp, const short *den_exp, long double *coef, long double *sigma,
-                double *c, int *e) {
-  const int nc = n_num + n_den;
-  double lo[ORC_MAX_VARS], hi[ORC_MAX_VARS];
-  orc_minmax(X, K, n, lo, hi);
-  orc_xform_from_box(n, lo, hi, c, e);
+/* one-sided Jacobi SVD of an explicit matrix A [K][nc] (row-major, long double copy made
+ * here): coef = the right singular vector of the smallest singular value with beta_0 (column
+ * n_num) = 1; sigma[nc] ascending.  Returns 0, or 3 if that vector's beta_0 is below 1e-300. */
+int orc_svd_rows(const long double *rows, long long K, int nc, int n_num, long double *coef,
+                 long double *sigma) {
   ld *A = (ld *)malloc(sizeof(ld) * (size_t)K * nc); /* column-major: A[j * K + r] */
-  ld *row = (ld *)malloc(sizeof(ld) * nc);
-  for (long long r = 0; r < K; ++r) {
-    orc_design_row(n, n_num, n_den, num_exp, den_exp, c, e, X + r * n, V[r], row);
-    for (int j = 0; j < nc; ++j) A[(size_t)j * K + r] = row[j];
-  }
+  for (long long r = 0; r < K; ++r)
+    for (int j = 0; j < nc; ++j) A[(size_t)j * K + r] = rows[(size_t)r * nc + j];
   ld *W = (ld *)calloc((size_t)nc * nc, sizeof(ld)); /* V of the SVD, column-major */
   for (int j = 0; j < nc; ++j) W[(size_t)j * nc + j] = 1.0L;
   for (int sweep = 0; sweep < 60; ++sweep) {
@@ -621,7 +616,21 @@ int orc_fit_svd(const double *X, const double *V, long long K, int n, int n_num,
   if (!(fabsl(b0) > 1e-300L)) status = 3;
   for (int r = 0; r < nc; ++r) coef[r] = status ? NAN : W[(size_t)jmin * nc + r] / b0;
   free(A);
-  free(row);
   free(W);
+  return status;
+}
+
+int orc_fit_svd(const double *X, const double *V, long long K, int n, int n_num, int n_den,
+                const short *num_exp, const short *den_exp, long double *coef, long double *sigma,
+                double *c, int *e) {
+  const int nc = n_num + n_den;
+  double lo[ORC_MAX_VARS], hi[ORC_MAX_VARS];
+  orc_minmax(X, K, n, lo, hi);
+  orc_xform_from_box(n, lo, hi, c, e);
+  ld *rows = (ld *)malloc(sizeof(ld) * (size_t)K * nc);
+  for (long long r = 0; r < K; ++r)
+    orc_design_row(n, n_num, n_den, num_exp, den_exp, c, e, X + r * n, V[r], rows + (size_t)r * nc);
+  const int status = orc_svd_rows(rows, K, nc, n_num, coef, sigma);
+  free(rows);
   return status;
 }

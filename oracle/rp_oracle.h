@@ -121,6 +121,8 @@ int orc_fit_sk(const double *X, const double *V, long long K, int n, int n_num, 
  * long double; one-sided (Hestenes) Jacobi SVD of A; coef = the right singular vector of the
  * smallest singular value scaled so that beta_0 = 1 (SPEC.md:33 canonical form).  sigma[n_c]
  * ascending.  Returns 0, or 3 if |beta_0| of that vector is below 1e-300 (degenerate).       */
+int orc_svd_rows(const long double *rows, long long K, int nc, int n_num, long double *coef,
+                 long double *sigma);
 int orc_fit_svd(const double *X, const double *V, long long K, int n, int n_num, int n_den,
                 const short *num_exp, const short *den_exp, long double *coef, long double *sigma,
                 double *c, int *e);

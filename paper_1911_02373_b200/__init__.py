@@ -88,6 +88,9 @@ _SIGS = {
     "rp_fit": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, C.POINTER(rp_xform), _vp, _vp],
     "rp_gram_accumulate_weighted": [_vp, _vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
     "rp_fit_sk": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _i32, _vp, C.POINTER(rp_xform), _vp, _vp],
+    "rp_fit_svd": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, C.POINTER(rp_xform), _vp, _vp],
+    "rp_tsqr_accumulate": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
+    "rp_svd_rows": [_vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, _vp, _vp],
     "rp_eval_metrics": [C.POINTER(rp_program), _vp, _i64, _vp, _vp],
     "rp_eval_argmin": [C.POINTER(rp_program), _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
     "rp_eval_argmin_batched": [_vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
@@ -459,6 +462,56 @@ def fit(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
         _check(st)
     n = b.num.shape[1]
     return coef, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)
+
+
+def fit_svd(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
+    """rp_fit_svd (NEXT row f1): the homogeneous system by SVD -- TSQR of the design rows, then
+    Jacobi SVD of R.  Returns (coef [n_v][n_c], sigma [n_v][n_c] ascending, (c, e), infos)."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    coef = np.zeros((n_v, b.n_c))
+    sigma = np.zeros((n_v, b.n_c))
+    xf = rp_xform()
+    infos = (rp_fit_info * n_v)()
+    st = _lib.rp_fit_svd(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), _ptr(coef), _ptr(sigma), C.byref(xf),
+                         C.cast(infos, _vp), _stream_of(X, V))
+    if st != 0 and (st != 3 or raise_on_degenerate):
+        _check(st)
+    n = b.num.shape[1]
+    return coef, sigma, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)
+
+
+def tsqr(X, V, num_exp, den_exp, c, e, out=None):
+    """rp_tsqr_accumulate: R [n_v][n_c][n_c] (upper triangular, A^T A = R^T R) of this shard's
+    design rows under the agreed transform (c, e)."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K = X.shape[0]
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    xf = _xform_struct(c, e)
+    R = out if out is not None else _empty_like_family(X, (n_v, b.n_c, b.n_c), np.float64)
+    _check(_lib.rp_tsqr_accumulate(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), C.byref(xf), _ptr(R), _stream_of(X, V, R)))
+    return R
+
+
+def svd_rows(rows, num_exp, den_exp, raise_on_degenerate: bool = True):
+    """rp_svd_rows: TSQR + SVD of dense rows [n_v][n_rows][n_c] (e.g. stacked per-rank R factors).
+    Returns (coef, sigma, infos)."""
+    b = Basis(num_exp, den_exp)
+    rows = _contig(rows, np.float64)
+    n_v, n_rows = rows.shape[0], rows.shape[1]
+    coef = np.zeros((n_v, b.n_c))
+    sigma = np.zeros((n_v, b.n_c))
+    infos = (rp_fit_info * n_v)()
+    st = _lib.rp_svd_rows(_ptr(rows), n_rows, n_v, C.byref(b.c), _ptr(coef), _ptr(sigma), C.cast(infos, _vp),
+                          _stream_of(rows))
+    if st != 0 and (st != 3 or raise_on_degenerate):
+        _check(st)
+    return coef, sigma, _infos(infos)
 
 
 def decisions_from_device(out) -> np.ndarray:

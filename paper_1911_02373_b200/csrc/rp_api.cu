@@ -708,6 +708,141 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
   return worst;
 }
 
+// ---------------------------------------------------------------------------------------------
+// f1: SVD of the homogeneous system
+// ---------------------------------------------------------------------------------------------
+static rp_status svd_finish(const double *dR, int32_t n_v, int nc, int n_num, double *coef_out,
+                            double *sigma_out, rp_fit_info *info, cudaStream_t s) {
+  Tmp to;
+  RP_CUDA(to.alloc((size_t)n_v * (2 * nc + 6) * 8, s));
+  double *dc = (double *)to.p, *dsg = dc + (size_t)n_v * nc, *di = dsg + (size_t)n_v * nc;
+  RP_CUDA(launch_svd_jacobi(dR, nc, n_num, n_v, dc, dsg, di, s));
+  std::vector<double> hinfo((size_t)n_v * 6);
+  RP_CUDA(cudaMemcpyAsync(coef_out, dc, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
+  if (sigma_out) RP_CUDA(cudaMemcpyAsync(sigma_out, dsg, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaMemcpyAsync(hinfo.data(), di, (size_t)n_v * 6 * 8, cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  rp_status worst = RP_OK;
+  for (int v = 0; v < n_v; ++v) {
+    const int stv = (int)hinfo[v * 6];
+    if (info) {
+      info[v].status = stv;
+      info[v].rank = (int32_t)hinfo[v * 6 + 1];
+      info[v].resid2 = hinfo[v * 6 + 2];
+      info[v].min_pivot = hinfo[v * 6 + 3];
+      info[v].cond_est = hinfo[v * 6 + 4];
+    }
+    if (stv != 0) worst = (rp_status)stv;
+  }
+  if (worst != RP_OK) set_error("SVD: beta_0 of the smallest right singular vector is zero");
+  return worst;
+}
+
+static rp_status svd_checks(const rp_basis *basis, int32_t n_v) {
+  RP_REQUIRE(basis, RP_ERR_INVALID_ARG, "null basis");
+  RP_REQUIRE(n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "n_v = %d", n_v);
+  rp_status st = check_basis(*basis, basis->n_vars, "svd", true);
+  if (st != RP_OK) return st;
+  const int nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc >= 2 && nc <= 144, RP_ERR_UNSUPPORTED, "svd: n_c = %d outside [2, 144]", nc);
+  return ensure_device();
+}
+
+rp_status rp_fit_svd(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                     double *coef_out, double *sigma_out, rp_xform *xform_out, rp_fit_info *info,
+                     rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(X && V && coef_out, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 1, RP_ERR_INVALID_ARG, "K = %lld", (long long)K);
+  rp_status st = svd_checks(basis, n_v);
+  if (st != RP_OK) return st;
+  const int n = basis->n_vars, nc = basis->n_num + basis->n_den;
+  Tmp tX, tV, tw, tb, tws, tR;
+  const double *dX, *dV;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  const int nblk = minmax_blocks(K);
+  RP_CUDA(tw.alloc(((size_t)nblk * n * 2 + 4 * RP_MAX_VARS) * sizeof(double), s));
+  double *part = (double *)tw.p, *lohi = part + (size_t)nblk * n * 2, *xf = lohi + 2 * RP_MAX_VARS;
+  RP_CUDA(launch_minmax(dX, K, n, part, nblk, lohi, s));
+  RP_CUDA(launch_xform(lohi, n, xf, s));
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, nullptr, &gb)) != RP_OK) return st;
+  RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+  RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+  RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
+  const size_t wsb = tsqr_workspace_bytes(nc, n_v, tsqr_leaves(K, n_v));
+  RP_CUDA(tws.alloc(wsb, s));
+  RP_CUDA(tR.alloc((size_t)n_v * nc * nc * 8, s));
+  RP_CUDA(launch_tsqr((const GramBasis *)tb.p, dX, dV, nullptr, nullptr, K, n, nc, n_v, tws.p, wsb,
+                      (double *)tR.p, s));
+  rp_status sst = svd_finish((const double *)tR.p, n_v, nc, basis->n_num, coef_out, sigma_out, info, s);
+  if (sst == RP_ERR_CUDA) return sst;
+  double hxf[2 * RP_MAX_VARS];
+  RP_CUDA(cudaMemcpyAsync(hxf, xf, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  if (xform_out) {
+    memset(xform_out, 0, sizeof *xform_out);
+    for (int k = 0; k < n; ++k) {
+      xform_out->c[k] = hxf[2 * k];
+      xform_out->e[k] = (int32_t)hxf[2 * k + 1];
+    }
+  }
+  return sst;
+}
+
+rp_status rp_tsqr_accumulate(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                             const rp_xform *xform, double *R, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(R && xform, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(K >= 0, RP_ERR_INVALID_ARG, "K = %lld", (long long)K);
+  RP_REQUIRE(K == 0 || (X && V), RP_ERR_INVALID_ARG, "null X / V");
+  rp_status st = svd_checks(basis, n_v);
+  if (st != RP_OK) return st;
+  const int n = basis->n_vars, nc = basis->n_num + basis->n_den;
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, xform, &gb)) != RP_OK) return st;
+  Tmp tX, tV, tR, tb, tws;
+  const double *dX = nullptr, *dV = nullptr;
+  double *dR;
+  bool hR;
+  if ((st = stage_in(X, (size_t)K * n, tX, &dX, s)) != RP_OK) return st;
+  if ((st = stage_in(V, (size_t)K * n_v, tV, &dV, s)) != RP_OK) return st;
+  if ((st = stage_out(R, (size_t)n_v * nc * nc, tR, &dR, &hR, s)) != RP_OK) return st;
+  if (K == 0) {
+    RP_CUDA(cudaMemsetAsync(dR, 0, (size_t)n_v * nc * nc * 8, s));
+  } else {
+    RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+    RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+    const size_t wsb = tsqr_workspace_bytes(nc, n_v, tsqr_leaves(K, n_v));
+    RP_CUDA(tws.alloc(wsb, s));
+    RP_CUDA(launch_tsqr((const GramBasis *)tb.p, dX, dV, nullptr, nullptr, K, n, nc, n_v, tws.p, wsb, dR, s));
+  }
+  if (hR) {
+    RP_CUDA(cudaMemcpyAsync(R, dR, (size_t)n_v * nc * nc * 8, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  }
+  return RP_OK;
+}
+
+rp_status rp_svd_rows(const double *rows, int64_t n_rows, int32_t n_v, const rp_basis *basis,
+                      double *coef_out, double *sigma_out, rp_fit_info *info, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(rows && coef_out, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(n_rows >= 1, RP_ERR_INVALID_ARG, "n_rows = %lld", (long long)n_rows);
+  rp_status st = svd_checks(basis, n_v);
+  if (st != RP_OK) return st;
+  const int n = basis->n_vars, nc = basis->n_num + basis->n_den;
+  Tmp tr, tws, tR;
+  const double *dr;
+  if ((st = stage_in(rows, (size_t)n_v * n_rows * nc, tr, &dr, s)) != RP_OK) return st;
+  const size_t wsb = tsqr_workspace_bytes(nc, n_v, tsqr_leaves(n_rows, n_v));
+  RP_CUDA(tws.alloc(wsb, s));
+  RP_CUDA(tR.alloc((size_t)n_v * nc * nc * 8, s));
+  RP_CUDA(launch_tsqr(nullptr, nullptr, nullptr, nullptr, dr, n_rows, n, nc, n_v, tws.p, wsb, (double *)tR.p, s));
+  return svd_finish((const double *)tR.p, n_v, nc, basis->n_num, coef_out, sigma_out, info, s);
+}
+
 rp_status rp_eval_metrics(const rp_program *prog, const double *X, int64_t K, double *out, rp_stream sv) {
   cudaStream_t s = (cudaStream_t)sv;
   RP_REQUIRE(prog && out && (X || K == 0) && K >= 0, RP_ERR_INVALID_ARG, "bad argument");

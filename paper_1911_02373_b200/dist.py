@@ -47,6 +47,12 @@ class LibOps:
     def solve(self, G, num, den):
         return self.rp.solve_normal(G, num, den)
 
+    def tsqr(self, X, V, num, den, c, e):
+        return self.rp.tsqr(X, V, num, den, c, e)
+
+    def svd_rows(self, rows, num, den):
+        return self.rp.svd_rows(rows, num, den)
+
     def sweep(self, plan_or_progs, D, F=None):
         if isinstance(plan_or_progs, self.rp.Plan):
             return plan_or_progs.eval(D, second=False)[:2]
@@ -86,6 +92,41 @@ def sharded_fit(X_local, V_local, num, den, ops, n_vars: int, group=None, determ
         dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
     coef, infos = ops.solve(G, num, den)
     return coef, (c, e), infos
+
+
+def sharded_fit_svd(X_local, V_local, num, den, ops, n_vars: int, group=None):
+    """NEXT row f1 sharded over K: agree the transform (all_reduce MAX of (-lo, hi)), factor this
+    rank's rows (TSQR: R_r with R_r^T R_r = A_r^T A_r, or any B_r with that property), all_gather
+    the factors in rank order and take the SVD of the stacked [R_0; R_1; ...] -- the same
+    singular vectors as the SVD of all K rows.  Returns (coef, sigma, (c, e), infos), identical
+    on every rank (deterministic: fixed stacking order)."""
+    dev = _comm_device(group)
+    K_r = X_local.shape[0]
+    if K_r > 0:
+        lo, hi = ops.minmax(X_local)
+    else:
+        lo, hi = np.full(n_vars, np.inf), np.full(n_vars, -np.inf)
+    box = torch.tensor(np.concatenate([-np.asarray(lo), np.asarray(hi)]), dtype=torch.float64, device=dev)
+    dist.all_reduce(box, op=dist.ReduceOp.MAX, group=group)
+    box = box.cpu().numpy()
+    lo, hi = -box[:n_vars], box[n_vars:]
+    c, e = ops.xform(lo, hi)
+    R = ops.tsqr(X_local, V_local, num, den, c, e)
+    R = R if isinstance(R, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(R, dtype=np.float64))
+    R = R.to(dev).contiguous()
+    # factors may have different row counts per rank (a generic B_r): gather the counts first
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([R.shape[1]], dtype=torch.int64, device=dev)
+    cnts = [torch.empty_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    m = max(int(x.item()) for x in cnts)
+    if R.shape[1] < m:  # zero rows change nothing (A^T A is unchanged)
+        R = torch.cat([R, torch.zeros((R.shape[0], m - R.shape[1], R.shape[2]), dtype=R.dtype, device=dev)], 1)
+    parts = [torch.empty_like(R) for _ in range(world)]
+    dist.all_gather(parts, R, group=group)
+    rows = torch.cat(parts, dim=1)
+    coef, sigma, infos = ops.svd_rows(rows, num, den)
+    return coef, sigma, (c, e), infos
 
 
 def gather_winners(idx_local, E_local, nD: int, group=None):

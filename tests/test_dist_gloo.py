@@ -36,6 +36,20 @@ class OracleOps:
         out = [oracle.solve(G[i].astype(np.longdouble), len(num)) for i in range(G.shape[0])]
         return np.stack([np.asarray(r["coef"], dtype=np.float64) for r in out]), out
 
+    def tsqr(self, X, V, num, den, c, e):
+        """Any B with B^T B = A^T A serves: the shard's design rows themselves."""
+        X = np.asarray(X)
+        V = np.atleast_2d(np.asarray(V))
+        nc = len(num) + len(den)
+        return np.stack([np.asarray([oracle.design_row(num, den, c, e, x, v) for x, v in zip(X, V[i])],
+                                    dtype=np.float64).reshape(len(X), nc) for i in range(V.shape[0])])
+
+    def svd_rows(self, rows, num, den):
+        rows = np.asarray(rows.cpu() if hasattr(rows, "cpu") else rows)
+        out = [oracle.svd_rows(rows[i], len(num)) for i in range(rows.shape[0])]
+        return (np.stack([np.asarray(r["coef"], dtype=np.float64) for r in out]),
+                np.stack([np.asarray(r["sigma"], dtype=np.float64) for r in out]), out)
+
     def sweep(self, progs, D, F):
         res = [oracle.sweep(p, np.asarray(D), F) for p in progs]
         return (torch.from_numpy(np.stack([r["idx"] for r in res])),
@@ -81,6 +95,16 @@ def _worker(rank, world, port, deterministic):
         t0 = t.clone()
         dist.broadcast(t0, 0)
         assert torch.equal(t, t0)
+        # f1: SVD of the stacked shard factors == SVD of all rows (zero-padded shards included)
+        coef, sigma, (c, e), _ = dist_mod.sharded_fit_svd(fc.X[lo:hi], V[:, lo:hi], fc.num_exp, fc.den_exp, ops,
+                                                          n_vars=3)
+        for i in range(3):
+            r = oracle.fit_svd(fc.X, V[i], fc.num_exp, fc.den_exp)
+            assert np.array_equal(r["c"], c) and np.array_equal(r["e"], e)
+            want = np.asarray(r["coef"], dtype=np.float64)
+            assert np.max(np.abs(coef[i] - want)) / np.max(np.abs(want)) < 1e-12
+            sref = np.asarray(r["sigma"], dtype=np.float64)
+            assert np.max(np.abs(sigma[i] - sref)) <= 1e-13 * sref[-1]
     finally:
         dist.destroy_process_group()
 

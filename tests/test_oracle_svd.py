@@ -54,3 +54,29 @@ def test_rayleigh_quotient_optimal():
 
     assert rq(r["coef"]) <= rq(ls["coef"]) * (1 + 1e-12)
     assert abs(rq(r["coef"]) - float(r["sigma"][0])) <= 1e-9 * float(r["sigma"][-1])
+
+
+def test_svd_rows_matches_numpy_and_row_stacking():
+    """orc_svd_rows on an explicit matrix: numpy.linalg.svd's singular values and smallest right
+    singular vector; zero rows and row order change nothing (A^T A is what matters)."""
+    g = np.random.default_rng(7)
+    A = g.standard_normal((40, 9))
+    A[:, 3] = A[:, 0] - 2 * A[:, 5] + 0.5 * A[:, 8]  # a (near) null vector
+    A += 1e-6 * g.standard_normal(A.shape)
+    r = oracle.svd_rows(A, 0)  # beta_0 slot = column 0 (a large component of the null vector)
+    U, s, Vt = np.linalg.svd(A)
+    np.testing.assert_allclose(np.asarray(r["sigma"], dtype=float), s[::-1], rtol=1e-9)
+    v = Vt[-1] / Vt[-1][0]
+    np.testing.assert_allclose(np.asarray(r["coef"], dtype=float), v, rtol=1e-8, atol=1e-12)
+    r2 = oracle.svd_rows(np.concatenate([A[20:], np.zeros((5, 9)), A[:20]]), 0)
+    np.testing.assert_allclose(np.asarray(r2["coef"], dtype=float), np.asarray(r["coef"], dtype=float), rtol=1e-12,
+                               atol=1e-16)
+
+
+def test_fit_svd_equals_svd_of_design_rows():
+    fc = synth.tiny_fit_box(sigma=0.05)
+    V = np.asarray(oracle.program_metrics(fc.truths[0], fc.X)[1], dtype=np.float64) * fc.noise[1]
+    r = oracle.fit_svd(fc.X, V, fc.num_exp, fc.den_exp)
+    A = np.stack([oracle.design_row(fc.num_exp, fc.den_exp, r["c"], r["e"], x, v) for x, v in zip(fc.X, V)])
+    r2 = oracle.svd_rows(A, len(fc.num_exp))
+    assert np.array_equal(r["coef"], r2["coef"]) and np.array_equal(r["sigma"], r2["sigma"])

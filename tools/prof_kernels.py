@@ -26,6 +26,17 @@ if which == "sweep":
     for _ in range(reps):
         plan.eval(D, out=out, second=False)
     ev[1].record()
+elif which == "svd":
+    fc = synth.fitheavy(sigma=0.01)
+    X = torch.from_numpy(fc.X).to(dev)
+    V = rp.eval_metrics(fc.truths[0], X) * torch.from_numpy(fc.noise).to(dev)
+    _, sig, _, infos = rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
+    print("jacobi sweeps / cond:", [(i["cond_est"]) for i in infos])
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
+    ev[1].record()
 else:
     fc = synth.fitheavy(sigma=0.01)
     X = torch.from_numpy(fc.X).to(dev)
