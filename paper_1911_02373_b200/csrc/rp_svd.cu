@@ -50,6 +50,7 @@ struct TsqrArgs {
   double *slots;           // [n_v][2P][packed]  tree-node factors
   unsigned *counters;      // [n_v][2P]          arrival counters (zero on entry, zero on exit)
   double *R_out;           // [n_v][nc][nc]      final R (upper, zeros below the diagonal)
+  int zero;                // 0 (opaque to the compiler; see opaque_zero)
 };
 
 // One chunk absorbed into the packed R in shared memory: reflector steps j = j0 .. nc-1.
@@ -93,6 +94,12 @@ __device__ __forceinline__ double2 lds2(const double *p) {
   return r;
 }
 
+// 0, computed from x in a way the compiler cannot see through: a data dependency that orders
+// shared-memory loads after the arithmetic producing x
+__device__ __forceinline__ int opaque_zero(double x, int zero) {
+  return __double2loint(x) & zero;  // `zero` is a kernel argument (0): nothing to fold
+}
+
 __device__ __forceinline__ void publish(double *vbuf, double *par, const double (&c)[kRPL], double a_kk,
                                         int slot) {
   const int l4 = threadIdx.x & 3;
@@ -115,7 +122,7 @@ __device__ __forceinline__ void publish(double *vbuf, double *par, const double 
 }
 
 __device__ __forceinline__ void absorb_chunk(double *Rp, double *vbuf, double *par, double (&c)[kRPL], int nc,
-                                             int j0) {
+                                             int j0, int zero) {
   const int k = threadIdx.x >> 2, l4 = threadIdx.x & 3;
   const bool own = k < nc;
   // the owner of column j0 publishes its reflector
@@ -126,9 +133,13 @@ __device__ __forceinline__ void absorb_chunk(double *Rp, double *vbuf, double *p
     const double tau = par[(j & 1) * 2 + 0];
     if (own && k > j) {
       double d0 = 0.0, d1 = 0.0;
+      int z = 0;
 #pragma unroll
       for (int i = 0; i < kRPL; i += 2) {
-        const double2 vv = lds2(v + i);
+        // groups of 8 rows: the next group's loads wait for this group's FMAs (an opaque zero
+        // offset), so at most 8 v values are live next to the 2 kRPL registers of c
+        if ((i & 7) == 0 && i > 0) z = opaque_zero(d0, zero);
+        const double2 vv = lds2(v + i + z);
         d0 = fma(vv.x, c[i], d0);
         d1 = fma(vv.y, c[i + 1], d1);
       }
@@ -138,10 +149,10 @@ __device__ __forceinline__ void absorb_chunk(double *Rp, double *vbuf, double *p
       const double tw = tau * w;
 #pragma unroll
       for (int i = 0; i < kRPL; i += 2) {
-        const double2 vv = lds2(v + i);
+        if ((i & 7) == 0 && i > 0) z = opaque_zero(c[i - 1], zero);
+        const double2 vv = lds2(v + i + z);
         c[i] = fma(-tw, vv.x, c[i]);
         c[i + 1] = fma(-tw, vv.y, c[i + 1]);
-        if ((i & 7) == 6) asm volatile("" ::: "memory");  // keep at most 8 v values live
       }
       if (l4 == 0) *rjk -= tw;
       if (k == j + 1) publish(vbuf, par, c, Rp[packed_off(k, nc)], (j + 1) & 1);  // look-ahead
@@ -161,16 +172,17 @@ __device__ __forceinline__ void fill_from_packed(double (&c)[kRPL], const double
   }
 }
 
-__device__ __forceinline__ void absorb_packed(double *Rp, double *vbuf, double *par, const double *R2, int nc) {
+__device__ __forceinline__ void absorb_packed(double *Rp, double *vbuf, double *par, const double *R2, int nc,
+                                              int zero) {
   double c[kRPL];
   for (int r0 = 0; r0 < nc; r0 += kChunk) {
     fill_from_packed(c, R2, nc, r0);
-    absorb_chunk(Rp, vbuf, par, c, nc, r0);  // rows >= r0 are zero left of column r0
+    absorb_chunk(Rp, vbuf, par, c, nc, r0, zero);  // rows >= r0 are zero left of column r0
   }
 }
 
 // Shared memory: Rp [packed] | vbuf [2][kVBuf] | par [4] | sU [kChunk][8] | sD [160][kSD] | flag
-__global__ void __maxnreg__(112) k_tsqr(TsqrArgs a) {
+__global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nc = a.nc, n = a.n;
   const int64_t psz = packed_size(nc);
@@ -230,7 +242,7 @@ __global__ void __maxnreg__(112) k_tsqr(TsqrArgs a) {
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii) c[ps * 8 + ii] = k < nc ? sD[k * kSD + l4 + 4 * ii] : 0.0;
     }
-    absorb_chunk(Rp, vbuf, par, c, nc, 0);
+    absorb_chunk(Rp, vbuf, par, c, nc, 0, a.zero);
   }
 
   // ---- tree merge (heap numbering: leaves P .. P + leaves - 1, root 1) -------------------------
@@ -262,9 +274,9 @@ __global__ void __maxnreg__(112) k_tsqr(TsqrArgs a) {
     if (node & 1) {  // right child: R := R_left, then absorb my own rows
       for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) Rp[i] = __ldcg(other + i);
       __syncthreads();
-      absorb_packed(Rp, vbuf, par, mine, nc);
+      absorb_packed(Rp, vbuf, par, mine, nc, a.zero);
     } else {
-      absorb_packed(Rp, vbuf, par, other, nc);
+      absorb_packed(Rp, vbuf, par, other, nc, a.zero);
     }
     node >>= 1;
     ++h;

@@ -94,12 +94,19 @@ def test_svd_ragged_K(K):
 
 
 def test_svd_fewer_rows_than_columns():
-    """K = 12 < n_c = 20: rank K, the chosen vector solves A coef = 0 to rounding."""
+    """K = 12 < n_c = 20: rank K and an 8-dimensional null space (the paper's rank deficiency,
+    PAPER.md:2609-2611).  Any null vector is a least-squares solution: the chosen one solves
+    A v = 0 to rounding, or -- when its beta_0 vanishes -- the call reports DEGENERATE."""
     fc = synth.tiny_fit_box(sigma=0.01)
     X, V = fc.X[:12], _metrics(fc)[:, :12]
-    coef, sigma, (c, e), infos = rp.fit_svd(_cuda(X), _cuda(V), fc.num_exp, fc.den_exp)
+    coef, sigma, (c, e), infos = rp.fit_svd(_cuda(X), _cuda(V), fc.num_exp, fc.den_exp, raise_on_degenerate=False)
     for i in range(3):
         assert infos[i]["rank"] == 12
+        assert np.all(sigma[i][:8] <= 1e-13 * sigma[i][-1])
+        if infos[i]["status"] == 3:
+            assert np.all(np.isnan(coef[i]))
+            continue
+        assert infos[i]["status"] == 0
         A = np.stack([np.asarray(oracle.design_row(fc.num_exp, fc.den_exp, c, e, x, v), dtype=np.float64)
                       for x, v in zip(X, V[i])])
         assert np.linalg.norm(A @ coef[i]) <= 1e-12 * np.linalg.norm(A) * np.linalg.norm(coef[i])
