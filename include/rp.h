@@ -110,6 +110,8 @@ typedef struct {
   double resid2;     /* coef^T G coef = sum_r (p(x_r) - V_r q(x_r))^2                        */
   double min_pivot;  /* smallest pivot of the equilibrated Cholesky factor (squared diag)   */
   double cond_est;   /* (max pivot / min pivot) of the equilibrated factorisation          */
+  int32_t iters;     /* solves (rp_fit: 1, rp_fit_sk: iters) or Jacobi sweeps (rp_fit_svd)  */
+  int32_t reserved;
 } rp_fit_info;
 
 /* ---- library --------------------------------------------------------------------------- */
@@ -179,7 +181,7 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
  * footnote PAPER.md:2595-2598): coef = the right singular vector of the smallest singular value
  * of A_m = [M(u_r) | -V_m[r] N(u_r)] (rows as in rp_gram_accumulate), scaled so that beta_0 = 1
  * (reading R12).  A is never formed in memory: a Householder TSQR builds R (A = QR) from design
- * rows generated on chip, and a one-sided Jacobi SVD of R (2-CTA cluster per metric) gives the
+ * rows generated on chip, and a one-sided Jacobi SVD of R (one CTA per metric) gives the
  * right singular vectors.  Deterministic (fixed merge tree).
  *
  * rp_fit_svd: transform from the sample box as rp_fit, then TSQR + SVD.  X [K][n], V [n_v][K]

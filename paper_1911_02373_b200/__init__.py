@@ -73,7 +73,7 @@ assert DECISION_DTYPE.itemsize == C.sizeof(rp_decision) == 48
 
 class rp_fit_info(C.Structure):
     _fields_ = [("rank", C.c_int32), ("status", C.c_int32), ("resid2", C.c_double),
-                ("min_pivot", C.c_double), ("cond_est", C.c_double)]
+                ("min_pivot", C.c_double), ("cond_est", C.c_double), ("iters", C.c_int32), ("reserved", C.c_int32)]
 
 
 _vp, _i32, _i64 = C.c_void_p, C.c_int32, C.c_int64
@@ -429,7 +429,8 @@ def fit_sk(X, V, num_exp, den_exp, iters: int = 3, raise_on_degenerate: bool = T
 
 
 def _infos(infos):
-    return [dict(rank=i.rank, status=i.status, resid2=i.resid2, min_pivot=i.min_pivot, cond_est=i.cond_est)
+    return [dict(rank=i.rank, status=i.status, resid2=i.resid2, min_pivot=i.min_pivot, cond_est=i.cond_est,
+                 iters=i.iters)
             for i in infos]
 
 

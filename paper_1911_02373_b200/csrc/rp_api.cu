@@ -574,6 +574,8 @@ static rp_status solve_impl(const double *dG, int32_t n_v, int nc, int beta0, do
       info[v].resid2 = hinfo[v * 5 + 2];
       info[v].min_pivot = hinfo[v * 5 + 3];
       info[v].cond_est = hinfo[v * 5 + 4];
+      info[v].iters = 1;
+      info[v].reserved = 0;
     }
     if (stv != 0) worst = (rp_status)stv;
   }
@@ -701,6 +703,8 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
       info[v].resid2 = hinfo[v * 5 + 2];
       info[v].min_pivot = hinfo[v * 5 + 3];
       info[v].cond_est = hinfo[v * 5 + 4];
+      info[v].iters = iters;
+      info[v].reserved = 0;
     }
     if (stv != 0) worst = (rp_status)stv;
   }
@@ -714,9 +718,10 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
 static rp_status svd_finish(const double *dR, int32_t n_v, int nc, int n_num, double *coef_out,
                             double *sigma_out, rp_fit_info *info, cudaStream_t s) {
   Tmp to;
-  RP_CUDA(to.alloc((size_t)n_v * (2 * nc + 6) * 8, s));
+  RP_CUDA(to.alloc((size_t)n_v * (2 * nc + 6 + nc * nc) * 8, s));
   double *dc = (double *)to.p, *dsg = dc + (size_t)n_v * nc, *di = dsg + (size_t)n_v * nc;
-  RP_CUDA(launch_svd_jacobi(dR, nc, n_num, n_v, dc, dsg, di, s));
+  double *dV = di + (size_t)n_v * 6;
+  RP_CUDA(launch_svd_jacobi(dR, nc, n_num, n_v, dV, dc, dsg, di, s));
   std::vector<double> hinfo((size_t)n_v * 6);
   RP_CUDA(cudaMemcpyAsync(coef_out, dc, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
   if (sigma_out) RP_CUDA(cudaMemcpyAsync(sigma_out, dsg, (size_t)n_v * nc * 8, cudaMemcpyDeviceToHost, s));
@@ -731,6 +736,8 @@ static rp_status svd_finish(const double *dR, int32_t n_v, int nc, int n_num, do
       info[v].resid2 = hinfo[v * 6 + 2];
       info[v].min_pivot = hinfo[v * 6 + 3];
       info[v].cond_est = hinfo[v * 6 + 4];
+      info[v].iters = (int32_t)hinfo[v * 6 + 5];
+      info[v].reserved = 0;
     }
     if (stv != 0) worst = (rp_status)stv;
   }

@@ -124,14 +124,14 @@ cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *co
                          double *info_out, cudaStream_t s);
 
 // f1 (rp_svd.cu): Householder TSQR of the design rows (X, V[, S] through d_basis) or of dense
-// rows [n_v][K][nc], then the one-sided Jacobi SVD of R on a 2-CTA cluster per metric.
+// rows [n_v][K][nc], then the one-sided Jacobi SVD of R (one CTA per metric, V in L2).
 int tsqr_leaves(int64_t K, int n_v);
 size_t tsqr_workspace_bytes(int nc, int n_v, int leaves);
 cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double *V, const double *S,
                         const double *rows, int64_t K, int n, int nc, int n_v, void *ws, size_t ws_bytes,
                         double *R_out, cudaStream_t s);
-cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *coef, double *sigma,
-                              double *info, cudaStream_t s);
+cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *V_ws, double *coef,
+                              double *sigma, double *info, cudaStream_t s);
 
 int num_sms();
 

@@ -15,22 +15,18 @@
 //      factors are merged by a binary tree inside the same launch: the second CTA to reach a
 //      tree node stacks [R_left; R_right] (fixed order: deterministic) and re-triangularises;
 //      the root writes R.
-//   2. k_svd_jacobi -- one-sided (Hestenes) Jacobi SVD of R on a 2-CTA thread-block cluster
-//      per metric: CTA 0 holds R (column-major, 157 KB at n_c = 140) and computes the
-//      rotations of one round-robin round (all pairs disjoint, one warp per pair); it writes
-//      them into CTA 1's shared memory (DSMEM), and CTA 1 applies them to the accumulated V
-//      while CTA 0 computes the next round.  Singular values are the final column norms.
-#include <cooperative_groups.h>
-
+//   2. k_svd_jacobi -- one-sided (Hestenes) Jacobi SVD of R, one CTA per metric: R lives in
+//      shared memory (column-major, 157 KB at n_c = 140), the accumulated rotations V in L2;
+//      each round of the round-robin ordering (all pairs disjoint) gives one pair per warp,
+//      whose V columns are fetched before the dot products so that their latency overlaps.
+//      Singular values are the final column norms.
 #include "rp_internal.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace rp {
 
-constexpr int kSvdMaxCols = 144;      // one quad per column, 8 quads per warp -> 576 threads
-constexpr int kRPL = 24;              // chunk rows per lane
-constexpr int kChunk = 4 * kRPL;      // rows per chunk (128)
+constexpr int kSvdMaxCols = 144;      // two columns per octet of lanes, 4 octets per warp -> 576 threads
+constexpr int kRPL = 12;              // chunk rows per lane (rows l8 + 8 i)
+constexpr int kChunk = 8 * kRPL;      // rows per chunk (96)
 constexpr int kSD = 36;               // staging stride (32 rows + pad, = 4 mod 16)
 constexpr int kTsqrMaxThreads = 576;
 constexpr int kJacThreads = 1024;
@@ -50,13 +46,16 @@ struct TsqrArgs {
   double *slots;           // [n_v][2P][packed]  tree-node factors
   unsigned *counters;      // [n_v][2P]          arrival counters (zero on entry, zero on exit)
   double *R_out;           // [n_v][nc][nc]      final R (upper, zeros below the diagonal)
-  int zero;                // 0 (opaque to the compiler; see opaque_zero)
 };
 
-// One chunk absorbed into the packed R in shared memory: reflector steps j = j0 .. nc-1.
-// Thread layout: quad q owns column k = q, lane l4 = lane & 3 owns chunk rows l4 + 4 i.
-// c[] holds this thread's chunk entries; vbuf[2][kChunk] the scaled Householder vector of the
-// current column (double-buffered), par[2][2] = (tau, beta).
+// One chunk of kChunk rows is absorbed into the packed R in shared memory by Householder
+// reflectors j = j0 .. nc-1 acting on [R; chunk].  Thread layout: octet o = tid / 8 owns
+// columns 2o and 2o + 1 of the chunk in registers (c[h][i] = row l8 + 8 i of column 2o + h,
+// l8 = tid % 8).  Reflector j is published by the octet owning column j once it has applied
+// reflectors 0 .. j-1 to that column: the scaled vector into RV[j], tau into par[j], beta onto
+// the diagonal of R, then flags[j] = seq (release).  Every octet applies the reflectors in order
+// as soon as they are published (acquire), so a chunk proceeds as a wavefront over the warps,
+// with no block-wide barrier per column.
 __device__ __forceinline__ void householder_params(double a, double sub, double &tau, double &beta,
                                                    double &s) {
   // H = I - tau v v^T with v = (1, s * x_sub): H (a, x_sub) = (beta, 0)
@@ -72,131 +71,161 @@ __device__ __forceinline__ void householder_params(double a, double sub, double 
   }
 }
 
-// sum over the 4 lanes of a quad; conditions on the quad's column keep quads convergent, so
-// the mask names only this quad's lanes
-__device__ __forceinline__ double quad_sum(double x) {
-  const unsigned m = 0xFu << (threadIdx.x & 28);
+// sum over the 8 lanes of an octet (conditions on the octet's columns keep octets convergent,
+// so the mask names only this octet's lanes)
+__device__ __forceinline__ double oct_sum(double x) {
+  const unsigned m = 0xFFu << (threadIdx.x & 24);
   x += __shfl_xor_sync(m, x, 1);
   x += __shfl_xor_sync(m, x, 2);
+  x += __shfl_xor_sync(m, x, 4);
   return x;
 }
 
-// Householder vector layout in vbuf: lane l4's 32 rows contiguous at l4 * kVS (kVS = 34: the
-// four 16-byte lane segments of a LDS.128 fall in distinct banks)
+// Householder vector layout in RV[j]: lane l8's kRPL rows contiguous at l8 * kVS (kVS = 14: the
+// eight 16-byte lane segments of a LDS.128 fall in distinct banks, one wavefront per load)
 constexpr int kVS = kRPL + 2;
-constexpr int kVBuf = 4 * kVS;
+constexpr int kVBuf = 8 * kVS;
 
-// shared-memory 2 x f64 load that the compiler may not cache in registers (the update pass
-// re-reads v instead of keeping 32 more doubles live)
-__device__ __forceinline__ double2 lds2(const double *p) {
-  double2 r;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return r;
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
 }
 
-// 0, computed from x in a way the compiler cannot see through: a data dependency that orders
-// shared-memory loads after the arithmetic producing x
-__device__ __forceinline__ int opaque_zero(double x, int zero) {
-  return __double2loint(x) & zero;  // `zero` is a kernel argument (0): nothing to fold
-}
-
-__device__ __forceinline__ void publish(double *vbuf, double *par, const double (&c)[kRPL], double a_kk,
-                                        int slot) {
-  const int l4 = threadIdx.x & 3;
+__device__ __forceinline__ void publish(double *Rp, double *RV, double *par, int *flags, const double (&c)[kRPL],
+                                        int k, int nc, int seq) {
+  const int l8 = threadIdx.x & 7;
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int i = 0; i < kRPL; i += 2) {
     s0 = fma(c[i], c[i], s0);
     s1 = fma(c[i + 1], c[i + 1], s1);
   }
-  const double sub = quad_sum(s0 + s1);
+  const double sub = oct_sum(s0 + s1);
+  double *rkk = Rp + packed_off(k, nc);
   double tau, beta, sc;
-  householder_params(a_kk, sub, tau, beta, sc);
-  double *vn = vbuf + slot * kVBuf + l4 * kVS;
+  householder_params(*rkk, sub, tau, beta, sc);
+  double *vn = RV + k * kVBuf + l8 * kVS;
 #pragma unroll
   for (int i = 0; i < kRPL; i += 2) *(double2 *)(vn + i) = make_double2(sc * c[i], sc * c[i + 1]);
-  if (l4 == 0) {
-    par[slot * 2 + 0] = tau;
-    par[slot * 2 + 1] = beta;
+  __syncwarp(0xFFu << (threadIdx.x & 24));  // the octet's eight slices are written (and ordered)
+  if (l8 == 0) {
+    par[k] = tau;
+    *rkk = beta;
+    st_release(flags + k, seq);
   }
 }
 
-__device__ __forceinline__ void absorb_chunk(double *Rp, double *vbuf, double *par, double (&c)[kRPL], int nc,
-                                             int j0, int zero) {
-  const int k = threadIdx.x >> 2, l4 = threadIdx.x & 3;
-  const bool own = k < nc;
-  // the owner of column j0 publishes its reflector
-  if (own && k == j0) publish(vbuf, par, c, Rp[packed_off(k, nc)], j0 & 1);
-  for (int j = j0; j < nc; ++j) {
-    __syncthreads();
-    const double *v = vbuf + (j & 1) * kVBuf + l4 * kVS;
-    const double tau = par[(j & 1) * 2 + 0];
-    if (own && k > j) {
-      double d0 = 0.0, d1 = 0.0;
-      int z = 0;
+// reflector j applied to column k (entries c): R[j][k] and c updated
+__device__ __forceinline__ void apply_col(double *Rp, double (&c)[kRPL], const double (&v)[kRPL], double tau,
+                                          int j, int k, int nc) {
+  double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < kRPL; i += 2) {
-        // groups of 8 rows: the next group's loads wait for this group's FMAs (an opaque zero
-        // offset), so at most 8 v values are live next to the 2 kRPL registers of c
-        if ((i & 7) == 0 && i > 0) z = opaque_zero(d0, zero);
-        const double2 vv = lds2(v + i + z);
-        d0 = fma(vv.x, c[i], d0);
-        d1 = fma(vv.y, c[i + 1], d1);
-      }
-      const double dot = quad_sum(d0 + d1);
-      double *rjk = Rp + packed_off(j, nc) + (k - j);
-      const double w = *rjk + dot;
-      const double tw = tau * w;
+  for (int i = 0; i < kRPL; i += 2) {
+    d0 = fma(v[i], c[i], d0);
+    d1 = fma(v[i + 1], c[i + 1], d1);
+  }
+  const double dot = oct_sum(d0 + d1);
+  double *rjk = Rp + packed_off(j, nc) + (k - j);
+  const double tw = tau * (*rjk + dot);
 #pragma unroll
-      for (int i = 0; i < kRPL; i += 2) {
-        if ((i & 7) == 0 && i > 0) z = opaque_zero(c[i - 1], zero);
-        const double2 vv = lds2(v + i + z);
-        c[i] = fma(-tw, vv.x, c[i]);
-        c[i + 1] = fma(-tw, vv.y, c[i + 1]);
+  for (int i = 0; i < kRPL; ++i) c[i] = fma(-tw, v[i], c[i]);
+  if ((threadIdx.x & 7) == 0) *rjk -= tw;
+}
+
+__device__ __forceinline__ void absorb_chunk(double *Rp, double *RV, double *par, int *flags,
+                                             double (&c)[2][kRPL], int nc, int j0, int seq) {
+  const int o = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int k0 = 2 * o, k1 = 2 * o + 1;
+  const int w0 = (threadIdx.x >> 5) * 8;  // first column of this warp
+  __syncthreads();                        // RV aliases the staging buffer of the chunk fill
+  if (w0 < nc && w0 + 7 >= j0) {
+    if (k0 == j0 && k0 < nc) publish(Rp, RV, par, flags, c[0], k0, nc, seq);
+    if (k1 == j0 && k1 < nc) publish(Rp, RV, par, flags, c[1], k1, nc, seq);
+    const int jend = min(w0 + 7, nc - 1);  // reflectors this warp needs: j < its last column
+    for (int j = j0; j < jend; ++j) {
+      if (j < w0) {
+        // warps far behind the wavefront front back off longer: spinning steals issue slots
+        // from the warp on the critical path (the owner of column j + 1)
+        const unsigned ns = (w0 - j) > 16 ? 256u : 16u;
+        while (ld_acquire(flags + j) != seq) __nanosleep(ns);
+      } else {
+        __syncwarp();  // published by an octet of this warp at iteration j - 1
       }
-      if (l4 == 0) *rjk -= tw;
-      if (k == j + 1) publish(vbuf, par, c, Rp[packed_off(k, nc)], (j + 1) & 1);  // look-ahead
+      const bool a0 = k0 > j && k0 < nc, a1 = k1 > j && k1 < nc;
+      if (a1) {  // k1 > j whenever k0 > j
+        double v[kRPL];
+        const double *vs = RV + j * kVBuf + l8 * kVS;
+#pragma unroll
+        for (int i = 0; i < kRPL; i += 2) {
+          const double2 t = *(const double2 *)(vs + i);
+          v[i] = t.x;
+          v[i + 1] = t.y;
+        }
+        const double tau = par[j];
+        if (a0) apply_col(Rp, c[0], v, tau, j, k0, nc);
+        apply_col(Rp, c[1], v, tau, j, k1, nc);
+        if (k0 == j + 1 && a0) publish(Rp, RV, par, flags, c[0], k0, nc, seq);
+        if (k1 == j + 1) publish(Rp, RV, par, flags, c[1], k1, nc, seq);
+      }
     }
-    if (own && k == j && l4 == 0) Rp[packed_off(j, nc)] = par[(j & 1) * 2 + 1];
   }
   __syncthreads();
 }
 
-// rows [r0, r0 + kChunk) of R2 (packed, global) as chunk entries of column k
-__device__ __forceinline__ void fill_from_packed(double (&c)[kRPL], const double *R2, int nc, int r0) {
-  const int k = threadIdx.x >> 2, l4 = threadIdx.x & 3;
+// rows [r0, r0 + kChunk) of R2 (packed, global) as chunk entries of columns 2o, 2o + 1
+__device__ __forceinline__ void fill_from_packed(double (&c)[2][kRPL], const double *R2, int nc, int r0) {
+  const int o = threadIdx.x >> 3, l8 = threadIdx.x & 7;
 #pragma unroll
-  for (int i = 0; i < kRPL; ++i) {
-    const int rho = r0 + l4 + 4 * i;
-    c[i] = (k < nc && rho < nc && k >= rho) ? __ldcg(R2 + packed_off(rho, nc) + (k - rho)) : 0.0;
+  for (int h = 0; h < 2; ++h) {
+    const int k = 2 * o + h;
+#pragma unroll
+    for (int i = 0; i < kRPL; ++i) {
+      const int rho = r0 + l8 + 8 * i;
+      c[h][i] = (k < nc && rho < nc && k >= rho) ? __ldcg(R2 + packed_off(rho, nc) + (k - rho)) : 0.0;
+    }
   }
 }
 
-__device__ __forceinline__ void absorb_packed(double *Rp, double *vbuf, double *par, const double *R2, int nc,
-                                              int zero) {
-  double c[kRPL];
+__device__ __forceinline__ void absorb_packed(double *Rp, double *RV, double *par, int *flags, const double *R2,
+                                              int nc, int &seq) {
+  double c[2][kRPL];
   for (int r0 = 0; r0 < nc; r0 += kChunk) {
     fill_from_packed(c, R2, nc, r0);
-    absorb_chunk(Rp, vbuf, par, c, nc, r0, zero);  // rows >= r0 are zero left of column r0
+    absorb_chunk(Rp, RV, par, flags, c, nc, r0, ++seq);  // rows >= r0 are zero left of column r0
   }
 }
 
-// Shared memory: Rp [packed] | vbuf [2][kVBuf] | par [4] | sU [kChunk][8] | sD [160][kSD] | flag
+__host__ __device__ inline int64_t tsqr_rv_elems(int nc) {  // reflector store, aliased by sD
+  const int64_t rv = (int64_t)nc * kVBuf, sd = (int64_t)kSD * kSvdMaxCols;
+  return rv > sd ? rv : sd;
+}
+
+// Shared memory: Rp [packed] | RV [nc][kVBuf] (aliased by sD [144][kSD] during the fill) |
+// par [144] | sU [8][kChunk] | flags [144] | flag
 __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nc = a.nc, n = a.n;
   const int64_t psz = packed_size(nc);
   double *Rp = sm;
-  double *vbuf = Rp + ((psz + 1) & ~1ll);
-  double *par = vbuf + 2 * kVBuf;
-  double *sU = par + 4;
-  double *sD = sU + kChunk * kMaxVars;
-  int *flag = (int *)(sD + kSD * kSvdMaxCols);
+  double *RV = Rp + ((psz + 1) & ~1ll);
+  double *sD = RV;
+  double *par = RV + tsqr_rv_elems(nc);
+  double *sU = par + kSvdMaxCols;
+  int *flags = (int *)(sU + kChunk * kMaxVars);
+  int *flag = flags + kSvdMaxCols;
+  int seq = 0;
   const int metric = blockIdx.y;
   const int leaf = blockIdx.x;
-  const int k = threadIdx.x >> 2, l4 = threadIdx.x & 3;
+  const int o = threadIdx.x >> 3, l8 = threadIdx.x & 7;
 
   for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) Rp[i] = 0.0;
+  for (int i = threadIdx.x; i < kSvdMaxCols; i += blockDim.x) flags[i] = 0;
   __syncthreads();
 
   // ---- leaf: the slab's rows ----------------------------------------------------------------
@@ -207,15 +236,15 @@ __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
   for (int64_t r0 = r_begin; r0 < r_end; r0 += kChunk) {
     const int cnt = (int)((r_end - r0) < kChunk ? (r_end - r0) : kChunk);
     if (!rows) {
-      // a10: u = (x - c) 2^-e of the chunk's rows
+      // a10: u = (x - c) 2^-e of the chunk's rows (variable-major: conflict-free reads below)
       for (int i = threadIdx.x; i < cnt * n; i += blockDim.x) {
         const int r = i / n, t = i % n;
-        sU[r * kMaxVars + t] = (a.X[(r0 + r) * n + t] - a.basis->xc[t]) * ldexp(1.0, -a.basis->xe[t]);
+        sU[t * kChunk + r] = (a.X[(r0 + r) * n + t] - a.basis->xc[t]) * ldexp(1.0, -a.basis->xe[t]);
       }
     }
-    // the chunk's entries are staged through sD in 4 passes of 32 rows (column-major, stride
-    // kSD = 36: a quad-row read pattern is conflict-free), then picked up into registers
-    double c[kRPL];
+    // the chunk's entries are staged through sD in passes of 32 rows (column-major, stride
+    // kSD = 36: the octet-row read pattern is conflict-free), then picked up into registers
+    double c[2][kRPL];
 #pragma unroll
     for (int ps = 0; ps < kChunk / 32; ++ps) {
       __syncthreads();
@@ -229,7 +258,7 @@ __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
             // a11: design row entry: M_col(u), or -V N_col(u) (times the row scale S)
             m = 1.0;
             for (int t = 0; t < n; ++t) {
-              const double u = sU[r * kMaxVars + t];
+              const double u = sU[t * kChunk + r];
               for (int e = 0; e < a.basis->exp[col][t]; ++e) m *= u;
             }
             if (col >= a.basis->n_num) m *= -V[r0 + r];
@@ -240,9 +269,12 @@ __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
       }
       __syncthreads();
 #pragma unroll
-      for (int ii = 0; ii < 8; ++ii) c[ps * 8 + ii] = k < nc ? sD[k * kSD + l4 + 4 * ii] : 0.0;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+          c[h][ps * 4 + ii] = 2 * o + h < nc ? sD[(2 * o + h) * kSD + l8 + 8 * ii] : 0.0;
     }
-    absorb_chunk(Rp, vbuf, par, c, nc, 0, a.zero);
+    absorb_chunk(Rp, RV, par, flags, c, nc, 0, ++seq);
   }
 
   // ---- tree merge (heap numbering: leaves P .. P + leaves - 1, root 1) -------------------------
@@ -274,9 +306,9 @@ __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
     if (node & 1) {  // right child: R := R_left, then absorb my own rows
       for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) Rp[i] = __ldcg(other + i);
       __syncthreads();
-      absorb_packed(Rp, vbuf, par, mine, nc, a.zero);
+      absorb_packed(Rp, RV, par, flags, mine, nc, seq);
     } else {
-      absorb_packed(Rp, vbuf, par, other, nc, a.zero);
+      absorb_packed(Rp, RV, par, flags, other, nc, seq);
     }
     node >>= 1;
     ++h;
@@ -290,19 +322,16 @@ __global__ void __maxnreg__(96) k_tsqr(TsqrArgs a) {
 }
 
 // ============================================================================================
-// one-sided Jacobi SVD of R on a 2-CTA cluster
+// one-sided Jacobi SVD of R (one CTA per metric)
 // ============================================================================================
 struct JacArgs {
   const double *R;  // [n_v][nc][nc] row-major (any square matrix works)
   int nc, n_num;
+  double *V;        // [n_v][nc][nc] workspace: accumulated rotations, column-major (L2-resident)
   double *coef;     // [n_v][nc]
   double *sigma;    // [n_v][nc] ascending
   double *info;     // [n_v][6]: status, rank, resid2, sigma_min, sigma_max / sigma_min, sweeps
 };
-
-__device__ __forceinline__ int rr_player(int pos, int t, int np) {  // round-robin tournament
-  return pos == 0 ? 0 : 1 + (pos - 1 + t) % (np - 1);
-}
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -310,158 +339,134 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
-// Shared memory (each CTA): M [nc][ld] column-major (CTA 0: A = R, CTA 1: V) | rot [2][kSvdMaxCols/2][2]
-// | ctl[4]
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kJacThreads, 1) k_svd_jacobi(JacArgs a) {
+constexpr int kJacPer16 = (kSvdMaxCols + 15) / 16;  // column entries per lane of a 16-lane pair group
+
+// Shared memory: A [nc][ld] column-major (ld odd) | sched [np-1][np/2] (p, q as uint8 pairs) |
+// sig [nc] | ctl[4]
+__global__ void __launch_bounds__(kJacThreads, 1) k_svd_jacobi(JacArgs a) {
   extern __shared__ __align__(16) double sj[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const unsigned crank = cluster.block_rank();
-  const int nc = a.nc, ld = nc | 1;  // odd stride: row-wise scans stay conflict-free
-  const int np = (nc + 1) & ~1;      // players (a dummy when nc is odd)
-  const int npairs = np / 2;
-  double *M = sj;
-  double *rot = M + (int64_t)nc * ld;
-  int *ctl = (int *)(rot + 2 * (kSvdMaxCols / 2) * 2);  // [0] rotated this sweep, [1] continue, [2] jmin
-  double *rot1 = cluster.map_shared_rank(rot, 1);
-  int *ctl1 = cluster.map_shared_rank(ctl, 1);
-  const int metric = blockIdx.y;
+  const int nc = a.nc, ld = nc | 1;
+  const int np = (nc + 1) & ~1;  // players (a dummy when nc is odd)
+  const int npairs = np / 2, nrounds = np - 1;
+  double *A = sj;
+  uint16_t *sched = (uint16_t *)(A + (int64_t)nc * ld);
+  double *sig = (double *)(sched + ((nrounds * npairs + 3) & ~3));
+  int *ctl = (int *)(sig + kSvdMaxCols);
+  const int metric = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double *R = a.R + (int64_t)metric * nc * nc;
+  double *V = a.V + (int64_t)metric * nc * nc;
 
-  if (crank == 0) {
-    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
-      const int r = i / nc, col = i % nc;
-      M[col * ld + r] = R[i];
-    }
-  } else {
-    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
-      const int r = i / nc, col = i % nc;
-      M[col * ld + r] = r == col ? 1.0 : 0.0;
-    }
+  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
+    const int r = i / nc, col = i % nc;
+    A[col * ld + r] = R[i];
+    V[i] = (i % (nc + 1)) == 0 ? 1.0 : 0.0;  // V = I (column-major == row-major for I)
   }
-  if (threadIdx.x == 0) ctl[0] = ctl[1] = 0;
-  cluster.sync();
+  // round-robin tournament: position 0 fixed, the others rotate; pair m of round t is
+  // (pos m, pos np-1-m).  Stored as (min, max) so every rotation acts on (p < q).
+  for (int i = threadIdx.x; i < nrounds * npairs; i += blockDim.x) {
+    const int t = i / npairs, m = i % npairs;
+    const int pm = m == 0 ? 0 : 1 + (m - 1 + t) % (np - 1);
+    const int pq = 1 + (np - 2 - m + t) % (np - 1);
+    const int p = pm < pq ? pm : pq, q = pm < pq ? pq : pm;
+    sched[i] = (uint16_t)(p | (q << 8));
+  }
+  if (threadIdx.x < 4) ctl[threadIdx.x] = 0;
+  __syncthreads();
 
   const double tol = 1e-15 * sqrt((double)nc);
   int sweep = 0;
   for (; sweep < kJacMaxSweeps; ++sweep) {
-    for (int t = 0; t <= np - 1; ++t) {  // rounds 0 .. np-2 computed, round t-1 applied
-      if (crank == 0 && t < np - 1) {
-        for (int m = wid; m < npairs; m += nw) {
-          int p = rr_player(m, t, np), q = rr_player(np - 1 - m, t, np);
-          if (p > q) {
-            const int x = p;
-            p = q;
-            q = x;
+    const int flag = sweep & 1;  // ctl[flag]: something rotated in this sweep
+    for (int t = 0; t < nrounds; ++t) {
+      // 16 lanes per pair, 2 pairs per warp: the scalar rotation math is shared by half a warp
+      // instead of repeated by all 32 lanes (the FP64 pipe is the bottleneck of a round)
+      for (int m0 = wid * 2; m0 < npairs; m0 += nw * 2) {
+        const int m = m0 + (lane >> 4), l16 = lane & 15;
+        const unsigned pqv = m < npairs ? sched[t * npairs + m] : 0xffffu;
+        const int p = pqv & 0xff, q = pqv >> 8;
+        const bool valid = q < nc;
+        double *ap = A + (valid ? p : 0) * ld, *aq = A + (valid ? q : 0) * ld;
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int i = 0; i < kJacPer16; ++i) {
+          const int r = l16 + 16 * i;
+          const double x = (valid && r < nc) ? ap[r] : 0.0;
+          const double y = (valid && r < nc) ? aq[r] : 0.0;
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (valid && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          double *vp = V + (int64_t)p * nc, *vq = V + (int64_t)q * nc;
+          double xv[kJacPer16], yv[kJacPer16];
+#pragma unroll
+          for (int i = 0; i < kJacPer16; ++i) {  // issued before the rotation math: latency overlap
+            const int r = l16 + 16 * i;
+            xv[i] = r < nc ? __ldcg(vp + r) : 0.0;
+            yv[i] = r < nc ? __ldcg(vq + r) : 0.0;
           }
-          double cs = 1.0, sn = 0.0;
-          if (q < nc) {
-            double *ap = M + p * ld, *aq = M + q * ld;
-            double al = 0.0, be = 0.0, ga = 0.0;
-            for (int r = lane; r < nc; r += 32) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = 1.0 / sqrt(fma(tt, tt, 1.0));
+          const double sn = cs * tt;
+#pragma unroll
+          for (int i = 0; i < kJacPer16; ++i) {
+            const int r = l16 + 16 * i;
+            if (r < nc) {  // A re-read from shared memory (fewer live registers)
               const double x = ap[r], y = aq[r];
-              al = fma(x, x, al);
-              be = fma(y, y, be);
-              ga = fma(x, y, ga);
-            }
-            al = warp_sum(al);
-            be = warp_sum(be);
-            ga = warp_sum(ga);
-            if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-              const double zeta = (be - al) / (2.0 * ga);
-              const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-              cs = 1.0 / sqrt(fma(tt, tt, 1.0));
-              sn = cs * tt;
-              for (int r = lane; r < nc; r += 32) {
-                const double x = ap[r], y = aq[r];
-                ap[r] = cs * x - sn * y;
-                aq[r] = sn * x + cs * y;
-              }
-              if (lane == 0) ctl[0] = 1;
+              ap[r] = cs * x - sn * y;
+              aq[r] = sn * x + cs * y;
+              __stcg(vp + r, cs * xv[i] - sn * yv[i]);
+              __stcg(vq + r, sn * xv[i] + cs * yv[i]);
             }
           }
-          if (lane == 0) {
-            rot1[((t & 1) * (kSvdMaxCols / 2) + m) * 2 + 0] = cs;
-            rot1[((t & 1) * (kSvdMaxCols / 2) + m) * 2 + 1] = sn;
-          }
+          if (l16 == 0) ctl[flag] = 1;
         }
       }
-      if (crank == 1 && t > 0) {  // apply round t-1 to V
-        const int tp = t - 1;
-        for (int m = wid; m < npairs; m += nw) {
-          int p = rr_player(m, tp, np), q = rr_player(np - 1 - m, tp, np);
-          if (p > q) {
-            const int x = p;
-            p = q;
-            q = x;
-          }
-          const double cs = rot[((tp & 1) * (kSvdMaxCols / 2) + m) * 2 + 0];
-          const double sn = rot[((tp & 1) * (kSvdMaxCols / 2) + m) * 2 + 1];
-          if (q < nc && sn != 0.0) {
-            double *vp = M + p * ld, *vq = M + q * ld;
-            for (int r = lane; r < nc; r += 32) {
-              const double x = vp[r], y = vq[r];
-              vp[r] = cs * x - sn * y;
-              vq[r] = sn * x + cs * y;
-            }
-          }
-        }
-      }
-      cluster.sync();
+      __syncthreads();
     }
-    // sweep done: CTA 0 tells CTA 1 whether anything rotated
-    if (crank == 0 && threadIdx.x == 0) {
-      const int cont = ctl[0];
-      ctl[1] = cont;
-      ctl1[1] = cont;
-      ctl[0] = 0;
-    }
-    cluster.sync();
-    if (!ctl[1]) break;
+    const int rotated = ctl[flag];
+    if (threadIdx.x == 0) ctl[flag ^ 1] = 0;  // next sweep's flag (nobody writes it before the barrier)
+    __syncthreads();
+    if (!rotated) break;
   }
 
-  // ---- singular values (CTA 0), the vector of the smallest (CTA 1) -----------------------------
-  double *sig = rot;  // reuse (CTA 0): sigma per column; needs nc <= kSvdMaxCols doubles
-  if (crank == 0) {
-    for (int col = wid; col < nc; col += nw) {
-      double s2 = 0.0;
-      for (int r = lane; r < nc; r += 32) s2 = fma(M[col * ld + r], M[col * ld + r], s2);
-      s2 = warp_sum(s2);
-      if (lane == 0) sig[col] = sqrt(s2);
-    }
-    __syncthreads();
-    // ascending order by rank counting (ties by column index), smallest -> jmin
-    double *so = a.sigma + (int64_t)metric * nc;
-    for (int col = threadIdx.x; col < nc; col += blockDim.x) {
-      const double v = sig[col];
-      int rank = 0;
-      for (int o = 0; o < nc; ++o) rank += (sig[o] < v) || (sig[o] == v && o < col);
-      so[rank] = v;
-      if (rank == 0) ctl1[2] = col;
-    }
+  // ---- singular values = column norms; the vector of the smallest -------------------------------
+  for (int col = wid; col < nc; col += nw) {
+    double s2 = 0.0;
+    for (int r = lane; r < nc; r += 32) s2 = fma(A[col * ld + r], A[col * ld + r], s2);
+    s2 = warp_sum(s2);
+    if (lane == 0) sig[col] = sqrt(s2);
   }
-  cluster.sync();
-  double *rot0 = cluster.map_shared_rank(rot, 0);
-  if (crank == 1) {
-    const int jm = ctl[2];
-    const double *vm = M + jm * ld;
-    const double b0 = vm[a.n_num];
-    const bool bad = !(fabs(b0) > 1e-300);
-    for (int r = threadIdx.x; r < nc; r += blockDim.x)
-      a.coef[(int64_t)metric * nc + r] = bad ? __longlong_as_double(0x7ff8000000000000ll) : vm[r] / b0;
-    if (threadIdx.x == 0) rot0[2 * (kSvdMaxCols / 2) * 2 - 1] = b0;  // to CTA 0 (DSMEM)
+  __syncthreads();
+  double *so = a.sigma + (int64_t)metric * nc;
+  for (int col = threadIdx.x; col < nc; col += blockDim.x) {  // ascending by rank counting
+    const double v = sig[col];
+    int rank = 0;
+    for (int o = 0; o < nc; ++o) rank += (sig[o] < v) || (sig[o] == v && o < col);
+    so[rank] = v;
+    if (rank == 0) ctl[2] = col;
   }
-  cluster.sync();
-  if (crank == 0 && threadIdx.x == 0) {
-    double smin = sig[0], smax = sig[0];
-    for (int o = 1; o < nc; ++o) {
-      smin = fmin(smin, sig[o]);
-      smax = fmax(smax, sig[o]);
-    }
+  __syncthreads();
+  const int jm = ctl[2];
+  const double *vm = V + (int64_t)jm * nc;
+  const double b0 = __ldcg(vm + a.n_num);
+  const bool bad = !(fabs(b0) > 1e-300);
+  for (int r = threadIdx.x; r < nc; r += blockDim.x)
+    a.coef[(int64_t)metric * nc + r] = bad ? __longlong_as_double(0x7ff8000000000000ll) : __ldcg(vm + r) / b0;
+  if (threadIdx.x == 0) {
+    const double smin = sig[jm];
+    double smax = sig[0];
+    for (int o = 1; o < nc; ++o) smax = fmax(smax, sig[o]);
     int rank = 0;
     for (int o = 0; o < nc; ++o) rank += sig[o] > 1e-13 * smax;
-    const double b0 = rot[2 * (kSvdMaxCols / 2) * 2 - 1];
-    const bool bad = !(fabs(b0) > 1e-300);
     double *inf = a.info + metric * 6;
     inf[0] = bad ? (double)RP_ERR_DEGENERATE : 0.0;
     inf[1] = rank;
@@ -494,8 +499,8 @@ size_t tsqr_workspace_bytes(int nc, int n_v, int leaves) {
 }
 
 static size_t tsqr_smem(int nc) {
-  return (size_t)((packed_size(nc) + 1) & ~1ll) * 8 + 2 * kVBuf * 8 + 4 * 8 +
-         (size_t)kChunk * kMaxVars * 8 + (size_t)kSD * kSvdMaxCols * 8 + 16;
+  return (size_t)((packed_size(nc) + 1) & ~1ll) * 8 + (size_t)tsqr_rv_elems(nc) * 8 + kSvdMaxCols * 8 +
+         (size_t)kChunk * kMaxVars * 8 + (kSvdMaxCols + 4) * 4;
 }
 
 cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double *V, const double *S,
@@ -524,19 +529,21 @@ cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double 
   const size_t smem = tsqr_smem(nc);
   e = cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int threads = 32 * ((nc + 7) / 8);
+  const int threads = 32 * ((nc + 7) / 8);  // 4 octets (8 columns) per warp
   k_tsqr<<<dim3(leaves, n_v), threads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *coef, double *sigma,
-                              double *info, cudaStream_t s) {
+cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *V_ws, double *coef,
+                              double *sigma, double *info, cudaStream_t s) {
   if (nc < 2 || nc > kSvdMaxCols) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)nc * (nc | 1) * 8 + 2 * (kSvdMaxCols / 2) * 2 * 8 + 16;
+  const int np = (nc + 1) & ~1;
+  const size_t smem = (size_t)nc * (nc | 1) * 8 + (size_t)(((np - 1) * (np / 2) + 3) & ~3) * 2 +
+                      kSvdMaxCols * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  JacArgs a{R, nc, n_num, coef, sigma, info};
-  k_svd_jacobi<<<dim3(2, n_v), kJacThreads, smem, s>>>(a);
+  JacArgs a{R, nc, n_num, V_ws, coef, sigma, info};
+  k_svd_jacobi<<<n_v, kJacThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(rp.rp_basis) == 4 * 3 + 4 + 8 * 2
     assert C.sizeof(rp.rp_xform) == 8 * 8 + 4 * 8
     assert C.sizeof(rp.rp_hw) == 4 * 4 + 8 * 2 + 8 * 8
-    assert C.sizeof(rp.rp_fit_info) == 4 * 2 + 8 * 3
+    assert C.sizeof(rp.rp_fit_info) == 4 * 2 + 8 * 3 + 4 * 2
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -31,7 +31,7 @@ elif which == "svd":
     X = torch.from_numpy(fc.X).to(dev)
     V = rp.eval_metrics(fc.truths[0], X) * torch.from_numpy(fc.noise).to(dev)
     _, sig, _, infos = rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
-    print("jacobi sweeps / cond:", [(i["cond_est"]) for i in infos])
+    print("jacobi sweeps / cond:", [(i["iters"], i["cond_est"]) for i in infos])
     torch.cuda.synchronize()
     ev[0].record()
     for _ in range(reps):
