@@ -34,6 +34,7 @@
 #ifndef RP_H
 #define RP_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -202,6 +203,27 @@ rp_status rp_tsqr_accumulate(const double *X, const double *V, int64_t K, int32_
                              const rp_basis *basis, const rp_xform *xform, double *R, rp_stream s);
 rp_status rp_svd_rows(const double *rows, int64_t n_rows, int32_t n_v, const rp_basis *basis,
                       double *coef_out, double *sigma_out, rp_fit_info *info, rp_stream s);
+
+/* ---- f3: step 3, "convert [the rational program] into code" ------------
+ * rp_codegen: the CUDA C source of the rational program R of `prog` with every constant an
+ *   immediate (fitted coefficients, transform, H, R, Z, grid rule; hexadecimal float literals,
+ *   exact): the occupancy flowchart, the masks, g_i as direct monomial sums, the MWP-CWP CFG of
+ *   DESIGN.md Appendix A line by line (or E = g_1), and `rp_jit_argmin`, the exhaustive per-D
+ *   search of steps 4-5.  Host buffer out_src of cap bytes (nullable:
+ *   query); *len = the source length without the NUL.  UNSUPPORTED if cap <= *len.
+ * rp_jit_create: rp_codegen, then NVRTC (libnvrtc.so.12, loaded with dlopen) for sm_100a and
+ *   cudaLibraryLoadData on the current device.  UNSUPPORTED without NVRTC; CUDA on a compile or
+ *   load failure (the NVRTC log is in rp_last_error()).  Free with rp_jit_destroy.
+ * rp_jit_eval_argmin: the generated search over D (device-or-host int32 [nD][d]) and F
+ *   (device-or-host int32 [nF][p]); outputs as rp_eval_argmin (best_idx [nD], best_E [nD],
+ *   second_E [nD] nullable), one warp per tuple.  Same masks and tie rule as rp_eval_argmin; E
+ *   is evaluated in the literal order of Appendix A (IEEE divisions).                         */
+typedef struct rp_jit_s *rp_jit;
+rp_status rp_codegen(const rp_program *prog, char *out_src, size_t cap, size_t *len);
+rp_status rp_jit_create(const rp_program *prog, rp_jit *out);
+rp_status rp_jit_eval_argmin(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *F, int32_t nF,
+                             int32_t *best_idx, double *best_E, double *second_E, rp_stream s);
+rp_status rp_jit_destroy(rp_jit jit);
 
 /* ---- a4 alone: fitted metrics at points ----------------------------------------------------
  * out[i][r] = g_i(X_r) = p_i(u_r)/q_i(u_r) for i < prog->n_metrics (device-or-host float64

@@ -91,6 +91,10 @@ _SIGS = {
     "rp_fit_svd": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, C.POINTER(rp_xform), _vp, _vp],
     "rp_tsqr_accumulate": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
     "rp_svd_rows": [_vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, _vp, _vp],
+    "rp_codegen": [C.POINTER(rp_program), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+    "rp_jit_create": [C.POINTER(rp_program), C.POINTER(_vp)],
+    "rp_jit_eval_argmin": [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
+    "rp_jit_destroy": [_vp],
     "rp_eval_metrics": [C.POINTER(rp_program), _vp, _i64, _vp, _vp],
     "rp_eval_argmin": [C.POINTER(rp_program), _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
     "rp_eval_argmin_batched": [_vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp],
@@ -287,6 +291,53 @@ def eval_argmin_batched(progs, D, F, second: bool = True, out=None):
 def eval_argmin(prog, D, F, second: bool = True):
     idx, E, S = eval_argmin_batched([prog], D, F, second)
     return idx[0], E[0], (S[0] if S is not None else None)
+
+
+def codegen(prog) -> str:
+    """rp_codegen (NEXT row f3): the CUDA C source of the rational program, constants as
+    immediates (step 3)."""
+    pr = prog if isinstance(prog, Program) else Program(prog)
+    n = C.c_size_t(0)
+    _check(_lib.rp_codegen(C.byref(pr.c), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(_lib.rp_codegen(C.byref(pr.c), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+class Jit:
+    """rp_jit_create / rp_jit_eval_argmin: the generated program compiled by NVRTC for sm_100a
+    and searched exhaustively, one warp per data tuple."""
+
+    def __init__(self, prog):
+        self.prog = prog if isinstance(prog, Program) else Program(prog)
+        self.d, self.p = self.prog.d, self.prog.p
+        h = _vp()
+        _check(_lib.rp_jit_create(C.byref(self.prog.c), C.byref(h)))
+        self.h = h
+
+    def eval(self, D, F, second: bool = True, out=None):
+        D = _contig(D, np.int32)
+        F = _contig(F, np.int32)
+        nD = D.shape[0] if D.ndim > 1 else len(D) // self.d
+        nF = F.shape[0] if F.ndim > 1 else len(F) // self.p
+        if out is None:
+            out = (_empty_like_family(D, (nD,), np.int32), _empty_like_family(D, (nD,), np.float64),
+                   _empty_like_family(D, (nD,), np.float64) if second else None)
+        idx, E, S = out
+        _check(_lib.rp_jit_eval_argmin(self.h, _ptr(D), nD, _ptr(F), nF, _ptr(idx), _ptr(E),
+                                       _ptr(S) if S is not None else None, _stream_of(D, F, idx)))
+        return idx, E, S
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.rp_jit_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Plan:

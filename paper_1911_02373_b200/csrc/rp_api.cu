@@ -440,6 +440,37 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
   return RP_OK;
 }
 
+namespace rp {
+rp_status check_program(const rp_program *prog) {
+  std::vector<DevProg> t(1);
+  return compile_program(prog, t.data());
+}
+
+rp_status jit_stage_and_launch(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *F, int32_t nF,
+                                   int32_t *best_idx, double *best_E, double *second_E, cudaStream_t s) {
+  if (nD == 0) return RP_OK;
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  const int d = rp_jit_dims(jit, 0), p = rp_jit_dims(jit, 1);
+  Tmp tD, tF, ti, tb, ts;
+  const int32_t *dD, *dF;
+  if ((st = stage_in(D, (size_t)nD * d, tD, &dD, s)) != RP_OK) return st;
+  if ((st = stage_in(F, (size_t)nF * p, tF, &dF, s)) != RP_OK) return st;
+  int32_t *di;
+  double *db, *ds;
+  bool hi, hb, hs;
+  if ((st = stage_out(best_idx, (size_t)nD, ti, &di, &hi, s)) != RP_OK) return st;
+  if ((st = stage_out(best_E, (size_t)nD, tb, &db, &hb, s)) != RP_OK) return st;
+  if ((st = stage_out(second_E, (size_t)nD, ts, &ds, &hs, s)) != RP_OK) return st;
+  RP_CUDA(launch_jit(jit, dD, nD, dF, nF, di, db, ds, s));
+  if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, (size_t)nD * 4, cudaMemcpyDeviceToHost, s));
+  if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, (size_t)nD * 8, cudaMemcpyDeviceToHost, s));
+  if (hs) RP_CUDA(cudaMemcpyAsync(second_E, ds, (size_t)nD * 8, cudaMemcpyDeviceToHost, s));
+  if (hi || hb || hs) RP_CUDA(cudaStreamSynchronize(s));
+  return RP_OK;
+}
+}  // namespace rp
+
 // =============================================================================================
 // ABI
 // =============================================================================================

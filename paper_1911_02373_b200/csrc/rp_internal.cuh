@@ -133,6 +133,13 @@ cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double 
 cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *V_ws, double *coef,
                               double *sigma, double *info, cudaStream_t s);
 
+}  // namespace rp
+int rp_jit_dims(rp_jit jit, int which);  // d (0) or p (1) of the program a jit was made from
+namespace rp {
+// f3 (rp_codegen.cu)
+cudaError_t launch_jit(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *F, int32_t nF, int32_t *idx,
+                       double *bestE, double *secondE, cudaStream_t s);
+
 int num_sms();
 
 }  // namespace rp

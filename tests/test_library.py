@@ -54,3 +54,28 @@ def test_invalid_arguments_rejected_before_launch():
     with pytest.raises(rp.RPError) as ei:
         rp.xform_from_box([2.0], [1.0])  # hi < lo
     assert ei.value.status == 1
+
+
+def test_codegen_compiles_for_sm100a(tmp_path):
+    """rp_codegen runs without a GPU (given the transform); its source is valid CUDA for sm_100a
+    and carries the program's constants as exact hexadecimal immediates."""
+    import copy
+    import shutil
+    import subprocess
+    import oracle
+    import paper_1911_02373_b200 as rp
+    import synth
+    spec = copy.deepcopy(synth.large_program())
+    c, e = oracle.xform_from_box(spec.box_lo, spec.box_hi)
+    spec.xform_c, spec.xform_e = list(c), list(e)
+    src = rp.codegen(spec)
+    assert float(spec.coef[0][1]).hex().replace("0x1.", "").rstrip("0")[:8] in src
+    assert 'extern "C" __global__' in src and "rp_jit_argmin" in src
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("no nvcc")
+    f = tmp_path / "gen.cu"
+    f.write_text(src)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-c", str(f), "-o", str(tmp_path / "gen.o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -26,6 +26,17 @@ if which == "sweep":
     for _ in range(reps):
         plan.eval(D, out=out, second=False)
     ev[1].record()
+elif which == "jit":
+    case = synth.large_sweep()
+    jit = rp.Jit(case.programs[0])
+    D = torch.from_numpy(case.D).to(dev)
+    F = torch.from_numpy(case.F).to(dev)
+    out = jit.eval(D, F, second=False)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        jit.eval(D, F, second=False, out=out)
+    ev[1].record()
 elif which == "svd":
     fc = synth.fitheavy(sigma=0.01)
     X = torch.from_numpy(fc.X).to(dev)
