@@ -162,6 +162,27 @@ rp_status rp_solve_normal(const double *G, int32_t n_v, const rp_basis *basis, d
 rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
                  double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream s);
 
+/* ---- stream-ordered (device-resident) forms of a10-a14 --------------------------------------
+ * No host synchronisation and no host round trip: every pointer is a device pointer (INVALID_ARG
+ * otherwise), results stay on the device, and the calls only enqueue work on the stream (their
+ * temporaries come from the stream-ordered pool).  The transform travels as xf [n][2] doubles
+ * (c_k, e_k) -- the layout rp_plan_update_program takes.
+ * rp_minmax_dev: lohi [n][2] = per-column (min, max) of X [K][n].
+ * rp_xform_dev: xf [n][2] from lohi [n][2] (reading R14).
+ * rp_gram_accumulate_dev: rp_gram_accumulate with the transform from xf; G [n_v][n_c][n_c].
+ * rp_solve_normal_dev: rp_solve_normal into coef [n_v][n_c] and info [n_v][5] (status, rank,
+ *   resid2, min_pivot, cond_est as doubles; nullable).  A degenerate system leaves NaN
+ *   coefficients and status 3 in info (no error is returned: nothing is read back).
+ * rp_fit_dev: the four above in order; xf_out [n][2] nullable.                               */
+rp_status rp_minmax_dev(const double *X, int64_t K, int32_t n, double *lohi, rp_stream s);
+rp_status rp_xform_dev(const double *lohi, int32_t n, double *xf, rp_stream s);
+rp_status rp_gram_accumulate_dev(const double *X, const double *V, int64_t K, int32_t n_v,
+                                 const rp_basis *basis, const double *xf, double *G, rp_stream s);
+rp_status rp_solve_normal_dev(const double *G, int32_t n_v, const rp_basis *basis, double *coef,
+                              double *info, rp_stream s);
+rp_status rp_fit_dev(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                     double *coef, double *xf_out, double *info, rp_stream s);
+
 /* ---- f4: Sanathanan-Koerner reweighted refit ---------------------------------------------------
  * The linearised rows p(x) - V q(x) of PAPER.md:2578-2584 weigh each sample by q(x), which biases
  * noisy fits.  rp_gram_accumulate_weighted is rp_gram_accumulate with every
@@ -266,6 +287,14 @@ rp_status rp_plan_create(const rp_program *progs, int32_t n_prog, const int32_t 
 rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_t *best_idx,
                               double *best_E, double *second_E, rp_stream s);
 rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible);
+/* rp_plan_update_program: replace the coefficients (and, if xform is non-null, the transform) of
+ * program `prog` from DEVICE memory -- coef [n_metrics][stride] in each metric's basis order
+ * (stride >= its n_c; rp_fit_dev's output has stride n_c), xform [n][2] (c_k, e_k) -- and redo
+ * a1 / a5 on the device.  Stream-ordered, no host synchronisation: a fit and the sweep that uses
+ * it chain on the device.  The bases (hence the term layout) are those of the plan's creation.
+ * Clears the plan's runtime history.                                                       */
+rp_status rp_plan_update_program(rp_plan plan, int32_t prog, const double *coef, int32_t stride,
+                                 const double *xform, rp_stream s);
 rp_status rp_plan_destroy(rp_plan plan);
 
 /* ---- f2: runtime decision service ----------------------------------------------------------

@@ -88,6 +88,12 @@ _SIGS = {
     "rp_fit": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, C.POINTER(rp_xform), _vp, _vp],
     "rp_gram_accumulate_weighted": [_vp, _vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
     "rp_fit_sk": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _i32, _vp, C.POINTER(rp_xform), _vp, _vp],
+    "rp_minmax_dev": [_vp, _i64, _i32, _vp, _vp],
+    "rp_xform_dev": [_vp, _i32, _vp, _vp],
+    "rp_gram_accumulate_dev": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, _vp],
+    "rp_solve_normal_dev": [_vp, _i32, C.POINTER(rp_basis), _vp, _vp, _vp],
+    "rp_fit_dev": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, _vp, _vp],
+    "rp_plan_update_program": [_vp, _i32, _vp, _i32, _vp, _vp],
     "rp_fit_svd": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, C.POINTER(rp_xform), _vp, _vp],
     "rp_tsqr_accumulate": [_vp, _vp, _i64, _i32, C.POINTER(rp_basis), C.POINTER(rp_xform), _vp, _vp],
     "rp_svd_rows": [_vp, _i64, _i32, C.POINTER(rp_basis), _vp, _vp, _vp, _vp],
@@ -353,6 +359,13 @@ class Plan:
         s = _stream_of(F)
         _check(_lib.rp_plan_create(C.cast(arr, _vp), len(self.progs), _ptr(F), self.nF, C.byref(self.handle), s))
 
+    def update(self, coef, xf=None, prog: int = 0):
+        """rp_plan_update_program: new coefficients [n_metrics][n_c] (and transform [n][2]) of
+        program `prog` from device tensors, a1 / a5 redone on the device (stream-ordered)."""
+        coef = coef.contiguous()
+        _check(_lib.rp_plan_update_program(self.handle, prog, _ptr(coef), coef.shape[-1],
+                                           _ptr(xf.contiguous()) if xf is not None else None, _stream_of(coef)))
+
     def static_feasible(self, prog: int = 0) -> int:
         v = C.c_int32()
         _check(_lib.rp_plan_static_feasible(self.handle, prog, C.byref(v)))
@@ -514,6 +527,65 @@ def fit(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
         _check(st)
     n = b.num.shape[1]
     return coef, (np.array(xf.c[:n]), np.array(xf.e[:n], dtype=np.int32)), _infos(infos)
+
+
+# ---- device-resident (stream-ordered) forms: torch CUDA tensors in and out, no host sync ----
+
+def _dev_empty(ref, shape):
+    return _torch().empty(shape, dtype=_torch().float64, device=ref.device)
+
+
+def minmax_dev(X, out=None):
+    """lohi [n][2] (min, max per column) on the device."""
+    X = _contig(X, np.float64)
+    K, n = X.shape
+    lohi = out if out is not None else _dev_empty(X, (n, 2))
+    _check(_lib.rp_minmax_dev(_ptr(X), K, n, _ptr(lohi), _stream_of(X)))
+    return lohi
+
+
+def xform_dev(lohi, out=None):
+    """xf [n][2] = (c_k, e_k) from lohi [n][2] on the device (reading R14)."""
+    n = lohi.shape[0]
+    xf = out if out is not None else _dev_empty(lohi, (n, 2))
+    _check(_lib.rp_xform_dev(_ptr(lohi), n, _ptr(xf), _stream_of(lohi)))
+    return xf
+
+
+def gram_dev(X, V, num_exp, den_exp, xf, out=None):
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    G = out if out is not None else _dev_empty(X, (n_v, b.n_c, b.n_c))
+    _check(_lib.rp_gram_accumulate_dev(_ptr(X), _ptr(V), X.shape[0], n_v, C.byref(b.c), _ptr(xf), _ptr(G),
+                                       _stream_of(X, V, G)))
+    return G
+
+
+def solve_dev(G, num_exp, den_exp, coef=None, info=None):
+    """coef [n_v][n_c] and info [n_v][5] (status, rank, resid2, min_pivot, cond_est) on the device."""
+    b = Basis(num_exp, den_exp)
+    n_v = G.shape[0]
+    coef = coef if coef is not None else _dev_empty(G, (n_v, b.n_c))
+    info = info if info is not None else _dev_empty(G, (n_v, 5))
+    _check(_lib.rp_solve_normal_dev(_ptr(G), n_v, C.byref(b.c), _ptr(coef), _ptr(info), _stream_of(G)))
+    return coef, info
+
+
+def fit_dev(X, V, num_exp, den_exp, coef=None, xf=None, info=None):
+    """rp_fit_dev: the fit entirely on the device, no host round trip.  Returns device tensors
+    (coef [n_v][n_c], xf [n][2], info [n_v][5])."""
+    b = Basis(num_exp, den_exp)
+    X = _contig(X, np.float64)
+    V = _contig(V, np.float64)
+    K, n = X.shape
+    n_v = V.shape[0] if V.ndim == 2 else 1
+    coef = coef if coef is not None else _dev_empty(X, (n_v, b.n_c))
+    xf = xf if xf is not None else _dev_empty(X, (n, 2))
+    info = info if info is not None else _dev_empty(X, (n_v, 5))
+    _check(_lib.rp_fit_dev(_ptr(X), _ptr(V), K, n_v, C.byref(b.c), _ptr(coef), _ptr(xf), _ptr(info), _stream_of(X, V)))
+    return coef, xf, info
 
 
 def fit_svd(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):

@@ -171,6 +171,7 @@ rp_status compile_program(const rp_program *prog, DevProg *o) {
     int k;
     std::vector<int> eD, eP;
     double c;
+    int src;
   };
   std::vector<Term> terms;
   for (int i = 0; i < nm; ++i) {
@@ -178,6 +179,7 @@ rp_status compile_program(const rp_program *prog, DevProg *o) {
     if (st != RP_OK) return st;
     const rp_basis &b = prog->basis[i];
     RP_REQUIRE(prog->coef[i], RP_ERR_INVALID_ARG, "program: null coef[%d]", i);
+    RP_REQUIRE(b.n_num + b.n_den < kMaxSrc, RP_ERR_UNSUPPORTED, "program: basis too large");
     for (int h2 = 0; h2 < 2; ++h2) {
       const int cnt = h2 ? b.n_den : b.n_num;
       const int16_t *ex = h2 ? b.den_exp : b.num_exp;
@@ -187,6 +189,7 @@ rp_status compile_program(const rp_program *prog, DevProg *o) {
         t.eD.assign(ex + j * n, ex + j * n + d);
         t.eP.assign(ex + j * n + d, ex + j * n + n);
         t.c = prog->coef[i][(h2 ? b.n_num : 0) + j];
+        t.src = i * kMaxSrc + (h2 ? b.n_num : 0) + j;
         terms.push_back(t);
       }
     }
@@ -221,18 +224,21 @@ rp_status compile_program(const rp_program *prog, DevProg *o) {
     for (int k = 0; k < d; ++k) o->de_exp[a][k] = (int8_t)DE[a][k];
   // rows r = k * nPE + pe; terms grouped by row keeping basis order within a row
   const int nrows = o->npoly * o->nPE;
-  std::vector<std::vector<std::pair<int, double>>> rows(nrows);
-  for (auto &t : terms) {
+  std::vector<std::vector<const Term *>> rows(nrows);
+  std::vector<int> tde(terms.size());
+  for (size_t i = 0; i < terms.size(); ++i) {
+    const Term &t = terms[i];
     const int pe = (int)(std::lower_bound(PE.begin(), PE.end(), t.eP, graded_less) - PE.begin());
-    const int de = (int)(std::lower_bound(DE.begin(), DE.end(), t.eD, graded_less) - DE.begin());
-    rows[t.k * o->nPE + pe].push_back({de, t.c});
+    tde[i] = (int)(std::lower_bound(DE.begin(), DE.end(), t.eD, graded_less) - DE.begin());
+    rows[t.k * o->nPE + pe].push_back(&t);
   }
   int pos = 0;
   for (int r = 0; r < nrows; ++r) {
     o->row_start[r] = (int16_t)pos;
-    for (auto &e : rows[r]) {
-      o->term_de[pos] = (int16_t)e.first;
-      o->term_coef[pos] = e.second;
+    for (const Term *t : rows[r]) {
+      o->term_de[pos] = (int16_t)tde[t - terms.data()];
+      o->term_coef[pos] = t->c;
+      o->term_src[pos] = (int16_t)t->src;
       ++pos;
     }
   }
@@ -301,6 +307,8 @@ struct rp_plan_s {
   DevProg *d_progs = nullptr;
   int32_t *buf_i = nullptr;
   double *buf_d = nullptr;
+  int32_t *d_F = nullptr;  // F kept on the device (rp_plan_update_program re-runs a1 / a5)
+  std::vector<int> nc_of;  // per program: max n_c over its metrics (coefficient row stride check)
   CfgTable tab{};
   cudaStream_t stream = nullptr;
   HistTable hist;
@@ -312,6 +320,7 @@ static void plan_free(rp_plan pl) {
   if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
   if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
   if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
+  if (pl->d_F) cudaFreeAsync(pl->d_F, pl->stream);
   if (pl->hist.slots) {
     cudaStreamSynchronize(pl->stream);
     cudaFree(pl->hist.slots);
@@ -388,14 +397,16 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   // the host buffer lifetime (cudaMemcpyAsync from pageable memory returns after staging)
   if ((e = cudaMemcpyAsync(pl->d_progs, hp.data(), sizeof(DevProg) * n_prog, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return fail(e, "H2D program");
-  Tmp tF;
-  const int32_t *dF = nullptr;
-  st = stage_in(F, (size_t)nF * pl->p, tF, &dF, s);
-  if (st != RP_OK) {
-    plan_free(pl);
-    return st;
+  if ((e = cudaMallocAsync((void **)&pl->d_F, (size_t)nF * pl->p * sizeof(int32_t), s)) != cudaSuccess)
+    return fail(e, "alloc");
+  if ((e = cudaMemcpyAsync(pl->d_F, F, (size_t)nF * pl->p * sizeof(int32_t), cudaMemcpyDefault, s)) != cudaSuccess)
+    return fail(e, "F");
+  for (int g = 0; g < n_prog; ++g) {
+    int m = 0;
+    for (int i = 0; i < progs[g].n_metrics; ++i) m = std::max(m, progs[g].basis[i].n_num + progs[g].basis[i].n_den);
+    pl->nc_of.push_back(m);
   }
-  if ((e = launch_plan_configs(pl->d_progs, n_prog, dF, nF, npe_pad, pl->tab, s)) != cudaSuccess)
+  if ((e = launch_plan_configs(pl->d_progs, n_prog, pl->d_F, nF, npe_pad, pl->tab, s)) != cudaSuccess)
     return fail(e, "k_plan_configs");
   *out = pl;
   return RP_OK;
@@ -674,6 +685,105 @@ rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const
   return sst;
 }
 
+// ---- stream-ordered (device-resident) forms ---------------------------------------------------
+static rp_status require_dev(const void *p, const char *what) {
+  RP_REQUIRE(p && is_device_ptr(p), RP_ERR_INVALID_ARG, "%s must be a device pointer", what);
+  return RP_OK;
+}
+
+rp_status rp_minmax_dev(const double *X, int64_t K, int32_t n, double *lohi, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(K >= 1 && n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "K = %lld, n = %d", (long long)K, n);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  if ((st = require_dev(X, "X")) != RP_OK || (st = require_dev(lohi, "lohi")) != RP_OK) return st;
+  const int nblk = minmax_blocks(K);
+  Tmp tw;
+  RP_CUDA(tw.alloc((size_t)nblk * n * 2 * sizeof(double), s));
+  RP_CUDA(launch_minmax(X, K, n, (double *)tw.p, nblk, lohi, s));
+  return RP_OK;
+}
+
+rp_status rp_xform_dev(const double *lohi, int32_t n, double *xf, rp_stream sv) {
+  RP_REQUIRE(n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "n = %d", n);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  if ((st = require_dev(lohi, "lohi")) != RP_OK || (st = require_dev(xf, "xf")) != RP_OK) return st;
+  RP_CUDA(launch_xform(lohi, n, xf, (cudaStream_t)sv));
+  return RP_OK;
+}
+
+rp_status rp_gram_accumulate_dev(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
+                                 const double *xf, double *G, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(basis && K >= 0 && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "bad argument");
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  if ((st = require_dev(xf, "xf")) != RP_OK || (st = require_dev(G, "G")) != RP_OK) return st;
+  if (K > 0 && ((st = require_dev(X, "X")) != RP_OK || (st = require_dev(V, "V")) != RP_OK)) return st;
+  GramBasis gb;
+  if ((st = build_gram_basis(basis, nullptr, &gb)) != RP_OK) return st;
+  const int nc = gb.nc, n = gb.n;
+  if (K == 0) {
+    RP_CUDA(cudaMemsetAsync(G, 0, (size_t)n_v * nc * nc * 8, s));
+    return RP_OK;
+  }
+  Tmp tb, tp;
+  RP_CUDA(tb.alloc(sizeof(GramBasis), s));
+  RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+  RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
+  const size_t pe = gram_partial_elems(gb, n_v, K, num_sms(), false);
+  RP_CUDA(tp.alloc(pe * 8, s));
+  RP_CUDA(launch_gram((const GramBasis *)tb.p, gb, X, V, nullptr, K, n_v, G, (double *)tp.p, pe, s));
+  return RP_OK;
+}
+
+rp_status rp_solve_normal_dev(const double *G, int32_t n_v, const rp_basis *basis, double *coef, double *info,
+                              rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(basis && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "bad argument");
+  rp_status st = check_basis(*basis, basis->n_vars, "solve", true);
+  if (st != RP_OK) return st;
+  const int nc = basis->n_num + basis->n_den;
+  RP_REQUIRE(nc >= 2 && nc <= 161, RP_ERR_UNSUPPORTED, "solve: n_c = %d outside [2, 161]", nc);
+  if ((st = ensure_device()) != RP_OK) return st;
+  if ((st = require_dev(G, "G")) != RP_OK || (st = require_dev(coef, "coef")) != RP_OK) return st;
+  if (info && (st = require_dev(info, "info")) != RP_OK) return st;
+  Tmp ti;
+  double *di = info;
+  if (!di) {
+    RP_CUDA(ti.alloc((size_t)n_v * 5 * 8, s));
+    di = (double *)ti.p;
+  }
+  RP_CUDA(launch_solve(G, n_v, nc, basis->n_num, coef, di, s));
+  return RP_OK;
+}
+
+rp_status rp_fit_dev(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis, double *coef,
+                     double *xf_out, double *info, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(basis && K >= 1 && n_v >= 1 && n_v <= 64, RP_ERR_INVALID_ARG, "bad argument");
+  const int n = basis->n_vars;
+  RP_REQUIRE(n >= 1 && n <= RP_MAX_VARS, RP_ERR_INVALID_ARG, "n_vars %d", n);
+  const int nc = basis->n_num + basis->n_den;
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  Tmp tl, tx, tG;
+  RP_CUDA(tl.alloc(2 * RP_MAX_VARS * sizeof(double), s));
+  double *xf = xf_out;
+  if (!xf) {
+    RP_CUDA(tx.alloc(2 * RP_MAX_VARS * sizeof(double), s));
+    xf = (double *)tx.p;
+  } else if ((st = require_dev(xf, "xf_out")) != RP_OK) {
+    return st;
+  }
+  if ((st = rp_minmax_dev(X, K, n, (double *)tl.p, sv)) != RP_OK) return st;
+  if ((st = rp_xform_dev((const double *)tl.p, n, xf, sv)) != RP_OK) return st;
+  RP_CUDA(tG.alloc((size_t)n_v * nc * nc * 8, s));
+  if ((st = rp_gram_accumulate_dev(X, V, K, n_v, basis, xf, (double *)tG.p, sv)) != RP_OK) return st;
+  return rp_solve_normal_dev((const double *)tG.p, n_v, basis, coef, info, sv);
+}
+
 rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
                     int32_t iters, double *coef_out, rp_xform *xform_out, rp_fit_info *info, rp_stream sv) {
   cudaStream_t s = (cudaStream_t)sv;
@@ -923,6 +1033,23 @@ rp_status rp_plan_create(const rp_program *progs, int32_t n_prog, const int32_t 
 rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_t *best_idx,
                               double *best_E, double *second_E, rp_stream sv) {
   return plan_eval(plan, D, nD, best_idx, best_E, second_E, (cudaStream_t)sv);
+}
+
+rp_status rp_plan_update_program(rp_plan plan, int32_t prog, const double *coef, int32_t stride,
+                                 const double *xform, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(plan && coef && prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "bad argument");
+  RP_REQUIRE(stride >= plan->nc_of[prog], RP_ERR_INVALID_ARG, "stride %d < n_c %d", stride, plan->nc_of[prog]);
+  RP_REQUIRE(is_device_ptr(coef) && (!xform || is_device_ptr(xform)), RP_ERR_INVALID_ARG,
+             "coef / xform must be device pointers (stream-ordered update)");
+  plan->stream = s;
+  RP_CUDA(launch_plan_set_coef(plan->d_progs + prog, coef, stride, xform, s));
+  RP_CUDA(launch_plan_configs(plan->d_progs, plan->n_prog, plan->d_F, plan->nF, plan->npe_pad, plan->tab, s));
+  if (plan->hist.enabled) {  // decisions of the old program are stale
+    RP_CUDA(cudaMemsetAsync(plan->hist.slots, 0, ((size_t)plan->hist.mask + 1) * sizeof(HistSlot), s));
+    RP_CUDA(cudaMemsetAsync(plan->hist.counters, 0, 3 * sizeof(unsigned long long), s));
+  }
+  return RP_OK;
 }
 
 rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible) {

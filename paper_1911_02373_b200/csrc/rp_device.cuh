@@ -35,10 +35,15 @@ __device__ __forceinline__ Best shfl_xor(const Best &a, int m) {
   return r;
 }
 
+#ifdef RP_DMMA_NV  // a pure function of its operands: let the scheduler move it
+#define RP_DMMA_ASM asm
+#else
+#define RP_DMMA_ASM asm volatile
+#endif
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  RP_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(c0), "+d"(c1)
+              : "d"(a), "d"(b));
 }
 
 // 1/x: MUFU.RCP64H seed + two Newton steps (relative error ~1 ulp; 0 and +-inf give NaN,

@@ -52,7 +52,9 @@ struct DevProg {
   int16_t row_start[kMaxRows + 1];  // terms of row (k * nPE + pe) are [row_start[r], row_start[r+1])
   int16_t term_de[kMaxTerms];
   double term_coef[kMaxTerms];
+  int16_t term_src[kMaxTerms];  // metric * kMaxSrc + index of the term's coefficient in coef[metric]
 };
+constexpr int kMaxSrc = 4096;   // term_src stride per metric (n_num + n_den < kMaxSrc)
 
 // Per-configuration table of a plan (SoA over the statically feasible, compacted configs in
 // ascending original index; program g at offset g * nFp, nFp = nF rounded up to 8 so that
@@ -136,6 +138,9 @@ cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, doubl
 }  // namespace rp
 int rp_jit_dims(rp_jit jit, int which);  // d (0) or p (1) of the program a jit was made from
 namespace rp {
+// device-resident refit of a plan's program (rp_plan_update_program)
+cudaError_t launch_plan_set_coef(DevProg *d_prog, const double *d_coef, int stride, const double *d_xf,
+                                 cudaStream_t s);
 // f3 (rp_codegen.cu)
 cudaError_t launch_jit(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *F, int32_t nF, int32_t *idx,
                        double *bestE, double *secondE, cudaStream_t s);

@@ -165,6 +165,26 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     tab.rSM[(int64_t)g * kRSMTab + k] = k > 0 ? 1.0 / (double)k : 0.0;
 }
 
+// rp_plan_update_program: new coefficients (and transform) of one program from device memory;
+// the term layout (which coefficient feeds which staging slot) is fixed by the basis
+__global__ void k_plan_set_coef(DevProg *pg, const double *coef, int stride, const double *xf) {
+  const int nterm = pg->nterm;
+  for (int j = threadIdx.x; j < nterm; j += blockDim.x) {
+    const int src = pg->term_src[j];
+    pg->term_coef[j] = coef[(int64_t)(src / kMaxSrc) * stride + src % kMaxSrc];
+  }
+  if (xf && threadIdx.x < pg->d + pg->p) {
+    pg->xc[threadIdx.x] = xf[2 * threadIdx.x];
+    pg->xe[threadIdx.x] = (int32_t)xf[2 * threadIdx.x + 1];
+  }
+}
+
+cudaError_t launch_plan_set_coef(DevProg *d_prog, const double *d_coef, int stride, const double *d_xf,
+                                 cudaStream_t s) {
+  k_plan_set_coef<<<1, 256, 0, s>>>(d_prog, d_coef, stride, d_xf);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_t *d_F, int nF,
                                 int npe_pad, CfgTable tab, cudaStream_t s) {
   k_plan_configs<<<n_prog, 1024, 0, s>>>(d_progs, d_F, nF, npe_pad, tab);

@@ -47,6 +47,18 @@ class LibOps:
     def solve(self, G, num, den):
         return self.rp.solve_normal(G, num, den)
 
+    def minmax_dev(self, X):
+        return self.rp.minmax_dev(X)
+
+    def xform_dev(self, lohi):
+        return self.rp.xform_dev(lohi)
+
+    def gram_dev(self, X, V, num, den, xf):
+        return self.rp.gram_dev(X, V, num, den, xf)
+
+    def solve_dev(self, G, num, den):
+        return self.rp.solve_dev(G, num, den)
+
     def tsqr(self, X, V, num, den, c, e):
         return self.rp.tsqr(X, V, num, den, c, e)
 
@@ -92,6 +104,29 @@ def sharded_fit(X_local, V_local, num, den, ops, n_vars: int, group=None, determ
         dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
     coef, infos = ops.solve(G, num, den)
     return coef, (c, e), infos
+
+
+def sharded_fit_dev(X_local, V_local, num, den, ops, n_vars: int, group=None):
+    """sharded_fit without a host round trip (the bench's N > 1 step): per-rank (min, max) on the
+    device, one all_reduce(MAX) of (-lo, hi), the transform on the device, the partial Gram,
+    all_reduce(SUM), the solve into device coefficients.  Returns device tensors (coef [n_v][n_c],
+    xf [n][2], info [n_v][5]); every rank holds the same values.  A rank with K_r = 0 contributes
+    (+inf, -inf) bounds and a zero Gram."""
+    K_r = X_local.shape[0]
+    if K_r > 0:
+        lohi = ops.minmax_dev(X_local)
+    else:
+        lohi = torch.stack([torch.full((n_vars,), float("inf"), dtype=torch.float64),
+                            torch.full((n_vars,), float("-inf"), dtype=torch.float64)], 1)
+        lohi = lohi.to(X_local.device if isinstance(X_local, torch.Tensor) else "cpu")
+    box = torch.stack([-lohi[:, 0], lohi[:, 1]], 1).contiguous()
+    dist.all_reduce(box, op=dist.ReduceOp.MAX, group=group)
+    lohi = torch.stack([-box[:, 0], box[:, 1]], 1).contiguous()
+    xf = ops.xform_dev(lohi)
+    G = ops.gram_dev(X_local, V_local, num, den, xf)
+    dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+    coef, info = ops.solve_dev(G, num, den)
+    return coef, xf, info
 
 
 def sharded_fit_svd(X_local, V_local, num, den, ops, n_vars: int, group=None):

@@ -36,6 +36,24 @@ class OracleOps:
         out = [oracle.solve(G[i].astype(np.longdouble), len(num)) for i in range(G.shape[0])]
         return np.stack([np.asarray(r["coef"], dtype=np.float64) for r in out]), out
 
+    # device-resident forms (here: CPU tensors through the oracle)
+    def minmax_dev(self, X):
+        lo, hi = oracle.minmax(np.asarray(X))
+        return torch.from_numpy(np.stack([lo, hi], 1))
+
+    def xform_dev(self, lohi):
+        lohi = lohi.numpy()
+        c, e = oracle.xform_from_box(lohi[:, 0], lohi[:, 1])
+        return torch.from_numpy(np.stack([c, e.astype(np.float64)], 1))
+
+    def gram_dev(self, X, V, num, den, xf):
+        xf = xf.numpy()
+        return torch.from_numpy(self.gram(X, V, num, den, xf[:, 0], xf[:, 1].astype(np.int32)))
+
+    def solve_dev(self, G, num, den):
+        coef, out = self.solve(G, num, den)
+        return torch.from_numpy(coef), out
+
     def tsqr(self, X, V, num, den, c, e):
         """Any B with B^T B = A^T A serves: the shard's design rows themselves."""
         X = np.asarray(X)
@@ -95,6 +113,10 @@ def _worker(rank, world, port, deterministic):
         t0 = t.clone()
         dist.broadcast(t0, 0)
         assert torch.equal(t, t0)
+        # the device-resident form of the same fit
+        coef_d, xf_d, _ = dist_mod.sharded_fit_dev(fc.X[lo:hi], V[:, lo:hi], fc.num_exp, fc.den_exp, ops, n_vars=3)
+        assert np.array_equal(xf_d.numpy()[:, 0], c) and np.array_equal(xf_d.numpy()[:, 1], e)
+        assert np.max(np.abs(coef_d.numpy() - coef)) <= 1e-12 * np.max(np.abs(coef))
         # f1: SVD of the stacked shard factors == SVD of all rows (zero-padded shards included)
         coef, sigma, (c, e), _ = dist_mod.sharded_fit_svd(fc.X[lo:hi], V[:, lo:hi], fc.num_exp, fc.den_exp, ops,
                                                           n_vars=3)

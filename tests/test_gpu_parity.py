@@ -306,3 +306,30 @@ def test_gram_weighted_vs_oracle_rows():
         Go = np.asarray(A.T @ A, dtype=np.float64)
         dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go)))
         assert np.max(np.abs(G[i] - Go) / dg) <= 1e-13
+
+
+def test_device_resident_fit_and_plan_update():
+    """rp_fit_dev == rp_fit (same kernels, bit for bit); rp_plan_update_program on a plan made
+    from another program gives the same sweep as a fresh plan of the fitted program."""
+    import copy
+    fc = synth.polybench_fit_box(sigma=0.01, K=2000)
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(fc.truths[0], fc.X)]) * fc.noise
+    X, Vd = _cuda(fc.X), _cuda(V)
+    coef, (c, e), infos = rp.fit(X, Vd, fc.num_exp, fc.den_exp)
+    cd, xf, info = rp.fit_dev(X, Vd, fc.num_exp, fc.den_exp)
+    assert np.array_equal(cd.cpu().numpy(), coef)
+    assert np.array_equal(xf.cpu().numpy()[:, 0], c) and np.array_equal(xf.cpu().numpy()[:, 1], e)
+    assert np.all(info.cpu().numpy()[:, 0] == 0)
+    # a plan of the truth program, then updated in place to the fitted coefficients / transform
+    case = synth.polybench_sweep(nD=3000)
+    truth = case.programs[0]
+    fitted = copy.deepcopy(truth)
+    fitted.coef = [coef[i] for i in range(3)]
+    fitted.xform_c, fitted.xform_e = list(c), list(e)
+    D, F = _cuda(case.D), _cuda(case.F)
+    plan = rp.Plan([truth], F)
+    plan.update(cd, xf)
+    i1, E1, S1 = plan.eval(D)
+    i2, E2, S2 = rp.eval_argmin(fitted, D, F)
+    assert torch.equal(i1[0], i2) and torch.equal(E1[0], E2) and torch.equal(S1[0], S2)
+    plan.close()
