@@ -46,15 +46,22 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
               : "d"(a), "d"(b));
 }
 
-// 1/x: MUFU.RCP64H seed + two Newton steps (relative error ~1 ulp; 0 and +-inf give NaN,
-// which the final finiteness test masks, as the literal program's x/0 would).
+// 1/x: MUFU.RCP64H seed r0 (relative error e0 < 2^-20) and one cubically convergent step
+// r = r0 (1 + e + e^2), e = 1 - x r0 (exact 1/x = r0 / (1 - e)): relative error e^3 + rounding,
+// ~1 ulp, in 3 DFMA instead of the 4 of two Newton steps.  0 and +-inf give NaN (e = NaN),
+// which the final finiteness test masks, as the literal program's x/0 would.
 __device__ __forceinline__ double frcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// positive finite doubles order like their bit patterns: the validity test and the argmin key
+// compare run on the integer pipes instead of the (shared, saturated) FP64 datapath
+__device__ __forceinline__ bool pos_finite(double x) {
+  const long long b = __double_as_longlong(x);
+  return b > 0 && b < 0x7ff0000000000000ll;
 }
 
 // exact ceil(D / P) = floor((D + P - 1) / P) for 1 <= D + P - 1 < 2^31 via the per-config
@@ -99,19 +106,23 @@ __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, doub
   const double MWP_nb = mc * frcp(dn);         // line 10: Mem_L / Dep
   const double MWP_bw = k.Kbw * mc * r23 * rSM;  // line 11: Mem_BW / (BW_per_warp SM_act)
   const double CWPf = 1.0 + mc * frcp(cc);     // line 14: (Mem_c + Comp_c) / Comp_c
-  double mwp = MWP_nb;                         // line 12
-  mwp = MWP_bw < mwp ? MWP_bw : mwp;
-  mwp = W < mwp ? W : mwp;
-  const double cwp = CWPf < W ? CWPf : W;  // line 14
+  // line 12: MWP = min(MWP_nb, MWP_bw, W_act); each comparison is made once and its outcome
+  // reused for the case tests (MWP == W_act <=> W_act <= min(MWP_nb, MWP_bw), also for NaN)
+  const bool bw = MWP_bw < MWP_nb;
+  const double mwp0 = bw ? MWP_bw : MWP_nb;
+  const bool mwpW = W <= mwp0;
+  const double mwp = mwpW ? W : mwp0;
+  const bool cwpf = CWPf < W;  // line 14: CWP = min(CWPf, W_act); CWP == W_act <=> !cwpf
+  const double cwp = cwpf ? CWPf : W;
   const double cpm = cc * r23;             // Comp_c / Mem
   const double tail = cpm * (mwp - 1.0);
   // Mem_c W / MWP for each operand of the min: W / W = 1; Mem_c / MWP_nb = Dep Mem = dn / Q;
-  // Mem_c / MWP_bw = Mem SM_act / K_bw = s23 SM_act / (Q K_bw)
-  const double mcw = (mwp == W) ? Mem_c : W * rQ * ((mwp == MWP_nb) ? dn : s23 * SMact * k.rKbw);
+  // Mem_c / MWP_bw = Mem SM_act / K_bw = s23 SM_act / (Q K_bw)  (MWP_nb NaN: tail is NaN)
+  const double mcw = mwpW ? Mem_c : W * rQ * (bw ? s23 * SMact * k.rKbw : dn);
   const double E1 = Mem_c + Comp_c + tail;         // line 16
   const double E2 = mcw + tail;                    // line 17
   const double E3 = mc * r23 + Comp_c * W;         // line 18 (Mem_L = Mem_c / Mem)
-  const bool c1 = (mwp == W) && (cwp == W);
+  const bool c1 = mwpW && !cwpf;
   const bool c2 = (cwp >= mwp) || (Comp_c > Mem_c);
   return (c1 ? E1 : (c2 ? E2 : E3)) * Rep;
 }

@@ -402,62 +402,108 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     maxD1sq = x > maxD1sq ? x : maxD1sq;
   }
   const int nOctF = (nFc + 7) >> 3;
-  if (wid * 8 < tmax) {
-    for (int oc = 0; oc < nOctF; ++oc) {
-      if (sorted && __ldg(&rec[oc * 8].P01) > maxD1sq) break;  // every later pair fails a3
-      // B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
-      double bfr[KS];
+  // a4 for one octet of configurations: p_k(D_t, P_c) for the octet of tuples x the octet of
+  // configurations (k-step major: the NPOLY accumulation chains are independent, so consecutive
+  // DMMAs do not wait).  B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
+#ifdef RP_SWEEP_AREG
+  double afr[NPOLY][KS];
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
-      // a4: p_k(D_t, P_c) for the octet of tuples x the octet of configurations (k-step major:
-      // the NPOLY accumulation chains are independent, so consecutive DMMAs do not wait)
-      double acc[NPOLY][2];
+  for (int k = 0; k < NPOLY; ++k)
 #pragma unroll
-      for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
+#define RP_AFR(k, ks) afr[k][ks]
+#else
+#define RP_AFR(k, ks) arow[(k) * NPE + (ks) * 4]
+#endif
+  auto mma_oct = [&](int oc, double (&acc)[NPOLY][2]) {
+    double bfr[KS];
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
+    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
 #pragma unroll
-        for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], arow[k * NPE + ks * 4], bfr[ks]);
-      }
+    for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        // output column 2 (lane % 4) + v; padded configurations (c >= nFc) have zero records
-        // and zero monomials, so their E is NaN and they are masked below
-        const CfgRec *cr = rec + oc * 8 + 2 * (lane & 3) + v;
-        const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));      // P01 | orig, Pm1_0
-        const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);             // Pm1_1, Pm1_2, M0, M1
-        const int32_t orig = (int32_t)(h0.y & 0xffffffff);
-        // a3: "P1 P2 <= D1^2 is meaningful"
-        const bool ok = tok && h0.x <= D1sq;
-        double E;
-        if (MWP) {
-          const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);           // M2, s012, W
-          const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);     // rB, rW
-          const int32_t Pm1_0 = (int32_t)(h0.y >> 32);
-          const uint32_t s012 = (uint32_t)h2.y;
-          const double W = __hiloint2double(h2.w, h2.z);
-          // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
-          int64_t blocks = 1;
-          if (map0 >= 0) blocks *= ceil_div_magic(Da, Pm1_0, (uint32_t)h1.z, s012 & 255);
-          if (map1 >= 0) blocks *= ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255);
-          if (map2 >= 0) blocks *= ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
-          const int64_t smact = blocks < n_sm ? blocks : n_sm;
-          const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
-          const double Rep = (double)blocks * h3.x * rSM;  // line 15: #Blocks / (B_act SM_act)
-          E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
-                       rSM, (double)smact, kc);
-        } else {
-          E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
-        }
-        // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
-        E = (ok && E > 0.0 && E < kInf) ? E : kInf;
-        // a8: exact lexicographic key (E, original index): ties go to the lowest index
-        const bool better = E < st.e || (E == st.e && orig < st.i);
-        if (SECOND) st.s = better ? st.e : fmin(st.s, E);
-        st.i = better ? orig : st.i;
-        st.e = better ? E : st.e;
-      }
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], RP_AFR(k, ks), bfr[ks]);
     }
+  };
+#undef RP_AFR
+  // a3, a6, a7, a8 for the 2 pairs of this lane in one octet
+  auto epi_oct = [&](int oc, const double (&acc)[NPOLY][2]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      // output column 2 (lane % 4) + v; padded configurations (c >= nFc) have zero records
+      // and zero monomials, so their E is NaN and they are masked below
+      const CfgRec *cr = rec + oc * 8 + 2 * (lane & 3) + v;
+      const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));      // P01 | orig, Pm1_0
+      const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);             // Pm1_1, Pm1_2, M0, M1
+      const int32_t orig = (int32_t)(h0.y & 0xffffffff);
+      // a3: "P1 P2 <= D1^2 is meaningful"
+      const bool ok = tok && h0.x <= D1sq;
+      double E;
+      if (MWP) {
+        const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);           // M2, s012, W
+        const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);     // rB, rW
+        const int32_t Pm1_0 = (int32_t)(h0.y >> 32);
+        const uint32_t s012 = (uint32_t)h2.y;
+        const double W = __hiloint2double(h2.w, h2.z);
+        // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
+        int64_t blocks = 1;
+        if (map0 >= 0) blocks *= ceil_div_magic(Da, Pm1_0, (uint32_t)h1.z, s012 & 255);
+        if (map1 >= 0) blocks *= ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255);
+        if (map2 >= 0) blocks *= ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+        const int64_t smact = blocks < n_sm ? blocks : n_sm;
+        const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
+        const double Rep = (double)blocks * h3.x * rSM;  // line 15: #Blocks / (B_act SM_act)
+        E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
+                     rSM, (double)smact, kc);
+      } else {
+        E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
+      }
+      // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
+      E = (ok && pos_finite(E)) ? E : kInf;
+      // a8: exact lexicographic key (E, original index): ties go to the lowest index (E and the
+      // running best are positive or +inf, so their bit patterns compare as integers)
+      const long long eb = __double_as_longlong(E), sb = __double_as_longlong(st.e);
+      const bool better = eb < sb || (eb == sb && orig < st.i);
+      if (SECOND) st.s = better ? st.e : fmin(st.s, E);
+      st.i = better ? orig : st.i;
+      st.e = better ? E : st.e;
+    }
+  };
+  if (wid * 8 < tmax) {
+    // a3 early exit: configurations are sorted by P1 P2, so every octet from the first one whose
+    // smallest P1 P2 exceeds the largest D1^2 of the warp's tuples fails the D rule
+    int nEff = nOctF;
+    if (sorted)
+      for (int b0 = 0; b0 < nOctF; b0 += 32) {
+        const int oc = b0 + lane;
+        const unsigned stop = __ballot_sync(0xffffffffu, oc < nOctF && __ldg(&rec[oc * 8].P01) > maxD1sq);
+        if (stop) {
+          nEff = b0 + __ffs(stop) - 1;
+          break;
+        }
+      }
+#ifdef RP_SWEEP_PIPE
+    // software pipeline: the DMMAs of octet oc + 1 are issued before the scalar E of octet oc,
+    // so the shared FP64 datapath has independent work from both while either chain waits
+    double acc0[NPOLY][2], acc1[NPOLY][2];
+    if (nEff > 0) mma_oct(0, acc0);
+    int oc = 0;
+    for (; oc + 1 < nEff; oc += 2) {
+      mma_oct(oc + 1, acc1);
+      epi_oct(oc, acc0);
+      if (oc + 2 < nEff) mma_oct(oc + 2, acc0);
+      epi_oct(oc + 1, acc1);
+    }
+    if (oc < nEff) epi_oct(oc, acc0);
+#else
+    for (int oc = 0; oc < nEff; ++oc) {
+      double acc[NPOLY][2];
+      mma_oct(oc, acc);
+      epi_oct(oc, acc);
+    }
+#endif
   }
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
   st = merge(st, shfl_xor(st, 1));
