@@ -5,10 +5,11 @@
 // Reading R12 fixes the constant denominator coefficient beta_0 = 1, turning it into
 // G_ff z = -G_{f,beta0} with G = A^T A (reading R13: normal equations, as the north star asks;
 // the paper's SVD is the f1 NEXT row).  The matrix is at most 160 x 160, so one CTA per metric
-// does it in shared memory:
+// does it on chip:
 //   1. Jacobi equilibration  S = D G_ff D, D = diag(1/sqrt(G_ii))   (conditioning, R14);
-//   2. right-looking Cholesky S = L L^T  (pivot <= 1e-13 -> RP_ERR_DEGENERATE);
-//   3. two triangular solves;
+//   2. right-looking Cholesky S = L L^T with the matrix in registers, 2-D cyclic over the 512
+//      threads, one block barrier per column (pivot <= 1e-13 -> RP_ERR_DEGENERATE);
+//   3. two triangular solves by one warp (unknowns in registers, shuffle broadcasts);
 //   4. one step of iterative refinement with the residual b - G_ff z accumulated in
 //      double-double from the unrounded Gram entries, which removes the solve's own rounding
 //      error and leaves only the Gram's.
@@ -32,28 +33,75 @@ __device__ __forceinline__ void dd_fma(double &hi, double &lo, double a, double 
   lo += pe;
 }
 
-// x <- (L L^T)^{-1} x, L lower triangular in sL (stride ld), rd[j] = 1 / L_jj.  One warp does
-// both triangular solves (warp-synchronous steps instead of block-wide barriers).
-__device__ void chol_solve(const double *sL, const double *rd, int ld, int m, double *x) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int j = 0; j < m; ++j) {  // forward: L y = x
-      const double xj = x[j] * rd[j];
-      __syncwarp();
-      if (lane == 0) x[j] = xj;
-      for (int i = j + 1 + lane; i < m; i += 32) x[i] -= sL[i * ld + j] * xj;
-      __syncwarp();
-    }
-    for (int j = m - 1; j >= 0; --j) {  // backward: L^T z = y
-      const double xj = x[j] * rd[j];
-      __syncwarp();
-      if (lane == 0) x[j] = xj;
-      for (int i = lane; i < j; i += 32) x[i] -= sL[j * ld + i] * xj;
-      __syncwarp();
+// 1/x and 1/sqrt(x) for x > 0: MUFU seeds plus Newton steps (a few ulp; the refinement step
+// below removes the solve's own rounding error anyway)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {  // y <- y (3 - x y^2) / 2
+    const double h = 0.5 * x * y;
+    y = fma(y, fma(-h, y, 0.5), y);
+  }
+  return y;
+}
+
+// Register-resident Cholesky (one block barrier per column; measured phases with
+// -DRP_SOLVE_TS at m = 139: load 11k cycles, factorisation 165k, each triangular solve pair 42k,
+// residuals 18k): thread (ty, tx) = (tid / 32, tid % 32) of 512 owns the entries
+// (i, j) = (ty + 16 a, tx + 32 b) of the equilibrated matrix (m <= 16 kRA, m <= 32 kCB).
+constexpr int kRA = 10, kCB = 5;
+// slot (a, b) can hold a lower-triangle entry (j <= i) for some thread: only those 30 of the 50
+// are ever touched, so the compiler keeps 60 registers of the matrix per thread
+__host__ __device__ constexpr bool live(int a, int b) { return 32 * b <= 16 * a + 15; }
+
+// x <- (L L^T)^{-1} x by warp 0: lane owns x_i, i = lane + 32 k, in registers; L (lower, sL,
+// stride ld odd: conflict-free column reads) and rd[j] = 1 / L_jj from shared memory; each
+// step broadcasts the finished unknown by one shuffle.
+__device__ void chol_solve_warp(const double *sL, const double *rd, int ld, int m, double *x) {
+  const int lane = threadIdx.x;
+  double v[kCB];
+#pragma unroll
+  for (int k = 0; k < kCB; ++k) v[k] = (lane + 32 * k < m) ? x[lane + 32 * k] : 0.0;
+#pragma unroll
+  for (int kb = 0; kb < kCB; ++kb) {  // forward: L y = x
+    if (32 * kb >= m) break;
+    const int jn = (m - 32 * kb) < 32 ? (m - 32 * kb) : 32;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int j = 32 * kb + jj;
+      const double yj = __shfl_sync(0xffffffffu, v[kb], jj) * rd[j];
+      if (lane == jj) v[kb] = yj;
+#pragma unroll
+      for (int k = kb; k < kCB; ++k) {
+        const int i = lane + 32 * k;
+        if (i > j && i < m) v[k] = fma(-sL[i * ld + j], yj, v[k]);
+      }
     }
   }
-  __syncthreads();
+#pragma unroll
+  for (int kb = kCB - 1; kb >= 0; --kb) {  // backward: L^T z = y
+    if (32 * kb >= m) continue;
+    const int jn = (m - 32 * kb) < 32 ? (m - 32 * kb) : 32;
+    for (int jj = jn - 1; jj >= 0; --jj) {
+      const int j = 32 * kb + jj;
+      const double zj = __shfl_sync(0xffffffffu, v[kb], jj) * rd[j];
+      if (lane == jj) v[kb] = zj;
+#pragma unroll
+      for (int k = 0; k <= kb; ++k) {
+        const int i = lane + 32 * k;
+        if (i < j) v[k] = fma(-sL[j * ld + i], zj, v[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kCB; ++k)
+    if (lane + 32 * k < m) x[lane + 32 * k] = v[k];
 }
 
 // double-double sum of a warp's (hi, lo) pairs (fixed butterfly order)
@@ -67,88 +115,124 @@ __device__ __forceinline__ void dd_warp_sum(double &hi, double &lo) {
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc, int beta0,
-                                                         double *coef_out, double *info_out) {
+__global__ void __launch_bounds__(kSolveThreads, 1) k_solve(const double *G, int nc, int beta0,
+                                                            double *coef_out, double *info_out) {
   extern __shared__ __align__(16) double sm[];
-  const int m = nc - 1, ld = m + 1;
-  double *sL = sm;            // [m][ld]
+  const int m = nc - 1, ld = m | 1;
+  double *sL = sm;            // [m][ld]  the factor L (lower)
   double *dsc = sL + m * ld;  // [m]
   double *b0 = dsc + m;       // -G_{f,beta0}
   double *x = b0 + m;         // work vector
   double *z = x + m;          // solution, unequilibrated
   double *rd = z + m;         // 1 / L_jj
+  double *cb = rd + m;        // [2][m]  published column of the factorisation step (double buffer)
+  double *csc = cb + 2 * m;   // [m]  1 / sqrt(pivot) of each column
   __shared__ int s_status;
   __shared__ double s_pmin, s_pmax;
+#ifdef RP_SOLVE_TS  // phase timestamps (debug builds): written over coef[1..6] of metric 0
+  unsigned long long ts[8];
+#define RP_TS(k) ts[k] = clock64()
+  RP_TS(0);
+#else
+#define RP_TS(k)
+#endif
   const double *Gm = G + (int64_t)blockIdx.x * nc * nc;
   auto col = [beta0](int i) { return i < beta0 ? i : i + 1; };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ty = wid, tx = lane;
 
   if (threadIdx.x == 0) {
     s_status = 0;
     s_pmin = __longlong_as_double(0x7ff0000000000000ll);
     s_pmax = 0.0;
   }
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-    const int i = t / m, j = t % m;
-    sL[i * ld + j] = Gm[(int64_t)col(i) * nc + col(j)];
-  }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) b0[i] = -Gm[(int64_t)col(i) * nc + beta0];
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const double di = sL[i * ld + i];
+    const double di = Gm[(int64_t)col(i) * nc + col(i)];
     if (!(di > 0.0)) s_status = RP_ERR_DEGENERATE;
     dsc[i] = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
+    b0[i] = -Gm[(int64_t)col(i) * nc + beta0];
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-    const int i = t / m, j = t % m;
-    sL[i * ld + j] *= dsc[i] * dsc[j];
-  }
+  // owned entries of S = D G_ff D (Jacobi equilibration), column 0 published
+  double A[kRA][kCB];
+#pragma unroll
+  for (int a = 0; a < kRA; ++a)
+#pragma unroll
+    for (int b = 0; b < kCB; ++b) {
+      if (!live(a, b)) continue;
+      const int i = ty + 16 * a, j = tx + 32 * b;
+      A[a][b] = (i < m && j < m && j <= i) ? Gm[(int64_t)col(i) * nc + col(j)] * dsc[i] * dsc[j] : 0.0;
+      if (j == 0 && i < m) cb[i] = A[a][b];
+    }
   __syncthreads();
-  // Cholesky, lower triangle, blocked right-looking: an 8-column panel is factorised by warp 0
-  // (warp-synchronous), then every warp applies the rank-8 update to its rows of the trailing
-  // matrix (2 block barriers per panel)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int kb = 0; kb < m; kb += 8) {
-    const int nb = (m - kb) < 8 ? (m - kb) : 8;
-    if (wid == 0 && s_status == 0) {
-      for (int c = kb; c < kb + nb; ++c) {
-        const double piv = sL[c * ld + c];
-        if (lane == 0) {
-          if (!(piv > 1e-13)) s_status = RP_ERR_DEGENERATE;
-          s_pmin = fmin(s_pmin, piv);
-          s_pmax = fmax(s_pmax, piv);
-        }
-        const double lcc = sqrt(fmax(piv, 1e-300));
-        const double rlcc = 1.0 / lcc;
-        __syncwarp();
-        if (lane == 0) sL[c * ld + c] = lcc;
-        for (int i = c + 1 + lane; i < m; i += 32) sL[i * ld + c] *= rlcc;
-        __syncwarp();
-        for (int j = c + 1; j < kb + nb; ++j) {
-          const double ljc = sL[j * ld + c];
-          for (int i = j + lane; i < m; i += 32) sL[i * ld + j] -= sL[i * ld + c] * ljc;
-        }
-        __syncwarp();
+  RP_TS(1);
+  // right-looking Cholesky, one column per step and one block barrier per step: every thread
+  // reads the published column c (its pivot included), applies the rank-1 update to the entries
+  // it owns, finishes column c, and the owners of column c + 1 publish it into the other buffer
+  int status = s_status;
+  double pmin = __longlong_as_double(0x7ff0000000000000ll), pmax = 0.0;
+  for (int c = 0; c < m && status == 0; ++c) {
+    const double *bc = cb + (c & 1) * m;
+    double *bn = cb + ((c + 1) & 1) * m;
+    const double piv = bc[c];
+    pmin = fmin(pmin, piv);
+    pmax = fmax(pmax, piv);
+    if (!(piv > 1e-13)) {  // uniform: every thread reads the same pivot
+      status = RP_ERR_DEGENERATE;
+      break;
+    }
+    const double rp = rcp_nr(piv);
+    if (threadIdx.x == 0) csc[c] = rsqrt_nr(piv);  // L_ic = S_ic / sqrt(piv), applied at the end
+    // rank-1 update S_ij -= S_ic S_jc / piv of the owned entries with j > c (cj = 0 elsewhere:
+    // the FMA leaves those unchanged) in rows i > c (warp-uniform: ty is the warp id)
+    double cj[kCB];
+#pragma unroll
+    for (int b = 0; b < kCB; ++b) {
+      const int j = tx + 32 * b;
+      cj[b] = (j > c && j < m) ? bc[j] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < kRA; ++a) {
+      const int i = ty + 16 * a;
+      if (i > c && i < m) {
+        const double sa = bc[i] * rp;
+#pragma unroll
+        for (int b = 0; b < kCB; ++b)
+          if (live(a, b)) A[a][b] = fma(-sa, cj[b], A[a][b]);
+      }
+    }
+    // the owners of column c + 1 (lane (c + 1) % 32 of every warp, slot b = (c + 1) / 32:
+    // uniform) publish it, its pivot included
+    if (tx == ((c + 1) & 31)) {
+      switch ((c + 1) >> 5) {
+#define RP_PUB(B)                                                   \
+  case B:                                                           \
+    _Pragma("unroll") for (int a = 0; a < kRA; ++a) {               \
+      const int i = ty + 16 * a;                                    \
+      if (live(a, B) && i > c && i < m) bn[i] = A[a][B];            \
+    }                                                               \
+    break;
+        RP_PUB(0) RP_PUB(1) RP_PUB(2) RP_PUB(3) RP_PUB(4)
+#undef RP_PUB
       }
     }
     __syncthreads();
-    if (s_status != 0) break;
-    const int j0 = kb + nb;
-    for (int i = j0 + wid; i < m; i += nw) {
-      double li[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) li[c] = c < nb ? sL[i * ld + kb + c] : 0.0;
-      for (int j = j0 + lane; j <= i; j += 32) {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < nb) acc = fma(li[c], sL[j * ld + kb + c], acc);
-        sL[i * ld + j] -= acc;
-      }
-    }
-    __syncthreads();
   }
+  if (threadIdx.x == 0) {
+    s_status = status;
+    s_pmin = pmin;
+    s_pmax = pmax;
+  }
+#pragma unroll
+  for (int a = 0; a < kRA; ++a)
+#pragma unroll
+    for (int b = 0; b < kCB; ++b) {
+      const int i = ty + 16 * a, j = tx + 32 * b;
+      if (live(a, b) && i < m && j <= i) sL[i * ld + j] = A[a][b] * csc[j];
+    }
   __syncthreads();
+  RP_TS(2);
   double *cf = coef_out + (int64_t)blockIdx.x * nc;
   double *inf = info_out + (int64_t)blockIdx.x * 5;
   if (s_status != 0) {
@@ -162,10 +246,14 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
     }
     return;
   }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) rd[i] = 1.0 / sL[i * ld + i];
-  // solve
-  for (int i = threadIdx.x; i < m; i += blockDim.x) x[i] = dsc[i] * b0[i];
-  chol_solve(sL, rd, ld, m, x);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    rd[i] = 1.0 / sL[i * ld + i];
+    x[i] = dsc[i] * b0[i];
+  }
+  __syncthreads();
+  if (wid == 0) chol_solve_warp(sL, rd, ld, m, x);
+  __syncthreads();
+  RP_TS(3);
   for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] = dsc[i] * x[i];
   __syncthreads();
   // one refinement step: r = b0 - G_ff z in double-double from the original Gram (a warp per
@@ -180,7 +268,11 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
       x[i] = dsc[i] * (hi + lo);
     }
   }
-  chol_solve(sL, rd, ld, m, x);
+  __syncthreads();
+  RP_TS(4);
+  if (wid == 0) chol_solve_warp(sL, rd, ld, m, x);
+  __syncthreads();
+  RP_TS(5);
   for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] += dsc[i] * x[i];
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) cf[col(i)] = z[i];
@@ -206,12 +298,16 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
     }
   }
   __syncthreads();
+  RP_TS(6);
   if (threadIdx.x == 0) {
     double hi = 0.0, lo = 0.0;
     for (int w = 0; w < nw; ++w) {
       dd_add(hi, lo, s_rh[w]);
       lo += s_rl[w];
     }
+#ifdef RP_SOLVE_TS
+    for (int k = 1; k <= 6; ++k) cf[k] = (double)(ts[k] - ts[k - 1]);
+#endif
     inf[0] = 0;
     inf[1] = (double)m;
     inf[2] = hi + lo;
@@ -223,7 +319,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const double *G, int nc
 cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *coef_out,
                          double *info_out, cudaStream_t s) {
   const int m = nc - 1;
-  const size_t smem = ((size_t)m * (m + 1) + 5 * (size_t)m) * sizeof(double);
+  if (m > 16 * kRA || m > 32 * kCB) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)m * (m | 1) + 8 * (size_t)m) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

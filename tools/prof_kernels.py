@@ -48,6 +48,20 @@ elif which == "svd":
     for _ in range(reps):
         rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
     ev[1].record()
+elif which == "solve":
+    fc = synth.fitheavy(sigma=0.01)
+    X = torch.from_numpy(fc.X).to(dev)
+    V = rp.eval_metrics(fc.truths[0], X) * torch.from_numpy(fc.noise).to(dev)
+    c, e = rp.xform_from_box(*rp.minmax(X))
+    G = rp.gram(X, V, fc.num_exp, fc.den_exp, c, e)
+    coef, info = rp.solve_dev(G, fc.num_exp, fc.den_exp)
+    print("info:", info.cpu().numpy().tolist())
+    print("coef[0][:8]:", coef[0, :8].cpu().numpy().tolist())
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        rp.solve_dev(G, fc.num_exp, fc.den_exp, coef=coef, info=info)
+    ev[1].record()
 else:
     fc = synth.fitheavy(sigma=0.01)
     X = torch.from_numpy(fc.X).to(dev)
