@@ -14,6 +14,8 @@
 // register accumulators are flushed into a shared-memory accumulator every kChunk rows
 // (two-level summation), the per-CTA partials are summed in a fixed order by k_gram_reduce.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "rp_internal.cuh"
 
@@ -505,10 +507,10 @@ __host__ __device__ constexpr int upper_index(int NB, int bi, int bj) {
   return bi * NB - bi * (bi - 1) / 2 + (bj - bi);
 }
 
-template <int NB, int NV>
+template <int NB, int NV, int NW = kFW>
 __host__ __device__ constexpr uint32_t fused_slot_off(int wid, int j, int S, int RT) {
   const int NT = (1 + 2 * NV) * NB * (NB + 1) / 2;
-  const int id = wid * ((NT + 15) / 16) + j;
+  const int id = wid * ((NT + NW - 1) / NW) + j;
   if (id >= NT) return kNoTile;
   int pa = 0, pb = 0, pair = 0, bi = 0, bj = 0;
   fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
@@ -518,14 +520,14 @@ __host__ __device__ constexpr uint32_t fused_slot_off(int wid, int j, int S, int
 // The MMA phase of one warp over the k-steps of a row tile: every operand offset is a
 // compile-time constant (template on the warp id), so fragment loads are immediate-offset LDS
 // and slots sharing an A fragment reuse the loaded value.
-template <int NB, int NV, int WID, int SLOTS, int S, int RT>
+template <int NB, int NV, int WID, int SLOTS, int S, int RT, int NW = kFW>
 __device__ __forceinline__ void fused_mma_warp(const double *sX, int lane, double (&acc)[SLOTS][2]) {
 #pragma unroll 2
   for (int ks = 0; ks < RT / 4; ++ks) {
     const double *row = sX + (ks * 4 + (lane & 3)) * S + (lane >> 2);
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
-      const uint32_t off = fused_slot_off<NB, NV>(WID, j, S, RT);
+      const uint32_t off = fused_slot_off<NB, NV, NW>(WID, j, S, RT);
       if (off != kNoTile) dmma_8x8x4(acc[j][0], acc[j][1], row[off & 0xffffu], row[off >> 16]);
     }
   }
@@ -642,6 +644,239 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_gram_fused(FusedArgs a) {
     for (int i = threadIdx.x; i < L::NT * 64; i += blockDim.x) part[i] = 0.0;
 }
 
+// ============================================================================================
+// Warp-specialised fused Gram (default).  In k_gram_fused every warp stages, then every warp
+// multiplies, so the FP64 tensor pipe idles during staging (~30% of a tile, measured with
+// -DRP_GRAM_TS).  Here warpgroup 3 (warps 12-15, one per SM sub-partition) only builds design
+// rows and warpgroups 0-2 (12 warps, 27 accumulator slots each) only multiply.  A stage holds
+// X_0 = M(u) of 32 rows and, per row, the scales V_v and V_v^2: since
+//   X_0^T diag(V_v) X_0  and  X_0^T diag(V_v^2) X_0
+// are the (0, 1+v) and (1+v, 1+v) blocks, the consumers scale their A fragment (one row per lane)
+// instead of the producers writing X_{1+v} = V_v X_0 (4x less staging and shared memory).  Stages
+// are handed over with named barriers (FULL[b]: producers arrive, consumers wait; EMPTY[b]:
+// consumers arrive, producers wait); setmaxnreg moves 72 registers per producer thread to the
+// consumers (56 / 152 of the 128 at launch).
+// ============================================================================================
+constexpr int kWsRT = 32;      // rows per tile
+constexpr int kWsMW = 12;      // MMA (consumer) warps
+constexpr int kWsPW = 4;       // staging (producer) warps
+#ifndef RP_WS_NS
+#define RP_WS_NS 3
+#endif
+constexpr int kWsNS = RP_WS_NS;  // stages
+#ifndef RP_WS_UNROLL
+#define RP_WS_UNROLL 1
+#endif
+constexpr int kWsUnroll = RP_WS_UNROLL;  // k-steps per MMA loop body (code size: instruction cache)
+constexpr int kWsFlush = 32;   // tiles between flushes of the register accumulators (1024 rows)
+constexpr int kWsThreads = 32 * (kWsMW + kWsPW);
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int NB, int NV>
+struct WsL {
+  static constexpr int S = FL<NB, NV>::S;
+  static constexpr int SCS = 2 * NV;                   // scales per row: V_v, V_v^2
+  static constexpr int XB = kWsRT * S + kWsRT * SCS;   // doubles per stage: X_0 | scales
+};
+
+// slot j of consumer warp WID: A = X_0 block bi scaled by sc (0: 1, 1 + v: V_v, 1 + NV + v: V_v^2),
+// B = X_0 block bj; packed as A offset | B offset << 12 | sc << 24
+template <int NB, int NV, int WID, int SLOTS>
+__host__ __device__ constexpr uint32_t ws_slot(int j) {
+  constexpr int NT = (1 + 2 * NV) * NB * (NB + 1) / 2;
+  const int id = WID * SLOTS + j;
+  if (id >= NT) return kNoTile;
+  int pa = 0, pb = 0, pair = 0, bi = 0, bj = 0;
+  fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
+  return (uint32_t)(8 * bi) | ((uint32_t)(8 * bj) << 12) | ((uint32_t)pair << 24);
+}
+
+template <int NB, int NV, int WID, int SLOTS>
+__device__ __forceinline__ void ws_mma_warp(const double *buf, int lane, double (&acc)[SLOTS][2]) {
+  using W = WsL<NB, NV>;
+  const double *scb = buf + kWsRT * W::S;
+#pragma unroll (kWsUnroll)
+  for (int ks = 0; ks < kWsRT / 4; ++ks) {
+    const int r = ks * 4 + (lane & 3);
+    const double *row = buf + r * W::S + (lane >> 2);
+    double sc[1 + 2 * NV];
+    sc[0] = 1.0;
+#pragma unroll
+    for (int v = 0; v < 2 * NV; ++v) sc[1 + v] = scb[r * W::SCS + v];
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      constexpr uint32_t kNo = kNoTile;
+      const uint32_t off = ws_slot<NB, NV, WID, SLOTS>(j);
+      if (off != kNo) {
+        const int pr = (int)(off >> 24);
+        const double a = row[off & 0xfff];
+        dmma_8x8x4(acc[j][0], acc[j][1], pr == 0 ? a : a * sc[pr], row[(off >> 12) & 0xfff]);
+      }
+    }
+  }
+}
+
+template <int NB, int NV>
+__global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
+  using L = FL<NB, NV>;
+  using W = WsL<NB, NV>;
+  constexpr int SLOTS = (L::NT + kWsMW - 1) / kWsMW;
+  extern __shared__ __align__(16) double fsm[];
+  const GramBasis &B = *a.basis;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *sX = fsm;  // [kWsNS][W::XB]
+
+  const int64_t r_begin = a.K * blockIdx.x / gridDim.x;
+  const int64_t r_end = a.K * (blockIdx.x + 1) / gridDim.x;
+  const int ntr = (int)((r_end - r_begin + kWsRT - 1) / kWsRT);
+  for (int i = threadIdx.x; i < kWsNS * W::XB; i += blockDim.x) sX[i] = 0.0;  // pads stay zero
+  __syncthreads();
+
+  if (wid >= kWsMW) {
+    // ---- producers: 8 rows per warp per tile --------------------------------------------------
+    // The inputs of the warp's 8 rows, [X (8 n) | V (8 NV) | S (8)], are loaded into registers one
+    // tile ahead (2 values per lane), so the HBM latency is off the staging path.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    const int pw = wid - kWsMW;
+    const int n = B.n, m = B.n_num, pwr = B.maxdeg + 1;
+    const int nXv = 8 * n, nVv = 8 * NV, nIn = nXv + nVv + (a.S ? 8 : 0);
+    double *sPow = sX + kWsNS * W::XB + pw * (8 * n * pwr + 16);  // [8][n][pwr]
+    double *sSw = sPow + 8 * n * pwr;                              // [8]   row scales
+    uint32_t *sExp = reinterpret_cast<uint32_t *>(sX + kWsNS * W::XB + kWsPW * (8 * n * pwr + 16)) + pw * L::M8;
+    for (int j = lane; j < m; j += 32) sExp[j] = B.pexp[j];
+    const double xc = lane < nXv ? B.xc[lane % n] : 0.0, xs = lane < nXv ? ldexp(1.0, -B.xe[lane % n]) : 0.0;
+    auto fetch = [&](int tr, int i) -> double {  // input i of the warp's rows of tile tr (0 past the slab)
+      const int64_t r0 = r_begin + (int64_t)tr * kWsRT + 8 * pw;
+      if (tr >= ntr || i >= nIn) return 0.0;
+      if (i < nXv) return r0 + i / n < r_end ? a.X[(r0 + i / n) * n + i % n] : 0.0;
+      i -= nXv;
+      if (i < nVv) return r0 + i % 8 < r_end ? a.V[(int64_t)(i / 8) * a.K + r0 + i % 8] : 0.0;
+      i -= nVv;
+      return r0 + i < r_end ? a.S[r0 + i] : 0.0;
+    };
+    double v0 = fetch(0, lane), v1 = fetch(0, lane + 32);
+    __syncwarp();
+    for (int tr = 0; tr < ntr; ++tr) {
+      const int b = tr % kWsNS;
+      double *buf = sX + b * W::XB;
+      double *scb = buf + kWsRT * W::S + 8 * pw * W::SCS;  // scales of the warp's 8 rows
+      const int64_t r0 = r_begin + (int64_t)tr * kWsRT + 8 * pw;
+      const int nvalid = (int)((r_end - r0) < 8 ? (r_end - r0) : 8);  // rows of the warp in the slab
+      const double cv0 = v0, cv1 = v1;
+      v0 = fetch(tr + 1, lane);  // the next tile's inputs: in flight while this one is built
+      v1 = fetch(tr + 1, lane + 32);
+      {  // row scales S
+        const int i0 = lane - nXv - nVv, i1 = lane + 32 - nXv - nVv;
+        if (i0 >= 0 && i0 < 8) sSw[i0] = cv0;
+        if (i1 >= 0 && i1 < 8) sSw[i1] = cv1;
+      }
+      __syncwarp();
+      // a10: powers of u = (x - c) 2^-e (X lanes: row lane / n, variable lane % n)
+      if (lane < nXv) {
+        const int r = lane / n, k = lane % n;
+        const double u = (cv0 - xc) * xs;
+        double p = r < nvalid ? ((a.S && k == 0) ? sSw[r] : 1.0) : 0.0;  // weighted rows: s_r via u_0
+        double *dst = sPow + (r * n + k) * pwr;
+        for (int e = 0; e < pwr; ++e) {
+          dst[e] = p;
+          p *= u;
+        }
+      }
+      if (tr >= kWsNS) named_sync(1 + kWsNS + b, kWsThreads);  // EMPTY[b]: consumers done with tile tr - NS
+      {  // per-row scales V_v, V_v^2 (V inputs: index i = v * 8 + r)
+        const int i0 = lane - nXv, i1 = lane + 32 - nXv;
+        if (i0 >= 0 && i0 < nVv) scb[(i0 % 8) * W::SCS + i0 / 8] = cv0, scb[(i0 % 8) * W::SCS + NV + i0 / 8] = cv0 * cv0;
+        if (i1 >= 0 && i1 < nVv) scb[(i1 % 8) * W::SCS + i1 / 8] = cv1, scb[(i1 % 8) * W::SCS + NV + i1 / 8] = cv1 * cv1;
+      }
+      __syncwarp();
+      // a11: X_0 = M(u) for the warp's 8 rows (the design row is [X_0 | -V X_0])
+      // entries j = lane + 32 it of the 8 m, two per iteration (independent chains)
+      int r = lane / m, col = lane % m;
+      int r2 = (lane + 32) / m, col2 = (lane + 32) % m;
+#ifdef RP_WS_NOSTAGE  // timing experiment only: no design rows (wrong results)
+      if (0)
+#endif
+      for (int j = lane; j < 8 * m; j += 64) {
+        const bool two = j + 32 < 8 * m;
+        const uint32_t w = sExp[col], w2 = sExp[two ? col2 : col];
+        const double *pr = sPow + r * n * pwr, *pr2 = sPow + (two ? r2 : r) * n * pwr;
+        double x = pr[w & 15], y = pr2[w2 & 15];
+        if (n == 4) {  // the BASELINE bases: a product tree, depth 2
+          x = (x * pr[pwr + ((w >> 4) & 15)]) * (pr[2 * pwr + ((w >> 8) & 15)] * pr[3 * pwr + ((w >> 12) & 15)]);
+          y = (y * pr2[pwr + ((w2 >> 4) & 15)]) * (pr2[2 * pwr + ((w2 >> 8) & 15)] * pr2[3 * pwr + ((w2 >> 12) & 15)]);
+        } else {
+          for (int k = 1; k < n; ++k) {
+            x *= pr[k * pwr + ((w >> (4 * k)) & 15)];
+            y *= pr2[k * pwr + ((w2 >> (4 * k)) & 15)];
+          }
+        }
+        buf[(8 * pw + r) * W::S + col] = x;
+        if (two) buf[(8 * pw + r2) * W::S + col2] = y;
+        col += 64;
+        while (col >= m) col -= m, ++r;
+        col2 += 64;
+        while (col2 >= m) col2 -= m, ++r2;
+      }
+      __threadfence_block();
+      named_arrive(1 + b, kWsThreads);  // FULL[b]
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---- consumers: the upper tiles of the 1 + 2 NV blocks ----------------------------------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
+  double acc[SLOTS][2];
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double *part = a.part + (int64_t)blockIdx.x * L::NT * 64;
+  bool first = true;
+  for (int tr = 0; tr < ntr; ++tr) {
+    const int b = tr % kWsNS;
+    named_sync(1 + b, kWsThreads);  // FULL[b]
+    const double *cur = sX + b * W::XB;
+    switch (wid) {
+#define RP_W(w) \
+  case w: ws_mma_warp<NB, NV, w, SLOTS>(cur, lane, acc); break;
+      RP_W(0) RP_W(1) RP_W(2) RP_W(3) RP_W(4) RP_W(5) RP_W(6) RP_W(7) RP_W(8) RP_W(9) RP_W(10) RP_W(11)
+#undef RP_W
+    }
+    named_arrive(1 + kWsNS + b, kWsThreads);  // EMPTY[b]
+    if (((tr + 1) % kWsFlush) == 0 || tr + 1 == ntr) {
+#pragma unroll
+      for (int j = 0; j < SLOTS; ++j) {
+        const int id = wid * SLOTS + j;
+        if (id < L::NT) {
+          int pa, pb, pair, bi, bj;
+          fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
+          double *dst = part + (int64_t)(pair * L::T + upper_index(NB, bi, bj)) * 64 + lane * 2;
+          if (first) {
+            dst[0] = acc[j][0];
+            dst[1] = acc[j][1];
+          } else {
+            dst[0] += acc[j][0];
+            dst[1] += acc[j][1];
+          }
+          acc[j][0] = acc[j][1] = 0.0;
+        }
+      }
+      first = false;
+    }
+  }
+  if (ntr == 0)  // empty slab: zero partial
+    for (int i = threadIdx.x; i < L::NT * 64; i += kWsMW * 32) part[i] = 0.0;
+}
+
+template <int NB, int NV>
+static size_t ws_smem(int n, int pw) {
+  using L = FL<NB, NV>;
+  using W = WsL<NB, NV>;
+  return sizeof(double) * ((size_t)kWsNS * W::XB + (size_t)kWsPW * (8 * n * pw + 16)) +
+         sizeof(uint32_t) * kWsPW * L::M8;
+}
+
 // G_v (v < n_v) assembled from the block partials, summed over CTAs in fixed order.
 __global__ void k_gram_fused_reduce(const double *part, int nblk, int NB, int NV, int m, double *G) {
   const int T = NB * (NB + 1) / 2, NT = (1 + 2 * NV) * T, nc = 2 * m;
@@ -691,12 +926,22 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
   using L = FL<NB, NV>;
   const int gx = fused_grid_x(K);
   if ((size_t)gx * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
-  const size_t smem = fused_smem<NB, NV>(h.n, h.maxdeg + 1);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_gram_fused<NB, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   FusedArgs fa{d_basis, X, V, S, K, d_part};
-  k_gram_fused<NB, NV><<<gx, kFW * 32, smem, s>>>(fa);
+  cudaError_t e;
+  static const bool ws = !(getenv("RP_GRAM_KERNEL") && strcmp(getenv("RP_GRAM_KERNEL"), "fused") == 0);
+  if (ws) {  // warp-specialised (default)
+    const size_t smem = ws_smem<NB, NV>(h.n, h.maxdeg + 1);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(k_gram_ws<NB, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gram_ws<NB, NV><<<gx, kWsThreads, smem, s>>>(fa);
+  } else {
+    const size_t smem = fused_smem<NB, NV>(h.n, h.maxdeg + 1);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(k_gram_fused<NB, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gram_fused<NB, NV><<<gx, kFW * 32, smem, s>>>(fa);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t total = (int64_t)NV * 4 * h.n_num * h.n_num;
   const int rb = (int)((total + 255) / 256);
