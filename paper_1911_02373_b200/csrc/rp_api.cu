@@ -283,6 +283,49 @@ static rp_status build_gram_basis(const rp_basis *basis, const rp_xform *xf, Gra
     for (int k = 0; k < n; ++k) w |= (uint32_t)(basis->num_exp[j * n + k] & 15) << (4 * k);
     gb->pexp[j] = w;
   }
+  // monomial tree (layout only): parent = the column with one unit less of the first variable
+  // that has a nonzero exponent
+  {
+    const int m = basis->n_num;
+    bool tree = same && m <= 256;
+    int nconst = 0, maxd = 0;
+    std::vector<int> deg(m, 0);
+    for (int j = 0; tree && j < m; ++j) {
+      const int16_t *e = basis->num_exp + j * n;
+      for (int k = 0; k < n; ++k) deg[j] += e[k];
+      maxd = std::max(maxd, deg[j]);
+      if (deg[j] == 0) {
+        ++nconst;
+        gb->parent[j] = -1;
+        gb->pvar[j] = 0;
+        continue;
+      }
+      int k0 = 0;
+      while (e[k0] == 0) ++k0;
+      int par = -1;
+      for (int i = 0; i < m && par < 0; ++i) {
+        const int16_t *f = basis->num_exp + i * n;
+        bool eq = true;
+        for (int k = 0; k < n && eq; ++k) eq = f[k] == e[k] - (k == k0 ? 1 : 0);
+        if (eq) par = i;
+      }
+      if (par < 0) tree = false;
+      gb->parent[j] = (int16_t)par;
+      gb->pvar[j] = (int8_t)k0;
+    }
+    tree = tree && nconst == 1 && maxd <= 16;
+    gb->tree = tree ? 1 : 0;
+    if (tree) {
+      int pos = 0;
+      for (int d = 0; d <= maxd; ++d) {
+        gb->lv_start[d] = (int16_t)pos;
+        for (int j = 0; j < m; ++j)
+          if (deg[j] == d) gb->lv_cols[pos++] = (int16_t)j;
+      }
+      gb->lv_start[maxd + 1] = (int16_t)pos;
+      gb->n_lv = maxd + 1;
+    }
+  }
   if (xf)
     for (int k = 0; k < n; ++k) {
       gb->xc[k] = xf->c[k];

@@ -744,8 +744,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
     const int nXv = 8 * n, nVv = 8 * NV, nIn = nXv + nVv + (a.S ? 8 : 0);
     double *sPow = sX + kWsNS * W::XB + pw * (8 * n * pwr + 16);  // [8][n][pwr]
     double *sSw = sPow + 8 * n * pwr;                              // [8]   row scales
-    uint32_t *sExp = reinterpret_cast<uint32_t *>(sX + kWsNS * W::XB + kWsPW * (8 * n * pwr + 16)) + pw * L::M8;
-    for (int j = lane; j < m; j += 32) sExp[j] = B.pexp[j];
+    uint32_t *sExp = reinterpret_cast<uint32_t *>(sX + kWsNS * W::XB + kWsPW * (8 * n * pwr + 16)) + pw * 3 * L::M8;
+    uint32_t *sInfo = sExp + L::M8;                 // tree: parent | var << 16 of column j
+    uint32_t *sLv = sInfo + L::M8;                  // tree: the columns level by level
+    double *sU = sPow;                              // tree: u of the 8 rows [8][n] (aliases sPow)
+    double *sK = sPow + 8 * n;                      // tree: the constant column of the 8 rows
+    const bool tree = B.tree != 0;
+    for (int j = lane; j < m; j += 32) {
+      sExp[j] = B.pexp[j];
+      sInfo[j] = (uint32_t)(uint16_t)B.parent[j] | ((uint32_t)(uint8_t)B.pvar[j] << 16);
+      sLv[j] = (uint32_t)B.lv_cols[j];
+    }
     const double xc = lane < nXv ? B.xc[lane % n] : 0.0, xs = lane < nXv ? ldexp(1.0, -B.xe[lane % n]) : 0.0;
     auto fetch = [&](int tr, int i) -> double {  // input i of the warp's rows of tile tr (0 past the slab)
       const int64_t r0 = r_begin + (int64_t)tr * kWsRT + 8 * pw;
@@ -773,8 +782,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
         if (i1 >= 0 && i1 < 8) sSw[i1] = cv1;
       }
       __syncwarp();
-      // a10: powers of u = (x - c) 2^-e (X lanes: row lane / n, variable lane % n)
-      if (lane < nXv) {
+      // a10: u = (x - c) 2^-e (X lanes: row lane / n, variable lane % n); the tree needs u and the
+      // constant column, the general path the power table
+      if (tree) {
+        if (lane < nXv) sU[lane] = (cv0 - xc) * xs;
+        if (lane < 8) sK[lane] = lane < nvalid ? (a.S ? sSw[lane] : 1.0) : 0.0;  // weighted rows: s_r
+      } else if (lane < nXv) {
         const int r = lane / n, k = lane % n;
         const double u = (cv0 - xc) * xs;
         double p = r < nvalid ? ((a.S && k == 0) ? sSw[r] : 1.0) : 0.0;  // weighted rows: s_r via u_0
@@ -792,12 +805,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
       }
       __syncwarp();
       // a11: X_0 = M(u) for the warp's 8 rows (the design row is [X_0 | -V X_0])
+      if (tree) {
+        // a11 by the monomial tree: level d columns are parent (level d - 1) times one u
+        for (int d = 0; d < B.n_lv; ++d) {
+          const int l0 = B.lv_start[d], cnt = B.lv_start[d + 1] - l0;
+          const float rc = 1.0f / (float)cnt;
+          for (int e = lane; e < 8 * cnt; e += 32) {
+            const int r = (int)(((float)e + 0.5f) * rc), col = (int)sLv[l0 + e - r * cnt];
+            double *row = buf + (8 * pw + r) * W::S;
+            if (d == 0) {
+              row[col] = sK[r];
+            } else {
+              const uint32_t inf = sInfo[col];
+              row[col] = row[inf & 0xffff] * sU[r * n + (inf >> 16)];
+            }
+          }
+          __syncwarp();
+        }
+      }
       // entries j = lane + 32 it of the 8 m, two per iteration (independent chains)
       int r = lane / m, col = lane % m;
       int r2 = (lane + 32) / m, col2 = (lane + 32) % m;
 #ifdef RP_WS_NOSTAGE  // timing experiment only: no design rows (wrong results)
       if (0)
 #endif
+      if (!tree)
       for (int j = lane; j < 8 * m; j += 64) {
         const bool two = j + 32 < 8 * m;
         const uint32_t w = sExp[col], w2 = sExp[two ? col2 : col];
@@ -874,7 +906,7 @@ static size_t ws_smem(int n, int pw) {
   using L = FL<NB, NV>;
   using W = WsL<NB, NV>;
   return sizeof(double) * ((size_t)kWsNS * W::XB + (size_t)kWsPW * (8 * n * pw + 16)) +
-         sizeof(uint32_t) * kWsPW * L::M8;
+         sizeof(uint32_t) * kWsPW * 3 * L::M8;
 }
 
 // G_v (v < n_v) assembled from the block partials, summed over CTAs in fixed order.

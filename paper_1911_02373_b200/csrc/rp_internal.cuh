@@ -114,6 +114,14 @@ struct GramBasis {  // exponents of the n_c design columns (numerator then denom
   // exponents packed 4 bits per variable
   int32_t fused;
   uint32_t pexp[256];
+  // monomial tree of the m numerator columns (fused path): column j of degree >= 1 is
+  // M_j = M_parent[j] * u_var[j]; levels lists the columns by degree (lv_start[d] .. lv_start[d+1])
+  int32_t tree;       // every non-constant column has its parent in the basis, one constant column
+  int32_t n_lv;       // number of levels (max degree + 1)
+  int16_t parent[256];
+  int8_t pvar[256];
+  int16_t lv_cols[256];
+  int16_t lv_start[18];
 };
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, const double *X,
                         const double *V, const double *S, int64_t K, int n_v, double *G,
