@@ -960,7 +960,8 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
   if ((size_t)gx * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
   FusedArgs fa{d_basis, X, V, S, K, d_part};
   cudaError_t e;
-  static const bool ws = !(getenv("RP_GRAM_KERNEL") && strcmp(getenv("RP_GRAM_KERNEL"), "fused") == 0);
+  const char *gk = getenv("RP_GRAM_KERNEL");  // "fused": the single-role kernel (tests, measurements)
+  const bool ws = !(gk && strcmp(gk, "fused") == 0);
   if (ws) {  // warp-specialised (default)
     const size_t smem = ws_smem<NB, NV>(h.n, h.maxdeg + 1);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;

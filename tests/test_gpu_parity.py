@@ -174,6 +174,33 @@ def test_fit_host_pointers_and_gram_edge_cases():
         assert np.max(np.abs(Gk - Go) / dg) <= 1e-13, K
 
 
+@pytest.mark.parametrize("kernel", ["ws", "fused"])
+@pytest.mark.parametrize("basis", ["tree", "no_tree"])
+def test_gram_fused_kernels(kernel, basis, monkeypatch):
+    """Both fused Gram kernels (warp-specialised default, single-role fallback) on a basis that
+    is closed under parents (monomial-tree staging) and on one that is not (power-table staging),
+    at ragged row counts, against the oracle's plain sum of outer products."""
+    if kernel == "fused":
+        monkeypatch.setenv("RP_GRAM_KERNEL", "fused")
+    fc = synth.polybench_fit_box()
+    if basis == "tree":
+        num = fc.num_exp
+    else:  # 12 monomials, most without their parent in the list (e.g. x0^2 without x0)
+        num = np.array([[0, 0, 0, 0], [2, 0, 0, 0], [0, 2, 0, 0], [0, 0, 1, 1], [2, 2, 0, 0], [1, 1, 1, 0],
+                        [0, 0, 0, 3], [3, 0, 0, 0], [0, 1, 2, 0], [2, 0, 0, 1], [1, 0, 1, 1], [0, 3, 0, 0]],
+                       dtype=np.int16)
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(fc.truths[0], fc.X)])
+    lo, hi = fc.X.min(axis=0), fc.X.max(axis=0)
+    c, e = rp.xform_from_box(lo, hi)
+    for K in (1, 31, 33, 517, 2000):
+        X = fc.X[:K]
+        G = rp.gram(_cuda(X), _cuda(V[:, :K]), num, num, c, e).cpu().numpy()
+        for i in range(len(V)):
+            Go = np.asarray(oracle.gram(X, V[i, :K], num, num, c, e), dtype=np.float64)
+            dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
+            assert np.max(np.abs(G[i] - Go) / dg) <= 1e-12, (kernel, basis, K, i)
+
+
 def test_fit_degenerate():
     X = np.ones((10, 1))
     V = np.full((1, 10), 3.0)
