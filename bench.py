@@ -385,8 +385,16 @@ def main():
     # 70*71/2 unique multiply-adds each
     gram_flop = (khi - klo) * (1 + 2 * 3) * 70 * 71
     gram_ach = gram_flop / (gram_ms * 1e-3) / 1e12
-    roofline_fit = {"bound": "tensor", "kernel": "k_gram (DMMA.8x8x4)", "achieved": gram_ach,
+    gtraffic = None
+    gprof = os.path.join(ROOT, "profiles", "gram_ncu_latest.json")
+    if os.path.exists(gprof):
+        try:
+            gtraffic = json.load(open(gprof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            gtraffic = None
+    roofline_fit = {"bound": "tensor", "kernel": "k_gram_ws (DMMA.8x8x4, warp-specialised)", "achieved": gram_ach,
                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gram_ach / FP64_PEAK_TFLOPS,
+                    "traffic": gtraffic,
                     "ms_per_call": gram_ms, "peak_source": "FP64 tensor = FP64 FMA rate on B200 "
                                                            "(measured DMMA 36.9 TF/s)"}
 
