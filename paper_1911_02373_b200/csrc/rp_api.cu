@@ -1086,8 +1086,7 @@ rp_status rp_plan_update_program(rp_plan plan, int32_t prog, const double *coef,
   RP_REQUIRE(is_device_ptr(coef) && (!xform || is_device_ptr(xform)), RP_ERR_INVALID_ARG,
              "coef / xform must be device pointers (stream-ordered update)");
   plan->stream = s;
-  RP_CUDA(launch_plan_set_coef(plan->d_progs + prog, coef, stride, xform, s));
-  RP_CUDA(launch_plan_configs(plan->d_progs, plan->n_prog, plan->d_F, plan->nF, plan->npe_pad, plan->tab, s));
+  RP_CUDA(launch_plan_refresh(plan->d_progs + prog, prog, coef, stride, xform, plan->npe_pad, plan->tab, s));
   if (plan->hist.enabled) {  // decisions of the old program are stale
     RP_CUDA(cudaMemsetAsync(plan->hist.slots, 0, ((size_t)plan->hist.mask + 1) * sizeof(HistSlot), s));
     RP_CUDA(cudaMemsetAsync(plan->hist.counters, 0, 3 * sizeof(unsigned long long), s));

@@ -909,9 +909,24 @@ static size_t ws_smem(int n, int pw) {
          sizeof(uint32_t) * kWsPW * 3 * L::M8;
 }
 
-// G_v (v < n_v) assembled from the block partials, summed over CTAs in fixed order.
-__global__ void k_gram_fused_reduce(const double *part, int nblk, int NB, int NV, int m, double *G) {
-  const int T = NB * (NB + 1) / 2, NT = (1 + 2 * NV) * T, nc = 2 * m;
+// The per-CTA partials summed over CTAs in a fixed order: 4 quarter sums per element (CTAs
+// q, q + 4, ...; each warp reads 32 consecutive elements of one CTA's partial), added as
+// (q0 + q1) + (q2 + q3).  red[e] for the NT * 64 unique accumulator elements.
+__global__ void __launch_bounds__(256) k_gram_fused_sum(const double *part, int nblk, int n_el, double *red) {
+  __shared__ double sq[4][64];
+  const int q = threadIdx.x >> 6, l = threadIdx.x & 63;
+  const int e = blockIdx.x * 64 + l;
+  double s = 0.0;
+  if (e < n_el)
+    for (int b = q; b < nblk; b += 4) s += part[(int64_t)b * n_el + e];
+  sq[q][l] = s;
+  __syncthreads();
+  if (q == 0 && e < n_el) red[e] = (sq[0][l] + sq[1][l]) + (sq[2][l] + sq[3][l]);
+}
+
+// G_v (v < n_v) assembled from the summed partials (red: NT * 64 elements).
+__global__ void k_gram_fused_reduce(const double *red, int NB, int NV, int m, double *G) {
+  const int T = NB * (NB + 1) / 2, nc = 2 * m;
   const int64_t total = (int64_t)NV * nc * nc;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -930,10 +945,7 @@ __global__ void k_gram_fused_reduce(const double *part, int nblk, int NB, int NV
     const int bi = x / 8, bj = y / 8, mr = x % 8, nn = y % 8;
     const int can = pair * T + upper_index(NB, bi, bj);
     const int e = (mr * 4 + nn / 2) * 2 + (nn & 1);
-    const double *src = part + (int64_t)can * 64 + e;
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += src[(int64_t)b * NT * 64];
-    G[idx] = sign * s;
+    G[idx] = sign * red[(int64_t)can * 64 + e];
   }
 }
 
@@ -957,7 +969,7 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
                                   double *d_part, size_t part_elems, cudaStream_t s) {
   using L = FL<NB, NV>;
   const int gx = fused_grid_x(K);
-  if ((size_t)gx * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
+  if ((size_t)(gx + 1) * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
   FusedArgs fa{d_basis, X, V, S, K, d_part};
   cudaError_t e;
   const char *gk = getenv("RP_GRAM_KERNEL");  // "fused": the single-role kernel (tests, measurements)
@@ -976,9 +988,12 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
     k_gram_fused<NB, NV><<<gx, kFW * 32, smem, s>>>(fa);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int n_el = L::NT * 64;
+  double *red = d_part + (size_t)gx * n_el;  // fused_partial_elems reserves it after the partials
+  k_gram_fused_sum<<<(n_el + 63) / 64, 256, 0, s>>>(d_part, gx, n_el, red);
   const int64_t total = (int64_t)NV * 4 * h.n_num * h.n_num;
   const int rb = (int)((total + 255) / 256);
-  k_gram_fused_reduce<<<rb, 256, 0, s>>>(d_part, gx, NB, NV, h.n_num, G);
+  k_gram_fused_reduce<<<rb, 256, 0, s>>>(red, NB, NV, h.n_num, G);
   return cudaGetLastError();
 }
 
@@ -992,7 +1007,7 @@ static bool fused_supported(const GramBasis &h, int n_v) {
 static size_t fused_partial_elems(const GramBasis &h, int n_v, int64_t K) {
   const int nb = (h.n_num + 7) / 8;
   const int NT = (1 + 2 * n_v) * nb * (nb + 1) / 2;
-  return (size_t)fused_grid_x(K) * NT * 64;
+  return (size_t)(fused_grid_x(K) + 1) * NT * 64;  // partials + their sum
 }
 
 static cudaError_t launch_fused(const GramBasis *d_basis, const GramBasis &h, const double *X,

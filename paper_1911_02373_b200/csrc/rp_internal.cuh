@@ -147,8 +147,8 @@ cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, doubl
 int rp_jit_dims(rp_jit jit, int which);  // d (0) or p (1) of the program a jit was made from
 namespace rp {
 // device-resident refit of a plan's program (rp_plan_update_program)
-cudaError_t launch_plan_set_coef(DevProg *d_prog, const double *d_coef, int stride, const double *d_xf,
-                                 cudaStream_t s);
+cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, int stride, const double *d_xf,
+                                int npe_pad, CfgTable tab, cudaStream_t s);
 // f3 (rp_codegen.cu)
 cudaError_t launch_jit(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *F, int32_t nF, int32_t *idx,
                        double *bestE, double *secondE, cudaStream_t s);

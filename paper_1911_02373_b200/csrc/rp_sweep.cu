@@ -165,23 +165,51 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     tab.rSM[(int64_t)g * kRSMTab + k] = k > 0 ? 1.0 / (double)k : 0.0;
 }
 
-// rp_plan_update_program: new coefficients (and transform) of one program from device memory;
-// the term layout (which coefficient feeds which staging slot) is fixed by the basis
-__global__ void k_plan_set_coef(DevProg *pg, const double *coef, int stride, const double *xf) {
-  const int nterm = pg->nterm;
+// rp_plan_update_program in one launch: the configuration table (a1 masks, a5 occupancy, the
+// P1 P2 order) depends on F, the hardware and the kernel's resources only, so a refit changes
+// just the coefficients (the dense staging matrix Cmat) and the transform (the program-part
+// monomials mP of the sorted feasible configurations).
+__global__ void __launch_bounds__(1024) k_plan_refresh(DevProg *pgp, int g, const double *coef, int stride,
+                                                       const double *xf, int npe_pad, CfgTable tab) {
+  DevProg &pg = *pgp;
+  const int nterm = pg.nterm;
   for (int j = threadIdx.x; j < nterm; j += blockDim.x) {
-    const int src = pg->term_src[j];
-    pg->term_coef[j] = coef[(int64_t)(src / kMaxSrc) * stride + src % kMaxSrc];
+    const int src = pg.term_src[j];
+    pg.term_coef[j] = coef[(int64_t)(src / kMaxSrc) * stride + src % kMaxSrc];
   }
-  if (xf && threadIdx.x < pg->d + pg->p) {
-    pg->xc[threadIdx.x] = xf[2 * threadIdx.x];
-    pg->xe[threadIdx.x] = (int32_t)xf[2 * threadIdx.x + 1];
+  if (xf && threadIdx.x < pg.d + pg.p) {
+    pg.xc[threadIdx.x] = xf[2 * threadIdx.x];
+    pg.xe[threadIdx.x] = (int32_t)xf[2 * threadIdx.x + 1];
+  }
+  __syncthreads();
+  const int nFp = tab.nFp, nFc = tab.nFc[2 * g];
+  const CfgRec *rec = tab.rec + (int64_t)g * nFp;
+  double *mP = tab.mP + (int64_t)g * npe_pad * nFp;
+  for (int t = threadIdx.x; t < nFc * npe_pad; t += blockDim.x) {
+    const int pos = t / npe_pad, pe = t % npe_pad;
+    double m = 0.0;
+    if (pe < pg.nPE) {
+      const CfgRec &r = rec[pos];
+      const int32_t Pk[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+      m = 1.0;
+      for (int k = 0; k < pg.p; ++k) {
+        const double u = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
+        for (int e = 0; e < pg.pe_exp[pe][k]; ++e) m *= u;
+      }
+    }
+    mP[(int64_t)pe * nFp + pos] = m;
+  }
+  double *Cm = tab.Cmat + (int64_t)g * kMaxPolys * npe_pad * tab.nde_pad;
+  for (int r = threadIdx.x; r < pg.npoly * pg.nPE; r += blockDim.x) {
+    const int k = r / pg.nPE, pe = r % pg.nPE;
+    for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
+      Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
   }
 }
 
-cudaError_t launch_plan_set_coef(DevProg *d_prog, const double *d_coef, int stride, const double *d_xf,
-                                 cudaStream_t s) {
-  k_plan_set_coef<<<1, 256, 0, s>>>(d_prog, d_coef, stride, d_xf);
+cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, int stride, const double *d_xf,
+                                int npe_pad, CfgTable tab, cudaStream_t s) {
+  k_plan_refresh<<<1, 1024, 0, s>>>(d_prog, g, d_coef, stride, d_xf, npe_pad, tab);
   return cudaGetLastError();
 }
 
