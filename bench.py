@@ -416,32 +416,35 @@ def main():
     pairs_eval = evaluated_pairs(inp["D"][dlo:dhi], inp["F"])
     flop_launch = pairs_eval * FLOP_PER_PAIR + (dhi - dlo) * FLOP_PER_D
     achieved = flop_launch / (sweep_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, counters = None, None
     prof = os.path.join(ROOT, "profiles", "sweep_ncu_latest.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic, counters = pj.get("dram_bytes_per_launch"), pj.get("counters")
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "alu", "kernel": "k_sweep", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DESIGN.md 'Peaks'); "
                                "measured DFMA microbenchmark 34.1 TF/s (profiles/r01_fp64_microbench.jsonl)",
-                "flop_per_launch": flop_launch, "evaluated_pairs": pairs_eval, "ms_per_launch": sweep_ms}
+                "flop_per_launch": flop_launch, "evaluated_pairs": pairs_eval, "ms_per_launch": sweep_ms,
+                "ncu": counters}
     # fused algorithm: 1 + 2*3 symmetric 70x70 blocks per row,
     # 70*71/2 unique multiply-adds each
     gram_flop = (khi - klo) * (1 + 2 * 3) * 70 * 71
     gram_ach = gram_flop / (gram_ms * 1e-3) / 1e12
-    gtraffic = None
+    gtraffic, gcounters = None, None
     gprof = os.path.join(ROOT, "profiles", "gram_ncu_latest.json")
     if os.path.exists(gprof):
         try:
-            gtraffic = json.load(open(gprof)).get("dram_bytes_per_launch")
+            gj = json.load(open(gprof))
+            gtraffic, gcounters = gj.get("dram_bytes_per_launch"), gj.get("counters")
         except (OSError, ValueError):
             gtraffic = None
     roofline_fit = {"bound": "tensor", "kernel": "k_gram_ws (DMMA.8x8x4, warp-specialised)", "achieved": gram_ach,
                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gram_ach / FP64_PEAK_TFLOPS,
-                    "traffic": gtraffic,
+                    "traffic": gtraffic, "ncu": gcounters,
                     "ms_per_call": gram_ms, "peak_source": "FP64 tensor = FP64 FMA rate on B200 "
                                                            "(measured DMMA 36.9 TF/s)"}
 
