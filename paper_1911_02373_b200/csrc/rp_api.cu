@@ -131,6 +131,7 @@ rp_status compile_program(const rp_program *prog, DevProg *o) {
   const rp_hw &h = prog->hw;
   RP_REQUIRE(h.n_sm >= 1 && h.w_max >= 1 && h.b_max >= 1 && h.t_max >= 1 && h.r_max >= 1 && h.z_max >= 1,
              RP_ERR_INVALID_ARG, "program: hardware limits must be >= 1");
+  RP_REQUIRE(h.n_sm < kRSMTab, RP_ERR_UNSUPPORTED, "program: n_sm = %d >= %d", h.n_sm, kRSMTab);
   RP_REQUIRE(prog->regs_per_thread >= 0 && prog->smem_words_base >= 0 && prog->smem_words_per_thread >= 0,
              RP_ERR_INVALID_ARG, "program: negative resource usage");
   for (int k = 0; k < 3; ++k)
@@ -487,6 +488,7 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
   }
   RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->mwp, pl->tab, pl->npe_pad, pl->nde_max, pl->n_sm_max,
                        pl->d, dD, nD, di, db, ds, perm, s));
+
   if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, no * 4, cudaMemcpyDeviceToHost, s));
   if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, no * 8, cudaMemcpyDeviceToHost, s));
   if (hs) RP_CUDA(cudaMemcpyAsync(second_E, ds, no * 8, cudaMemcpyDeviceToHost, s));
