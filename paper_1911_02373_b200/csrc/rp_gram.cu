@@ -826,9 +826,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
       // entries j = lane + 32 it of the 8 m, two per iteration (independent chains)
       int r = lane / m, col = lane % m;
       int r2 = (lane + 32) / m, col2 = (lane + 32) % m;
-#ifdef RP_WS_NOSTAGE  // timing experiment only: no design rows (wrong results)
-      if (0)
-#endif
       if (!tree)
       for (int j = lane; j < 8 * m; j += 64) {
         const bool two = j + 32 < 8 * m;

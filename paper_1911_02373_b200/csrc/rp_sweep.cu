@@ -433,16 +433,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   // a4 for one octet of configurations: p_k(D_t, P_c) for the octet of tuples x the octet of
   // configurations (k-step major: the NPOLY accumulation chains are independent, so consecutive
   // DMMAs do not wait).  B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
-#ifdef RP_SWEEP_AREG
-  double afr[NPOLY][KS];
-#pragma unroll
-  for (int k = 0; k < NPOLY; ++k)
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
-#define RP_AFR(k, ks) afr[k][ks]
-#else
 #define RP_AFR(k, ks) arow[(k) * NPE + (ks) * 4]
-#endif
   auto mma_oct = [&](int oc, double (&acc)[NPOLY][2]) {
     double bfr[KS];
 #pragma unroll
@@ -512,26 +503,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           break;
         }
       }
-#ifdef RP_SWEEP_PIPE
-    // software pipeline: the DMMAs of octet oc + 1 are issued before the scalar E of octet oc,
-    // so the shared FP64 datapath has independent work from both while either chain waits
-    double acc0[NPOLY][2], acc1[NPOLY][2];
-    if (nEff > 0) mma_oct(0, acc0);
-    int oc = 0;
-    for (; oc + 1 < nEff; oc += 2) {
-      mma_oct(oc + 1, acc1);
-      epi_oct(oc, acc0);
-      if (oc + 2 < nEff) mma_oct(oc + 2, acc0);
-      epi_oct(oc + 1, acc1);
-    }
-    if (oc < nEff) epi_oct(oc, acc0);
-#else
     for (int oc = 0; oc < nEff; ++oc) {
       double acc[NPOLY][2];
       mma_oct(oc, acc);
       epi_oct(oc, acc);
     }
-#endif
   }
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
   st = merge(st, shfl_xor(st, 1));
