@@ -127,4 +127,77 @@ __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, doub
   return (c1 ? E1 : (c2 ? E2 : E3)) * Rep;
 }
 
+// ---- the screening estimate of the warp-specialised sweep: Appendix A in FP32, proven bound ----
+// Every quantity below is a product, quotient or sum of positive values (the inputs are checked
+// positive; MWP >= 2 makes MWP - 1 >= MWP / 2, so no subtraction cancels), which bounds the
+// relative error of each by a count of roundings: ~70 u (u = 2^-24, ~4.2e-6) for E, ~25 u for
+// every compared quantity.  A pair is flagged `unc` (its FP32 value
+// is not trusted and it is re-evaluated in FP64) when an input lies outside [1e-9, 1e9],
+// MWP < 2, a case comparison is within kScreenCmp relative, or E is not positive and finite.
+constexpr float kScreenCmp = 1e-5f;  // comparisons closer than this are decided in FP64
+constexpr double kScreenEta = 1e-5;  // |E32 - E| <= kScreenEta E for pairs not flagged
+
+struct EConst32 {
+  float Lunc, Lcoal, DdU, ddc, issue, Kbw, rKbw;
+};
+__device__ __forceinline__ EConst32 to_econst32(const EConst &k) {
+  return EConst32{(float)k.Lunc, (float)k.Lcoal, (float)k.DdU, (float)k.ddc, (float)k.issue, (float)k.Kbw,
+                  (float)k.rKbw};
+}
+__device__ __forceinline__ bool fclose(float x, float y) {  // |x - y| <= kScreenCmp max(x, y), x, y > 0
+  return fabsf(x - y) <= kScreenCmp * fmaxf(x, y);
+}
+__device__ __forceinline__ float rcp32(float x) {  // MUFU.RCP: relative error <= 2^-23
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// x in [1e-9, 1e9] (positive, normal, not NaN) by one unsigned compare on the bit pattern
+__device__ __forceinline__ bool in_range32(float x) {
+  return (uint32_t)(__float_as_uint(x) - 0x3089705fu) <= (uint32_t)(0x4e6e6b28u - 0x3089705fu);
+}
+
+__device__ __forceinline__ float mwpcwp_E32(float p1, float q1, float p2, float q2, float p3, float q3, float W,
+                                            float Rep, float rSM, float SMact, const EConst32 &k, bool &unc) {
+  // inputs in [1e-9, 1e9]: every intermediate stays a normal float (products of three inputs and
+  // the hardware constants lie within ~1e-30 .. 1e33)
+  unc = !(in_range32(p1) & in_range32(q1) & in_range32(p2) & in_range32(q2) & in_range32(p3) & in_range32(q3));
+  const float q23 = q2 * q3, q13 = q1 * q3, q12 = q1 * q2;
+  const float Q = q1 * q23;
+  const float a1 = p1 * q23, a2 = p2 * q13, a3 = p3 * q12;
+  const float s23 = a2 + a3, s = a1 + s23;
+  const float mc = fmaf(k.Lunc, a3, k.Lcoal * a2);
+  const float dn = fmaf(k.DdU, a3, k.ddc * a2);
+  const float cc = k.issue * s;
+  const float rQ = rcp32(Q), r23 = rcp32(s23);
+  const float Mem_c = mc * rQ, Comp_c = cc * rQ;
+  const float MWP_nb = mc * rcp32(dn);
+  const float MWP_bw = k.Kbw * mc * r23 * rSM;
+  const float CWPf = fmaf(mc, rcp32(cc), 1.0f);
+  const bool bw = MWP_bw < MWP_nb;
+  const float mwp0 = bw ? MWP_bw : MWP_nb;
+  const bool mwpW = W <= mwp0;
+  const float mwp = mwpW ? W : mwp0;
+  const bool cwpf = CWPf < W;
+  const float cwp = cwpf ? CWPf : W;
+  const float cpm = cc * r23;
+  const float tail = cpm * (mwp - 1.0f);
+  const float mcw = mwpW ? Mem_c : W * rQ * (bw ? s23 * SMact * k.rKbw : dn);
+  const float E1 = Mem_c + Comp_c + tail;
+  const float E2 = mcw + tail;
+  const float E3 = mc * r23 + Comp_c * W;
+  const bool c1 = mwpW && !cwpf;
+  const bool c2 = (cwp >= mwp) || (Comp_c > Mem_c);
+  const float E = (c1 ? E1 : (c2 ? E2 : E3)) * Rep;
+  // a comparison is checked only where its outcome is used: W <= min(MWP_nb, MWP_bw) decides
+  // MWP = W_act (case 1); which of MWP_nb, MWP_bw is smaller picks the formula of Mem_c W / MWP
+  // (line 17) when MWP < W_act; CWPf < W_act decides case 1 when MWP = W_act; CWP >= MWP and then
+  // Comp_c > Mem_c decide case 2 when case 1 does not hold.  (The values of the mins are accurate
+  // whichever operand is smaller.)
+  // (bitwise | and &: branch-free)
+  unc = unc | !(mwp >= 2.0f) | fclose(W, mwp0) | (!mwpW & fclose(MWP_bw, MWP_nb)) | (mwpW & fclose(CWPf, W)) |
+        (!c1 & fclose(cwp, mwp)) | (!c1 & !(cwp >= mwp) & fclose(Comp_c, Mem_c)) | !(E > 0.f & E < 3.0e38f);
+  return E;
+}
+
 }  // namespace rp

@@ -65,7 +65,8 @@ struct CfgRec {      // one statically feasible configuration, 64 B (4 x 16-byte
   int32_t Pm1_1, Pm1_2;      // P_k - 1 (0 for k >= p)
   uint32_t M0, M1, M2;       // ceil(n / P_k) = (n + P_k - 1) * M_k >> s_k  (exact, n < 2^31)
   uint32_t s012;             // s_k in bits 8k..8k+7
-  double W, rB, rW;          // W_active, 1/B_active, 1/W_active
+  double W, rB;              // W_active, 1/B_active
+  float W32, rB32;           // the same in FP32 (the screened sweep's inputs)
 };
 static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
 

@@ -17,6 +17,8 @@
 //                     4-5 Newton reciprocals instead of ~11 divisions), a8 (argmin on the exact
 //                     key (E, original index) + runner-up, lane -> quad -> warp -> CTA).
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "rp_device.cuh"
 
@@ -108,7 +110,8 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
       r.s012 = ss[0] | (ss[1] << 8) | (ss[2] << 16);
       r.W = (double)W;
       r.rB = 1.0 / (double)B;
-      r.rW = 1.0 / (double)W;
+      r.W32 = (float)W;
+      r.rB32 = (float)r.rB;
       tab.srec[off + pos] = r;
       double u[3];
       for (int k = 0; k < pg.p; ++k)
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       double E;
       if (MWP) {
         const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);           // M2, s012, W
-        const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);     // rB, rW
+        const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);     // rB, (W32, rB32)
         const int32_t Pm1_0 = (int32_t)(h0.y >> 32);
         const uint32_t s012 = (uint32_t)h2.y;
         const double W = __hiloint2double(h2.w, h2.z);
@@ -520,6 +523,412 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   }
 }
 
+// ============================================================================================
+// Warp-specialised screened sweep (RP_SWEEP_KERNEL=ws; measured 6.1 ms vs k_sweep's 5.1 ms at
+// `large`, see DESIGN.md -- kept, parity-tested, as the base of the next round's persistent,
+// octet-scheduled version).
+//
+// k_sweep issues its DMMAs and its E epilogue from the same warps, and the measured kernel time
+// is close to the sum of the two (contraction alone 2.35 ms, whole kernel 5.1 ms at `large`):
+// the tensor pipe idles while a warp's epilogue chain runs.  Here each CTA pairs, per octet of
+// tuples, an MMA warp and a screen warp on the same SM sub-partition:
+//   MMA warp:    A fragments (the octet's staged C) in registers, one DMMA tile (8 tuples x 8
+//                configurations x 2l polynomials) per configuration octet into a 3-slot ring in
+//                shared memory (mbarrier full / empty handshake);
+//   screen warp: reads the tile, evaluates E in FP32 with a proven relative error bound
+//                (mwpcwp_E32, kScreenEta), keeps per lane the smallest screened keys, and at the
+//                end re-evaluates those candidates exactly in FP64; the tuple falls back to the
+//                full FP64 sweep (DMMA, on the screen warp) whenever a key that was not kept could
+//                reach the winner or the runner-up (rare).
+// The FP64 datapath then carries only the DMMAs; the screen's FP32/integer work runs on the other
+// pipes of the sub-partition (tools/microbench/ws_overlap.cu: DMMA warps and FFMA warps of a
+// sub-partition overlap to within 1.11x of the slower).
+// ============================================================================================
+constexpr int kSwPairs = 4;                  // tuple octets per CTA: one MMA warp each (one per SMSP)
+constexpr int kSwScreens = 3;                // screen warps per octet (same SMSP), tiles round-robin
+constexpr int kSwThreads = 32 * kSwPairs * (1 + kSwScreens);  // 512
+constexpr int kSwSlots = 2 * kSwScreens;     // ring slots per octet (slot oc % 6, consumer oc % 3)
+
+template <int NPOLY, int NPE>
+size_t sweep_ws_smem_bytes(int nde_stride, int n_sm) {
+  const int rsm = (n_sm + 2) & ~1;
+  return sizeof(double) * ((size_t)kTD * c_stride<NPOLY, NPE>() + (size_t)kTD * nde_stride + rsm) +
+         sizeof(float) * ((rsm + 3) & ~3) + sizeof(uint64_t) * 2 * kSwPairs * kSwSlots +
+         sizeof(double) * (size_t)kSwPairs * kSwSlots * NPOLY * 64 + sizeof(int32_t) * kTD * kMaxVars +
+         sizeof(double) * 4 * kSwPairs * kSwScreens * 8;  // the screens' partial results per quad
+}
+
+__device__ __forceinline__ uint32_t sw_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sw_mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sw_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void sw_mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sw_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void sw_mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(sw_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int NPE, bool SECOND>
+__global__ void __launch_bounds__(kSwThreads, 1) k_sweep_ws(SweepArgs a) {
+  constexpr int NPOLY = 6;
+  constexpr int KS = NPE / 4;
+  constexpr int CS = c_stride<NPOLY, NPE>();
+  constexpr int KC = SECOND ? 2 : 1;  // screened candidates kept per lane (4 lanes per tuple)
+  constexpr double kInf = __builtin_huge_val();
+  const int g = blockIdx.y;
+  const DevProg &pg = a.progs[g];
+  const int d = a.d;
+  const int64_t d0 = (int64_t)blockIdx.x * kTD;
+  const int tmax = (int)((a.nD - d0) < kTD ? (a.nD - d0) : kTD);
+  const int nde = a.nde_stride;
+  const int n_sm = pg.n_sm;  // < kRSMTab (compile_program)
+  const int rsm = (n_sm + 2) & ~1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+  extern __shared__ __align__(16) double smem[];
+  double *sC = smem;                                          // [kTD][CS]
+  double *sMD = sC + kTD * CS;                                // [kTD][nde]
+  double *sRSM = sMD + kTD * nde;                             // [rsm]
+  float *sRSM32 = reinterpret_cast<float *>(sRSM + rsm);      // [rsm]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sRSM32 + ((rsm + 3) & ~3));  // [kSwPairs][kSwSlots][2]: full, empty
+  // (bars: 2 kSwPairs kSwSlots = 24 words, so the ring below stays 16-byte aligned for double2)
+  double *ring = reinterpret_cast<double *>(bars + 2 * kSwPairs * kSwSlots);  // [kSwPairs][kSwSlots][NPOLY][64]
+  double *part = ring + kSwPairs * kSwSlots * NPOLY * 64;  // [kSwPairs][kSwScreens][8 quads][4]: e, s, i, tnc|ovf
+  int32_t *sDv = reinterpret_cast<int32_t *>(part + 4 * kSwPairs * kSwScreens * 8);  // [kTD][kMaxVars]
+
+  if (threadIdx.x < 2 * kSwPairs * kSwSlots) sw_mbar_init(bars + threadIdx.x, 32);
+  // ---- a2: stage the tile (D values, data monomials, data polynomials), all warps ---------------
+  const int nDE = pg.nDE, ndp = a.tab.nde_pad;
+  for (int i = threadIdx.x; i < kTD * d; i += blockDim.x) {
+    const int t = i / d, k = i % d;
+    const int64_t src = (t < tmax) ? (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t) : 0;
+    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[src * d + k] : 1;
+  }
+  const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
+  for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) {
+    sRSM[i] = gRSM[i];
+    sRSM32[i] = (float)gRSM[i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTD * ndp; i += blockDim.x) {
+    const int t = i / ndp, de = i % ndp;
+    double m = 0.0;
+    if (de < nDE) {
+      m = 1.0;
+      for (int k = 0; k < d; ++k) {
+        const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+        for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
+      }
+    }
+    sMD[t * nde + de] = m;
+  }
+  __syncthreads();
+  {
+    const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
+    constexpr int MT = NPOLY * NPE / 8;
+    constexpr int NT = kTD / 8;
+    for (int tile = wid; tile < MT * NT; tile += kSwThreads / 32) {
+      const int mt = tile / NT, nt = tile % NT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < ndp / 4; ++ks) {
+        const double av = __ldg(Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3));
+        const double bv = sMD[(nt * 8 + (lane >> 2)) * nde + ks * 4 + (lane & 3)];
+        dmma(c0, c1, av, bv);
+      }
+      const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
+      sC[t * CS + row] = c0;
+      sC[(t + 1) * CS + row] = c1;
+    }
+  }
+  __syncthreads();
+
+  const int o = wid & (kSwPairs - 1);         // this warp's tuple octet
+  const bool mma_role = wid < kSwPairs;       // warps o, o + 4, o + 8, o + 12 share a sub-partition
+  const int sub = (wid >> 2) - 1;             // screen warps: 0 .. kSwScreens - 1
+  const int t = o * 8 + (lane >> 2);
+  const bool tok = t < tmax;
+  const int nFc = a.tab.nFc[2 * g];
+  const bool sorted = a.tab.nFc[2 * g + 1] != 0;
+  const int nFp = a.tab.nFp;
+  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
+  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
+  const double *arow = sC + t * CS + (lane & 3);
+  const int32_t *Dt = sDv + t * kMaxVars;
+  const int64_t D1 = Dt[0];
+  const int64_t D1sq = D1 * D1;
+  int64_t maxD1sq = tok ? D1sq : 0;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const int64_t x = __shfl_xor_sync(0xffffffffu, maxD1sq, off);
+    maxD1sq = x > maxD1sq ? x : maxD1sq;
+  }
+  const int nOctF = (nFc + 7) >> 3;
+  int nEff = (o * 8 < tmax) ? nOctF : 0;  // a3 early exit (configurations sorted by P1 P2)
+  if (sorted && nEff > 0)
+    for (int b0 = 0; b0 < nOctF; b0 += 32) {
+      const int oc = b0 + lane;
+      const unsigned stop = __ballot_sync(0xffffffffu, oc < nOctF && __ldg(&rec[oc * 8].P01) > maxD1sq);
+      if (stop) {
+        nEff = b0 + __ffs(stop) - 1;
+        break;
+      }
+    }
+  uint64_t *full = bars + o * kSwSlots * 2, *empty = full + 1;  // slot s: full[2 s], empty[2 s]
+  double *myring = ring + (size_t)o * kSwSlots * NPOLY * 64;
+
+  auto mma_tile = [&](int oc, double (&acc)[NPOLY][2], const double (&afr)[NPOLY][KS]) {
+    double bfr[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], afr[k][ks], bfr[ks]);
+  };
+
+  if (mma_role) {
+    // ---- MMA warp: a4 tiles into the ring (B fragments of the next tile prefetched) ----------
+    double afr[NPOLY][KS];
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
+    double bnext[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+      bnext[ks] = nEff > 0 ? __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + (lane >> 2)) : 0.0;
+    for (int oc = 0; oc < nEff; ++oc) {
+      const int sl = oc % kSwSlots, use = oc / kSwSlots;
+      double bfr[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) bfr[ks] = bnext[ks];
+      if (oc + 1 < nEff)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+          bnext[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + (oc + 1) * 8 + (lane >> 2));
+      double acc[NPOLY][2];
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], afr[k][ks], bfr[ks]);
+      if (use > 0) sw_mbar_wait(empty + 2 * sl, (use - 1) & 1);
+      double *dst = myring + sl * NPOLY * 64 + 2 * lane;
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) *reinterpret_cast<double2 *>(dst + k * 64) = make_double2(acc[k][0], acc[k][1]);
+      sw_mbar_arrive(full + 2 * sl);
+    }
+    return;
+  }
+
+  // ---- screen warp ---------------------------------------------------------------------------
+  const EConst kc = make_econst(pg);
+  const EConst32 kc32 = to_econst32(kc);
+  const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
+            map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
+  const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
+  // a6: #Blocks = prod ceil(D / P), exact integers.  A grid dimension with no
+  // data parameter has D = 1, whose factor ceil(1 / P) is 1: all three are multiplied (branch-free)
+  auto grid_blocks = [&](const longlong2 &h0, const int4 &h1, const int4 &h2) -> int64_t {
+    const uint32_t s012 = (uint32_t)h2.y;
+    return ceil_div_magic(Da, (int32_t)(h0.y >> 32), (uint32_t)h1.z, s012 & 255) *
+           ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) *
+           ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+  };
+  // the exact FP64 evaluation of one pair (a3, a6, a7): E, +inf when masked
+  auto pair_E64 = [&](const CfgRec *cr, const double *pk, int32_t &orig) -> double {
+    const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
+    const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
+    const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
+    const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);
+    orig = (int32_t)(h0.y & 0xffffffff);
+    const bool ok = tok && h0.x <= D1sq;  // a3
+    const int64_t blocks = grid_blocks(h0, h1, h2);
+    const int64_t smact = blocks < n_sm ? blocks : n_sm;
+    const double rSM = sRSM[smact];
+    const double Rep = (double)blocks * h3.x * rSM;  // line 15
+    const double E = mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], __hiloint2double(h2.w, h2.z), Rep, rSM,
+                              (double)smact, kc);
+    return (ok && pos_finite(E)) ? E : kInf;  // line 19, R17
+  };
+  auto take = [](Best &b, double E, int32_t orig) {  // a8: exact key (E, original index)
+    const long long eb = __double_as_longlong(E), sb = __double_as_longlong(b.e);
+    const bool better = eb < sb || (eb == sb && orig < b.i);
+    if (SECOND) b.s = better ? b.e : fmin(b.s, E);
+    b.i = better ? orig : b.i;
+    b.e = better ? E : b.e;
+  };
+
+  float ck[KC];
+  int cp[KC];
+#pragma unroll
+  for (int i = 0; i < KC; ++i) {
+    ck[i] = __int_as_float(0x7f800000);
+    cp[i] = 0x7fffffff;
+  }
+  float tnc = __int_as_float(0x7f800000);  // smallest screened key not kept
+  bool ovf = false;                        // an untrusted pair (key -1) fell off the list
+  for (int oc = sub; oc < nEff; oc += kSwScreens) {
+    const int sl = oc % kSwSlots, use = oc / kSwSlots;
+    sw_mbar_wait(full + 2 * sl, use & 1);
+    const double *src = myring + sl * NPOLY * 64 + 2 * lane;
+    double2 pv[NPOLY];
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k) pv[k] = *reinterpret_cast<const double2 *>(src + k * 64);
+    sw_mbar_arrive(empty + 2 * sl);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int pos = oc * 8 + 2 * (lane & 3) + v;
+      const CfgRec *cr = rec + pos;
+      const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
+      const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
+      const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
+      const int2 h3 = __ldg(reinterpret_cast<const int2 *>(cr) + 7);  // W32, rB32
+      const bool ok = tok && h0.x <= D1sq;                               // a3
+      const int64_t blocks = grid_blocks(h0, h1, h2);
+      const int smact = (int)(blocks < n_sm ? blocks : n_sm);
+      const float rSMf = sRSM32[smact];
+      const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
+      double p[NPOLY];
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) p[k] = v ? pv[k].y : pv[k].x;
+      bool unc;
+      const float E32 = mwpcwp_E32((float)p[0], (float)p[1], (float)p[2], (float)p[3], (float)p[4], (float)p[5],
+                                   __int_as_float(h3.x), Rep, rSMf, (float)smact, kc32, unc);
+      // masked pairs enter as +inf: never kept, never counted (branch-free insertion)
+      float k = ok ? (unc ? -1.0f : E32) : __int_as_float(0x7f800000);
+      int q = pos;
+#pragma unroll
+      for (int i = 0; i < KC; ++i) {  // positions grow along the stream: ties keep the earlier
+        const bool lt = k < ck[i];
+        const float tk = ck[i];
+        const int tq = cp[i];
+        ck[i] = lt ? k : tk;
+        cp[i] = lt ? q : tq;
+        k = lt ? tk : k;
+        q = lt ? tq : q;
+      }
+      ovf = ovf | (k < 0.f);  // (k, q) fell off the list (or was never kept)
+      tnc = fminf(tnc, k);
+    }
+  }
+  // the lane's candidates in FP64: scalar dot products over the staged data polynomials and the
+  // configuration's monomials, then the exact pair evaluation; the quad's exact argmin
+  Best st;
+  st.e = kInf;
+  st.i = 0x7fffffff;
+  st.s = kInf;
+#pragma unroll
+  for (int i = 0; i < KC; ++i) {
+    if (cp[i] != 0x7fffffff) {
+      const int pos = cp[i];
+      double mv[NPE];
+#pragma unroll
+      for (int pe = 0; pe < NPE; ++pe) mv[pe] = __ldg(mP + (int64_t)pe * nFp + pos);
+      const double *crow = sC + t * CS;
+      double pk[NPOLY];
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int pe = 0; pe < NPE; ++pe) sacc = fma(crow[k * NPE + pe], mv[pe], sacc);
+        pk[k] = sacc;
+      }
+      int32_t orig;
+      const double E = pair_E64(rec + pos, pk, orig);
+      take(st, E, orig);
+    }
+  }
+  st = merge(st, shfl_xor(st, 1));
+  st = merge(st, shfl_xor(st, 2));
+  tnc = fminf(tnc, __shfl_xor_sync(0xffffffffu, tnc, 1));
+  tnc = fminf(tnc, __shfl_xor_sync(0xffffffffu, tnc, 2));
+  {
+    int ov = ovf ? 1 : 0;
+    ov |= __shfl_xor_sync(0xffffffffu, ov, 1);
+    ov |= __shfl_xor_sync(0xffffffffu, ov, 2);
+    ovf = ov != 0;
+  }
+  // the octet's screen warps saw disjoint tiles: their quad results merged in sub order
+  {
+    double *pq = part + ((size_t)(o * kSwScreens + sub) * 8 + (lane >> 2)) * 4;
+    if ((lane & 3) == 0) {
+      pq[0] = st.e;
+      pq[1] = st.s;
+      pq[2] = __longlong_as_double((long long)st.i);
+      pq[3] = ovf ? -1.0 : (double)tnc;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kSwPairs * kSwScreens) : "memory");  // screen warps only
+    if (sub != 0) return;
+    for (int j = 1; j < kSwScreens; ++j) {
+      const double *pj = part + ((size_t)(o * kSwScreens + j) * 8 + (lane >> 2)) * 4;
+      Best bj;
+      bj.e = pj[0];
+      bj.s = pj[1];
+      bj.i = (int32_t)__double_as_longlong(pj[2]);
+      st = merge(st, bj);
+      if (pj[3] < 0.0) ovf = true;
+      else tnc = fminf(tnc, (float)pj[3]);
+    }
+  }
+  // exact unless a key that was not kept could reach the winner (or the runner-up)
+  const double lim = (double)tnc * (1.0 - kScreenEta);
+  const bool fb = tok && (ovf || (tnc < __int_as_float(0x7f800000) && (!(st.e < lim) || (SECOND && !(st.s < lim)))));
+  if (__any_sync(0xffffffffu, fb)) {  // rare: the tuple redone by the full FP64 sweep (DMMA here)
+    Best sf;
+    sf.e = kInf;
+    sf.i = 0x7fffffff;
+    sf.s = kInf;
+    double afr[NPOLY][KS];
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
+    for (int oc = 0; oc < nEff; ++oc) {
+      double acc[NPOLY][2];
+      mma_tile(oc, acc, afr);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double pk[NPOLY];
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) pk[k] = acc[k][v];
+        int32_t orig;
+        const double E = pair_E64(rec + oc * 8 + 2 * (lane & 3) + v, pk, orig);
+        take(sf, E, orig);
+      }
+    }
+    sf = merge(sf, shfl_xor(sf, 1));
+    sf = merge(sf, shfl_xor(sf, 2));
+    if (fb) st = sf;
+  }
+  if ((lane & 3) == 0 && tok) {
+    const int64_t out = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t);
+    a.idx[out] = (st.e < kInf) ? st.i : -1;
+    a.bestE[out] = st.e;
+    if (SECOND) a.secondE[out] = st.s;
+  }
+}
+
+template <int NPE, bool SECOND>
+static cudaError_t launch_ws(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
+  const size_t smem = sweep_ws_smem_bytes<6, NPE>(a.nde_stride, n_sm_max);
+  const int64_t tiles = (a.nD + kTD - 1) / kTD;
+  if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_ws<NPE, SECOND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_sweep_ws<NPE, SECOND><<<dim3((unsigned)tiles, (unsigned)n_prog), kSwThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int NPE, bool MWP, bool SECOND>
 static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
   const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_stride, n_sm_max);
@@ -535,6 +944,11 @@ static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStr
 template <int NPE>
 static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm_max, cudaStream_t s) {
   const bool second = a.secondE != nullptr;
+  // RP_SWEEP_KERNEL=ws: the warp-specialised screened sweep (MWP-CWP programs; parity-tested, not
+  // yet faster: DESIGN.md "Warp-specialised screened sweep"); default: k_sweep
+  const char *kern = getenv("RP_SWEEP_KERNEL");
+  if (mwp && kern && strcmp(kern, "ws") == 0)
+    return second ? launch_ws<NPE, true>(a, n_prog, n_sm_max, s) : launch_ws<NPE, false>(a, n_prog, n_sm_max, s);
   if (mwp)
     return second ? launch3<NPE, true, true>(a, n_prog, n_sm_max, s)
                   : launch3<NPE, true, false>(a, n_prog, n_sm_max, s);
@@ -547,7 +961,7 @@ cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable 
                          int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
                          cudaStream_t s) {
   if (nD == 0) return cudaSuccess;
-  if (n_sm_max >= kRSMTab) n_sm_max = 0;  // no table: 1/SM_act computed directly
+  // n_sm < kRSMTab for every program (compile_program): the 1/SM_act tables always exist
   (void)nde_max;
   SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE, perm};
   switch (npe_pad) {

@@ -360,3 +360,23 @@ def test_device_resident_fit_and_plan_update():
     i2, E2, S2 = rp.eval_argmin(fitted, D, F)
     assert torch.equal(i1[0], i2) and torch.equal(E1[0], E2) and torch.equal(S1[0], S2)
     plan.close()
+
+
+@pytest.mark.parametrize("second", [False, True])
+def test_sweep_warp_specialised_screen(second, monkeypatch):
+    """RP_SWEEP_KERNEL=ws: the warp-specialised sweep (FP32 screen with a proven bound, FP64 for
+    the candidates, full-FP64 fallback) under the same gates as the default kernel, on
+    polybench (4 programs), tiny and a `large` subsample."""
+    monkeypatch.setenv("RP_SWEEP_KERNEL", "ws")
+    for case in (synth.tiny_sweep(), synth.polybench_sweep(nD=2000)):
+        idx, E, S = rp.eval_argmin_batched(case.programs, _cuda(case.D), _cuda(case.F), second=second)
+        for g, spec in enumerate(case.programs):
+            ref = oracle.sweep(spec, case.D, case.F)
+            check_sweep(idx[g], E[g], S[g] if second else None, ref, spec, case.D, case.F, tag=case.name)
+    case = synth.large_sweep(nD=20_000)
+    spec = case.programs[0]
+    sel = np.arange(0, 20_000, 7)
+    idx, E, S = rp.eval_argmin(spec, _cuda(case.D), _cuda(case.F), second=second)
+    ref = oracle.sweep(spec, case.D[sel], case.F)
+    check_sweep(np.asarray(idx.cpu())[sel], np.asarray(E.cpu())[sel],
+                np.asarray(S.cpu())[sel] if second else None, ref, spec, case.D[sel], case.F, tag="large")
