@@ -206,10 +206,20 @@ def main():
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # RP_BENCH_SHARED_GPU=1 (test only): every rank on cuda:0 with gloo, so the N > 1 code path can be
+    # exercised on a one-GPU box; the numbers of such a run mean nothing
+    shared = os.environ.get("RP_BENCH_SHARED_GPU") == "1"
+    if shared:  # a hang in this test mode dumps every thread's stack
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ.get("RP_BENCH_HANG_S", "150")), exit=True)
+    local_dev = 0 if shared else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
 
     inp = workload_inputs(args.nD, args.K)
@@ -284,9 +294,9 @@ def main():
     if sampler:
         sampler.start()
         time.sleep(0.5)  # nvidia-smi up before the timed region
-        for _ in range(2):
-            step_dev()
-        torch.cuda.synchronize()
+    for _ in range(2):  # every rank: the step has collectives at N > 1
+        step_dev()
+    torch.cuda.synchronize()
     times, t_fit, t_sweep_k, t_plan = [], [], [], []
     for _ in range(args.steps):
         flush.zero_()  # L2 (126 MB) flushed between timed steps
@@ -370,7 +380,7 @@ def main():
         t1.record(pipe.d2h)
         barrier()
         e_ms = t0.elapsed_time(t1) / n_e
-        ok_e2e = bool(torch.equal(oi.reshape(-1).to(dev), i_dev.reshape(-1)))
+        ok_e2e = bool(torch.equal(oi.reshape(-1), i_dev.reshape(-1).cpu()))
         pipe.close()
         # call by call (no overlap)
         Xn, Vn, Dn = Xh.numpy(), Vh.numpy(), Dh.numpy()

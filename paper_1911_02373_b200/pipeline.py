@@ -73,8 +73,9 @@ class FitSweepPipeline:
             self.comp_done[s].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.comp_done[s])
-            idx.record_stream(self.d2h)
-            E.record_stream(self.d2h)
+            for t in (idx, E):  # (a gloo gather hands back host tensors)
+                if t.is_cuda:
+                    t.record_stream(self.d2h)
             idx_h.copy_(idx.reshape(idx_h.shape), non_blocking=True)
             E_h.copy_(E.reshape(E_h.shape), non_blocking=True)
             self.out_done[s].record(self.d2h)
