@@ -469,8 +469,9 @@ def main():
                         "seconds": dt, "sample": f"1/{div} of the step (second slice): fit of 3 metrics on "
                                                f"{K // div} rows + sweep of {nD // div} D x {nF} F"}
 
-    # fit: minmax x2, xform, xform_to_basis, gram_fused, gram_fused_reduce, solve (7);
-    # plan update: set_coef, plan_configs (2); sweep: bucket count / scan / scatter, sweep (4)
+    # fit: minmax part / final, xform, xform_to_basis, gram_ws, gram_fused_sum, gram_fused_reduce,
+    # solve (8); plan update: plan_refresh (1); sweep: bucket count / scan / scatter, sweep (4)
+    # (the ncu launch list of this command, profiles/r01_launches_bench.txt, shows the same 13)
     launches_per_step = 13
     out = {"metric": METRIC, "value": nD * nF / (step_ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
