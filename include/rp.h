@@ -289,9 +289,12 @@ rp_status rp_plan_eval_argmin(rp_plan plan, const int32_t *D, int64_t nD, int32_
 rp_status rp_plan_static_feasible(rp_plan plan, int32_t prog, int32_t *n_static_feasible);
 /* rp_plan_update_program: replace the coefficients (and, if xform is non-null, the transform) of
  * program `prog` from DEVICE memory -- coef [n_metrics][stride] in each metric's basis order
- * (stride >= its n_c; rp_fit_dev's output has stride n_c), xform [n][2] (c_k, e_k) -- and redo
- * a1 / a5 on the device.  Stream-ordered, no host synchronisation: a fit and the sweep that uses
- * it chain on the device.  The bases (hence the term layout) are those of the plan's creation.
+ * (stride >= its n_c; rp_fit_dev's output has stride n_c), xform [n][2] (c_k, e_k).  The
+ * configuration table (a1 masks, a5 occupancy, its order) depends on F, the hardware and the
+ * kernel's resources only, so one device launch refreshes what the new values change: the
+ * staging matrix of the coefficients and the configurations' program-part monomials.
+ * Stream-ordered, no host synchronisation: a fit and the sweep that uses it chain on the device.
+ * The bases (hence the term layout) are those of the plan's creation.
  * Clears the plan's runtime history.                                                       */
 rp_status rp_plan_update_program(rp_plan plan, int32_t prog, const double *coef, int32_t stride,
                                  const double *xform, rp_stream s);

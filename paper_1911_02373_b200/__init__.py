@@ -361,7 +361,8 @@ class Plan:
 
     def update(self, coef, xf=None, prog: int = 0):
         """rp_plan_update_program: new coefficients [n_metrics][n_c] (and transform [n][2]) of
-        program `prog` from device tensors, a1 / a5 redone on the device (stream-ordered)."""
+        program `prog` from device tensors: the staging matrix and the configurations' monomials are
+        refreshed on the device in one launch (stream-ordered)."""
         coef = coef.contiguous()
         _check(_lib.rp_plan_update_program(self.handle, prog, _ptr(coef), coef.shape[-1],
                                            _ptr(xf.contiguous()) if xf is not None else None, _stream_of(coef)))
