@@ -79,3 +79,24 @@ def test_codegen_compiles_for_sm100a(tmp_path):
     r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-c", str(f), "-o", str(tmp_path / "gen.o")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_program_limits_rejected_without_gpu():
+    """Host-side program checks (rp_codegen validates without a device): n_SM must fit the sweep's
+    1/SM_act table (n_sm < 1024), and the MWP-CWP template needs 3 metrics."""
+    import copy
+    import oracle
+    import paper_1911_02373_b200 as rp
+    import synth
+    spec = copy.deepcopy(synth.large_program())
+    c, e = oracle.xform_from_box(spec.box_lo, spec.box_hi)
+    spec.xform_c, spec.xform_e = list(c), list(e)
+    rp.codegen(spec)  # valid as generated
+    big = copy.deepcopy(spec)
+    big.hw = dict(spec.hw, n_sm=1024)
+    with pytest.raises(rp.RPError) as ei:
+        rp.codegen(big)
+    assert ei.value.status == 5  # RP_ERR_UNSUPPORTED
+    ok = copy.deepcopy(spec)
+    ok.hw = dict(spec.hw, n_sm=1023)
+    rp.codegen(ok)
