@@ -71,6 +71,12 @@ __device__ __forceinline__ int64_t ceil_div_magic(int32_t D, int32_t Pm1, uint32
   return (int64_t)((n * (uint64_t)M) >> s);
 }
 
+// the same in 32 bits (the quotient is < 2^32): one IMAD.WIDE.U32 and one funnel shift
+__device__ __forceinline__ uint32_t ceil_div32(int32_t D, int32_t Pm1, uint32_t M, uint32_t s) {
+  const uint64_t n = (uint64_t)(uint32_t)(D + Pm1);
+  return (uint32_t)((n * (uint64_t)M) >> s);
+}
+
 // E for one (D, P) pair from its 2l polynomial values (Appendix A in
 // common-denominator form g_i = a_i / Q; every division is a Newton reciprocal).  Straight-line
 // code: masked pairs are carried to the end and returned as +inf.

@@ -416,6 +416,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   const int32_t *Dt = sDv + t * kMaxVars;
   const int64_t D1 = Dt[0];
   const int64_t D1sq = D1 * D1;
+  // the a3 test in 32 bits: P1 P2 of a compacted configuration is <= T_max < 2^31
+  const int32_t D1sq32 = D1sq < 0x7fffffffll ? (int32_t)D1sq : 0x7fffffff;
   const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1,
                 Dc = map2 >= 0 ? Dt[map2] : 1;
   const double *arow = sC + t * CS + (lane & 3);
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);             // Pm1_1, Pm1_2, M0, M1
       const int32_t orig = (int32_t)(h0.y & 0xffffffff);
       // a3: "P1 P2 <= D1^2 is meaningful"
-      const bool ok = tok && h0.x <= D1sq;
+      const bool ok = tok && (int32_t)(h0.x & 0xffffffff) <= D1sq32;
       double E;
       if (MWP) {
         const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);           // M2, s012, W
@@ -470,10 +472,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
         const uint32_t s012 = (uint32_t)h2.y;
         const double W = __hiloint2double(h2.w, h2.z);
         // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
-        int64_t blocks = 1;
-        if (map0 >= 0) blocks *= ceil_div_magic(Da, Pm1_0, (uint32_t)h1.z, s012 & 255);
-        if (map1 >= 0) blocks *= ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255);
-        if (map2 >= 0) blocks *= ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+        // (each factor is < 2^32: 32-bit factors, 64-bit products only where needed)
+        const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, Pm1_0, (uint32_t)h1.z, s012 & 255) : 1u;
+        const uint32_t f1 = map1 >= 0 ? ceil_div32(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) : 1u;
+        int64_t blocks = (int64_t)((uint64_t)f0 * f1);
+        if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
         const int64_t smact = blocks < n_sm ? blocks : n_sm;
         const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
         const double Rep = (double)blocks * h3.x * rSM;  // line 15: #Blocks / (B_act SM_act)
