@@ -103,6 +103,9 @@ def test_sweep_large_full_size_sampled():
     plan = rp.Plan([spec], _cuda(case.F))
     assert plan.static_feasible() == 464
     idx, E, S = plan.eval(_cuda(case.D))
+    # the bench times the runner-up-free template: identical winners and estimates
+    idx2, E2, _ = plan.eval(_cuda(case.D), second=False)
+    assert torch.equal(idx2, idx) and torch.equal(E2, E)
     sub = synth.large_subsample_index(len(case.D))
     ref = oracle.sweep(spec, case.D[sub], case.F)
     strict, feas = check_sweep(idx[0][sub], E[0][sub], S[0][sub], ref, spec, case.D[sub], case.F, "large")
