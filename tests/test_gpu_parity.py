@@ -383,3 +383,32 @@ def test_sweep_warp_specialised_screen(second, monkeypatch):
     ref = oracle.sweep(spec, case.D[sel], case.F)
     check_sweep(np.asarray(idx.cpu())[sel], np.asarray(E.cpu())[sel],
                 np.asarray(S.cpu())[sel] if second else None, ref, spec, case.D[sel], case.F, tag="large")
+
+
+@pytest.mark.parametrize("shape", ["p1_d1_deg3", "p2_d3_deg2", "p3_d1_deg4"])
+def test_sweep_other_program_shapes(shape):
+    """Program shapes the BASELINE configs do not use: one program variable (a 1-D block, grid
+    rule on one dimension), three data parameters, and 35 program-part monomials (the NPE = 36
+    kernel), each against the oracle on the full grid."""
+    g = np.random.default_rng(20260 + len(shape))
+    if shape == "p1_d1_deg3":
+        spec = synth.classf_program("shape_p1", 1, 1, 3, [8, 1], [8192, 1024], synth.HW_GTX1080TI, R=32,
+                                    Z0=0, Z1=0, grid_map=(0, -1, -1))
+        F = np.concatenate([np.arange(32, 1025, 32), [1, 16, 48, 100, 2048]]).astype(np.int32)[:, None]
+        D = synth.log_uniform_ints(g, 8, 8192, (3000, 1)).astype(np.int32)
+    elif shape == "p2_d3_deg2":
+        spec = synth.classf_program("shape_d3", 3, 2, 2, [8, 8, 8, 1, 1], [4096, 4096, 512, 1024, 1024],
+                                    synth.HW_B200, R=40, Z0=1024, Z1=1, grid_map=(1, 0, -1))
+        F = synth.F_pow2_2d()
+        D = synth.log_uniform_ints(g, 8, 4096, (3000, 3)).astype(np.int32)
+        D[:, 2] = np.minimum(D[:, 2], 512)
+    else:
+        spec = synth.classf_program("shape_p3", 1, 3, 4, [8, 1, 1, 1], [16384, 1024, 1024, 64],
+                                    synth.HW_GTX1080TI, R=24, Z0=0, Z1=0, grid_map=(0, 0, -1))
+        F = synth.F_pow2_3d()
+        D = synth.log_uniform_ints(g, 8, 16384, (2000, 1)).astype(np.int32)
+    ref = oracle.sweep(spec, D, F)
+    for second in (True, False):
+        idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=second)
+        strict, feas = check_sweep(idx, E, S if second else None, ref, spec, D, F, tag=shape)
+        assert feas > 0 and strict >= 0.95 * feas
