@@ -412,3 +412,27 @@ def test_sweep_other_program_shapes(shape):
         idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=second)
         strict, feas = check_sweep(idx, E, S if second else None, ref, spec, D, F, tag=shape)
         assert feas > 0 and strict >= 0.95 * feas
+
+
+def test_fit_different_numerator_denominator_bases():
+    """Numerator and denominator bases that differ (degree 3 over degree 1, and a box basis over a
+    total-degree one): the generic Gram kernel (not the fused symmetric-block one), its Gram and
+    coefficients against the oracle, at ragged K."""
+    fc = synth.polybench_fit_box(sigma=0.01)
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(fc.truths[0], fc.X)]) * fc.noise
+    bases = [(synth.basis_total_degree(4, 3), synth.basis_total_degree(4, 1)),
+             (synth.basis_box([1, 2, 1, 1]), synth.basis_total_degree(4, 2))]
+    for num, den in bases:
+        for K in (97, 2000):
+            X = fc.X[:K]
+            coef, (c, e), infos = rp.fit(_cuda(X), _cuda(V[:, :K]), num, den)
+            for i in range(len(V)):
+                r = oracle.fit(X, V[i, :K], num, den, nthreads=8)
+                assert np.array_equal(r["c"], c) and np.array_equal(r["e"], e)
+                want = np.asarray(r["coef"], dtype=np.float64)
+                err = np.max(np.abs(coef[i] - want)) / np.max(np.abs(want))
+                assert err <= 1e-9, (len(num), len(den), K, i, err)
+                G = rp.gram(_cuda(X), _cuda(V[i:i + 1, :K]), num, den, c, e)[0].cpu().numpy()
+                Go = np.asarray(r["G"], dtype=np.float64)
+                dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
+                assert np.max(np.abs(G - Go) / dg) <= 1e-12, (len(num), len(den), K, i)
