@@ -333,6 +333,23 @@ rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capaci
 rp_status rp_plan_history_stats(rp_plan plan, int64_t *hits, int64_t *misses, int64_t *entries);
 rp_status rp_plan_history_clear(rp_plan plan, rp_stream s);
 
+/* Single-launch decider (the per-launch use of PAPER.md:2094-2099, "immediately preceding the
+ * launch of a kernel", with the lowest host-visible latency the library offers): one data tuple
+ * in, one rp_decision out, through host-mapped pinned memory (no copy nodes) and a CUDA graph of
+ * the rp_plan_decide kernel captured once on a private stream.
+ *   rp_decider_create  -- for program `prog` of `plan` and `margin`; if the plan's runtime history
+ *                         is used, enable it BEFORE creating the decider (the graph captures the
+ *                         table) and do not re-enable it while the decider lives.
+ *   rp_decider_decide  -- D: host array of the plan's d data parameters; out: host rp_decision.
+ *                         Synchronous (returns when `out` is written).  Not thread-safe.
+ *   rp_decider_destroy -- frees the mapped buffers, the graph and the stream.
+ * The plan must outlive the decider.  Errors: RP_ERR_INVALID_ARG, RP_ERR_UNSUPPORTED (nF beyond
+ * the decide kernel's limit), RP_ERR_CUDA.                                                    */
+typedef struct rp_decider_s *rp_decider;
+rp_status rp_decider_create(rp_plan plan, int32_t prog, double margin, rp_decider *out);
+rp_status rp_decider_decide(rp_decider dc, const int32_t *D, rp_decision *out);
+rp_status rp_decider_destroy(rp_decider dc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,9 @@ _SIGS = {
     "rp_plan_destroy": [_vp],
     "rp_plan_decide": [_vp, _i32, _vp, _i64, C.c_double, _vp, _vp],
     "rp_plan_history_enable": [_vp, _i32, _i32, C.c_double],
+    "rp_decider_create": [_vp, _i32, C.c_double, _vp],
+    "rp_decider_decide": [_vp, _vp, _vp],
+    "rp_decider_destroy": [_vp],
     "rp_plan_history_stats": [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)],
     "rp_plan_history_clear": [_vp, _vp],
 }
@@ -644,50 +647,57 @@ def decisions_from_device(out) -> np.ndarray:
     return np.frombuffer(out.cpu().numpy().tobytes(), dtype=DECISION_DTYPE)
 
 
+class Decider:
+    """rp_decider: one data tuple in, one decision out, through host-mapped pinned memory and a
+    CUDA graph of the decide kernel captured once (no copy nodes, no per-call allocation).
+    Enable the plan's history (Plan.enable_history) before creating one if it is to be used."""
+
+    def __init__(self, plan: "Plan", prog: int = 0, margin: float = 0.0):
+        self.plan = plan
+        self.handle = C.c_void_p()
+        _check(_lib.rp_decider_create(plan.handle, prog, float(margin), C.byref(self.handle)))
+        self._D = (C.c_int32 * max(plan.d, 1))()
+        self._out = np.zeros(1, dtype=DECISION_DTYPE)
+
+    def __call__(self, D) -> np.void:
+        for k, v in enumerate(np.asarray(D).ravel()[: self.plan.d]):
+            self._D[k] = int(v)
+        _check(_lib.rp_decider_decide(self.handle, C.cast(self._D, _vp), _ptr(self._out)))
+        return self._out[0].copy()
+
+    def close(self):
+        if self.handle:
+            _lib.rp_decider_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DecisionService:
-    """The single-launch latency path of NEXT row f2: one rp_plan_decide on pre-allocated device
-    buffers, captured with the pinned host <-> device copies in one CUDA graph, replayed per
-    kernel launch of the user's program (the rational program runs
-    "immediately preceding the launch of a kernel")."""
+    """The single-launch latency path of NEXT row f2, for a user's launch site: a host memo in
+    front of a Decider (rp_decider: mapped memory, the decide kernel as a captured CUDA graph),
+    which itself probes the plan's device history (the rational program runs
+    "immediately preceding the launch of a kernel"; 2120-2122: the runtime history)."""
 
     def __init__(self, plan: "Plan", prog: int = 0, margin: float = 0.0, history_log2: int | None = 16,
                  host_memo: int = 1 << 16):
-        torch = _torch()
         self.plan, self.prog, self.margin = plan, prog, margin
         self.memo = {} if host_memo else None
         self.memo_cap = host_memo
         if history_log2:
             plan.enable_history(prog, history_log2, margin)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.D_host = torch.zeros((1, plan.d), dtype=torch.int32).pin_memory()
-        self.out_host = torch.zeros((1, 48), dtype=torch.uint8).pin_memory()
-        self.D_dev = torch.zeros((1, plan.d), dtype=torch.int32, device=dev)
-        self.out_dev = torch.zeros((1, 48), dtype=torch.uint8, device=dev)
-        self.stream = torch.cuda.Stream(dev)
-        # warm up (kernel attributes, modules) outside the capture
-        with torch.cuda.stream(self.stream):
-            plan.decide(self.D_dev, prog, margin, out=self.out_dev)
-        self.stream.synchronize()
-        if history_log2:
-            plan.clear_history()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=self.stream, capture_error_mode="thread_local"):
-            self.D_dev.copy_(self.D_host, non_blocking=True)
-            plan.decide(self.D_dev, prog, margin, out=self.out_dev)
-            self.out_host.copy_(self.out_dev, non_blocking=True)
-        self.stream.synchronize()
+        self.decider = Decider(plan, prog, margin)
 
     def __call__(self, D) -> np.void:
-        torch = _torch()
         key = tuple(int(v) for v in np.asarray(D).ravel()[: self.plan.d])
         hit = self.memo.get(key) if self.memo is not None else None
         if hit is not None:  # host memo in front of the device history: no GPU round trip
             return hit
-        self.D_host.numpy()[0, :] = key
-        with torch.cuda.stream(self.stream):
-            self.graph.replay()
-        self.stream.synchronize()
-        r = np.frombuffer(self.out_host.numpy().tobytes(), dtype=DECISION_DTYPE)[0].copy()
+        r = self.decider(key)
         if self.memo is not None and len(self.memo) < self.memo_cap:
             self.memo[key] = r
         return r

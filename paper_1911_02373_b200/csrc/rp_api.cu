@@ -1134,6 +1134,92 @@ rp_status rp_plan_decide(rp_plan plan, int32_t prog, const int32_t *D, int64_t n
   return RP_OK;
 }
 
+// ---- single-launch decider: mapped pinned buffers + a captured graph of the decide kernel ------
+struct rp_decider_s {
+  rp_plan plan = nullptr;
+  int32_t *hD = nullptr, *dD = nullptr;            // d ints, host-mapped
+  rp_decision *hout = nullptr, *dout = nullptr;    // one decision, host-mapped
+  cudaStream_t s = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int d = 0;
+};
+
+static void decider_free(rp_decider dc) {
+  if (!dc) return;
+  if (dc->s) cudaStreamSynchronize(dc->s);
+  if (dc->exec) cudaGraphExecDestroy(dc->exec);
+  if (dc->graph) cudaGraphDestroy(dc->graph);
+  if (dc->s) cudaStreamDestroy(dc->s);
+  if (dc->hD) cudaFreeHost(dc->hD);
+  if (dc->hout) cudaFreeHost(dc->hout);
+  delete dc;
+}
+
+rp_status rp_decider_create(rp_plan plan, int32_t prog, double margin, rp_decider *out) {
+  RP_REQUIRE(out, RP_ERR_INVALID_ARG, "null decider out");
+  *out = nullptr;
+  RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
+  RP_REQUIRE(prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "prog %d out of range", prog);
+  RP_REQUIRE(margin >= 0.0, RP_ERR_INVALID_ARG, "margin < 0 / NaN");
+  RP_REQUIRE(plan->nF <= kDecideMaxF, RP_ERR_UNSUPPORTED, "decide: nF = %d > %d", plan->nF, kDecideMaxF);
+  if (plan->hist.enabled)
+    RP_REQUIRE(plan->hist.prog == prog && plan->hist.margin == margin, RP_ERR_INVALID_ARG,
+               "the runtime history was enabled for program %d, margin %g", plan->hist.prog, plan->hist.margin);
+  rp_decider dc = new rp_decider_s;
+  dc->plan = plan;
+  dc->d = plan->d;
+  auto fail = [&](cudaError_t e, const char *w) {
+    rp_status r = cuda_fail(e, w, __FILE__, __LINE__);
+    decider_free(dc);
+    return r;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamSynchronize(plan->stream)) != cudaSuccess) return fail(e, "plan stream");
+  if ((e = cudaHostAlloc((void **)&dc->hD, sizeof(int32_t) * kMaxVars, cudaHostAllocMapped)) != cudaSuccess)
+    return fail(e, "mapped D");
+  if ((e = cudaHostAlloc((void **)&dc->hout, sizeof(rp_decision), cudaHostAllocMapped)) != cudaSuccess)
+    return fail(e, "mapped out");
+  if ((e = cudaHostGetDevicePointer((void **)&dc->dD, dc->hD, 0)) != cudaSuccess) return fail(e, "map D");
+  if ((e = cudaHostGetDevicePointer((void **)&dc->dout, dc->hout, 0)) != cudaSuccess) return fail(e, "map out");
+  for (int k = 0; k < kMaxVars; ++k) dc->hD[k] = 1;
+  if ((e = cudaStreamCreateWithFlags(&dc->s, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "stream");
+  DecideArgs a{plan->d_progs, plan->tab, plan->npe_pad, prog, dc->dD, 1, margin, dc->dout, plan->hist};
+  // warm-up outside the capture (kernel attributes, module load); a history insert of D = 1...
+  // would be a real decision, so the history is cleared afterwards when it is on
+  if ((e = launch_decide(a, plan->mwp, dc->s)) != cudaSuccess) return fail(e, "warm-up");
+  if ((e = cudaStreamSynchronize(dc->s)) != cudaSuccess) return fail(e, "warm-up sync");
+  if (plan->hist.enabled) {
+    if ((e = cudaMemsetAsync(plan->hist.slots, 0, ((size_t)plan->hist.mask + 1) * sizeof(HistSlot), dc->s)) != cudaSuccess)
+      return fail(e, "history clear");
+    if ((e = cudaMemsetAsync(plan->hist.counters, 0, 3 * sizeof(unsigned long long), dc->s)) != cudaSuccess)
+      return fail(e, "history clear");
+    if ((e = cudaStreamSynchronize(dc->s)) != cudaSuccess) return fail(e, "history clear");
+  }
+  if ((e = cudaStreamBeginCapture(dc->s, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return fail(e, "capture");
+  e = launch_decide(a, plan->mwp, dc->s);
+  cudaError_t e2 = cudaStreamEndCapture(dc->s, &dc->graph);
+  if (e != cudaSuccess) return fail(e, "capture launch");
+  if (e2 != cudaSuccess) return fail(e2, "end capture");
+  if ((e = cudaGraphInstantiate(&dc->exec, dc->graph, 0)) != cudaSuccess) return fail(e, "instantiate");
+  *out = dc;
+  return RP_OK;
+}
+
+rp_status rp_decider_decide(rp_decider dc, const int32_t *D, rp_decision *out) {
+  RP_REQUIRE(dc && D && out, RP_ERR_INVALID_ARG, "null argument");
+  for (int k = 0; k < dc->d; ++k) dc->hD[k] = D[k];
+  RP_CUDA(cudaGraphLaunch(dc->exec, dc->s));
+  RP_CUDA(cudaStreamSynchronize(dc->s));
+  *out = *dc->hout;
+  return RP_OK;
+}
+
+rp_status rp_decider_destroy(rp_decider dc) {
+  decider_free(dc);
+  return RP_OK;
+}
+
 rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capacity, double margin) {
   RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
   RP_REQUIRE(prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "prog %d out of range", prog);

@@ -113,3 +113,27 @@ def test_decision_service_graph():
             assert r["from_history"] == 1  # served by the device history
         else:
             assert len(svc.memo) == len(np.unique(case.D))  # served by the host memo
+
+
+@pytest.mark.parametrize("history", [False, True])
+def test_decider_matches_batched_decide(history):
+    """rp_decider (mapped memory + captured graph) returns, tuple by tuple, the decisions of the
+    batched rp_plan_decide; with the history on, repeats come from the table."""
+    case = synth.polybench_sweep(nD=64)
+    D = np.concatenate([synth.random_D_edge_cases(1), case.D])
+    plan = rp.Plan(case.programs, _cuda(case.F))
+    want = plan.decide(D, prog=1, margin=0.02)
+    if history:
+        plan.enable_history(1, 10, 0.02)
+    dc = rp.Decider(plan, prog=1, margin=0.02)
+    for rep in range(2 if history else 1):
+        for i, d in enumerate(D):
+            r = dc(d)
+            assert r["idx"] == want[i]["idx"] and r["E"] == want[i]["E"], (rep, i)
+            assert tuple(r["launch"]) == tuple(want[i]["launch"]), (rep, i)
+            if history and rep == 1 and want[i]["idx"] >= 0:
+                assert r["from_history"] == 1
+    dc.close()
+    with pytest.raises(rp.RPError):  # a history for another program/margin is refused
+        plan.enable_history(0, 8, 0.0)
+        rp.Decider(plan, prog=1, margin=0.02)

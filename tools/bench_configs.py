@@ -54,8 +54,8 @@ out["tiny"] = {"pairs": int(len(tiny.D) * len(tiny.F)), "eval_argmin_us": 1e3 * 
                "plan_eval_device_us": 1e3 * ms_plan,
                "plan_eval_host_wall_us": 1e6 * (time.perf_counter() - t0) / 200}
 
-# f2: single-decision latency through the CUDA-graph'd DecisionService (host wall per call,
-# pinned copies in and out included), fresh decisions and history hits
+# f2: single-decision latency through the DecisionService (host wall per call: rp_decider's
+# mapped-memory graph launch and synchronisation included), fresh decisions and history hits
 case = synth.polybench_sweep(nD=2000)
 plan = rp.Plan(case.programs[:1], torch.from_numpy(case.F).to(dev))
 svc = rp.DecisionService(plan, prog=0, margin=0.01, history_log2=16)
@@ -74,9 +74,20 @@ t0 = time.perf_counter()
 for d in case.D[50:1050]:
     svc(d)
 hit_us = 1e6 * (time.perf_counter() - t0) / 1000
-out["decision_service"] = {"program": "polybench gemm, 266 configs", "fresh_decision_us": fresh_us,
-                           "device_history_hit_us": hit_us, "host_memo_hit_us": memo_us,
-                           "history": plan.history_stats()}
+stats = plan.history_stats()
+svc.decider.close()
+plan2 = rp.Plan(case.programs[:1], torch.from_numpy(case.F).to(dev))
+dc = rp.Decider(plan2, prog=0, margin=0.01)  # no history, no memo: every call a full decision
+for d in case.D[:50]:
+    dc(d)
+t0 = time.perf_counter()
+for d in case.D[50:1050]:
+    dc(d)
+nohist_us = 1e6 * (time.perf_counter() - t0) / 1000
+out["decision_service"] = {"program": "polybench gemm, 266 configs", "path": "rp_decider (mapped memory + graph)",
+                           "fresh_decision_us": fresh_us, "device_history_hit_us": hit_us,
+                           "host_memo_hit_us": memo_us, "no_history_decision_us": nohist_us,
+                           "history": stats}
 
 for name, case in (("polybench", synth.polybench_sweep()), ("multikernel", synth.multikernel_sweep())):
     D, F = torch.from_numpy(case.D).to(dev), torch.from_numpy(case.F).to(dev)
