@@ -363,6 +363,16 @@ def test_device_resident_fit_and_plan_update():
     i2, E2, S2 = rp.eval_argmin(fitted, D, F)
     assert torch.equal(i1[0], i2) and torch.equal(E1[0], E2) and torch.equal(S1[0], S2)
     plan.close()
+    # a batched plan: updating program 2 in place changes program 2 only
+    progs = case.programs[:3]
+    bplan = rp.Plan(progs, F)
+    before = bplan.eval(D)
+    bplan.update(cd, xf, prog=2)
+    after = bplan.eval(D)
+    for g in (0, 1):
+        assert torch.equal(after[0][g], before[0][g]) and torch.equal(after[1][g], before[1][g])
+    assert torch.equal(after[0][2], i2) and torch.equal(after[1][2], E2) and torch.equal(after[2][2], S2)
+    bplan.close()
 
 
 @pytest.mark.parametrize("second", [False, True])
