@@ -446,3 +446,29 @@ def test_fit_different_numerator_denominator_bases():
                 Go = np.asarray(r["G"], dtype=np.float64)
                 dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
                 assert np.max(np.abs(G - Go) / dg) <= 1e-12, (len(num), len(den), K, i)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sweep_randomised_programs(seed):
+    """Randomised stress: class-F programs with random hardware fixtures (SM count, warp / block /
+    register / shared-memory limits), kernel resources (R, Z0, Z1) and a random subset of F with
+    odd shapes, against the oracle on the full grid (both templates)."""
+    g = np.random.default_rng(7000 + seed)
+    hw = dict(synth.HW_GTX1080TI)
+    hw.update(n_sm=int(g.integers(1, 200)), w_max=int(g.choice([32, 48, 64])), b_max=int(g.choice([8, 16, 32])),
+              t_max=int(g.choice([512, 1024])), r_max=int(g.choice([32768, 65536])),
+              z_max=int(g.choice([12288, 24576, 49152])))
+    p = int(g.integers(1, 4))
+    lo = [8] + [1] * p
+    hi = [int(g.choice([2048, 16384]))] + [1024] * p
+    spec = synth.classf_program(f"rand{seed}", 1, p, int(g.integers(1, 4)), lo, hi, hw,
+                                R=int(g.integers(8, 256)), Z0=int(g.choice([0, 512, 4096])), Z1=int(g.integers(0, 3)),
+                                grid_map=tuple([0] * p + [-1] * (3 - p)), stream=f"s{seed}")
+    nF = int(g.integers(40, 400))
+    F = np.stack([g.choice([1, 2, 3, 4, 8, 16, 24, 32, 48, 64, 96, 128, 256, 512, 1024], nF) for _ in range(p)], 1)
+    F = F.astype(np.int32)
+    D = synth.log_uniform_ints(g, 1, hi[0], (1500, 1)).astype(np.int32)
+    ref = oracle.sweep(spec, D, F)
+    for second in (True, False):
+        idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=second)
+        check_sweep(idx, E, S if second else None, ref, spec, D, F, tag=f"rand{seed}")
