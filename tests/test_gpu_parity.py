@@ -472,3 +472,35 @@ def test_sweep_randomised_programs(seed):
     for second in (True, False):
         idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=second)
         check_sweep(idx, E, S if second else None, ref, spec, D, F, tag=f"rand{seed}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gram_randomised_bases(seed):
+    """Randomised stress of the Gram kernels: random variable counts, exponent lists (equal
+    numerator / denominator lists of 16, 40 or 72 monomials take the fused warp-specialised path,
+    others the generic one), row counts and metric values, against the oracle's plain sum of outer
+    products at 1e-12 sqrt(G_ii G_jj)."""
+    g = np.random.default_rng(9100 + seed)
+    n = int(g.integers(1, 6))
+    full = synth.basis_total_degree(n, 6 if n <= 2 else (4 if n <= 4 else 3))
+    def pick(m):
+        m = min(m, len(full))
+        idx = np.sort(g.choice(len(full), m, replace=False))
+        if 0 not in idx:
+            idx[0] = 0
+        return np.ascontiguousarray(full[np.unique(idx)])
+    if g.random() < 0.5:
+        num = pick(int(g.choice([16, 40, 72])))
+        den = num.copy()
+    else:
+        num, den = pick(int(g.integers(3, 40))), pick(int(g.integers(2, 30)))
+    K = int(g.integers(1, 5000))
+    X = g.uniform(-50, 800, (K, n)).round()
+    V = g.uniform(0.1, 100.0, (2, K))
+    lo, hi = X.min(axis=0), X.max(axis=0)
+    c, e = rp.xform_from_box(lo, hi)
+    G = rp.gram(_cuda(X), _cuda(V), num, den, c, e).cpu().numpy()
+    for i in range(2):
+        Go = np.asarray(oracle.gram(X, V[i], num, den, c, e), dtype=np.float64)
+        dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
+        assert np.max(np.abs(G[i] - Go) / dg) <= 1e-12, (seed, n, len(num), len(den), K, i)
