@@ -150,8 +150,8 @@ __device__ __forceinline__ EConst32 to_econst32(const EConst &k) {
   return EConst32{(float)k.Lunc, (float)k.Lcoal, (float)k.DdU, (float)k.ddc, (float)k.issue, (float)k.Kbw,
                   (float)k.rKbw};
 }
-__device__ __forceinline__ bool fclose(float x, float y) {  // |x - y| <= kScreenCmp max(x, y), x, y > 0
-  return fabsf(x - y) <= kScreenCmp * fmaxf(x, y);
+__device__ __forceinline__ bool fclose(float x, float y, float tol = kScreenCmp) {  // |x - y| <= tol max(x, y)
+  return fabsf(x - y) <= tol * fmaxf(x, y);
 }
 __device__ __forceinline__ float rcp32(float x) {  // MUFU.RCP: relative error <= 2^-23
   float r;
@@ -163,8 +163,11 @@ __device__ __forceinline__ bool in_range32(float x) {
   return (uint32_t)(__float_as_uint(x) - 0x3089705fu) <= (uint32_t)(0x4e6e6b28u - 0x3089705fu);
 }
 
+// tol: the relative closeness below which a case comparison is not trusted (kScreenCmp for inputs
+// that are rounded FP64 values; the tensor-core screen passes its per-pair bound)
 __device__ __forceinline__ float mwpcwp_E32(float p1, float q1, float p2, float q2, float p3, float q3, float W,
-                                            float Rep, float rSM, float SMact, const EConst32 &k, bool &unc) {
+                                            float Rep, float rSM, float SMact, const EConst32 &k, bool &unc,
+                                            float tol = kScreenCmp) {
   // inputs in [1e-9, 1e9]: every intermediate stays a normal float (products of three inputs and
   // the hardware constants lie within ~1e-30 .. 1e33)
   unc = !(in_range32(p1) & in_range32(q1) & in_range32(p2) & in_range32(q2) & in_range32(p3) & in_range32(q3));
@@ -201,8 +204,9 @@ __device__ __forceinline__ float mwpcwp_E32(float p1, float q1, float p2, float 
   // Comp_c > Mem_c decide case 2 when case 1 does not hold.  (The values of the mins are accurate
   // whichever operand is smaller.)
   // (bitwise | and &: branch-free)
-  unc = unc | !(mwp >= 2.0f) | fclose(W, mwp0) | (!mwpW & fclose(MWP_bw, MWP_nb)) | (mwpW & fclose(CWPf, W)) |
-        (!c1 & fclose(cwp, mwp)) | (!c1 & !(cwp >= mwp) & fclose(Comp_c, Mem_c)) | !(E > 0.f & E < 3.0e38f);
+  unc = unc | !(mwp >= 2.0f) | fclose(W, mwp0, tol) | (!mwpW & fclose(MWP_bw, MWP_nb, tol)) |
+        (mwpW & fclose(CWPf, W, tol)) | (!c1 & fclose(cwp, mwp, tol)) |
+        (!c1 & !(cwp >= mwp) & fclose(Comp_c, Mem_c, tol)) | !(E > 0.f & E < 3.0e38f);
   return E;
 }
 

@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "rp_device.cuh"
+#include "rp_umma.cuh"
 
 namespace rp {
 
@@ -921,6 +922,465 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_sweep_ws(SweepArgs a) {
   }
 }
 
+// ============================================================================================
+// Tensor-core screened sweep (RP_SWEEP_KERNEL=tc; MWP-CWP programs with nPE <= 16, no runner-up).
+//
+// The contraction p_k(D, P) = sum_pe C_{k,pe}(D) m_pe(P) runs on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM) as a 3-term split product
+//   C m ~ C_hi m_hi + C_hi m_lo + C_lo m_hi      (x_hi = tf32(x), x_lo = tf32(x - x_hi)),
+// asynchronously to the warps that screen E in FP32 (mwpcwp_E32 with a per-pair bound), so the
+// FP64 datapath carries only the exact re-evaluation of the few candidates.  One CTA = 128 data
+// tuples (the MMA M side, one TMEM lane each) x all configurations in tiles of 32 (N):
+//   warp 16:     builds the B operands of tile i (m splits, K-major no-swizzle layout) into ring
+//                slot i % 2, issues 36 MMAs (6 polynomials x 2 K-steps x 3 split terms) into TMEM
+//                buffer i % 2, commits to full[i % 2];
+//   warps 0-15:  warpgroups 2b, 2b+1 screen the tiles of buffer b (16 configurations each), keep
+//                per thread the kKC smallest lower bounds E32 (1 - eta), then re-evaluate them
+//                exactly in FP64; a tuple whose dropped lower bounds could reach its winner is
+//                re-swept in FP64 by one warp (rare).
+// Error model: |p32 - p| <= 64 u S, S = sum |C m| <=
+// ||C_k||_2 ||m||_2 (Cauchy-Schwarz; u = 2^-24; measured <= 9.8 u S, tools/microbench/umma_tf32.cu),
+// so with rho = max_k ||C_k|| ||m|| / |p32_k| <= 64 each input carries eps = 64 u rho relative error;
+// E is a product / quotient / positive-sum expression in which each input enters at most 18 times
+// (6 for every compared quantity), hence |E32 - E| <= 1.1 (18 eps + 80 u) E + 1e-6 E.
+// ============================================================================================
+constexpr int kTcM = 128;           // tuples per CTA (TMEM lanes)
+constexpr int kTcN = 32;            // configurations per MMA tile
+constexpr int kTcNPE = 16;          // MMA K (program-part monomials, padded)
+constexpr int kTcKC = 4;            // kept candidates per screening thread
+constexpr int kTcEpi = 512;         // screening threads (4 warpgroups)
+constexpr int kTcThreads = kTcEpi + 32;
+constexpr uint32_t kTcLBO = 128, kTcSBO = 512;        // K-major no-swizzle core-matrix strides
+constexpr uint32_t kTcAbytes = kTcM / 8 * kTcSBO;     // one [128 x 16] tf32 operand: 8 KB
+constexpr uint32_t kTcBbytes = kTcN / 8 * kTcSBO;     // one [32 x 16] tf32 operand: 2 KB
+constexpr int kTcMaxNdp = 32;
+// shared-memory map (bytes)
+constexpr uint32_t kTcOffA = 0;                                   // [2 splits][6 polys] A operands; later FP64 C [128][96]
+constexpr uint32_t kTcOffB = kTcOffA + 12 * kTcAbytes;            // [2 slots][2 splits] B operands
+constexpr uint32_t kTcOffMn = kTcOffB + 4 * kTcBbytes;            // [2 slots][32] ||m(P)||
+constexpr uint32_t kTcOffMD = kTcOffMn + 2 * kTcN * 4;            // [128][ndp <= 32] data monomials (FP64)
+constexpr uint32_t kTcOffRSM = kTcOffMD + kTcM * kTcMaxNdp * 8;   // [kRSMTab] 1/SM_act (FP32)
+constexpr uint32_t kTcOffDv = kTcOffRSM + kRSMTab * 4;            // [128][kMaxVars] D values
+constexpr uint32_t kTcOffCn = kTcOffDv + kTcM * kMaxVars * 4;     // [128][6] ||C_k(D)||
+constexpr uint32_t kTcOffPart = kTcOffCn + kTcM * 6 * 4;          // [4][128] {e, i, tnl, ovf}
+constexpr uint32_t kTcOffFb = kTcOffPart + 4 * kTcM * 24;         // [128] fallback tuples + count
+constexpr uint32_t kTcOffBar = (kTcOffFb + (kTcM + 2) * 4 + 7) & ~7u;  // full[2], empty[2], tmem base, maxD1sq
+constexpr uint32_t kTcSmem = kTcOffBar + 64;
+static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared memory");
+static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
+
+__device__ unsigned long long g_tc_stats[2];  // [0] tuples re-swept in FP64, [1] tuples
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
+  constexpr int NPOLY = 6, NPE = kTcNPE;
+  constexpr double kInf = __builtin_huge_val();
+  const int g = blockIdx.y;
+  const DevProg &pg = a.progs[g];
+  const int d = a.d;
+  const int64_t d0 = (int64_t)blockIdx.x * kTcM;
+  const int tmax = (int)((a.nD - d0) < kTcM ? (a.nD - d0) : kTcM);
+  const int n_sm = pg.n_sm;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char *sA = sm + kTcOffA, *sB = sm + kTcOffB;
+  float *sMn = reinterpret_cast<float *>(sm + kTcOffMn);
+  double *sMD = reinterpret_cast<double *>(sm + kTcOffMD);
+  float *sRSM32 = reinterpret_cast<float *>(sm + kTcOffRSM);
+  int32_t *sDv = reinterpret_cast<int32_t *>(sm + kTcOffDv);
+  float *sCn = reinterpret_cast<float *>(sm + kTcOffCn);
+  unsigned char *sPart = sm + kTcOffPart;
+  int32_t *sFb = reinterpret_cast<int32_t *>(sm + kTcOffFb);  // [0]: count, [1..]: tuples
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kTcOffBar);  // full[0..1], empty[0..1]
+  uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 4);
+  unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 5);
+  double *sCd = reinterpret_cast<double *>(sm + kTcOffA);  // FP64 C [128][96] after the sweep
+  const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
+  const int nDE = pg.nDE, ndp = a.tab.nde_pad;
+  const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
+
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(bars + i), 1);      // full: the MMA commit
+      mbar_init(smem_u32(bars + 2 + i), 8);  // empty: the 8 warps screening buffer i
+    }
+    sFb[0] = 0;
+    *sMaxD1 = 0ull;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (wid == 16) tmem_alloc(smem_u32(sTmem), 512);
+  for (int i = tid; i < kTcM * d; i += kTcThreads) {
+    const int t = i / d, k = i % d;
+    const int64_t src = (t < tmax) ? (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t) : 0;
+    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[src * d + k] : 1;
+  }
+  for (int i = tid; i <= n_sm; i += kTcThreads) sRSM32[i] = (float)gRSM[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // data monomials m_de(u_D) (FP64), and the largest D1^2 of the tile (a3 early exit)
+  for (int i = tid; i < kTcM * ndp; i += kTcThreads) {
+    const int t = i / ndp, de = i % ndp;
+    double m = 0.0;
+    if (de < nDE) {
+      m = 1.0;
+      for (int k = 0; k < d; ++k) {
+        const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+        for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
+      }
+    }
+    sMD[t * ndp + de] = m;
+  }
+  if (tid < tmax) {
+    const long long D1 = sDv[tid * kMaxVars];
+    atomicMax(sMaxD1, (unsigned long long)(D1 * D1));
+  }
+  __syncthreads();
+  // staged data polynomials C_{k,pe}(D) in FP64 (a2): the (96 x ndp) x (ndp x 128) product of the
+  // plan's coefficient matrix and the tile's data monomials on DMMA.8x8x4 (8x8 output tiles spread
+  // over the warps, as in k_sweep).  to_ops: stored as tf32 splits in the A operands, with
+  // ||C_k(D)||_2^2 summed into sNrm (shared FP64 atomics: two addends onto 0, order-independent);
+  // else stored as FP64 rows sCd[t][96] for the exact re-evaluation.
+  double *sNrm = reinterpret_cast<double *>(sPart);  // [128][6], before the merge needs sPart
+  auto stage_C = [&](bool to_ops, int nwarps) {
+    constexpr int MT = NPOLY * NPE / 8, NT = kTcM / 8;
+    for (int tile = wid; tile < MT * NT; tile += nwarps) {
+      const int mt = tile / NT, nt = tile % NT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < ndp / 4; ++ks) {
+        const double av = __ldg(Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3));
+        const double bv = sMD[(nt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3)];
+        dmma(c0, c1, av, bv);
+      }
+      const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
+      const int k = row / NPE, pe = row % NPE;
+      if (to_ops) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double c = j ? c1 : c0;
+          const float hi = to_tf32((float)c), lo = to_tf32((float)(c - (double)hi));
+          const uint32_t o = umma_off(t + j, pe, kTcLBO, kTcSBO);
+          *reinterpret_cast<float *>(sA + k * kTcAbytes + o) = hi;
+          *reinterpret_cast<float *>(sA + (NPOLY + k) * kTcAbytes + o) = lo;
+        }
+        double q0 = c0 * c0, q1 = c1 * c1;
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+          q0 += __shfl_xor_sync(0xffffffffu, q0, m);
+          q1 += __shfl_xor_sync(0xffffffffu, q1, m);
+        }
+        if (lane < 4) {
+          atomicAdd(&sNrm[t * 6 + k], q0);
+          atomicAdd(&sNrm[(t + 1) * 6 + k], q1);
+        }
+      } else {
+        sCd[t * 96 + row] = c0;
+        sCd[(t + 1) * 96 + row] = c1;
+      }
+    }
+  };
+  for (int i = tid; i < kTcM * 6; i += kTcThreads) sNrm[i] = 0.0;
+  __syncthreads();
+  stage_C(true, kTcThreads / 32);
+  __syncthreads();
+  for (int i = tid; i < kTcM * 6; i += kTcThreads) sCn[i] = (float)(sqrt(sNrm[i]) * (1.0 + 1e-6));
+  fence_async_smem();
+  __syncthreads();
+
+  const int nFc = a.tab.nFc[2 * g];
+  const bool sorted = a.tab.nFc[2 * g + 1] != 0;
+  const int nFp = a.tab.nFp;
+  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
+  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
+  const int nTiles = (nFc + kTcN - 1) / kTcN;
+  int nEff = tmax > 0 ? nTiles : 0;
+  if (sorted && nEff > 0) {  // configurations sorted by P1 P2: stop at the first tile past max D1^2
+    const long long mx = (long long)*sMaxD1;
+    for (int b0 = 0; b0 < nTiles; b0 += 32) {
+      const int j = b0 + lane;
+      const unsigned stop = __ballot_sync(0xffffffffu, j < nTiles && __ldg(&rec[j * kTcN].P01) > mx);
+      if (stop) {
+        nEff = b0 + __ffs(stop) - 1;
+        break;
+      }
+    }
+  }
+  const uint32_t tm = *sTmem;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 2);
+
+  if (wid == 16) {
+    // ---- producer / MMA warp ------------------------------------------------------------------
+    const uint32_t idesc = umma_idesc_tf32(kTcM, kTcN);
+    double mv[NPE];
+#pragma unroll
+    for (int pe = 0; pe < NPE; ++pe) mv[pe] = (nEff > 0 && lane < nFp) ? __ldg(mP + (int64_t)pe * nFp + lane) : 0.0;
+    for (int i = 0; i < nEff; ++i) {
+      const int s = i & 1, use = i >> 1;
+      if (use > 0) mbar_wait(empty0 + 8 * s, (use - 1) & 1);
+      unsigned char *bh = sB + (2 * s) * kTcBbytes, *bl = bh + kTcBbytes;
+      double mn2 = 0.0;
+#pragma unroll
+      for (int pe = 0; pe < NPE; ++pe) {
+        const double m = mv[pe];
+        const float hi = to_tf32((float)m), lo = to_tf32((float)(m - (double)hi));
+        const uint32_t o = umma_off(lane, pe, kTcLBO, kTcSBO);
+        *reinterpret_cast<float *>(bh + o) = hi;
+        *reinterpret_cast<float *>(bl + o) = lo;
+        mn2 = fma(m, m, mn2);
+      }
+      sMn[s * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
+      if (i + 1 < nEff) {
+        const int pos = (i + 1) * kTcN + lane;
+#pragma unroll
+        for (int pe = 0; pe < NPE; ++pe) mv[pe] = pos < nFp ? __ldg(mP + (int64_t)pe * nFp + pos) : 0.0;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tc_fence_after();
+        const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + NPOLY * kTcAbytes;
+        const uint32_t b_hi = smem_u32(bh), b_lo = smem_u32(bl);
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) {
+          const uint32_t dcol = tm + s * 256 + k * kTcN;
+#pragma unroll
+          for (int kk = 0; kk < NPE / 8; ++kk) {
+            const uint32_t ko = kk * 2 * kTcLBO;
+            const uint32_t ah = a_hi + k * kTcAbytes + ko, al = a_lo + k * kTcAbytes + ko;
+            umma_tf32(dcol, umma_sdesc(ah, kTcLBO, kTcSBO), umma_sdesc(b_hi + ko, kTcLBO, kTcSBO), idesc, kk > 0);
+            umma_tf32(dcol, umma_sdesc(ah, kTcLBO, kTcSBO), umma_sdesc(b_lo + ko, kTcLBO, kTcSBO), idesc, 1);
+            umma_tf32(dcol, umma_sdesc(al, kTcLBO, kTcSBO), umma_sdesc(b_hi + ko, kTcLBO, kTcSBO), idesc, 1);
+          }
+        }
+        umma_commit(full0 + 8 * s);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- screening warps ----------------------------------------------------------------------
+    const int wg = wid >> 2, b = wg >> 1, half = wg & 1;
+    const int t = (wid & 3) * 32 + lane;  // TMEM lane = tuple
+    const bool tok = t < tmax;
+    const int32_t *Dt = sDv + t * kMaxVars;
+    const int64_t D1sq = (int64_t)Dt[0] * Dt[0];
+    const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
+    const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
+    const EConst32 kc32 = to_econst32(make_econst(pg));
+    float cn[NPOLY];
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k) cn[k] = sCn[t * 6 + k];
+    float ck[kTcKC];
+    int cp[kTcKC];
+#pragma unroll
+    for (int i = 0; i < kTcKC; ++i) {
+      ck[i] = __int_as_float(0x7f800000);
+      cp[i] = 0x7fffffff;
+    }
+    float tnl = __int_as_float(0x7f800000);  // smallest lower bound not kept
+    float ub = __int_as_float(0x7f800000);   // smallest upper bound E32 (1 + eta) of a trusted pair
+    bool ovf = false;                        // an untrusted pair fell off the list
+    const uint32_t tl = tm + ((uint32_t)((wid & 3) * 32) << 16);
+    constexpr float u = 5.9604645e-8f;  // 2^-24
+    for (int i = b; i < nEff; i += 2) {
+      mbar_wait(full0 + 8 * b, (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int col = half * 16 + c * 8;
+        float pv[NPOLY][8];
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) tmem_ld8(tl + b * 256 + k * kTcN + col, pv[k]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int pos = i * kTcN + col + v;
+          const CfgRec *cr = rec + (pos < nFp ? pos : nFp - 1);
+          const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
+          const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
+          const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
+          const int2 h3 = __ldg(reinterpret_cast<const int2 *>(cr) + 7);  // W32, rB32
+          const bool ok = tok && pos < nFc && h0.x <= D1sq;               // a3
+          const uint32_t s012 = (uint32_t)h2.y;
+          // a6 (as k_sweep): 32-bit factors, the 64-bit product only where needed
+          const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, (int32_t)(h0.y >> 32), (uint32_t)h1.z, s012 & 255) : 1u;
+          const uint32_t f1 = map1 >= 0 ? ceil_div32(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) : 1u;
+          int64_t blocks = (int64_t)((uint64_t)f0 * f1);
+          if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+          const int smact = (int)(blocks < n_sm ? blocks : n_sm);
+          const float rSMf = sRSM32[smact];
+          const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
+          const float mn = sMn[b * kTcN + col + v];
+          float rho = 0.f;
+#pragma unroll
+          for (int k = 0; k < NPOLY; ++k) rho = fmaxf(rho, cn[k] * mn * rcp32(fabsf(pv[k][v])));
+          const float eps = 64.f * u * 1.001f * rho;
+          const float tol = 2.2f * (6.f * eps + 25.f * u) + 1e-6f;
+          bool unc;
+          const float E32 = mwpcwp_E32(pv[0][v], pv[1][v], pv[2][v], pv[3][v], pv[4][v], pv[5][v],
+                                       __int_as_float(h3.x), Rep, rSMf, (float)smact, kc32, unc, tol);
+          const float eta = 1.1f * (18.f * eps + 80.f * u) + 1e-6f;
+          unc = unc | !(rho <= 64.f);
+          ub = (ok && !unc) ? fminf(ub, E32 * (1.0f + eta)) : ub;
+          float key = ok ? (unc ? -1.0f : E32 * (1.0f - eta)) : __int_as_float(0x7f800000);
+          int q = pos;
+#pragma unroll
+          for (int j = 0; j < kTcKC; ++j) {  // positions grow along the stream: ties keep the earlier
+            const bool lt = key < ck[j];
+            const float tk = ck[j];
+            const int tq = cp[j];
+            ck[j] = lt ? key : tk;
+            cp[j] = lt ? q : tq;
+            key = lt ? tk : key;
+            q = lt ? tq : q;
+          }
+          ovf = ovf | (key < 0.f);
+          tnl = fminf(tnl, key);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * b);
+    }
+    // ---- exact re-evaluation of the kept candidates --------------------------------------------
+    *reinterpret_cast<float *>(sPart + (wg * kTcM + t) * 24 + 20) = ub;
+    asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");  // every MMA consumed: A space free
+    stage_C(false, kTcEpi / 32);
+    asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");
+    // only candidates whose lower bound reaches the tuple's smallest upper bound can win
+    float ubt = ub;
+#pragma unroll
+    for (int w2 = 0; w2 < 4; ++w2) ubt = fminf(ubt, *reinterpret_cast<const float *>(sPart + (w2 * kTcM + t) * 24 + 20));
+    const EConst kc = make_econst(pg);
+    auto pair_E64 = [&](int tt, int pos, const double *pk, int32_t &orig) -> double {
+      const int32_t *Dq = sDv + tt * kMaxVars;
+      const int64_t D1q = (int64_t)Dq[0] * Dq[0];
+      const int32_t qa = map0 >= 0 ? Dq[map0] : 1, qb = map1 >= 0 ? Dq[map1] : 1, qc = map2 >= 0 ? Dq[map2] : 1;
+      const CfgRec *cr = rec + pos;
+      const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
+      const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
+      const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
+      const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);
+      orig = (int32_t)(h0.y & 0xffffffff);
+      const bool ok = tt < tmax && pos < nFc && h0.x <= D1q;  // a3
+      const uint32_t s012 = (uint32_t)h2.y;
+      const int64_t blocks = ceil_div_magic(qa, (int32_t)(h0.y >> 32), (uint32_t)h1.z, s012 & 255) *
+                             ceil_div_magic(qb, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) *
+                             ceil_div_magic(qc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+      const int64_t smact = blocks < n_sm ? blocks : n_sm;
+      const double rSM = __ldg(gRSM + smact);
+      const double Rep = (double)blocks * h3.x * rSM;  // line 15
+      const double E = mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], __hiloint2double(h2.w, h2.z), Rep, rSM,
+                                (double)smact, kc);
+      return (ok && pos_finite(E)) ? E : kInf;  // line 19, R17
+    };
+    auto exact_pk = [&](int tt, int pos, double (&pk)[NPOLY]) {
+      double mvv[NPE];
+#pragma unroll
+      for (int pe = 0; pe < NPE; ++pe) mvv[pe] = __ldg(mP + (int64_t)pe * nFp + pos);
+      const double *crow = sCd + tt * 96;
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int pe = 0; pe < NPE; ++pe) sacc = fma(crow[k * NPE + pe], mvv[pe], sacc);
+        pk[k] = sacc;
+      }
+    };
+    auto take = [](Best &bb, double E, int32_t orig) {  // a8: exact key (E, original index)
+      const long long eb = __double_as_longlong(E), sb = __double_as_longlong(bb.e);
+      const bool better = eb < sb || (eb == sb && orig < bb.i);
+      bb.i = better ? orig : bb.i;
+      bb.e = better ? E : bb.e;
+    };
+    Best st;
+    st.e = kInf;
+    st.i = 0x7fffffff;
+    st.s = kInf;
+#pragma unroll 1
+    for (int j = 0; j < kTcKC; ++j) {
+      if (cp[j] != 0x7fffffff && !(ck[j] > ubt)) {
+        double pk[NPOLY];
+        exact_pk(t, cp[j], pk);
+        int32_t orig;
+        const double E = pair_E64(t, cp[j], pk, orig);
+        take(st, E, orig);
+      }
+    }
+    unsigned char *pp = sPart + (wg * kTcM + t) * 24;
+    *reinterpret_cast<double *>(pp) = st.e;
+    *reinterpret_cast<int32_t *>(pp + 8) = st.i;
+    *reinterpret_cast<float *>(pp + 12) = tnl;
+    *reinterpret_cast<int32_t *>(pp + 16) = ovf ? 1 : 0;
+    asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");
+    if (wg == 0 && tok) {
+      for (int w2 = 1; w2 < 4; ++w2) {
+        const unsigned char *qq = sPart + (w2 * kTcM + t) * 24;
+        take(st, *reinterpret_cast<const double *>(qq), *reinterpret_cast<const int32_t *>(qq + 8));
+        tnl = fminf(tnl, *reinterpret_cast<const float *>(qq + 12));
+        ovf = ovf || *reinterpret_cast<const int32_t *>(qq + 16) != 0;
+      }
+      // exact unless a dropped pair's lower bound reaches the winner (E > lower bound > winner)
+      const bool fb = ovf || (tnl < __int_as_float(0x7f800000) && !((double)tnl > st.e));
+      if (fb) {
+        sFb[1 + atomicAdd(&sFb[0], 1)] = t;
+      } else {
+        const int64_t o = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t);
+        a.idx[o] = (st.e < kInf) ? st.i : -1;
+        a.bestE[o] = st.e;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");
+    // ---- rare: a flagged tuple re-swept exactly in FP64 by one warp (lanes over configurations)
+    const int nfb = sFb[0];
+    if (tid == 0 && nfb > 0) atomicAdd(&g_tc_stats[0], (unsigned long long)nfb);
+    if (tid == 0) atomicAdd(&g_tc_stats[1], (unsigned long long)tmax);
+    for (int f = wid; f < nfb; f += kTcEpi / 32) {
+      const int tt = sFb[1 + f];
+      Best sf;
+      sf.e = kInf;
+      sf.i = 0x7fffffff;
+      sf.s = kInf;
+      for (int pos = lane; pos < nEff * kTcN && pos < nFc; pos += 32) {
+        double pk[NPOLY];
+        exact_pk(tt, pos, pk);
+        int32_t orig;
+        const double E = pair_E64(tt, pos, pk, orig);
+        take(sf, E, orig);
+      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) sf = merge(sf, shfl_xor(sf, m));
+      if (lane == 0) {
+        const int64_t o = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + tt] : d0 + tt);
+        a.idx[o] = (sf.e < kInf) ? sf.i : -1;
+        a.bestE[o] = sf.e;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 16) {
+    tc_fence_after();
+    tmem_dealloc(tm, 512);
+  }
+}
+
+static cudaError_t launch_tc(const SweepArgs &a, int n_prog, cudaStream_t s) {
+  const int64_t tiles = (a.nD + kTcM - 1) / kTcM;
+  if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+  if (e != cudaSuccess) return e;
+  k_sweep_tc<<<dim3((unsigned)tiles, (unsigned)n_prog), kTcThreads, kTcSmem, s>>>(a);
+  e = cudaGetLastError();
+  if (e == cudaSuccess && getenv("RP_SWEEP_TC_STATS")) {
+    unsigned long long st[2];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(st, g_tc_stats, sizeof(st));
+    fprintf(stderr, "[k_sweep_tc] tuples re-swept in FP64: %llu of %llu\n", st[0], st[1]);
+    const unsigned long long z[2] = {0ull, 0ull};
+    cudaMemcpyToSymbol(g_tc_stats, z, sizeof(z));
+  }
+  return e;
+}
+
 template <int NPE, bool SECOND>
 static cudaError_t launch_ws(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
   const size_t smem = sweep_ws_smem_bytes<6, NPE>(a.nde_stride, n_sm_max);
@@ -950,6 +1410,8 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
   // RP_SWEEP_KERNEL=ws: the warp-specialised screened sweep (MWP-CWP programs; parity-tested, not
   // yet faster: DESIGN.md "Warp-specialised screened sweep"); default: k_sweep
   const char *kern = getenv("RP_SWEEP_KERNEL");
+  if (NPE == kTcNPE && mwp && !second && kern && strcmp(kern, "tc") == 0 && a.tab.nde_pad <= kTcMaxNdp)
+    return launch_tc(a, n_prog, s);
   if (mwp && kern && strcmp(kern, "ws") == 0)
     return second ? launch_ws<NPE, true>(a, n_prog, n_sm_max, s) : launch_ws<NPE, false>(a, n_prog, n_sm_max, s);
   if (mwp)

@@ -395,6 +395,36 @@ def test_sweep_warp_specialised_screen(second, monkeypatch):
                 np.asarray(S.cpu())[sel] if second else None, ref, spec, case.D[sel], case.F, tag="large")
 
 
+def test_sweep_tensor_core_screen(monkeypatch):
+    """RP_SWEEP_KERNEL=tc: the tcgen05 screened sweep (split-tf32 contraction in TMEM, FP32 screen
+    with a per-pair bound, FP64 for the candidates, FP64 re-sweep of flagged tuples) under the
+    default kernel's gates on tiny, polybench and a `large` subsample; and at the bench's full
+    `large` launch, winners identical to the default kernel's."""
+    monkeypatch.setenv("RP_SWEEP_KERNEL", "tc")
+    for case in (synth.tiny_sweep(), synth.polybench_sweep(nD=2000)):
+        idx, E, _ = rp.eval_argmin_batched(case.programs, _cuda(case.D), _cuda(case.F), second=False)
+        for g, spec in enumerate(case.programs):
+            ref = oracle.sweep(spec, case.D, case.F)
+            check_sweep(idx[g], E[g], None, ref, spec, case.D, case.F, tag=case.name)
+    case = synth.large_sweep(nD=1_000_000)
+    spec = case.programs[0]
+    sel = synth.large_subsample_index(1_000_000, every=500)
+    plan = rp.Plan([spec], _cuda(case.F))
+    D = _cuda(case.D)
+    idx, E, _ = plan.eval(D, second=False)
+    ref = oracle.sweep(spec, case.D[sel], case.F)
+    check_sweep(np.asarray(idx.cpu()).ravel()[sel], np.asarray(E.cpu()).ravel()[sel], None, ref, spec,
+                case.D[sel], case.F, tag="large")
+    monkeypatch.delenv("RP_SWEEP_KERNEL")
+    idx0, E0, _ = plan.eval(D, second=False)
+    plan.close()
+    assert torch.equal(idx.cpu(), idx0.cpu())
+    fin = torch.isfinite(E0)
+    assert torch.equal(fin, torch.isfinite(E))
+    rel = ((E - E0).abs()[fin] / E0[fin]).max().item() if bool(fin.any()) else 0.0
+    assert rel <= 1e-12, rel
+
+
 @pytest.mark.parametrize("shape", ["p1_d1_deg3", "p2_d3_deg2", "p3_d1_deg4"])
 def test_sweep_other_program_shapes(shape):
     """Program shapes the BASELINE configs do not use: one program variable (a 1-D block, grid
