@@ -945,7 +945,13 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_sweep_ws(SweepArgs a) {
 // (6 for every compared quantity), hence |E32 - E| <= 1.1 (18 eps + 80 u) E + 1e-6 E.
 // ============================================================================================
 constexpr int kTcM = 128;           // tuples per CTA (TMEM lanes)
-constexpr int kTcN = 32;            // configurations per MMA tile
+#ifndef RP_TC_N
+#define RP_TC_N 32
+#endif
+constexpr int kTcN = RP_TC_N;       // configurations per MMA tile (32: 2 TMEM buffers, 16: 4)
+constexpr int kTcNB = kTcN == 32 ? 2 : 4;  // TMEM buffers = B ring slots
+constexpr int kTcColStride = 512 / kTcNB;  // TMEM columns per buffer (6 kTcN used)
+constexpr int kTcWGB = 4 / kTcNB;          // warpgroups per buffer (16 configurations each)
 constexpr int kTcNPE = 16;          // MMA K (program-part monomials, padded)
 constexpr int kTcKC = 4;            // kept candidates per screening thread
 constexpr int kTcEpi = 512;         // screening threads (4 warpgroups)
@@ -957,15 +963,15 @@ constexpr int kTcMaxNdp = 32;
 // shared-memory map (bytes)
 constexpr uint32_t kTcOffA = 0;                                   // [2 splits][6 polys] A operands; later FP64 C [128][96]
 constexpr uint32_t kTcOffB = kTcOffA + 12 * kTcAbytes;            // [2 slots][2 splits] B operands
-constexpr uint32_t kTcOffMn = kTcOffB + 4 * kTcBbytes;            // [2 slots][32] ||m(P)||
-constexpr uint32_t kTcOffMD = kTcOffMn + 2 * kTcN * 4;            // [128][ndp <= 32] data monomials (FP64)
+constexpr uint32_t kTcOffMn = kTcOffB + 2 * kTcNB * kTcBbytes;    // [slots][kTcN] ||m(P)||
+constexpr uint32_t kTcOffMD = kTcOffMn + kTcNB * kTcN * 4;           // [128][ndp <= 32] data monomials (FP64)
 constexpr uint32_t kTcOffRSM = kTcOffMD + kTcM * kTcMaxNdp * 8;   // [kRSMTab] 1/SM_act (FP32)
 constexpr uint32_t kTcOffDv = kTcOffRSM + kRSMTab * 4;            // [128][kMaxVars] D values
 constexpr uint32_t kTcOffCn = kTcOffDv + kTcM * kMaxVars * 4;     // [128][6] ||C_k(D)||
 constexpr uint32_t kTcOffPart = kTcOffCn + kTcM * 6 * 4;          // [4][128] {e, i, tnl, ovf}
 constexpr uint32_t kTcOffFb = kTcOffPart + 4 * kTcM * 24;         // [128] fallback tuples + count
 constexpr uint32_t kTcOffBar = (kTcOffFb + (kTcM + 2) * 4 + 7) & ~7u;  // full[2], empty[2], tmem base, maxD1sq
-constexpr uint32_t kTcSmem = kTcOffBar + 64;
+constexpr uint32_t kTcSmem = kTcOffBar + 128;
 static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared memory");
 static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
 
@@ -990,18 +996,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   float *sCn = reinterpret_cast<float *>(sm + kTcOffCn);
   unsigned char *sPart = sm + kTcOffPart;
   int32_t *sFb = reinterpret_cast<int32_t *>(sm + kTcOffFb);  // [0]: count, [1..]: tuples
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kTcOffBar);  // full[0..1], empty[0..1]
-  uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 4);
-  unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 5);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kTcOffBar);  // full[kTcNB], empty[kTcNB]
+  uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 2 * kTcNB);
+  unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 2 * kTcNB + 1);
   double *sCd = reinterpret_cast<double *>(sm + kTcOffA);  // FP64 C [128][96] after the sweep
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
   const int nDE = pg.nDE, ndp = a.tab.nde_pad;
   const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
 
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(bars + i), 1);      // full: the MMA commit
-      mbar_init(smem_u32(bars + 2 + i), 8);  // empty: the 8 warps screening buffer i
+    for (int i = 0; i < kTcNB; ++i) {
+      mbar_init(smem_u32(bars + i), 1);                  // full: the MMA commit
+      mbar_init(smem_u32(bars + kTcNB + i), 4 * kTcWGB);  // empty: the warps screening buffer i
     }
     sFb[0] = 0;
     *sMaxD1 = 0ull;
@@ -1105,19 +1111,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     }
   }
   const uint32_t tm = *sTmem;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 2);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcNB);
 
   if (wid == 16) {
     // ---- producer / MMA warp ------------------------------------------------------------------
     const uint32_t idesc = umma_idesc_tf32(kTcM, kTcN);
     double mv[NPE];
 #pragma unroll
-    for (int pe = 0; pe < NPE; ++pe) mv[pe] = (nEff > 0 && lane < nFp) ? __ldg(mP + (int64_t)pe * nFp + lane) : 0.0;
+    for (int pe = 0; pe < NPE; ++pe)
+      mv[pe] = (nEff > 0 && lane < kTcN && lane < nFp) ? __ldg(mP + (int64_t)pe * nFp + lane) : 0.0;
     for (int i = 0; i < nEff; ++i) {
-      const int s = i & 1, use = i >> 1;
+      const int s = i % kTcNB, use = i / kTcNB;
       if (use > 0) mbar_wait(empty0 + 8 * s, (use - 1) & 1);
       unsigned char *bh = sB + (2 * s) * kTcBbytes, *bl = bh + kTcBbytes;
       double mn2 = 0.0;
+      if (lane < kTcN)
 #pragma unroll
       for (int pe = 0; pe < NPE; ++pe) {
         const double m = mv[pe];
@@ -1127,11 +1135,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
         *reinterpret_cast<float *>(bl + o) = lo;
         mn2 = fma(m, m, mn2);
       }
-      sMn[s * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
+      if (lane < kTcN) sMn[s * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
       if (i + 1 < nEff) {
         const int pos = (i + 1) * kTcN + lane;
 #pragma unroll
-        for (int pe = 0; pe < NPE; ++pe) mv[pe] = pos < nFp ? __ldg(mP + (int64_t)pe * nFp + pos) : 0.0;
+        for (int pe = 0; pe < NPE; ++pe) mv[pe] = (lane < kTcN && pos < nFp) ? __ldg(mP + (int64_t)pe * nFp + pos) : 0.0;
       }
       fence_async_smem();
       __syncwarp();
@@ -1141,7 +1149,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
         const uint32_t b_hi = smem_u32(bh), b_lo = smem_u32(bl);
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) {
-          const uint32_t dcol = tm + s * 256 + k * kTcN;
+          const uint32_t dcol = tm + s * kTcColStride + k * kTcN;
 #pragma unroll
           for (int kk = 0; kk < NPE / 8; ++kk) {
             const uint32_t ko = kk * 2 * kTcLBO;
@@ -1157,7 +1165,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     }
   } else {
     // ---- screening warps ----------------------------------------------------------------------
-    const int wg = wid >> 2, b = wg >> 1, half = wg & 1;
+    const int wg = wid >> 2, b = wg / kTcWGB, half = wg % kTcWGB;
     const int t = (wid & 3) * 32 + lane;  // TMEM lane = tuple
     const bool tok = t < tmax;
     const int32_t *Dt = sDv + t * kMaxVars;
@@ -1180,15 +1188,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     bool ovf = false;                        // an untrusted pair fell off the list
     const uint32_t tl = tm + ((uint32_t)((wid & 3) * 32) << 16);
     constexpr float u = 5.9604645e-8f;  // 2^-24
-    for (int i = b; i < nEff; i += 2) {
-      mbar_wait(full0 + 8 * b, (i >> 1) & 1);
+    for (int i = b; i < nEff; i += kTcNB) {
+      mbar_wait(full0 + 8 * b, (i / kTcNB) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         const int col = half * 16 + c * 8;
         float pv[NPOLY][8];
 #pragma unroll
-        for (int k = 0; k < NPOLY; ++k) tmem_ld8(tl + b * 256 + k * kTcN + col, pv[k]);
+        for (int k = 0; k < NPOLY; ++k) tmem_ld8(tl + b * kTcColStride + k * kTcN + col, pv[k]);
         tmem_ld_wait();
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
