@@ -945,13 +945,10 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_sweep_ws(SweepArgs a) {
 // (6 for every compared quantity), hence |E32 - E| <= 1.1 (18 eps + 80 u) E + 1e-6 E.
 // ============================================================================================
 constexpr int kTcM = 128;           // tuples per CTA (TMEM lanes)
-#ifndef RP_TC_N
-#define RP_TC_N 32
-#endif
-constexpr int kTcN = RP_TC_N;       // configurations per MMA tile (32: 2 TMEM buffers, 16: 4)
-constexpr int kTcNB = kTcN == 32 ? 2 : 4;  // TMEM buffers = B ring slots
-constexpr int kTcColStride = 512 / kTcNB;  // TMEM columns per buffer (6 kTcN used)
-constexpr int kTcWGB = 4 / kTcNB;          // warpgroups per buffer (16 configurations each)
+constexpr int kTcN = 32;            // configurations per MMA tile (8 per screening warpgroup)
+constexpr int kTcNB = 2;            // TMEM buffers = B operand ring slots
+constexpr int kTcNR = 4;            // ring slots of the tile's records and ||m||
+constexpr int kTcColStride = 256;   // TMEM columns per buffer (6 kTcN used)
 constexpr int kTcNPE = 16;          // MMA K (program-part monomials, padded)
 constexpr int kTcKC = 4;            // kept candidates per screening thread
 constexpr int kTcEpi = 512;         // screening threads (4 warpgroups)
@@ -964,14 +961,15 @@ constexpr int kTcMaxNdp = 32;
 constexpr uint32_t kTcOffA = 0;                                   // [2 splits][6 polys] A operands; later FP64 C [128][96]
 constexpr uint32_t kTcOffB = kTcOffA + 12 * kTcAbytes;            // [2 slots][2 splits] B operands
 constexpr uint32_t kTcOffMn = kTcOffB + 2 * kTcNB * kTcBbytes;    // [slots][kTcN] ||m(P)||
-constexpr uint32_t kTcOffMD = kTcOffMn + kTcNB * kTcN * 4;           // [128][ndp <= 32] data monomials (FP64)
+constexpr uint32_t kTcOffMD = kTcOffMn + kTcNR * kTcN * 4;           // [128][ndp <= 32] data monomials (FP64)
 constexpr uint32_t kTcOffRSM = kTcOffMD + kTcM * kTcMaxNdp * 8;   // [kRSMTab] 1/SM_act (FP32)
 constexpr uint32_t kTcOffDv = kTcOffRSM + kRSMTab * 4;            // [128][kMaxVars] D values
 constexpr uint32_t kTcOffCn = kTcOffDv + kTcM * kMaxVars * 4;     // [128][6] ||C_k(D)||
 constexpr uint32_t kTcOffPart = kTcOffCn + kTcM * 6 * 4;          // [4][128] {e, i, tnl, ovf}
 constexpr uint32_t kTcOffFb = kTcOffPart + 4 * kTcM * 24;         // [128] fallback tuples + count
 constexpr uint32_t kTcOffBar = (kTcOffFb + (kTcM + 2) * 4 + 7) & ~7u;  // full[2], empty[2], tmem base, maxD1sq
-constexpr uint32_t kTcSmem = kTcOffBar + 128;
+constexpr uint32_t kTcOffRec = (kTcOffBar + 128 + 15) & ~15u;                // [slots][kTcN] CfgRec of the tile
+constexpr uint32_t kTcSmem = kTcOffRec + kTcNR * kTcN * 64;
 static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared memory");
 static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
 
@@ -999,6 +997,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kTcOffBar);  // full[kTcNB], empty[kTcNB]
   uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 2 * kTcNB);
   unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 2 * kTcNB + 1);
+  int4 *sRec = reinterpret_cast<int4 *>(sm + kTcOffRec);  // [slots][kTcN][4]
   double *sCd = reinterpret_cast<double *>(sm + kTcOffA);  // FP64 C [128][96] after the sweep
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
   const int nDE = pg.nDE, ndp = a.tab.nde_pad;
@@ -1007,7 +1006,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   if (tid == 0) {
     for (int i = 0; i < kTcNB; ++i) {
       mbar_init(smem_u32(bars + i), 1);                  // full: the MMA commit
-      mbar_init(smem_u32(bars + kTcNB + i), 4 * kTcWGB);  // empty: the warps screening buffer i
+      mbar_init(smem_u32(bars + kTcNB + i), kTcEpi / 32);  // empty: every screening warp copied it out
     }
     sFb[0] = 0;
     *sMaxD1 = 0ull;
@@ -1135,7 +1134,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
         *reinterpret_cast<float *>(bl + o) = lo;
         mn2 = fma(m, m, mn2);
       }
-      if (lane < kTcN) sMn[s * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
+      if (lane < kTcN) {
+        // ring of kTcNR: slot i % 4 was last read for tile i - 4, finished by every warp before its
+        // empty arrival for tile i - 2 (waited above)
+        const int r = i % kTcNR;
+        sMn[r * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
+        // the tile's configuration records, read by every screening warp (shared-memory broadcast)
+        const int pos = i * kTcN + lane;
+        const int4 *src = reinterpret_cast<const int4 *>(rec + (pos < nFp ? pos : nFp - 1));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sRec[(r * kTcN + lane) * 4 + j] = __ldg(src + j);
+      }
       if (i + 1 < nEff) {
         const int pos = (i + 1) * kTcN + lane;
 #pragma unroll
@@ -1165,7 +1174,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     }
   } else {
     // ---- screening warps ----------------------------------------------------------------------
-    const int wg = wid >> 2, b = wg / kTcWGB, half = wg % kTcWGB;
+    const int wg = wid >> 2;  // configurations 8 wg .. 8 wg + 7 of every tile
     const int t = (wid & 3) * 32 + lane;  // TMEM lane = tuple
     const bool tok = t < tmax;
     const int32_t *Dt = sDv + t * kMaxVars;
@@ -1188,24 +1197,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     bool ovf = false;                        // an untrusted pair fell off the list
     const uint32_t tl = tm + ((uint32_t)((wid & 3) * 32) << 16);
     constexpr float u = 5.9604645e-8f;  // 2^-24
-    for (int i = b; i < nEff; i += kTcNB) {
+    for (int i = 0; i < nEff; ++i) {
+      const int b = i % kTcNB, r = i % kTcNR;
       mbar_wait(full0 + 8 * b, (i / kTcNB) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        const int col = half * 16 + c * 8;
+      {
+        const int col = wg * 8;
         float pv[NPOLY][8];
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) tmem_ld8(tl + b * kTcColStride + k * kTcN + col, pv[k]);
         tmem_ld_wait();
+        // the buffer is free for the MMAs of tile i + 2 as soon as every warp holds its values
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * b);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const int pos = i * kTcN + col + v;
-          const CfgRec *cr = rec + (pos < nFp ? pos : nFp - 1);
-          const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
-          const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
-          const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
-          const int2 h3 = __ldg(reinterpret_cast<const int2 *>(cr) + 7);  // W32, rB32
+          const int4 *cr = sRec + (r * kTcN + col + v) * 4;
+          const int4 r0 = cr[0];
+          const longlong2 h0 = make_longlong2(((long long)(uint32_t)r0.y << 32) | (uint32_t)r0.x,
+                                              ((long long)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
+          const int4 h1 = cr[1];
+          const int4 h2 = cr[2];
+          const int4 r3 = cr[3];
+          const int2 h3 = make_int2(r3.z, r3.w);  // W32, rB32
           const bool ok = tok && pos < nFc && h0.x <= D1sq;               // a3
           const uint32_t s012 = (uint32_t)h2.y;
           // a6 (as k_sweep): 32-bit factors, the 64-bit product only where needed
@@ -1216,7 +1232,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           const int smact = (int)(blocks < n_sm ? blocks : n_sm);
           const float rSMf = sRSM32[smact];
           const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
-          const float mn = sMn[b * kTcN + col + v];
+          const float mn = sMn[r * kTcN + col + v];
           float rho = 0.f;
 #pragma unroll
           for (int k = 0; k < NPOLY; ++k) rho = fmaxf(rho, cn[k] * mn * rcp32(fabsf(pv[k][v])));
@@ -1244,9 +1260,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           tnl = fminf(tnl, key);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * b);
     }
     // ---- exact re-evaluation of the kept candidates --------------------------------------------
     *reinterpret_cast<float *>(sPart + (wg * kTcM + t) * 24 + 20) = ub;
