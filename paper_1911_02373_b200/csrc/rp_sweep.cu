@@ -974,6 +974,10 @@ static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared mem
 static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
 
 __device__ unsigned long long g_tc_stats[2];  // [0] tuples re-swept in FP64, [1] tuples
+// FP64 staged C of the CTA's tuples for the exact re-evaluation, one slot per SM (the kernel's
+// shared memory admits one CTA per SM, so a slot has one owner at a time; 14.7 MB, L2-resident)
+constexpr int kTcMaxSM = 160;
+__device__ double g_tc_C[kTcMaxSM][kTcM * 96];
 
 __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   constexpr int NPOLY = 6, NPE = kTcNPE;
@@ -998,7 +1002,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 2 * kTcNB);
   unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 2 * kTcNB + 1);
   int4 *sRec = reinterpret_cast<int4 *>(sm + kTcOffRec);  // [slots][kTcN][4]
-  double *sCd = reinterpret_cast<double *>(sm + kTcOffA);  // FP64 C [128][96] after the sweep
+  uint32_t smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  double *gCd = g_tc_C[smid % kTcMaxSM];  // FP64 C [128][96] of this CTA's tuples
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
   const int nDE = pg.nDE, ndp = a.tab.nde_pad;
   const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
@@ -1044,7 +1050,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   // plan's coefficient matrix and the tile's data monomials on DMMA.8x8x4 (8x8 output tiles spread
   // over the warps, as in k_sweep).  to_ops: stored as tf32 splits in the A operands, with
   // ||C_k(D)||_2^2 summed into sNrm (shared FP64 atomics: two addends onto 0, order-independent);
-  // else stored as FP64 rows sCd[t][96] for the exact re-evaluation.
+  // the FP64 rows also go to gCd[t][96] for the exact re-evaluation.
   double *sNrm = reinterpret_cast<double *>(sPart);  // [128][6], before the merge needs sPart
   auto stage_C = [&](bool to_ops, int nwarps) {
     constexpr int MT = NPOLY * NPE / 8, NT = kTcM / 8;
@@ -1058,6 +1064,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
       }
       const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
       const int k = row / NPE, pe = row % NPE;
+      gCd[t * 96 + row] = c0;
+      gCd[(t + 1) * 96 + row] = c1;
       if (to_ops) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -1077,9 +1085,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           atomicAdd(&sNrm[t * 6 + k], q0);
           atomicAdd(&sNrm[(t + 1) * 6 + k], q1);
         }
-      } else {
-        sCd[t * 96 + row] = c0;
-        sCd[(t + 1) * 96 + row] = c1;
       }
     }
   };
@@ -1211,6 +1216,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * b);
+#ifdef RP_TC_SKEL  // timing experiment: the pipeline without the screen
+        {
+          float acc = 0.f;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+#pragma unroll
+            for (int k = 0; k < NPOLY; ++k) acc += pv[k][v];
+          tnl = fminf(tnl, acc > 1e30f ? acc : __int_as_float(0x7f800000));
+          continue;
+        }
+#endif
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const int pos = i * kTcN + col + v;
@@ -1264,7 +1280,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     // ---- exact re-evaluation of the kept candidates --------------------------------------------
     *reinterpret_cast<float *>(sPart + (wg * kTcM + t) * 24 + 20) = ub;
     asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");  // every MMA consumed: A space free
-    stage_C(false, kTcEpi / 32);
     asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");
     // only candidates whose lower bound reaches the tuple's smallest upper bound can win
     float ubt = ub;
@@ -1297,7 +1312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
       double mvv[NPE];
 #pragma unroll
       for (int pe = 0; pe < NPE; ++pe) mvv[pe] = __ldg(mP + (int64_t)pe * nFp + pos);
-      const double *crow = sCd + tt * 96;
+      const double *crow = gCd + tt * 96;
 #pragma unroll
       for (int k = 0; k < NPOLY; ++k) {
         double sacc = 0.0;
