@@ -534,3 +534,32 @@ def test_gram_randomised_bases(seed):
         Go = np.asarray(oracle.gram(X, V[i], num, den, c, e), dtype=np.float64)
         dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
         assert np.max(np.abs(G[i] - Go) / dg) <= 1e-12, (seed, n, len(num), len(den), K, i)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fit_randomised(seed):
+    """Randomised fits: class-F truths with random data / program dimensions (d, p in 1..2), total
+    degree 1..3, box, K (from 3 n_c to 20,000) and noise (0 or 1%); the GPU fit of all l metrics
+    (symmetric-block Gram, equilibrated Cholesky + refinement) against the oracle's
+    (long double Gauss with partial pivoting): same transform, coefficients within 1e-9."""
+    g = np.random.default_rng(9100 + seed)
+    d, p, deg = int(g.integers(1, 3)), int(g.integers(1, 3)), int(g.integers(1, 4))
+    lo = [int(g.choice([1, 8, 32]))] * d + [1] * p
+    hi = [int(g.choice([2048, 16384]))] * d + [int(g.choice([64, 1024]))] * p
+    spec = synth.classf_program(f"fitrand{seed}", d, p, deg, lo, hi, synth.HW_GTX1080TI, R=32, Z0=0, Z1=0,
+                                grid_map=tuple([0] * p + [-1] * (3 - p)), stream=f"f{seed}")
+    n_c = 2 * len(spec.num_exp[0])
+    K = int(g.integers(3 * n_c, 20_000))
+    X = synth.box_random_design(g, lo, hi, K)
+    sigma = float(g.choice([0.0, 0.01]))
+    V = np.stack([np.asarray(v, dtype=np.float64) for v in oracle.program_metrics(spec, X)])
+    if sigma:
+        V = V * np.stack([synth.noise_multipliers(g, K, sigma) for _ in range(len(V))])
+    num = den = spec.num_exp[0]
+    coef, (c, e), _ = rp.fit(_cuda(X), _cuda(V), num, den)
+    for i in range(len(V)):
+        r = oracle.fit(X, V[i], num, den, nthreads=8)
+        assert np.array_equal(r["c"], c) and np.array_equal(r["e"], e)
+        want = np.asarray(r["coef"], dtype=np.float64)
+        err = np.max(np.abs(coef[i] - want)) / np.max(np.abs(want))
+        assert err <= 1e-9, (seed, d, p, deg, K, sigma, i, err)
