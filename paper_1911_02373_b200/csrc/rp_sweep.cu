@@ -300,6 +300,8 @@ struct SweepArgs {
   double *bestE;
   double *secondE;
   const int32_t *perm;  // tuple order of the tiles (grouped by D1), or null: identity
+  const unsigned char *tcpack = nullptr;  // k_sweep_tc: per-tile B operands, ||m||, records
+  int tc_ntiles = 0;
 };
 
 #ifndef RP_SWEEP_MINB
@@ -970,10 +972,17 @@ constexpr uint32_t kTcOffFb = kTcOffPart + 4 * kTcM * 24;         // [128] fallb
 constexpr uint32_t kTcOffBar = (kTcOffFb + (kTcM + 2) * 4 + 7) & ~7u;  // full[2], empty[2], tmem base, maxD1sq
 constexpr uint32_t kTcOffRec = (kTcOffBar + 128 + 15) & ~15u;                // [slots][kTcN] CfgRec of the tile
 constexpr uint32_t kTcSmem = kTcOffRec + kTcNR * kTcN * 64;
+// per-tile pack built once per launch by k_tc_pack (the tile's B operands in their shared-memory
+// layout, ||m(P)|| and records), moved by three bulk copies per tile
+constexpr uint32_t kTcPackB = 2 * kTcBbytes, kTcPackMn = kTcN * 4, kTcPackRec = kTcN * 64;
+constexpr uint32_t kTcPack = kTcPackB + kTcPackMn + kTcPackRec;  // 6272 B
 static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared memory");
 static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
 
-__device__ unsigned long long g_tc_stats[2];  // [0] tuples re-swept in FP64, [1] tuples
+__device__ unsigned long long g_tc_stats[2];
+#ifdef RP_TC_TRACE  // timeline of CTA 0: [tile][0..3] = producer empty-wait done, copy landed, committed; screen start (warp 0)
+__device__ long long g_tc_trace[64][6];
+#endif  // [0] tuples re-swept in FP64, [1] tuples
 // FP64 staged C of the CTA's tuples for the exact re-evaluation, one slot per SM (the kernel's
 // shared memory admits one CTA per SM, so a slot has one owner at a time; 14.7 MB, L2-resident)
 constexpr int kTcMaxSM = 160;
@@ -999,8 +1008,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   unsigned char *sPart = sm + kTcOffPart;
   int32_t *sFb = reinterpret_cast<int32_t *>(sm + kTcOffFb);  // [0]: count, [1..]: tuples
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kTcOffBar);  // full[kTcNB], empty[kTcNB]
-  uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 2 * kTcNB);
-  unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 2 * kTcNB + 1);
+  uint32_t *sTmem = reinterpret_cast<uint32_t *>(bars + 3 * kTcNB);  // (bars + 2 kTcNB: bulk-copy barriers)
+  unsigned long long *sMaxD1 = reinterpret_cast<unsigned long long *>(bars + 3 * kTcNB + 1);
   int4 *sRec = reinterpret_cast<int4 *>(sm + kTcOffRec);  // [slots][kTcN][4]
   uint32_t smid;
   asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1013,6 +1022,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     for (int i = 0; i < kTcNB; ++i) {
       mbar_init(smem_u32(bars + i), 1);                  // full: the MMA commit
       mbar_init(smem_u32(bars + kTcNB + i), kTcEpi / 32);  // empty: every screening warp copied it out
+      mbar_init(smem_u32(bars + 2 * kTcNB + i), 1);        // the tile pack's bulk copies landed
     }
     sFb[0] = 0;
     *sMaxD1 = 0ull;
@@ -1120,47 +1130,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   if (wid == 16) {
     // ---- producer / MMA warp ------------------------------------------------------------------
     const uint32_t idesc = umma_idesc_tf32(kTcM, kTcN);
-    double mv[NPE];
-#pragma unroll
-    for (int pe = 0; pe < NPE; ++pe)
-      mv[pe] = (nEff > 0 && lane < kTcN && lane < nFp) ? __ldg(mP + (int64_t)pe * nFp + lane) : 0.0;
+    const uint32_t bfull0 = smem_u32(bars + 2 * kTcNB);
+    const unsigned char *pack = a.tcpack + (int64_t)g * a.tc_ntiles * kTcPack;
     for (int i = 0; i < nEff; ++i) {
-      const int s = i % kTcNB, use = i / kTcNB;
+      const int s = i % kTcNB, use = i / kTcNB, r = i % kTcNR;
+      // TMEM buffer s and B slot s free (every warp copied tile i - 2 out); record slot r was last
+      // read for tile i - 4, finished by every warp before its empty arrival for tile i - 2
       if (use > 0) mbar_wait(empty0 + 8 * s, (use - 1) & 1);
-      unsigned char *bh = sB + (2 * s) * kTcBbytes, *bl = bh + kTcBbytes;
-      double mn2 = 0.0;
-      if (lane < kTcN)
-#pragma unroll
-      for (int pe = 0; pe < NPE; ++pe) {
-        const double m = mv[pe];
-        const float hi = to_tf32((float)m), lo = to_tf32((float)(m - (double)hi));
-        const uint32_t o = umma_off(lane, pe, kTcLBO, kTcSBO);
-        *reinterpret_cast<float *>(bh + o) = hi;
-        *reinterpret_cast<float *>(bl + o) = lo;
-        mn2 = fma(m, m, mn2);
-      }
-      if (lane < kTcN) {
-        // ring of kTcNR: slot i % 4 was last read for tile i - 4, finished by every warp before its
-        // empty arrival for tile i - 2 (waited above)
-        const int r = i % kTcNR;
-        sMn[r * kTcN + lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
-        // the tile's configuration records, read by every screening warp (shared-memory broadcast)
-        const int pos = i * kTcN + lane;
-        const int4 *src = reinterpret_cast<const int4 *>(rec + (pos < nFp ? pos : nFp - 1));
-#pragma unroll
-        for (int j = 0; j < 4; ++j) sRec[(r * kTcN + lane) * 4 + j] = __ldg(src + j);
-      }
-      if (i + 1 < nEff) {
-        const int pos = (i + 1) * kTcN + lane;
-#pragma unroll
-        for (int pe = 0; pe < NPE; ++pe) mv[pe] = (lane < kTcN && pos < nFp) ? __ldg(mP + (int64_t)pe * nFp + pos) : 0.0;
-      }
-      fence_async_smem();
-      __syncwarp();
+#ifdef RP_TC_TRACE
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][0] = clock64();
+#endif
       if (lane == 0) {
+        const unsigned char *src = pack + (int64_t)i * kTcPack;
+        const uint32_t bar = bfull0 + 8 * s;
+        mbar_expect_tx(bar, kTcPack);
+        bulk_g2s(smem_u32(sB + 2 * s * kTcBbytes), src, kTcPackB, bar);
+        bulk_g2s(smem_u32(sMn + r * kTcN), src + kTcPackB, kTcPackMn, bar);
+        bulk_g2s(smem_u32(sRec + r * kTcN * 4), src + kTcPackB + kTcPackMn, kTcPackRec, bar);
+        mbar_wait(bar, use & 1);
+#ifdef RP_TC_TRACE
+        if (blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][1] = clock64();
+#endif
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + NPOLY * kTcAbytes;
-        const uint32_t b_hi = smem_u32(bh), b_lo = smem_u32(bl);
+        // (opaque base: keeps the loop-invariant A descriptors from being hoisted out of the tile
+        // loop as live registers)
+        uint32_t a_hi;
+        asm volatile("mov.u32 %0, %1;" : "=r"(a_hi) : "r"(smem_u32(sA)));
+        const uint32_t a_lo = a_hi + NPOLY * kTcAbytes;
+        const uint32_t b_hi = smem_u32(sB + 2 * s * kTcBbytes), b_lo = b_hi + kTcBbytes;
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) {
           const uint32_t dcol = tm + s * kTcColStride + k * kTcN;
@@ -1174,6 +1171,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           }
         }
         umma_commit(full0 + 8 * s);
+#ifdef RP_TC_TRACE
+        if (blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][2] = clock64();
+#endif
       }
       __syncwarp();
     }
@@ -1204,23 +1204,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     constexpr float u = 5.9604645e-8f;  // 2^-24
     for (int i = 0; i < nEff; ++i) {
       const int b = i % kTcNB, r = i % kTcNR;
+#ifdef RP_TC_TRACE
+      if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][3] = clock64();
+      if (tid == 480 && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][5] = clock64();
+#endif
       mbar_wait(full0 + 8 * b, (i / kTcNB) & 1);
+#ifdef RP_TC_TRACE
+      if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_tc_trace[i][4] = clock64();
+#endif
       tc_fence_after();
-      {
-        const int col = wg * 8;
-        float pv[NPOLY][8];
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {  // two halves of 4 configurations: 24 live TMEM values, not 48
+        const int col = wg * 8 + 4 * h;
+        float pv[NPOLY][4];
 #pragma unroll
-        for (int k = 0; k < NPOLY; ++k) tmem_ld8(tl + b * kTcColStride + k * kTcN + col, pv[k]);
+        for (int k = 0; k < NPOLY; ++k) tmem_ld4(tl + b * kTcColStride + k * kTcN + col, pv[k]);
         tmem_ld_wait();
-        // the buffer is free for the MMAs of tile i + 2 as soon as every warp holds its values
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * b);
+        if (h == 1) {  // the buffer is free for the MMAs of tile i + 2 once every warp holds its values
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty0 + 8 * b);
+        }
 #ifdef RP_TC_SKEL  // timing experiment: the pipeline without the screen
         {
           float acc = 0.f;
 #pragma unroll
-          for (int v = 0; v < 8; ++v)
+          for (int v = 0; v < 4; ++v)
 #pragma unroll
             for (int k = 0; k < NPOLY; ++k) acc += pv[k][v];
           tnl = fminf(tnl, acc > 1e30f ? acc : __int_as_float(0x7f800000));
@@ -1228,7 +1237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
         }
 #endif
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
+        for (int v = 0; v < 4; ++v) {
           const int pos = i * kTcN + col + v;
           const int4 *cr = sRec + (r * kTcN + col + v) * 4;
           const int4 r0 = cr[0];
@@ -1399,13 +1408,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   }
 }
 
-static cudaError_t launch_tc(const SweepArgs &a, int n_prog, cudaStream_t s) {
+// one warp per (configuration tile, program): the tile's B operands (tf32 splits of m(P) in the
+// K-major no-swizzle layout), ||m(P)||_2 and its records, as k_sweep_tc's producer copies them
+__global__ void k_tc_pack(SweepArgs a, unsigned char *pack) {
+  const int g = blockIdx.y, j = blockIdx.x, lane = threadIdx.x;
+  const int nFp = a.tab.nFp;
+  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
+  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
+  unsigned char *dst = pack + ((int64_t)g * a.tc_ntiles + j) * kTcPack;
+  const int pos = j * kTcN + lane;
+  double mn2 = 0.0;
+  for (int pe = 0; pe < kTcNPE; ++pe) {
+    const double m = pos < nFp ? mP[(int64_t)pe * nFp + pos] : 0.0;
+    const float hi = to_tf32((float)m), lo = to_tf32((float)(m - (double)hi));
+    const uint32_t o = umma_off(lane, pe, kTcLBO, kTcSBO);
+    *reinterpret_cast<float *>(dst + o) = hi;
+    *reinterpret_cast<float *>(dst + kTcBbytes + o) = lo;
+    mn2 = fma(m, m, mn2);
+  }
+  reinterpret_cast<float *>(dst + kTcPackB)[lane] = (float)(sqrt(mn2) * (1.0 + 1e-6));
+  const int4 *src = reinterpret_cast<const int4 *>(rec + (pos < nFp ? pos : nFp - 1));
+  int4 *rd = reinterpret_cast<int4 *>(dst + kTcPackB + kTcPackMn) + lane * 4;
+  for (int q = 0; q < 4; ++q) rd[q] = src[q];
+}
+
+static cudaError_t launch_tc(SweepArgs a, int n_prog, cudaStream_t s) {
   const int64_t tiles = (a.nD + kTcM - 1) / kTcM;
   if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_sweep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
   if (e != cudaSuccess) return e;
+  a.tc_ntiles = (a.tab.nFp + kTcN - 1) / kTcN;
+  unsigned char *pack = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void **>(&pack), (size_t)n_prog * a.tc_ntiles * kTcPack, s);
+  if (e != cudaSuccess) return e;
+  k_tc_pack<<<dim3((unsigned)a.tc_ntiles, (unsigned)n_prog), 32, 0, s>>>(a, pack);
+  a.tcpack = pack;
   k_sweep_tc<<<dim3((unsigned)tiles, (unsigned)n_prog), kTcThreads, kTcSmem, s>>>(a);
   e = cudaGetLastError();
+  cudaFreeAsync(pack, s);
   if (e == cudaSuccess && getenv("RP_SWEEP_TC_STATS")) {
     unsigned long long st[2];
     cudaStreamSynchronize(s);
@@ -1414,6 +1454,17 @@ static cudaError_t launch_tc(const SweepArgs &a, int n_prog, cudaStream_t s) {
     const unsigned long long z[2] = {0ull, 0ull};
     cudaMemcpyToSymbol(g_tc_stats, z, sizeof(z));
   }
+#ifdef RP_TC_TRACE
+  {
+    long long tr[64][6];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(tr, g_tc_trace, sizeof(tr));
+    for (int i = 0; i < 40; ++i)
+      fprintf(stderr, "tile %2d: empty_ok %8lld copy %8lld commit %8lld | w0 start %8lld full_ok %8lld | w15 start %8lld\n", i,
+              tr[i][0] - tr[0][0], tr[i][1] - tr[0][0], tr[i][2] - tr[0][0], tr[i][3] - tr[0][0], tr[i][4] - tr[0][0],
+              tr[i][5] - tr[0][0]);
+  }
+#endif
   return e;
 }
 
