@@ -1187,9 +1187,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
     const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
     const EConst32 kc32 = to_econst32(make_econst(pg));
-    float cn[NPOLY];
+    float rcn[NPOLY];  // 1 / ||C_k(D)||: rho = ||m|| / min_k (|p_k| / ||C_k||), one reciprocal per pair
 #pragma unroll
-    for (int k = 0; k < NPOLY; ++k) cn[k] = sCn[t * 6 + k];
+    for (int k = 0; k < NPOLY; ++k) rcn[k] = 1.0f / sCn[t * 6 + k];
     float ck[kTcKC];
     int cp[kTcKC];
 #pragma unroll
@@ -1258,9 +1258,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           const float rSMf = sRSM32[smact];
           const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
           const float mn = sMn[r * kTcN + col + v];
-          float rho = 0.f;
+          float qmin = fabsf(pv[0][v]) * rcn[0];
 #pragma unroll
-          for (int k = 0; k < NPOLY; ++k) rho = fmaxf(rho, cn[k] * mn * rcp32(fabsf(pv[k][v])));
+          for (int k = 1; k < NPOLY; ++k) qmin = fminf(qmin, fabsf(pv[k][v]) * rcn[k]);
+          const float rho = mn * rcp32(qmin);  // = max_k ||C_k|| ||m|| / |p32_k| (to a few ulp)
           const float eps = 64.f * u * 1.001f * rho;
           const float tol = 2.2f * (6.f * eps + 25.f * u) + 1e-6f;
           bool unc;
