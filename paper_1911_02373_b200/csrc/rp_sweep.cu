@@ -1272,15 +1272,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           ub = (ok && !unc) ? fminf(ub, E32 * (1.0f + eta)) : ub;
           float key = ok ? (unc ? -1.0f : E32 * (1.0f - eta)) : __int_as_float(0x7f800000);
           int q = pos;
+          if (key < ck[kTcKC - 1]) {  // (mostly warp-uniform false once the list holds small keys)
 #pragma unroll
-          for (int j = 0; j < kTcKC; ++j) {  // positions grow along the stream: ties keep the earlier
-            const bool lt = key < ck[j];
-            const float tk = ck[j];
-            const int tq = cp[j];
-            ck[j] = lt ? key : tk;
-            cp[j] = lt ? q : tq;
-            key = lt ? tk : key;
-            q = lt ? tq : q;
+            for (int j = 0; j < kTcKC; ++j) {  // positions grow along the stream: ties keep the earlier
+              const bool lt = key < ck[j];
+              const float tk = ck[j];
+              const int tq = cp[j];
+              ck[j] = lt ? key : tk;
+              cp[j] = lt ? q : tq;
+              key = lt ? tk : key;
+              q = lt ? tq : q;
+            }
           }
           ovf = ovf | (key < 0.f);
           tnl = fminf(tnl, key);
