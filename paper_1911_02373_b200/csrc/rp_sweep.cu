@@ -1187,6 +1187,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
     const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
     const EConst32 kc32 = to_econst32(make_econst(pg));
+    const float rNSM32 = sRSM32[n_sm];
     float rcn[NPOLY];  // 1 / ||C_k(D)||: rho = ||m|| / min_k (|p_k| / ||C_k||), one reciprocal per pair
 #pragma unroll
     for (int k = 0; k < NPOLY; ++k) rcn[k] = 1.0f / sCn[t * 6 + k];
@@ -1248,6 +1249,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           const int4 r3 = cr[3];
           const int2 h3 = make_int2(r3.z, r3.w);  // W32, rB32
           const bool ok = tok && pos < nFc && h0.x <= D1sq;               // a3
+          if (!ok) continue;  // masked: never a candidate (mostly warp-uniform: tuples sorted by D1)
           const uint32_t s012 = (uint32_t)h2.y;
           // a6 (as k_sweep): 32-bit factors, the 64-bit product only where needed
           const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, (int32_t)(h0.y >> 32), (uint32_t)h1.z, s012 & 255) : 1u;
@@ -1255,7 +1257,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           int64_t blocks = (int64_t)((uint64_t)f0 * f1);
           if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
           const int smact = (int)(blocks < n_sm ? blocks : n_sm);
-          const float rSMf = sRSM32[smact];
+          float rSMf = rNSM32;  // SM_act = n_SM for most pairs: the table read only otherwise
+          if (smact < n_sm) rSMf = sRSM32[smact];
           const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
           const float mn = sMn[r * kTcN + col + v];
           float qmin = fabsf(pv[0][v]) * rcn[0];
@@ -1269,8 +1272,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
                                        __int_as_float(h3.x), Rep, rSMf, (float)smact, kc32, unc, tol);
           const float eta = 1.1f * (18.f * eps + 80.f * u) + 1e-6f;
           unc = unc | !(rho <= 64.f);
-          ub = (ok && !unc) ? fminf(ub, E32 * (1.0f + eta)) : ub;
-          float key = ok ? (unc ? -1.0f : E32 * (1.0f - eta)) : __int_as_float(0x7f800000);
+          ub = unc ? ub : fminf(ub, E32 * (1.0f + eta));
+          float key = unc ? -1.0f : E32 * (1.0f - eta);
           int q = pos;
           if (key < ck[kTcKC - 1]) {  // (mostly warp-uniform false once the list holds small keys)
 #pragma unroll
