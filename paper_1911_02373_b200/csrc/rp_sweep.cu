@@ -952,7 +952,10 @@ constexpr int kTcNB = 2;            // TMEM buffers = B operand ring slots
 constexpr int kTcNR = 4;            // ring slots of the tile's records and ||m||
 constexpr int kTcColStride = 256;   // TMEM columns per buffer (6 kTcN used)
 constexpr int kTcNPE = 16;          // MMA K (program-part monomials, padded)
-constexpr int kTcKC = 4;            // kept candidates per screening thread
+#ifndef RP_TC_KC
+#define RP_TC_KC 4
+#endif
+constexpr int kTcKC = RP_TC_KC;     // kept candidates per screening thread
 constexpr int kTcEpi = 512;         // screening threads (4 warpgroups)
 constexpr int kTcThreads = kTcEpi + 32;
 constexpr uint32_t kTcLBO = 128, kTcSBO = 512;        // K-major no-swizzle core-matrix strides
