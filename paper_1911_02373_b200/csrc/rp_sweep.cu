@@ -956,7 +956,13 @@ constexpr int kTcNPE = 16;          // MMA K (program-part monomials, padded)
 #define RP_TC_KC 4
 #endif
 constexpr int kTcKC = RP_TC_KC;     // kept candidates per screening thread
-constexpr int kTcEpi = 512;         // screening threads (4 warpgroups)
+#ifndef RP_TC_EPI
+#define RP_TC_EPI 512
+#endif
+constexpr int kTcEpi = RP_TC_EPI;   // screening threads (512: 4 warpgroups at 96 registers; 256: 2 at 168)
+constexpr int kTcWG = kTcEpi / 128;             // screening warpgroups
+constexpr int kTcCfgWG = kTcN / kTcWG;          // configurations of a tile per warpgroup
+constexpr int kTcProd = kTcEpi / 32;            // the producer warp's index
 constexpr int kTcThreads = kTcEpi + 32;
 constexpr uint32_t kTcLBO = 128, kTcSBO = 512;        // K-major no-swizzle core-matrix strides
 constexpr uint32_t kTcAbytes = kTcM / 8 * kTcSBO;     // one [128 x 16] tf32 operand: 8 KB
@@ -1031,7 +1037,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     *sMaxD1 = 0ull;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (wid == 16) tmem_alloc(smem_u32(sTmem), 512);
+  if (wid == kTcProd) tmem_alloc(smem_u32(sTmem), 512);
   for (int i = tid; i < kTcM * d; i += kTcThreads) {
     const int t = i / d, k = i % d;
     const int64_t src = (t < tmax) ? (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t) : 0;
@@ -1130,7 +1136,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   const uint32_t tm = *sTmem;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcNB);
 
-  if (wid == 16) {
+  if (wid == kTcProd) {
     // ---- producer / MMA warp ------------------------------------------------------------------
     const uint32_t idesc = umma_idesc_tf32(kTcM, kTcN);
     const uint32_t bfull0 = smem_u32(bars + 2 * kTcNB);
@@ -1218,13 +1224,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
 #endif
       tc_fence_after();
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {  // two halves of 4 configurations: 24 live TMEM values, not 48
-        const int col = wg * 8 + 4 * h;
+      for (int h = 0; h < kTcCfgWG / 4; ++h) {  // groups of 4 configurations: 24 live TMEM values
+        const int col = wg * kTcCfgWG + 4 * h;
         float pv[NPOLY][4];
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) tmem_ld4(tl + b * kTcColStride + k * kTcN + col, pv[k]);
         tmem_ld_wait();
-        if (h == 1) {  // the buffer is free for the MMAs of tile i + 2 once every warp holds its values
+        if (h == kTcCfgWG / 4 - 1) {  // the buffer is free for the MMAs of tile i + 2 once every warp holds its values
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(empty0 + 8 * b);
@@ -1302,7 +1308,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     // only candidates whose lower bound reaches the tuple's smallest upper bound can win
     float ubt = ub;
 #pragma unroll
-    for (int w2 = 0; w2 < 4; ++w2) ubt = fminf(ubt, *reinterpret_cast<const float *>(sPart + (w2 * kTcM + t) * 24 + 20));
+    for (int w2 = 0; w2 < kTcWG; ++w2) ubt = fminf(ubt, *reinterpret_cast<const float *>(sPart + (w2 * kTcM + t) * 24 + 20));
     const EConst kc = make_econst(pg);
     auto pair_E64 = [&](int tt, int pos, const double *pk, int32_t &orig) -> double {
       const int32_t *Dq = sDv + tt * kMaxVars;
@@ -1366,7 +1372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     *reinterpret_cast<int32_t *>(pp + 16) = ovf ? 1 : 0;
     asm volatile("bar.sync 1, %0;" ::"r"(kTcEpi) : "memory");
     if (wg == 0 && tok) {
-      for (int w2 = 1; w2 < 4; ++w2) {
+      for (int w2 = 1; w2 < kTcWG; ++w2) {
         const unsigned char *qq = sPart + (w2 * kTcM + t) * 24;
         take(st, *reinterpret_cast<const double *>(qq), *reinterpret_cast<const int32_t *>(qq + 8));
         tnl = fminf(tnl, *reinterpret_cast<const float *>(qq + 12));
@@ -1411,7 +1417,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (wid == 16) {
+  if (wid == kTcProd) {
     tc_fence_after();
     tmem_dealloc(tm, 512);
   }
