@@ -987,6 +987,8 @@ constexpr uint32_t kTcPackB = 2 * kTcBbytes, kTcPackMn = kTcN * 4, kTcPackRec = 
 constexpr uint32_t kTcPack = kTcPackB + kTcPackMn + kTcPackRec;  // 6272 B
 static_assert(kTcOffB % 1024 == 0 && kTcSmem <= 227 * 1024, "tc sweep shared memory");
 static_assert(12 * kTcAbytes >= kTcM * 96 * 8, "FP64 C fits the A operands' space");
+// the per-SM scratch slot of g_tc_C has one owner at a time only if two CTAs cannot share an SM
+static_assert(2 * kTcSmem > 228 * 1024, "k_sweep_tc must hold its SM alone");
 
 __device__ unsigned long long g_tc_stats[2];
 #ifdef RP_TC_TRACE  // timeline of CTA 0: [tile][0..3] = producer empty-wait done, copy landed, committed; screen start (warp 0)
@@ -1512,7 +1514,8 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
   // RP_SWEEP_KERNEL=ws: the warp-specialised screened sweep (MWP-CWP programs; parity-tested, not
   // yet faster: DESIGN.md "Warp-specialised screened sweep"); default: k_sweep
   const char *kern = getenv("RP_SWEEP_KERNEL");
-  if (NPE == kTcNPE && mwp && !second && kern && strcmp(kern, "tc") == 0 && a.tab.nde_pad <= kTcMaxNdp)
+  if (NPE == kTcNPE && mwp && !second && kern && strcmp(kern, "tc") == 0 && a.tab.nde_pad <= kTcMaxNdp &&
+      num_sms() <= kTcMaxSM)
     return launch_tc(a, n_prog, s);
   if (mwp && kern && strcmp(kern, "ws") == 0)
     return second ? launch_ws<NPE, true>(a, n_prog, n_sm_max, s) : launch_ws<NPE, false>(a, n_prog, n_sm_max, s);
