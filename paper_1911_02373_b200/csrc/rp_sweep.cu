@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
   // over the warps, as in k_sweep).  to_ops: stored as tf32 splits in the A operands, with
   // ||C_k(D)||_2^2 summed into sNrm (shared FP64 atomics: two addends onto 0, order-independent);
   // the FP64 rows also go to gCd[t][96] for the exact re-evaluation.
-  double *sNrm = reinterpret_cast<double *>(sPart);  // [128][6], before the merge needs sPart
+  double *sNrm = reinterpret_cast<double *>(sPart);  // [128][6][2] half sums, before the merge needs sPart
   auto stage_C = [&](bool to_ops, int nwarps) {
     constexpr int MT = NPOLY * NPE / 8, NT = kTcM / 8;
     for (int tile = wid; tile < MT * NT; tile += nwarps) {
@@ -1102,18 +1102,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
           q0 += __shfl_xor_sync(0xffffffffu, q0, m);
           q1 += __shfl_xor_sync(0xffffffffu, q1, m);
         }
-        if (lane < 4) {
-          atomicAdd(&sNrm[t * 6 + k], q0);
-          atomicAdd(&sNrm[(t + 1) * 6 + k], q1);
+        if (lane < 4) {  // each (tuple, polynomial, row-tile half) written by one lane: no atomics
+          sNrm[(t * 6 + k) * 2 + (mt & 1)] = q0;
+          sNrm[((t + 1) * 6 + k) * 2 + (mt & 1)] = q1;
         }
       }
     }
   };
-  for (int i = tid; i < kTcM * 6; i += kTcThreads) sNrm[i] = 0.0;
-  __syncthreads();
   stage_C(true, kTcThreads / 32);
   __syncthreads();
-  for (int i = tid; i < kTcM * 6; i += kTcThreads) sCn[i] = (float)(sqrt(sNrm[i]) * (1.0 + 1e-6));
+  for (int i = tid; i < kTcM * 6; i += kTcThreads) sCn[i] = (float)(sqrt(sNrm[2 * i] + sNrm[2 * i + 1]) * (1.0 + 1e-6));
   fence_async_smem();
   __syncthreads();
 
