@@ -1062,9 +1062,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     }
     sMD[t * ndp + de] = m;
   }
-  if (tid < tmax) {
-    const long long D1 = sDv[tid * kMaxVars];
-    atomicMax(sMaxD1, (unsigned long long)(D1 * D1));
+  if (tid < kTcM) {  // warps 0-3: a shuffle max, then one shared atomic per warp
+    const long long D1 = tid < tmax ? sDv[tid * kMaxVars] : 0;
+    unsigned long long m = (unsigned long long)(D1 * D1);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x > m ? x : m;
+    }
+    if (lane == 0) atomicMax(sMaxD1, m);
   }
   __syncthreads();
   // staged data polynomials C_{k,pe}(D) in FP64 (a2): the (96 x ndp) x (ndp x 128) product of the
