@@ -1530,6 +1530,101 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
                 : launch3<NPE, false, false>(a, n_prog, n_sm_max, s);
 }
 
+// ============================================================================================
+// Winner refinement (RP_SWEEP_REFINE=1, opt-in; reading R31).  A program fitted to
+// noisy samples has polynomials whose terms cancel (condition numbers to 1e6), so the FP64 sweep's
+// E can differ from the exact value by up to ~1e-9 relative.  This pass re-evaluates, per tuple,
+// the winner the sweep chose with the staged contraction in double-double (error-free products by
+// FMA, compensated sums): p_k to ~2^-100 relative to sum |terms|, then Appendix A in FP64.  The
+// winner index is unchanged; E becomes accurate to the formula's own rounding.
+// ============================================================================================
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_two_prod(double a, double b) {
+  const double p = a * b;
+  return DD{p, fma(a, b, -p)};
+}
+__device__ __forceinline__ DD dd_add(DD x, DD y) {  // Knuth two-sum on the high parts, then renormalise
+  const double s = x.hi + y.hi, bb = s - x.hi;
+  const double e = (x.hi - (s - bb)) + (y.hi - bb) + x.lo + y.lo;
+  const double h = s + e;
+  return DD{h, e - (h - s)};
+}
+__device__ __forceinline__ DD dd_mul(DD x, DD y) {
+  DD p = dd_two_prod(x.hi, y.hi);
+  p.lo = fma(x.hi, y.lo, fma(x.lo, y.hi, p.lo));
+  const double h = p.hi + p.lo;
+  return DD{h, p.lo - (h - p.hi)};
+}
+
+__global__ void k_refine_winners(SweepArgs a) {
+  const int g = blockIdx.y;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.nD) return;
+  const int64_t o = (int64_t)g * a.nD + t;
+  const int32_t win = a.idx[o];
+  if (win < 0) return;
+  const DevProg &pg = a.progs[g];
+  const int d = a.d, nFp = a.tab.nFp, nFc = a.tab.nFc[2 * g], npe = a.npe_pad, ndp = a.tab.nde_pad;
+  // the winner's record: compacted configurations in ascending original index (binary search)
+  const CfgRec *sr = a.tab.srec + (int64_t)g * nFp;
+  int lo = 0, hi = nFc - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sr[mid].orig < win) lo = mid + 1;
+    else hi = mid;
+  }
+  const CfgRec r = sr[lo];
+  if (r.orig != win) return;
+  const int32_t *Dt = a.D + t * d;
+  // data monomials in double-double (u exact in FP64: integer minus the box centre, times 2^-e)
+  DD md[kMaxDE];
+  for (int de = 0; de < pg.nDE; ++de) {
+    DD m{1.0, 0.0};
+    for (int k = 0; k < d; ++k) {
+      const double u = ((double)Dt[k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+      for (int e = 0; e < pg.de_exp[de][k]; ++e) m = dd_mul(m, DD{u, 0.0});
+    }
+    md[de] = m;
+  }
+  const int P[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+  const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * npe * ndp;
+  double pk[kMaxPolys];
+  for (int k = 0; k < pg.npoly; ++k) {
+    DD acc{0.0, 0.0};
+    for (int pe = 0; pe < pg.nPE; ++pe) {
+      DD mp{1.0, 0.0};
+      for (int q = 0; q < pg.p; ++q) {
+        const double u = ((double)P[q] - pg.xc[d + q]) * ldexp(1.0, -pg.xe[d + q]);
+        for (int e = 0; e < pg.pe_exp[pe][q]; ++e) mp = dd_mul(mp, DD{u, 0.0});
+      }
+      DD c{0.0, 0.0};
+      const double *row = Cm + (int64_t)(k * npe + pe) * ndp;
+      for (int de = 0; de < pg.nDE; ++de) {
+        if (row[de] == 0.0) continue;
+        c = dd_add(c, dd_mul(md[de], DD{row[de], 0.0}));
+      }
+      acc = dd_add(acc, dd_mul(c, mp));
+    }
+    pk[k] = acc.hi + acc.lo;
+  }
+  // a6 and Appendix A exactly as the sweep does them, on the refined polynomial values
+  const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
+  int64_t blocks = 1;
+  if (map0 >= 0) blocks *= ((int64_t)Dt[map0] + P[0] - 1) / P[0];
+  if (map1 >= 0) blocks *= ((int64_t)Dt[map1] + P[1] - 1) / P[1];
+  if (map2 >= 0) blocks *= ((int64_t)Dt[map2] + P[2] - 1) / P[2];
+  const int n_sm = pg.n_sm;
+  const int64_t smact = blocks < n_sm ? blocks : n_sm;
+  const double rSM = a.tab.rSM[(int64_t)g * kRSMTab + smact];
+  const double Rep = (double)blocks * r.rB * rSM;
+  double E;
+  if (pg.npoly == 6) E = mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], r.W, Rep, rSM, (double)smact, make_econst(pg));
+  else E = pk[0] * frcp(pk[1]);
+  if (pos_finite(E)) a.bestE[o] = E;
+}
+
 cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
                          int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
                          int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
@@ -1538,15 +1633,24 @@ cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable 
   // n_sm < kRSMTab for every program (compile_program): the 1/SM_act tables always exist
   (void)nde_max;
   SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE, perm};
+  cudaError_t e;
   switch (npe_pad) {
-    case 4: return launch_npe<4>(a, n_prog, mwp, n_sm_max, s);
-    case 8: return launch_npe<8>(a, n_prog, mwp, n_sm_max, s);
-    case 16: return launch_npe<16>(a, n_prog, mwp, n_sm_max, s);
-    case 20: return launch_npe<20>(a, n_prog, mwp, n_sm_max, s);
-    case 24: return launch_npe<24>(a, n_prog, mwp, n_sm_max, s);
-    case 36: return launch_npe<36>(a, n_prog, mwp, n_sm_max, s);
+    case 4: e = launch_npe<4>(a, n_prog, mwp, n_sm_max, s); break;
+    case 8: e = launch_npe<8>(a, n_prog, mwp, n_sm_max, s); break;
+    case 16: e = launch_npe<16>(a, n_prog, mwp, n_sm_max, s); break;
+    case 20: e = launch_npe<20>(a, n_prog, mwp, n_sm_max, s); break;
+    case 24: e = launch_npe<24>(a, n_prog, mwp, n_sm_max, s); break;
+    case 36: e = launch_npe<36>(a, n_prog, mwp, n_sm_max, s); break;
     default: return cudaErrorInvalidValue;
   }
+  const char *refine = getenv("RP_SWEEP_REFINE");
+  if (e == cudaSuccess && refine && refine[0] == '1') {  // opt-in: the winners' E in double-double
+    const int64_t blocks = (nD + 127) / 128;
+    if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
+    k_refine_winners<<<dim3((unsigned)blocks, (unsigned)n_prog), 128, 0, s>>>(a);
+    e = cudaGetLastError();
+  }
+  return e;
 }
 
 }  // namespace rp

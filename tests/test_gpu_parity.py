@@ -594,3 +594,26 @@ def test_sweep_tensor_core_fitted_program(monkeypatch):
     ref = oracle.sweep(spec, D[sel], F)
     check_sweep(np.asarray(idx1.cpu()).ravel()[sel], np.asarray(E1.cpu()).ravel()[sel], None, ref, spec, D[sel], F,
                 tag="fitted", kappa_gate=1024)
+
+
+def test_sweep_refined_winners_fitted_program(monkeypatch):
+    """RP_SWEEP_REFINE=1 (reading R31): the winners of a fitted, ill-conditioned program
+    re-evaluated in double-double meet the strict 1e-12 E gate; winners unchanged."""
+    fc = synth.fitheavy(sigma=0.01, K=20_000)
+    prog = fc.truths[0]
+    X = _cuda(fc.X)
+    V = (rp.eval_metrics(prog, X) * _cuda(fc.noise)).contiguous()
+    coef, (c, e), _ = rp.fit(X, V, fc.num_exp, fc.den_exp)
+    spec = copy.deepcopy(prog)
+    spec.coef = [np.asarray(coef[i]) for i in range(3)]
+    spec.xform_c, spec.xform_e = list(c), list(e)
+    D = synth.large_D(3000)
+    F = synth.F_large()
+    idx0, _, _ = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=False)
+    monkeypatch.setenv("RP_SWEEP_REFINE", "1")
+    idx1, E1, _ = rp.eval_argmin(spec, _cuda(D), _cuda(F), second=False)
+    assert torch.equal(idx0.cpu(), idx1.cpu())
+    sel = np.arange(0, 3000, 10)
+    ref = oracle.sweep(spec, D[sel], F)
+    check_sweep(np.asarray(idx1.cpu()).ravel()[sel], np.asarray(E1.cpu()).ravel()[sel], None, ref, spec, D[sel], F,
+                tag="fitted-refined")
