@@ -328,7 +328,10 @@ rp_status rp_plan_decide(rp_plan plan, int32_t prog, const int32_t *D, int64_t n
  * launches"): a device-resident open-addressing hash table D -> decision,
  * owned by the plan, 2^log2_capacity slots (4..24), for one program of the plan and one
  * margin; rp_plan_decide then probes it first and inserts its fresh decisions (a full table
- * keeps serving hits and computes the rest).  Enabling twice clears it.                       */
+ * keeps serving hits and computes the rest).  Enabling again clears it: with the same capacity
+ * in place (a live rp_decider of the same program and margin keeps working; another program or
+ * margin is INVALID_ARG while deciders live), with another capacity by reallocation (refused,
+ * INVALID_ARG, while any rp_decider of the plan lives: its graph holds the table).             */
 rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capacity, double margin);
 rp_status rp_plan_history_stats(rp_plan plan, int64_t *hits, int64_t *misses, int64_t *entries);
 rp_status rp_plan_history_clear(rp_plan plan, rp_stream s);

@@ -149,8 +149,15 @@ int orc_eval_pair(const orc_program *pr, const int *D, const int *P, orc_trace *
   /* Appendix A line 1 -- "multiple of the warp size (32)" and "bounded over by the maximum
    * number of threads per block" (reading R5: <= T_max), and the footnote
    * "P1 P2 <= D1^2 is meaningful" (reading R6: non-strict). */
+  /* reading R32: data parameters are sizes, D_k >= 1; a block dimension is >= 1 */
+  for (int k = 0; k < pr->d; ++k)
+    if (D[k] < 1) { t.mask = 6; goto done; }
   long long T = 1;
-  for (int k = 0; k < pr->p; ++k) T *= P[k];
+  for (int k = 0; k < pr->p; ++k) {
+    if (P[k] < 1) { t.mask = 1; goto done; }
+    T *= P[k];
+    if (T > hw->t_max) { t.T = T; t.mask = 2; goto done; } /* stop before the product can wrap */
+  }
   t.T = T;
   if (T % 32 != 0) { t.mask = 1; goto done; }
   if (T > hw->t_max) { t.mask = 2; goto done; }

@@ -49,7 +49,8 @@ typedef struct {
 /* per-pair trace for tests */
 typedef struct {
   int feasible;   /* 1 if E is a candidate */
-  int mask;       /* 0 ok, 1 warp rule, 2 T > T_max, 3 P1*P2 > D1^2, 4 B_active = 0, 5 E invalid */
+  int mask;       /* 0 ok, 1 warp rule / P_k < 1, 2 T > T_max, 3 P1*P2 > D1^2, 4 B_active = 0, 5 E invalid,
+                     6 some D_k < 1 (reading R32) */
   int branch;     /* occupancy flowchart branch 1..5 (0 if not reached) */
   int mwp_case;   /* 1..3 (0 if not reached / template g1) */
   long long T, B_active, W_active, blocks, sm_active;

@@ -359,6 +359,8 @@ class Plan:
         F = _contig(F, np.int32)
         self.nF = F.shape[0] if F.ndim > 1 else len(F) // self.p
         self.handle = C.c_void_p()
+        self.generation = 0  # bumped by update(): host-side caches of decisions key on it
+        self._history = None  # (prog, log2_capacity, margin) of the enabled runtime history
         s = _stream_of(F)
         _check(_lib.rp_plan_create(C.cast(arr, _vp), len(self.progs), _ptr(F), self.nF, C.byref(self.handle), s))
 
@@ -369,6 +371,7 @@ class Plan:
         coef = coef.contiguous()
         _check(_lib.rp_plan_update_program(self.handle, prog, _ptr(coef), coef.shape[-1],
                                            _ptr(xf.contiguous()) if xf is not None else None, _stream_of(coef)))
+        self.generation += 1
 
     def static_feasible(self, prog: int = 0) -> int:
         v = C.c_int32()
@@ -406,6 +409,7 @@ class Plan:
 
     def enable_history(self, prog: int = 0, log2_capacity: int = 16, margin: float = 0.0):
         _check(_lib.rp_plan_history_enable(self.handle, prog, log2_capacity, float(margin)))
+        self._history = (prog, log2_capacity, float(margin))
 
     def history_stats(self) -> dict:
         h, m, e = _i64(), _i64(), _i64()
@@ -688,11 +692,18 @@ class DecisionService:
         self.plan, self.prog, self.margin = plan, prog, margin
         self.memo = {} if host_memo else None
         self.memo_cap = host_memo
-        if history_log2:
+        self._gen = plan.generation
+        # the history may already serve another service of the same (program, margin): enabling
+        # it again would only clear it (rp.h), so it is left as it is
+        if history_log2 and plan._history != (prog, history_log2, float(margin)):
             plan.enable_history(prog, history_log2, margin)
         self.decider = Decider(plan, prog, margin)
 
     def __call__(self, D) -> np.void:
+        if self.plan.generation != self._gen:  # Plan.update: every memoised decision is stale
+            self._gen = self.plan.generation
+            if self.memo is not None:
+                self.memo.clear()
         key = tuple(int(v) for v in np.asarray(D).ravel()[: self.plan.d])
         hit = self.memo.get(key) if self.memo is not None else None
         if hit is not None:  # host memo in front of the device history: no GPU round trip

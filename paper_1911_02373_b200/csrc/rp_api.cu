@@ -356,6 +356,7 @@ struct rp_plan_s {
   CfgTable tab{};
   cudaStream_t stream = nullptr;
   HistTable hist;
+  int n_deciders = 0;  // live rp_decider objects whose captured graph holds hist.slots
 };
 
 static void plan_free(rp_plan pl) {
@@ -1202,6 +1203,7 @@ rp_status rp_decider_create(rp_plan plan, int32_t prog, double margin, rp_decide
   if (e != cudaSuccess) return fail(e, "capture launch");
   if (e2 != cudaSuccess) return fail(e2, "end capture");
   if ((e = cudaGraphInstantiate(&dc->exec, dc->graph, 0)) != cudaSuccess) return fail(e, "instantiate");
+  ++plan->n_deciders;
   *out = dc;
   return RP_OK;
 }
@@ -1216,6 +1218,7 @@ rp_status rp_decider_decide(rp_decider dc, const int32_t *D, rp_decision *out) {
 }
 
 rp_status rp_decider_destroy(rp_decider dc) {
+  if (dc && dc->exec && dc->plan) --dc->plan->n_deciders;
   decider_free(dc);
   return RP_OK;
 }
@@ -1225,13 +1228,27 @@ rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capaci
   RP_REQUIRE(prog >= 0 && prog < plan->n_prog, RP_ERR_INVALID_ARG, "prog %d out of range", prog);
   RP_REQUIRE(log2_capacity >= 4 && log2_capacity <= 24 && margin >= 0.0, RP_ERR_INVALID_ARG,
              "log2_capacity in [4, 24], margin >= 0");
+  const size_t cap = (size_t)1 << log2_capacity;
   RP_CUDA(cudaStreamSynchronize(plan->stream));
+  if (plan->hist.slots && (size_t)plan->hist.mask + 1 == cap) {
+    // same capacity: clear in place, so the table a live decider's graph captured stays valid
+    RP_REQUIRE(plan->n_deciders == 0 || (plan->hist.prog == prog && plan->hist.margin == margin),
+               RP_ERR_INVALID_ARG, "%d decider(s) use the history of program %d, margin %g",
+               plan->n_deciders, plan->hist.prog, plan->hist.margin);
+    RP_CUDA(cudaMemset(plan->hist.slots, 0, cap * sizeof(HistSlot)));
+    RP_CUDA(cudaMemset(plan->hist.counters, 0, 3 * sizeof(unsigned long long)));
+    plan->hist.prog = prog;
+    plan->hist.margin = margin;
+    return RP_OK;
+  }
+  // a new allocation would leave a live decider's captured graph with a freed table
+  RP_REQUIRE(plan->n_deciders == 0, RP_ERR_INVALID_ARG,
+             "cannot resize the runtime history while %d decider(s) use it", plan->n_deciders);
   if (plan->hist.slots) {
     cudaFree(plan->hist.slots);
     cudaFree(plan->hist.counters);
     plan->hist = HistTable();
   }
-  const size_t cap = (size_t)1 << log2_capacity;
   RP_CUDA(cudaMalloc((void **)&plan->hist.slots, cap * sizeof(HistSlot)));
   RP_CUDA(cudaMalloc((void **)&plan->hist.counters, 3 * sizeof(unsigned long long)));
   RP_CUDA(cudaMemset(plan->hist.slots, 0, cap * sizeof(HistSlot)));

@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(DecideArgs a) {
             map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
   const int32_t Da = map0 >= 0 ? sD[map0] : 1, Db = map1 >= 0 ? sD[map1] : 1, Dc = map2 >= 0 ? sD[map2] : 1;
   const int64_t D1sq = (int64_t)sD[0] * sD[0];
+  bool dpos = true;  // reading R32: data parameters are sizes >= 1
+  for (int k = 0; k < d; ++k) dpos = dpos && sD[k] >= 1;
   const int n_sm = pg.n_sm;
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
 
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(DecideArgs a) {
     } else {
       E = pk[0] * frcp(pk[1]);
     }
-    const bool ok = cr.P01 <= D1sq;
+    const bool ok = cr.P01 <= D1sq && dpos;
     E = (ok && E > 0.0 && E < kInf) ? E : kInf;
     sE[c] = E;
     if (E < kInf && (E < be || (E == be && cr.orig < bo))) {

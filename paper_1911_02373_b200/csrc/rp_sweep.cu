@@ -56,14 +56,19 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     int64_t T = 1, B = 0, W = 0;
     if (c < nF) {
       for (int k = 0; k < pg.p; ++k) Pk[k] = F[(int64_t)c * pg.p + k];
-      bool pos = true;
+      // running product with an early bound: every P_k >= 1, so once T exceeds T_max it stays
+      // above it (no int64 wrap-around for P_k up to 2^31 - 1)
+      bool pos = true, big = false;
       for (int k = 0; k < pg.p; ++k) {
-        T *= Pk[k];
         pos = pos && Pk[k] >= 1;
+        if (pos && !big) {
+          T *= Pk[k];
+          big = T > pg.t_max;
+        }
       }
       // "a multiple of the warp size (32)" and "bounded over by the maximum number of threads
       // per block"
-      ok = pos && (T % 32 == 0) && (T <= pg.t_max);
+      ok = pos && !big && (T % 32 == 0) && (T <= pg.t_max);
       if (ok) {
         const int64_t Z = pg.Z0 + pg.Z1 * T;
         B = occupancy_blocks(T, pg.R, Z, pg);
@@ -415,8 +420,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
 
   // this warp's octet of tuples: row lane/4 of the DMMA tiles
   const int t = wid * 8 + (lane >> 2);
-  const bool tok = t < tmax;
   const int32_t *Dt = sDv + t * kMaxVars;
+  // data parameters are sizes: a tuple with some D_k < 1 has no meaningful P (reading R32)
+  bool dpos = true;
+  for (int k = 0; k < d; ++k) dpos = dpos && Dt[k] >= 1;
+  const bool tok = t < tmax && dpos;
   const int64_t D1 = Dt[0];
   const int64_t D1sq = D1 * D1;
   // the a3 test in 32 bits: P1 P2 of a compacted configuration is <= T_max < 2^31

@@ -1,5 +1,7 @@
 """Parity of the runtime decision service (NEXT row f2, rp_plan_decide) with the oracle's
 orc_decide, and the runtime history."""
+import copy
+
 import numpy as np
 import pytest
 
@@ -137,3 +139,45 @@ def test_decider_matches_batched_decide(history):
     with pytest.raises(rp.RPError):  # a history for another program/margin is refused
         plan.enable_history(0, 8, 0.0)
         rp.Decider(plan, prog=1, margin=0.02)
+
+
+def test_history_reenable_keeps_live_deciders_valid():
+    """re-enabling the history must not free the table a live decider's graph holds.
+    Same capacity: cleared in place, the decider keeps answering; another capacity: refused."""
+    case = synth.polybench_sweep(nD=16)
+    plan = rp.Plan(case.programs[:1], _cuda(case.F))
+    want = plan.decide(case.D, prog=0, margin=0.0)
+    svc1 = rp.DecisionService(plan, prog=0, margin=0.0, history_log2=10, host_memo=0)
+    svc2 = rp.DecisionService(plan, prog=0, margin=0.0, history_log2=10, host_memo=0)
+    plan.enable_history(0, 10, 0.0)  # same capacity: in place
+    for i in range(len(case.D)):
+        assert svc1(case.D[i])["idx"] == want[i]["idx"]
+        assert svc2(case.D[i])["idx"] == want[i]["idx"]
+    with pytest.raises(rp.RPError):  # reallocation while deciders live
+        plan.enable_history(0, 11, 0.0)
+    with pytest.raises(rp.RPError):  # another margin while deciders live
+        plan.enable_history(0, 10, 0.5)
+    svc1.decider.close()
+    svc2.decider.close()
+    plan.enable_history(0, 11, 0.0)  # no decider left: allowed
+
+
+def test_decision_service_memo_invalidated_by_update():
+    """Plan.update (a refit) invalidates the service's host memo, so the next call
+    decides with the new program instead of serving the pre-refit decision."""
+    case = synth.polybench_sweep(nD=8)
+    progs = case.programs
+    plan = rp.Plan(progs[:1], _cuda(case.F))
+    svc = rp.DecisionService(plan, prog=0, margin=0.0, history_log2=None, host_memo=1 << 10)
+    d = case.D[0]
+    before = svc(d)
+    # refit: program 0's coefficients replaced by program 3's (same bases and transform box);
+    # the resources (R, Z) stay program 0's
+    refit = copy.deepcopy(progs[0])
+    refit.coef = [np.asarray(c, dtype=np.float64) for c in progs[3].coef]
+    plan.update(torch.from_numpy(np.stack(refit.coef)).to(DEV))
+    ref = rp.Plan([refit], _cuda(case.F)).decide(case.D[:1], prog=0, margin=0.0)
+    after = svc(d)
+    assert after["idx"] == ref[0]["idx"] and after["E"] == ref[0]["E"]
+    assert len(svc.memo) == 1 and svc.memo[tuple(int(v) for v in d)]["E"] == ref[0]["E"]
+    assert before["E"] != after["E"]

@@ -617,3 +617,26 @@ def test_sweep_refined_winners_fitted_program(monkeypatch):
     ref = oracle.sweep(spec, D[sel], F)
     check_sweep(np.asarray(idx1.cpu()).ravel()[sel], np.asarray(E1.cpu()).ravel()[sel], None, ref, spec, D[sel], F,
                 tag="fitted-refined")
+
+
+def test_sweep_nonpositive_data_and_huge_blocks():
+    """Reading R32: tuples with some D_k < 1 have no meaningful configuration, and
+    configurations whose product P1 P2 P3 would wrap around in 64 bits are masked (T > T_max)
+    instead of passing the warp rule as T = 0.  GPU sweep, decide and JIT against the oracle."""
+    case = synth.polybench_sweep(nD=50)
+    spec = case.programs[0]
+    F = np.concatenate([case.F, np.array([[1 << 30, 1 << 30, 16], [2147483647, 2147483647, 2147483647],
+                                          [0, 32, 1], [-32, -1, 1], [64, 1 << 28, 1 << 4]], dtype=np.int32)])
+    D = np.concatenate([np.array([[0], [-1], [-2147483647], [1]], dtype=np.int32), case.D])
+    ref = oracle.sweep(spec, D, F)
+    assert ref["idx"][:3].tolist() == [-1, -1, -1]
+    idx, E, S = rp.eval_argmin(spec, _cuda(D), _cuda(F))
+    check_sweep(idx, E, S, ref, spec, D, F, "R32")
+    plan = rp.Plan([spec], _cuda(F))
+    assert plan.static_feasible() == int(np.sum([oracle.eval_pair(spec, np.array([16384], np.int32), P)["mask"]
+                                                 not in (1, 2, 4) for P in F]))
+    dec = plan.decide(D, prog=0, margin=0.0)
+    assert np.array_equal(dec["idx"], ref["idx"])
+    jit = rp.Jit(spec)
+    ji, jE, _ = jit.eval(_cuda(D), _cuda(F))
+    assert np.array_equal(ji.cpu().numpy().ravel(), ref["idx"])

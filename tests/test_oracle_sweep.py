@@ -131,3 +131,20 @@ def test_thread_count_does_not_change_result():
     b = oracle.sweep(case.programs[0], case.D, case.F, nthreads=4)
     for k in ("idx", "best", "second"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_nonpositive_data_and_huge_blocks_are_masked():
+    """Reading R32: data parameters are sizes (D_k >= 1) and block dimensions are >= 1; the
+    product T = P1 P2 P3 stops at T_max instead of wrapping around in 64 bits."""
+    case = synth.tiny_sweep()
+    spec = case.programs[0]
+    res = oracle.sweep(spec, np.array([[0], [-64], [-2147483647], [64]], dtype=np.int32), case.F)
+    assert res["idx"][:3].tolist() == [-1, -1, -1] and res["idx"][3] >= 0
+    for d in ([0], [-5]):
+        tr = oracle.eval_pair(spec, np.array(d, dtype=np.int32), case.F[0])
+        assert not tr["feasible"] and tr["mask"] == 6
+    # (2^30, 2^30): the product 2^60 fits, but with a third factor of 16 it would wrap to 0 mod 2^64
+    spec3 = synth.polybench_sweep(nD=1).programs[0]
+    for P in ([1 << 30, 1 << 30, 16], [0, 32, 1], [-32, -1, 1], [2147483647, 2147483647, 2147483647]):
+        tr = oracle.eval_pair(spec3, np.array([1000], dtype=np.int32), np.array(P, dtype=np.int32))
+        assert not tr["feasible"] and tr["mask"] in (1, 2), P
