@@ -29,8 +29,8 @@ LD = np.longdouble
 
 def build() -> str:
     path = os.path.join(_HERE, "liboracle.so")
-    src = os.path.join(_HERE, "rp_oracle.c")
-    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, f) for f in ("rp_oracle.c", "rp_oracle_q.c", "rp_oracle_pair.inc", "rp_oracle.h")]
+    if not os.path.exists(path) or os.path.getmtime(path) < max(os.path.getmtime(f) for f in srcs):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return path
 
@@ -74,9 +74,11 @@ def lib():
             L.orc_active_warps.argtypes = [C.POINTER(_HW), ll, ll, ll]
             L.orc_active_warps.restype = ll
             L.orc_eval_ratfunc.argtypes = [C.POINTER(_RatFunc), vp, vp, vp, ll, vp, vp]
-            L.orc_eval_pair.argtypes = [C.POINTER(_Program), vp, vp, C.POINTER(_Trace)]
-            L.orc_eval_pair.restype = i
-            L.orc_sweep.argtypes = [C.POINTER(_Program), vp, ll, vp, i, vp, vp, vp, vp, vp, vp, i]
+            for q in ("", "_q"):
+                getattr(L, "orc_eval_pair" + q).argtypes = [C.POINTER(_Program), vp, vp, C.POINTER(_Trace)]
+                getattr(L, "orc_eval_pair" + q).restype = i
+                getattr(L, "orc_sweep" + q).argtypes = [C.POINTER(_Program), vp, ll, vp, i, vp, vp, vp, vp, vp, vp, i,
+                                                        vp, vp]
             L.orc_decide.argtypes = [C.POINTER(_Program), vp, vp, i, d, vp, vp, vp]
             L.orc_decide.restype = i
             L.orc_design_row.argtypes = [i, i, i, vp, vp, vp, vp, vp, d, vp]
@@ -181,12 +183,13 @@ class _ProgramHolder:
         self.pr = pr
 
 
-def eval_pair(spec, D, P) -> dict:
+def eval_pair(spec, D, P, quad: bool = False) -> dict:
+    """Trace of one (D, P) pair; quad=True evaluates in IEEE binary128 (orc_eval_pair_q)."""
     h = _ProgramHolder(spec)
     Da = np.ascontiguousarray(D, dtype=np.int32)
     Pa = np.ascontiguousarray(P, dtype=np.int32)
     tr = _Trace()
-    lib().orc_eval_pair(C.byref(h.pr), _p(Da), _p(Pa), C.byref(tr))
+    (lib().orc_eval_pair_q if quad else lib().orc_eval_pair)(C.byref(h.pr), _p(Da), _p(Pa), C.byref(tr))
     out = {k: getattr(tr, k) for k, _ in _Trace._fields_ if k != "g"}
     out["g"] = [LD(tr.g[i]) for i in range(spec.n_metrics)]
     for k in ("kappa", "MWP", "CWP", "E", "case_margin"):
@@ -198,22 +201,26 @@ COUNTER_NAMES = ["branch1", "branch2", "branch3", "branch4", "branch5", "case1",
                  "feasible", "pairs", "masked_static", "masked_D", "masked_B0", "masked_E"]
 
 
-def sweep(spec, D, F, nthreads: int = 0) -> dict:
+def sweep(spec, D, F, nthreads: int = 0, quad: bool = False) -> dict:
     """Per-D argmin of E over F (lowest index on exact ties): idx (-1 if none), best, second
-    (+inf if none), kappa and case margin at winner/runner-up, and coverage counters."""
+    (+inf if none), idx2 (the runner-up's index), kappa / kappa2 at the winner / runner-up, the
+    case margin, and coverage counters.  quad=True: the binary128 instance (orc_sweep_q)."""
     h = _ProgramHolder(spec)
     D = np.ascontiguousarray(D, dtype=np.int32).reshape(-1, spec.d)
     F = np.ascontiguousarray(F, dtype=np.int32).reshape(-1, spec.p)
     nD = len(D)
     idx = np.zeros(nD, dtype=np.int32)
+    idx2 = np.zeros(nD, dtype=np.int32)
     best = np.zeros(nD)
     second = np.zeros(nD)
     kappa = np.zeros(nD)
+    kappa2 = np.zeros(nD)
     margin = np.zeros(nD)
     cnt = np.zeros(16, dtype=np.int64)
-    lib().orc_sweep(C.byref(h.pr), _p(D), nD, _p(F), len(F), _p(idx), _p(best), _p(second), _p(kappa),
-                    _p(margin), _p(cnt), nthreads)
-    return dict(idx=idx, best=best, second=second, kappa=kappa, margin=margin,
+    (lib().orc_sweep_q if quad else lib().orc_sweep)(C.byref(h.pr), _p(D), nD, _p(F), len(F), _p(idx), _p(best),
+                                                     _p(second), _p(kappa), _p(margin), _p(cnt), nthreads, _p(idx2),
+                                                     _p(kappa2))
+    return dict(idx=idx, best=best, second=second, kappa=kappa, margin=margin, idx2=idx2, kappa2=kappa2,
                 counters={k: int(cnt[i]) for i, k in enumerate(COUNTER_NAMES)})
 
 

@@ -52,16 +52,6 @@ void orc_minmax(const double *X, long long K, int n, double *lo, double *hi) {
     }
 }
 
-static ld to_u(double x, double c, int e) { return ldexpl((ld)x - (ld)c, -e); }
-
-/* Pi_k u_k^{e_k} by repeated multiplication (X_1^{u_1} ... X_n^{u_n}) */
-static ld monomial(const short *exps, int n, const ld *u) {
-  ld m = 1.0L;
-  for (int k = 0; k < n; ++k)
-    for (int t = 0; t < exps[k]; ++t) m *= u[k];
-  return m;
-}
-
 /* ------------------------------------------------------------------------------------------
  * a5 -- occupancy.  Fig. occupancysimpleflowchart: four decision
  * diamonds tried top to bottom, first "Yes" wins, else "Failure to Launch" (B_active = 0).
@@ -100,27 +90,11 @@ long long orc_active_warps(const orc_hw *hw, long long R, long long Z, long long
   return w < hw->w_max ? w : hw->w_max;
 }
 
-/* ------------------------------------------------------------------------------------------
- * a4 -- g(x) = p(u)/q(u), direct monomial sums in basis order.
- * ---------------------------------------------------------------------------------------- */
-static ld eval_pq(const orc_ratfunc *f, const ld *u, ld *kappa) {
-  ld p = 0, q = 0, pa = 0, qa = 0;
-  for (int j = 0; j < f->n_num; ++j) {
-    ld t = (ld)f->coef[j] * monomial(f->num_exp + (long)j * f->n_vars, f->n_vars, u);
-    p += t;
-    pa += fabsl(t);
-  }
-  for (int j = 0; j < f->n_den; ++j) {
-    ld t = (ld)f->coef[f->n_num + j] * monomial(f->den_exp + (long)j * f->n_vars, f->n_vars, u);
-    q += t;
-    qa += fabsl(t);
-  }
-  if (kappa) {
-    ld kp = pa / fabsl(p), kq = qa / fabsl(q);
-    *kappa = kp > kq ? kp : kq;
-  }
-  return p / q;
-}
+#define REAL ld
+#define RABS(x) fabsl(x)
+#define RFINITE(x) isfinite(x)
+#define ORC_PFX(name) name
+#include "rp_oracle_pair.inc"
 
 void orc_eval_ratfunc(const orc_ratfunc *f, const double *xc, const int *xe, const double *X,
                       long long K, long double *out, long double *kappa) {
@@ -129,197 +103,6 @@ void orc_eval_ratfunc(const orc_ratfunc *f, const double *xc, const int *xe, con
     for (int k = 0; k < f->n_vars; ++k) u[k] = to_u(X[r * f->n_vars + k], xc[k], xe[k]);
     out[r] = eval_pq(f, u, kappa ? &kappa[r] : NULL);
   }
-}
-
-static ld rel_gap(ld a, ld b) {
-  ld m = fabsl(a) > fabsl(b) ? fabsl(a) : fabsl(b);
-  return m > 0 ? fabsl(a - b) / m : 0.0L;
-}
-
-/* ------------------------------------------------------------------------------------------
- * a1..a7 -- one (D, P) pair: masks, occupancy, grid, g_i, then E (DESIGN.md Appendix A).
- * ---------------------------------------------------------------------------------------- */
-int orc_eval_pair(const orc_program *pr, const int *D, const int *P, orc_trace *tr) {
-  orc_trace t;
-  memset(&t, 0, sizeof t);
-  t.E = INFINITY;
-  t.case_margin = INFINITY;
-  const orc_hw *hw = &pr->hw;
-
-  /* Appendix A line 1 -- "multiple of the warp size (32)" and "bounded over by the maximum
-   * number of threads per block" (reading R5: <= T_max), and the footnote
-   * "P1 P2 <= D1^2 is meaningful" (reading R6: non-strict). */
-  /* reading R32: data parameters are sizes, D_k >= 1; a block dimension is >= 1 */
-  for (int k = 0; k < pr->d; ++k)
-    if (D[k] < 1) { t.mask = 6; goto done; }
-  long long T = 1;
-  for (int k = 0; k < pr->p; ++k) {
-    if (P[k] < 1) { t.mask = 1; goto done; }
-    T *= P[k];
-    if (T > hw->t_max) { t.T = T; t.mask = 2; goto done; } /* stop before the product can wrap */
-  }
-  t.T = T;
-  if (T % 32 != 0) { t.mask = 1; goto done; }
-  if (T > hw->t_max) { t.mask = 2; goto done; }
-  {
-    long long pp = P[0];
-    if (pr->p >= 2) pp *= P[1];
-    if (pp > (long long)D[0] * D[0]) { t.mask = 3; goto done; }
-  }
-
-  /* line 2 -- B_active by the flowchart; B_active = 0 cannot launch */
-  long long Z = pr->Z0 + pr->Z1 * T;
-  t.B_active = orc_active_blocks(hw, pr->R, Z, T, &t.branch);
-  if (t.B_active == 0) { t.mask = 4; goto done; }
-  /* line 3 -- Eq. (1) */
-  t.W_active = (t.B_active * T) / 32;
-  if (t.W_active > hw->w_max) t.W_active = hw->w_max;
-  /* line 4 -- grid "gx = ceil[N/bx]", one factor per tiled dimension */
-  long long blocks = 1;
-  for (int k = 0; k < pr->p && k < 3; ++k) {
-    int j = pr->grid_map[k];
-    if (j >= 0) blocks *= ((long long)D[j] + P[k] - 1) / P[k];
-  }
-  t.blocks = blocks;
-  t.sm_active = blocks < hw->n_sm ? blocks : hw->n_sm;
-
-  /* a4 -- fitted low-level metrics g_i(D, P) */
-  {
-    ld u[ORC_MAX_VARS];
-    int n = pr->d + pr->p;
-    for (int k = 0; k < pr->d; ++k) u[k] = to_u((double)D[k], pr->xc[k], pr->xe[k]);
-    for (int k = 0; k < pr->p; ++k) u[pr->d + k] = to_u((double)P[k], pr->xc[pr->d + k], pr->xe[pr->d + k]);
-    (void)n;
-    t.kappa = 0;
-    for (int i = 0; i < pr->n_metrics; ++i) {
-      ld kap;
-      t.g[i] = eval_pq(&pr->g[i], u, &kap);
-      if (kap > t.kappa) t.kappa = kap;
-    }
-  }
-
-  ld E;
-  if (pr->e_template == ORC_TEMPLATE_G1) {
-    E = t.g[0]; /* E := g_1 (used for SPEC.md:492-style pins) */
-  } else {
-    /* Appendix A lines 5-18 (Hong & Kim ISCA'09 Eqs. 1-18; reading R1, R2) */
-    const ld g1 = t.g[0], g2 = t.g[1], g3 = t.g[2];
-    const ld U = hw->uncoal_per_mw;
-    const ld Wact = (ld)t.W_active, Bact = (ld)t.B_active, SMact = (ld)t.sm_active;
-    ld Mem = g2 + g3;                                     /* 5 */
-    ld Tot = g1 + g2 + g3;                                /* 5 */
-    ld W_unc = g3 / Mem;                                  /* 6 [HK Eq.4] */
-    ld W_coal = g2 / Mem;                                 /* 6 [HK Eq.5] */
-    ld L_unc = (ld)hw->mem_ld + (U - 1) * (ld)hw->dd_unc; /* 7 [HK Eq.1] */
-    ld L_coal = (ld)hw->mem_ld;                           /* 7 [HK Eq.2] */
-    ld Mem_L = L_unc * W_unc + L_coal * W_coal;           /* 8 [HK Eq.3] */
-    ld Dep = (ld)hw->dd_unc * U * W_unc + (ld)hw->dd_coal * W_coal; /* 9 [HK Eq.6] */
-    ld MWP_nb = Mem_L / Dep;                              /* 10 [HK Eq.7] */
-    ld BWpw = (ld)hw->freq_hz * (ld)hw->load_bytes_per_warp / Mem_L; /* 11 [HK Eq.8] */
-    ld MWP_bw = (ld)hw->mem_bw / (BWpw * SMact);          /* 11 [HK Eq.9] */
-    ld MWP = MWP_nb;                                      /* 12 [HK Eq.10] */
-    if (MWP_bw < MWP) MWP = MWP_bw;
-    if (Wact < MWP) MWP = Wact;
-    ld Comp_c = (ld)hw->issue_cycles * Tot;               /* 13 [HK Eq.11] */
-    ld Mem_c = L_unc * g3 + L_coal * g2;                  /* 13 [HK Eq.12] */
-    ld CWP_full = (Mem_c + Comp_c) / Comp_c;              /* 14 [HK Eq.13] */
-    ld CWP = CWP_full < Wact ? CWP_full : Wact;           /* 14 [HK Eq.14] */
-    ld Rep = (ld)t.blocks / (Bact * SMact);               /* 15 [HK Eq.15], not ceiled (R18) */
-    ld mwp_free = MWP_nb < MWP_bw ? MWP_nb : MWP_bw;
-    ld margin = rel_gap(mwp_free, Wact);
-    ld m2 = rel_gap(CWP_full, Wact);
-    if (m2 < margin) margin = m2;
-    if (MWP == Wact && CWP == Wact) {                     /* 16 [HK Eq.16] */
-      t.mwp_case = 1;
-      E = (Mem_c + Comp_c + Comp_c / Mem * (MWP - 1)) * Rep;
-    } else {
-      ld m3 = rel_gap(CWP, MWP);
-      if (m3 < margin) margin = m3;
-      if (CWP >= MWP || (Comp_c > Mem_c)) {               /* 17 [HK Eq.17] */
-        if (!(CWP >= MWP)) {
-          ld m4 = rel_gap(Comp_c, Mem_c);
-          if (m4 < margin) margin = m4;
-        }
-        t.mwp_case = 2;
-        E = (Mem_c * Wact / MWP + Comp_c / Mem * (MWP - 1)) * Rep;
-      } else {                                            /* 18 [HK Eq.18] */
-        ld m4 = rel_gap(Comp_c, Mem_c);
-        if (m4 < margin) margin = m4;
-        t.mwp_case = 3;
-        E = (Mem_L + Comp_c * Wact) * Rep;
-      }
-    }
-    t.MWP = MWP;
-    t.CWP = CWP;
-    t.case_margin = margin;
-  }
-  /* line 19 -- reading R17: a non-finite or non-positive estimate is not a candidate */
-  if (!(isfinite(E) && E > 0)) { t.mask = 5; t.E = E; goto done; }
-  t.E = E;
-  t.feasible = 1;
-done:
-  if (tr) *tr = t;
-  return t.feasible;
-}
-
-/* ------------------------------------------------------------------------------------------
- * a8 -- "an exhaustive search is feasible": for each D, the lowest index
- * j minimising E over the candidates, by a strict-< scan in index order (reading R15: exact
- * ties go to the lowest index).  OpenMP over D: disjoint outputs, so the result does not
- * depend on the thread count.
- * ---------------------------------------------------------------------------------------- */
-void orc_sweep(const orc_program *pr, const int *D, long long nD, const int *F, int nF, int *idx,
-               double *best, double *second, double *kappa, double *margin, long long *counters,
-               int nthreads) {
-  long long cnt[16];
-  memset(cnt, 0, sizeof cnt);
-#ifdef _OPENMP
-  if (nthreads <= 0) nthreads = omp_get_max_threads();
-#endif
-#pragma omp parallel num_threads(nthreads)
-  {
-    long long lc[16];
-    memset(lc, 0, sizeof lc);
-#pragma omp for schedule(static)
-    for (long long i = 0; i < nD; ++i) {
-      const int *Di = D + i * pr->d;
-      ld b = INFINITY, s = INFINITY, kb = 0, mb = INFINITY, ms = INFINITY;
-      int bi = -1;
-      for (int j = 0; j < nF; ++j) {
-        orc_trace tr;
-        int ok = orc_eval_pair(pr, Di, F + (long)j * pr->p, &tr);
-        lc[9]++;
-        if (tr.branch >= 1 && tr.branch <= 5) lc[tr.branch - 1]++;
-        if (tr.mask == 1 || tr.mask == 2) lc[10]++;
-        if (tr.mask == 3) lc[11]++;
-        if (tr.mask == 4) lc[12]++;
-        if (tr.mask == 5) lc[13]++;
-        if (!ok) continue;
-        lc[8]++;
-        if (tr.mwp_case >= 1) lc[4 + tr.mwp_case]++;
-        if (tr.E < b) {
-          s = b;
-          ms = mb;
-          b = tr.E;
-          bi = j;
-          kb = tr.kappa;
-          mb = tr.case_margin;
-        } else if (tr.E < s) {
-          s = tr.E;
-          ms = tr.case_margin;
-        }
-      }
-      idx[i] = bi;
-      best[i] = (double)b;
-      second[i] = (double)s;
-      if (kappa) kappa[i] = (double)kb;
-      if (margin) margin[i] = (double)(mb < ms ? mb : ms);
-    }
-#pragma omp critical
-    for (int k = 0; k < 16; ++k) cnt[k] += lc[k];
-  }
-  if (counters)
-    for (int k = 0; k < 16; ++k) counters[k] = cnt[k];
 }
 
 /* ------------------------------------------------------------------------------------------

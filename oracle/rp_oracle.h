@@ -84,7 +84,19 @@ int orc_eval_pair(const orc_program *prog, const int *D, const int *P, orc_trace
  * [10] masked by warp/T_max, [11] masked by P1P2<=D1^2, [12] B_active=0, [13] E invalid.   */
 void orc_sweep(const orc_program *prog, const int *D, long long nD, const int *F, int nF,
                int *idx, double *best, double *second, double *kappa, double *margin,
-               long long *counters, int nthreads);
+               long long *counters, int nthreads, int *idx2, double *kappa2);
+/* idx2[nD] (nullable): the runner-up's index (-1 if none; on an exact tie with the winner, the
+ * next lowest index); kappa2[nD] (nullable): kappa at the runner-up.                          */
+
+/* The same two functions in IEEE binary128 (__float128, 113-bit mantissa): the identical
+ * transcription (rp_oracle_pair.inc) with 49 more mantissa bits than x87 long double.  For
+ * fitted programs whose polynomials cancel (kappa up to ~1e7) the long double evaluation is
+ * accurate to ~1e-13 only; these are accurate to ~1e-28 there.  Trace values are rounded to long
+ * double on output.  Soft-float: ~50x slower than orc_eval_pair.                              */
+int orc_eval_pair_q(const orc_program *prog, const int *D, const int *P, orc_trace *tr);
+void orc_sweep_q(const orc_program *prog, const int *D, long long nD, const int *F, int nF,
+                 int *idx, double *best, double *second, double *kappa, double *margin,
+                 long long *counters, int nthreads, int *idx2, double *kappa2);
 
 /* ---- f2: runtime decision (PAPER.md:2292-2305 step 5, 2490-2491 the six launch integers) --
  * margin == 0: the argmin of orc_sweep.  margin > 0: among the candidates with
