@@ -37,8 +37,10 @@ METRIC = "RP evals/s over (D,P) grid incl. per-D argmin at 1/2/4/8 B200; fit row
 UNIT = "evals/s"
 SAMPLE_DIV = 200  # CPU oracle sample: 1/200 of the step (5,000 D x 1,024 F and 5,000 rows x 3 metrics)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
-FLOP_PER_PAIR = 220  # a4 183 + a6 1 + a7 36 (division = 1 flop)
-FLOP_PER_D = 860     # a2 staging: 6 polys x 70 terms x 2 + data monomials
+# SURVEY.md 8(d) "Algorithmic work per unit" (large): 235 flop per evaluated (D,P) pair
+# (a4 3*2*(15+15) + 14 P-monomials + ~30 + 11 divisions) and 2*3*2*70 = 840 per D tuple (a2)
+FLOP_PER_PAIR = 235
+FLOP_PER_D = 840
 
 
 def _env_int(k, d):
@@ -178,6 +180,26 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def parity_summary():
+    """What the timed program's parity is: the -m gpu test that gates this exact workload at full
+    size (tests/test_gpu_fullsize.py) and its last committed report (profiles/)."""
+    out = {"test": "tests/test_gpu_fullsize.py::test_bench_workload_noisy_fit_sweep",
+           "gate": "SURVEY 8(c) #25 (long double oracle, kappa <= 1e3: idx exact where margin > 1e-9, "
+                   "E <= 1e-12) and, on every sampled D, E <= 1e-12 vs the binary128 oracle at the GPU's pick"}
+    for f in ("r02_parity_bench_workload.json",):
+        path = os.path.join(ROOT, "profiles", f)
+        if os.path.exists(path):
+            try:
+                rep = json.load(open(path))
+                out["report"] = "profiles/" + f
+                out["vs_binary128"] = rep.get("vs_binary128")
+                out["survey_8c_25"] = rep.get("survey_8c_25")
+                out["fit_coef_gap_inf_norm"] = rep.get("fit_coef_gap_inf_norm")
+            except (OSError, ValueError):
+                pass
+    return out
+
+
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
@@ -250,6 +272,7 @@ def main():
     # (made once: allocation and F staging are setup) is refitted in place and re-planned (a1/a5)
     # on the device, the sweep follows -- no host round trip inside a step
     plan_dev = rp.Plan([inp["truth"]], F_dev)
+    plan_dev.enable_timing()  # CUDA events around the sweep kernel / refinement inside each eval
 
     def step_dev(ev=None):
         if world == 1:
@@ -297,7 +320,7 @@ def main():
     for _ in range(2):  # every rank: the step has collectives at N > 1
         step_dev()
     torch.cuda.synchronize()
-    times, t_fit, t_sweep_k, t_plan = [], [], [], []
+    times, t_fit, t_sweep_k, t_plan, t_kern, t_ref = [], [], [], [], [], []
     for _ in range(args.steps):
         flush.zero_()  # L2 (126 MB) flushed between timed steps
         barrier()
@@ -311,18 +334,21 @@ def main():
         t_fit.append(a.elapsed_time(ev[0]))
         t_sweep_k.append(ev[1].elapsed_time(ev[2]))
         t_plan.append(ev[0].elapsed_time(ev[1]))
+        lt = plan_dev.last_timing()  # the same launch, events on its stream (rp_plan_last_timing)
+        t_kern.append(lt["sweep_ms"])
+        t_ref.append(lt["refine_ms"])
     clocks = sampler.stop() if sampler else None
     # self-check: the device-resident step and the host-API step give identical winners
     i_dev, E_dev = (t.clone() for t in step_dev())
     i_host, E_host = step()
     selfcheck = bool(torch.equal(i_dev.reshape(-1), i_host.reshape(-1)) and torch.equal(E_dev.reshape(-1), E_host.reshape(-1)))
-    step_ms = sum(times) / len(times)
-    fit_ms = sum(t_fit) / len(t_fit)
-    sweep_ms = sum(t_sweep_k) / len(t_sweep_k)
+    med = statistics.median  # the median of the timed steps
+    step_ms, fit_ms, sweep_ms = med(times), med(t_fit), med(t_sweep_k)
+    kern_ms, refine_ms = med(t_kern), med(t_ref)
     if world > 1:
-        t = torch.tensor([step_ms, fit_ms, sweep_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([step_ms, fit_ms, sweep_ms, kern_ms, refine_ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        step_ms, fit_ms, sweep_ms = t.tolist()
+        step_ms, fit_ms, sweep_ms, kern_ms, refine_ms = t.tolist()
 
     # ---- alternative sweep kernel (informational, after the timed region): k_sweep_tc, the
     # tcgen05 split-tf32 contraction + FP32 screen (RP_SWEEP_KERNEL=tc), on the same launch; its
@@ -452,7 +478,7 @@ def main():
     # ---- roofline of the dominant kernel (k_sweep) ----------------------------------------------
     pairs_eval = evaluated_pairs(inp["D"][dlo:dhi], inp["F"])
     flop_launch = pairs_eval * FLOP_PER_PAIR + (dhi - dlo) * FLOP_PER_D
-    achieved = flop_launch / (sweep_ms * 1e-3) / 1e12
+    achieved = flop_launch / (kern_ms * 1e-3) / 1e12
     traffic, counters = None, None
     prof = os.path.join(ROOT, "profiles", "sweep_ncu_latest.json")
     if os.path.exists(prof):
@@ -465,8 +491,10 @@ def main():
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DESIGN.md 'Peaks'); "
                                "measured DFMA microbenchmark 34.1 TF/s (profiles/r01_fp64_microbench.jsonl)",
-                "flop_per_launch": flop_launch, "evaluated_pairs": pairs_eval, "ms_per_launch": sweep_ms,
-                "ncu": counters}
+                "flop_per_launch": flop_launch, "flop_per_pair": FLOP_PER_PAIR, "flop_per_D": FLOP_PER_D,
+                "evaluated_pairs": pairs_eval, "ms_per_launch": kern_ms,
+                "timing": "CUDA events recorded by librp around k_sweep on its stream inside every timed step "
+                          "(rp_plan_last_timing), median", "ncu": counters}
     # fused algorithm: 1 + 2*3 symmetric 70x70 blocks per row,
     # 70*71/2 unique multiply-adds each
     gram_flop = (khi - klo) * (1 + 2 * 3) * 70 * 71
@@ -488,18 +516,24 @@ def main():
     cpu_baseline = None
     if world == 1 and not args.no_cpu_baseline:
         cores, model = cpu_info()
-        # size the sample for ~12 s of oracle work: probe on 1/SAMPLE_DIV, then rescale
+        # size each sample for ~10 s of oracle work: probe on 1/SAMPLE_DIV, then rescale
         _, dt0 = oracle_step(inp, 0, cores)
-        div = max(2, min(SAMPLE_DIV, int(SAMPLE_DIV * dt0 / 12.0)))
+        div = max(2, min(SAMPLE_DIV, int(SAMPLE_DIV * dt0 / 10.0)))
         v, dt = oracle_step(inp, 1, cores, div)
+        _, dt1 = oracle_step(inp, 2, 1, 4 * SAMPLE_DIV)
+        div1 = max(2, min(4 * SAMPLE_DIV, int(4 * SAMPLE_DIV * dt1 / 10.0)))
+        v1, dt1 = oracle_step(inp, 3, 1, div1)
         cpu_baseline = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
                         "seconds": dt, "sample": f"1/{div} of the step (second slice): fit of 3 metrics on "
-                                               f"{K // div} rows + sweep of {nD // div} D x {nF} F"}
+                                               f"{K // div} rows + sweep of {nD // div} D x {nF} F",
+                        "one_core": {"value": v1, "cores": 1, "seconds": dt1,
+                                     "sample": f"1/{div1} of the step (fourth slice): fit on {K // div1} rows + "
+                                               f"sweep of {nD // div1} D x {nF} F"}}
 
     # fit: minmax part / final, xform, xform_to_basis, gram_ws, gram_fused_sum, gram_fused_reduce,
-    # solve (8); plan update: plan_refresh (1); sweep: bucket count / scan / scatter, sweep (4)
+    # solve (8); plan update: plan_refresh (1); sweep: bucket count / scan / scatter, sweep, refine (5)
     # (the ncu launch list of this command, profiles/r01_launches_bench.txt, shows the same 13)
-    launches_per_step = 13
+    launches_per_step = 14
     out = {"metric": METRIC, "value": nD * nF / (step_ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -508,7 +542,8 @@ def main():
                       "parallelism": f"dp{world}: D and K rows sharded, Gram all_reduce, winners all_gather",
                       "l2": "flushed between timed steps (256 MiB write); inputs 64 MB"},
            "fit_rows_per_s": K / (fit_ms * 1e-3), "fit_ms": fit_ms,
-           "sweep_evals_per_s": nD * nF / (sweep_ms * 1e-3), "sweep_kernel_ms": sweep_ms,
+           "sweep_evals_per_s": nD * nF / (sweep_ms * 1e-3), "sweep_ms": sweep_ms, "sweep_kernel_ms": kern_ms,
+           "refine_ms": refine_ms, "parity": parity_summary(),
            "plan_update_ms": sum(t_plan) / len(t_plan),
            "evaluated_pairs_per_s": (pairs_eval if world == 1 else evaluated_pairs(inp["D"], inp["F"])) / (sweep_ms * 1e-3),
            "roofline": roofline, "roofline_fit": roofline_fit, "cpu_baseline": cpu_baseline, "e2e": e2e,

@@ -300,6 +300,15 @@ rp_status rp_plan_update_program(rp_plan plan, int32_t prog, const double *coef,
                                  const double *xform, rp_stream s);
 rp_status rp_plan_destroy(rp_plan plan);
 
+/* Per-phase device timing of rp_plan_eval_argmin (measurement support; off by default).
+ * rp_plan_enable_timing(plan, 1) creates CUDA events that every later rp_plan_eval_argmin records
+ * on its stream around its phases; rp_plan_last_timing waits for the last call's final event and
+ * writes ms[0] = tuple grouping (the D1 buckets), ms[1] = the sweep kernel (a1-a8),
+ * ms[2] = the winner refinement (k_refine; 0 when disabled by RP_SWEEP_REFINE=0).  ms host
+ * float[3].  INVALID_ARG if timing was not enabled.  Events add ~2 us per call.               */
+rp_status rp_plan_enable_timing(rp_plan plan, int32_t on);
+rp_status rp_plan_last_timing(rp_plan plan, float *ms);
+
 /* ---- f2: runtime decision service ----------------------------------------------------------
  * One decision per data tuple, as the paper's driver program makes before every kernel launch
  * (PAPER.md:2094-2099): evaluate R over F, take the optimum (step 5) and

@@ -115,6 +115,8 @@ _SIGS = {
     "rp_decider_destroy": [_vp],
     "rp_plan_history_stats": [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)],
     "rp_plan_history_clear": [_vp, _vp],
+    "rp_plan_enable_timing": [_vp, _i32],
+    "rp_plan_last_timing": [_vp, _vp],
 }
 for _name, _args in _SIGS.items():
     getattr(_lib, _name).argtypes = _args
@@ -418,6 +420,16 @@ class Plan:
 
     def clear_history(self):
         _check(_lib.rp_plan_history_clear(self.handle, C.c_void_p(0)))
+
+    def enable_timing(self, on: bool = True):
+        """Per-phase CUDA events in every later eval (rp_plan_enable_timing)."""
+        _check(_lib.rp_plan_enable_timing(self.handle, 1 if on else 0))
+
+    def last_timing(self) -> dict:
+        """ms of the last eval's phases: D1 grouping, sweep kernel, winner refinement."""
+        ms = (C.c_float * 3)()
+        _check(_lib.rp_plan_last_timing(self.handle, ms))
+        return {"group_ms": ms[0], "sweep_ms": ms[1], "refine_ms": ms[2]}
 
     def close(self):
         if self.handle:

@@ -357,6 +357,9 @@ struct rp_plan_s {
   cudaStream_t stream = nullptr;
   HistTable hist;
   int n_deciders = 0;  // live rp_decider objects whose captured graph holds hist.slots
+  // rp_plan_enable_timing: events around the phases of the last rp_plan_eval_argmin
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, sweep, refine, end
 };
 
 static void plan_free(rp_plan pl) {
@@ -371,6 +374,8 @@ static void plan_free(rp_plan pl) {
     cudaFree(pl->hist.slots);
     cudaFree(pl->hist.counters);
   }
+  for (cudaEvent_t &e : pl->ev)
+    if (e) cudaEventDestroy(e);
   delete pl;
 }
 
@@ -421,13 +426,16 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   const int nde_pad = std::max(4, (pl->nde_max + 3) & ~3);
   const size_t nrec = (size_t)n_prog * nFp;                               // CfgRec (64 B)
   const size_t ncm = (size_t)n_prog * kMaxPolys * npe_pad * nde_pad;      // Cmat
-  const size_t nd = 2 * (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab + ncm;  // mP x2, rSM, Cmat
+  const size_t nrt = (size_t)n_prog * npe_pad * nde_pad;                  // refinement terms
+  const size_t nd = 2 * (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab + ncm +  // mP x2, rSM, Cmat,
+                    nrt * kMaxPolys + (size_t)n_prog * 8;                                   // rcoef, rinfo
+  const size_t ni = 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16 + nrt * 4 + nrec * 4;  // rec, srec, nFc, rterm, inv
   // stream-ordered pool allocations (a synchronous cudaMalloc/cudaFree per plan costs ms)
   if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
-  if ((e = cudaMallocAsync((void **)&pl->buf_i, 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16, s)) != cudaSuccess) return fail(e, "alloc");
+  if ((e = cudaMallocAsync((void **)&pl->buf_i, ni, s)) != cudaSuccess) return fail(e, "alloc");
   if ((e = cudaMallocAsync((void **)&pl->buf_d, nd * 8, s)) != cudaSuccess) return fail(e, "alloc");
   // zero padding entries: padded configurations read as m_pe = 0 by the DMMA tiles
-  if ((e = cudaMemsetAsync(pl->buf_i, 0, 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16, s)) != cudaSuccess) return fail(e, "memset");
+  if ((e = cudaMemsetAsync(pl->buf_i, 0, ni, s)) != cudaSuccess) return fail(e, "memset");
   if ((e = cudaMemsetAsync(pl->buf_d, 0, nd * 8, s)) != cudaSuccess) return fail(e, "memset");
   pl->tab.nFp = nFp;
   pl->tab.rec = reinterpret_cast<CfgRec *>(pl->buf_i);
@@ -438,6 +446,22 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   pl->tab.rSM = pl->tab.smP + (size_t)n_prog * nFp * npe_pad;
   pl->tab.Cmat = pl->tab.rSM + (size_t)n_prog * kRSMTab;
   pl->tab.nde_pad = nde_pad;
+  pl->tab.rcoef = pl->tab.Cmat + ncm;  // even offset (ncm and kRSMTab even): 16-byte aligned
+  pl->tab.rinfo = pl->tab.rcoef + nrt * kMaxPolys;
+  pl->tab.rterm = pl->tab.nFc + 2 * n_prog + 4;
+  pl->tab.inv = pl->tab.rterm + nrt;
+  pl->tab.nrt_max = 1;
+  for (int g = 0; g < n_prog; ++g) {  // distinct (pe, de) pairs over the polynomials' terms
+    std::vector<char> seen((size_t)npe_pad * nde_pad, 0);
+    int cnt = 0;
+    for (int r = 0; r < hp[g].npoly * hp[g].nPE; ++r)
+      for (int j = hp[g].row_start[r]; j < hp[g].row_start[r + 1]; ++j) {
+        char &c = seen[(size_t)(r % hp[g].nPE) * nde_pad + hp[g].term_de[j]];
+        cnt += c == 0;
+        c = 1;
+      }
+    pl->tab.nrt_max = std::max(pl->tab.nrt_max, cnt);
+  }
   // the DevProg blob is staged through pinned-free pageable memory: copy synchronously w.r.t.
   // the host buffer lifetime (cudaMemcpyAsync from pageable memory returns after staging)
   if ((e = cudaMemcpyAsync(pl->d_progs, hp.data(), sizeof(DevProg) * n_prog, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -478,6 +502,7 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
   if ((st = stage_out(second_E, no, ts, &ds, &hs, s)) != RP_OK) return st;
   // group tuples by D1 (only D1 < kb, kb^2 > T_max >= P1 P2, can fail the D rule) so whole
   // configuration octets are skipped by the sweep's early exit; pays off on large batches
+  if (pl->timing) RP_CUDA(cudaEventRecord(pl->ev[0], s));
   Tmp tperm;
   const int32_t *perm = nullptr;
   if (nD >= 4096 && nD <= 0x7fffffffll && pl->kb < 255) {
@@ -487,8 +512,16 @@ static rp_status plan_eval(rp_plan pl, const int32_t *D, int64_t nD, int32_t *be
     RP_CUDA(launch_bucket_perm(dD, nD, pl->d, kb, (unsigned *)(p + nD), p, s));
     perm = p;
   }
+  // the runner-ups' indices, for the refinement of the runner-up (rp_sweep.cu k_refine)
+  Tmp tidx2;
+  int32_t *idx2 = nullptr;
+  if (ds) {
+    RP_CUDA(tidx2.alloc(no * 4, s));
+    idx2 = (int32_t *)tidx2.p;
+  }
   RP_CUDA(launch_sweep(pl->d_progs, pl->n_prog, pl->mwp, pl->tab, pl->npe_pad, pl->nde_max, pl->n_sm_max,
-                       pl->d, dD, nD, di, db, ds, perm, s));
+                       pl->d, dD, nD, di, db, ds, perm, idx2, pl->timing ? pl->ev : nullptr, s));
+  if (pl->timing) RP_CUDA(cudaEventRecord(pl->ev[3], s));
 
   if (hi) RP_CUDA(cudaMemcpyAsync(best_idx, di, no * 4, cudaMemcpyDeviceToHost, s));
   if (hb) RP_CUDA(cudaMemcpyAsync(best_E, db, no * 8, cudaMemcpyDeviceToHost, s));
@@ -1279,6 +1312,24 @@ rp_status rp_plan_history_clear(rp_plan plan, rp_stream sv) {
   cudaStream_t s = (cudaStream_t)sv;
   RP_CUDA(cudaMemsetAsync(plan->hist.slots, 0, ((size_t)plan->hist.mask + 1) * sizeof(HistSlot), s));
   RP_CUDA(cudaMemsetAsync(plan->hist.counters, 0, 3 * sizeof(unsigned long long), s));
+  return RP_OK;
+}
+
+rp_status rp_plan_enable_timing(rp_plan plan, int32_t on) {
+  RP_REQUIRE(plan, RP_ERR_INVALID_ARG, "null plan");
+  if (on && !plan->ev[0])
+    for (cudaEvent_t &e : plan->ev) RP_CUDA(cudaEventCreate(&e));
+  plan->timing = on != 0;
+  return RP_OK;
+}
+
+rp_status rp_plan_last_timing(rp_plan plan, float *ms) {
+  RP_REQUIRE(plan && ms, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(plan->timing, RP_ERR_INVALID_ARG, "timing not enabled (rp_plan_enable_timing)");
+  RP_CUDA(cudaEventSynchronize(plan->ev[3]));
+  RP_CUDA(cudaEventElapsedTime(&ms[0], plan->ev[0], plan->ev[1]));
+  RP_CUDA(cudaEventElapsedTime(&ms[1], plan->ev[1], plan->ev[2]));
+  RP_CUDA(cudaEventElapsedTime(&ms[2], plan->ev[2], plan->ev[3]));
   return RP_OK;
 }
 

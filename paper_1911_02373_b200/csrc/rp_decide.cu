@@ -144,10 +144,12 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(DecideArgs a) {
   const EConst kc = make_econst(pg);
   const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
             map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
-  const int32_t Da = map0 >= 0 ? sD[map0] : 1, Db = map1 >= 0 ? sD[map1] : 1, Dc = map2 >= 0 ? sD[map2] : 1;
-  const int64_t D1sq = (int64_t)sD[0] * sD[0];
   bool dpos = true;  // reading R32: data parameters are sizes >= 1
   for (int k = 0; k < d; ++k) dpos = dpos && sD[k] >= 1;
+  // (a masked tuple's grid is computed from 1s so that no table index goes out of range)
+  const int32_t Da = map0 >= 0 && dpos ? sD[map0] : 1, Db = map1 >= 0 && dpos ? sD[map1] : 1,
+                Dc = map2 >= 0 && dpos ? sD[map2] : 1;
+  const int64_t D1sq = (int64_t)sD[0] * sD[0];
   const int n_sm = pg.n_sm;
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
 

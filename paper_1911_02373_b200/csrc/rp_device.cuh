@@ -9,22 +9,22 @@ namespace rp {
 struct Best {
   double e;   // best E (+inf: none)
   int32_t i;  // its original config index (INT_MAX: none)
-  double s;   // second-smallest E among the others
+  double s;   // the runner-up's E: the second-smallest (E, index) key among the others
+  int32_t j;  // the runner-up's original index (meaningful where s < +inf)
 };
 __device__ __forceinline__ bool key_less(double e1, int32_t i1, double e2, int32_t i2) {
   return e1 < e2 || (e1 == e2 && i1 < i2);
 }
 __device__ __forceinline__ Best merge(const Best &a, const Best &b) {
+  const bool aw = key_less(a.e, a.i, b.e, b.i);
+  const Best &w = aw ? a : b, &l = aw ? b : a;
   Best r;
-  if (key_less(a.e, a.i, b.e, b.i)) {
-    r.e = a.e;
-    r.i = a.i;
-    r.s = fmin(a.s, b.e);
-  } else {
-    r.e = b.e;
-    r.i = b.i;
-    r.s = fmin(b.s, a.e);
-  }
+  r.e = w.e;
+  r.i = w.i;
+  // runner-up: the better of the winner's runner-up and the loser's best
+  const bool ls = key_less(l.e, l.i, w.s, w.j);
+  r.s = ls ? l.e : w.s;
+  r.j = ls ? l.i : w.j;
   return r;
 }
 __device__ __forceinline__ Best shfl_xor(const Best &a, int m) {
@@ -32,6 +32,7 @@ __device__ __forceinline__ Best shfl_xor(const Best &a, int m) {
   r.e = __shfl_xor_sync(0xffffffffu, a.e, m);
   r.i = __shfl_xor_sync(0xffffffffu, a.i, m);
   r.s = __shfl_xor_sync(0xffffffffu, a.s, m);
+  r.j = __shfl_xor_sync(0xffffffffu, a.j, m);
   return r;
 }
 

@@ -81,6 +81,12 @@ struct CfgTable {
                    // row k * npe_pad + pe, column de: coef of m_de(u_D) m_pe(u_P) in poly k
   int32_t nde_pad; // data-part monomials padded to a multiple of 4 (the DMMA K step)
   int32_t *nFc;    // [n_prog][2]: number of feasible configurations, sorted flag
+  // winner refinement (k_refine): the union of the polynomials' (de, pe) terms
+  int32_t *rterm;  // [n_prog][npe_pad * nde_pad]: de | pe << 16 of term j (j < nRT)
+  double *rcoef;   // [n_prog][npe_pad * nde_pad][kMaxPolys]: coefficient of term j in poly k
+  double *rinfo;   // [n_prog][8]: A_k = sum_j |rcoef[j][k]| (k < 6), max total degree, nRT
+  int32_t *inv;    // [n_prog][nFp]: original index -> position in srec (-1: statically infeasible)
+  int32_t nrt_max; // host bound on the union term count of any program (shared-memory sizing)
 };
 constexpr int kRSMTab = 1024;  // n_sm <= 1023 uses the table
 
@@ -94,7 +100,8 @@ cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_
 cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
                          int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
                          int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
-                         cudaStream_t s);
+                         int32_t *idx2, cudaEvent_t *ev /* nullable: [1] before the sweep kernel,
+                         [2] before the refinement */, cudaStream_t s);
 cudaError_t launch_bucket_perm(const int32_t *d_D, int64_t nD, int d, int kb, unsigned *d_hist,
                                int32_t *d_perm, cudaStream_t s);
 cudaError_t launch_eval_metrics(const DevProg *d_prog, int nm, const double *X, int64_t K,

@@ -38,6 +38,8 @@ __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_
   return 0;                                                                             // fail
 }
 
+__device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab, int npe_pad);
+
 // ---- a1 + a5 + P-monomials, compaction in index order --------------------------------------
 __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, const int32_t *F,
                                                        int nF, int npe_pad, CfgTable tab) {
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
     }
     __syncthreads();
     const int pos = base + warp_tot[wid] + pre;
+    if (c < nF) tab.inv[(int64_t)g * nFp + c] = ok ? pos : -1;
     if (ok) {
       const int64_t off = (int64_t)g * nFp;
       CfgRec r;
@@ -172,6 +175,8 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
   // 1/k for SM_act = k (line 15 of Appendix A); correctly rounded, computed once per plan
   for (int k = threadIdx.x; k < kRSMTab; k += blockDim.x)
     tab.rSM[(int64_t)g * kRSMTab + k] = k > 0 ? 1.0 / (double)k : 0.0;
+  __syncthreads();
+  build_refine_terms(g, pg, tab, npe_pad);
 }
 
 // rp_plan_update_program in one launch: the configuration table (a1 masks, a5 occupancy, the
@@ -214,6 +219,8 @@ __global__ void __launch_bounds__(1024) k_plan_refresh(DevProg *pgp, int g, cons
     for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
       Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
   }
+  __syncthreads();
+  build_refine_terms(g, pg, tab, npe_pad);
 }
 
 cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, int stride, const double *d_xf,
@@ -305,6 +312,7 @@ struct SweepArgs {
   double *bestE;
   double *secondE;
   const int32_t *perm;  // tuple order of the tiles (grouped by D1), or null: identity
+  int32_t *idx2 = nullptr;  // runner-up's original index [n_prog][nD] (SECOND; for the refinement)
   const unsigned char *tcpack = nullptr;  // k_sweep_tc: per-tile B operands, ||m||, records
   int tc_ntiles = 0;
 };
@@ -429,14 +437,16 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   const int64_t D1sq = D1 * D1;
   // the a3 test in 32 bits: P1 P2 of a compacted configuration is <= T_max < 2^31
   const int32_t D1sq32 = D1sq < 0x7fffffffll ? (int32_t)D1sq : 0x7fffffff;
-  const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1,
-                Dc = map2 >= 0 ? Dt[map2] : 1;
+  // (a tuple with some D_k < 1 is masked; its grid is computed from 1s so no index goes wild)
+  const int32_t Da = map0 >= 0 && dpos ? Dt[map0] : 1, Db = map1 >= 0 && dpos ? Dt[map1] : 1,
+                Dc = map2 >= 0 && dpos ? Dt[map2] : 1;
   const double *arow = sC + t * CS + (lane & 3);
 
   Best st;
   st.e = kInf;
   st.i = 0x7fffffff;
   st.s = kInf;
+  st.j = 0x7fffffff;
 
   // the largest D1^2 among the warp's tuples (a3 early exit over configurations sorted by P1 P2)
   int64_t maxD1sq = tok ? D1sq : 0;
@@ -502,7 +512,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       // running best are positive or +inf, so their bit patterns compare as integers)
       const long long eb = __double_as_longlong(E), sb = __double_as_longlong(st.e);
       const bool better = eb < sb || (eb == sb && orig < st.i);
-      if (SECOND) st.s = better ? st.e : fmin(st.s, E);
+      if (SECOND) {  // runner-up on the same exact key
+        const bool sec = !better && key_less(E, orig, st.s, st.j);
+        st.s = better ? st.e : (sec ? E : st.s);
+        st.j = better ? st.i : (sec ? orig : st.j);
+      }
       st.i = better ? orig : st.i;
       st.e = better ? E : st.e;
     }
@@ -529,406 +543,14 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
   st = merge(st, shfl_xor(st, 1));
   st = merge(st, shfl_xor(st, 2));
-  if ((lane & 3) == 0 && tok) {
+  if ((lane & 3) == 0 && t < tmax) {  // every tuple of the tile is written (-1 / +inf if none)
     const int64_t o = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t);
     a.idx[o] = (st.e < kInf) ? st.i : -1;
     a.bestE[o] = st.e;
-    if (SECOND) a.secondE[o] = st.s;
-  }
-}
-
-// ============================================================================================
-// Warp-specialised screened sweep (RP_SWEEP_KERNEL=ws; measured 6.1 ms vs k_sweep's 5.1 ms at
-// `large`, see DESIGN.md -- kept, parity-tested, as the base of the next round's persistent,
-// octet-scheduled version).
-//
-// k_sweep issues its DMMAs and its E epilogue from the same warps, and the measured kernel time
-// is close to the sum of the two (contraction alone 2.35 ms, whole kernel 5.1 ms at `large`):
-// the tensor pipe idles while a warp's epilogue chain runs.  Here each CTA pairs, per octet of
-// tuples, an MMA warp and a screen warp on the same SM sub-partition:
-//   MMA warp:    A fragments (the octet's staged C) in registers, one DMMA tile (8 tuples x 8
-//                configurations x 2l polynomials) per configuration octet into a 3-slot ring in
-//                shared memory (mbarrier full / empty handshake);
-//   screen warp: reads the tile, evaluates E in FP32 with a proven relative error bound
-//                (mwpcwp_E32, kScreenEta), keeps per lane the smallest screened keys, and at the
-//                end re-evaluates those candidates exactly in FP64; the tuple falls back to the
-//                full FP64 sweep (DMMA, on the screen warp) whenever a key that was not kept could
-//                reach the winner or the runner-up (rare).
-// The FP64 datapath then carries only the DMMAs; the screen's FP32/integer work runs on the other
-// pipes of the sub-partition (tools/microbench/ws_overlap.cu: DMMA warps and FFMA warps of a
-// sub-partition overlap to within 1.11x of the slower).
-// ============================================================================================
-constexpr int kSwPairs = 4;                  // tuple octets per CTA: one MMA warp each (one per SMSP)
-constexpr int kSwScreens = 3;                // screen warps per octet (same SMSP), tiles round-robin
-constexpr int kSwThreads = 32 * kSwPairs * (1 + kSwScreens);  // 512
-constexpr int kSwSlots = 2 * kSwScreens;     // ring slots per octet (slot oc % 6, consumer oc % 3)
-
-template <int NPOLY, int NPE>
-size_t sweep_ws_smem_bytes(int nde_stride, int n_sm) {
-  const int rsm = (n_sm + 2) & ~1;
-  return sizeof(double) * ((size_t)kTD * c_stride<NPOLY, NPE>() + (size_t)kTD * nde_stride + rsm) +
-         sizeof(float) * ((rsm + 3) & ~3) + sizeof(uint64_t) * 2 * kSwPairs * kSwSlots +
-         sizeof(double) * (size_t)kSwPairs * kSwSlots * NPOLY * 64 + sizeof(int32_t) * kTD * kMaxVars +
-         sizeof(double) * 4 * kSwPairs * kSwScreens * 8;  // the screens' partial results per quad
-}
-
-__device__ __forceinline__ uint32_t sw_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void sw_mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sw_smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void sw_mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sw_smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void sw_mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(sw_smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-template <int NPE, bool SECOND>
-__global__ void __launch_bounds__(kSwThreads, 1) k_sweep_ws(SweepArgs a) {
-  constexpr int NPOLY = 6;
-  constexpr int KS = NPE / 4;
-  constexpr int CS = c_stride<NPOLY, NPE>();
-  constexpr int KC = SECOND ? 2 : 1;  // screened candidates kept per lane (4 lanes per tuple)
-  constexpr double kInf = __builtin_huge_val();
-  const int g = blockIdx.y;
-  const DevProg &pg = a.progs[g];
-  const int d = a.d;
-  const int64_t d0 = (int64_t)blockIdx.x * kTD;
-  const int tmax = (int)((a.nD - d0) < kTD ? (a.nD - d0) : kTD);
-  const int nde = a.nde_stride;
-  const int n_sm = pg.n_sm;  // < kRSMTab (compile_program)
-  const int rsm = (n_sm + 2) & ~1;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
-  extern __shared__ __align__(16) double smem[];
-  double *sC = smem;                                          // [kTD][CS]
-  double *sMD = sC + kTD * CS;                                // [kTD][nde]
-  double *sRSM = sMD + kTD * nde;                             // [rsm]
-  float *sRSM32 = reinterpret_cast<float *>(sRSM + rsm);      // [rsm]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sRSM32 + ((rsm + 3) & ~3));  // [kSwPairs][kSwSlots][2]: full, empty
-  // (bars: 2 kSwPairs kSwSlots = 24 words, so the ring below stays 16-byte aligned for double2)
-  double *ring = reinterpret_cast<double *>(bars + 2 * kSwPairs * kSwSlots);  // [kSwPairs][kSwSlots][NPOLY][64]
-  double *part = ring + kSwPairs * kSwSlots * NPOLY * 64;  // [kSwPairs][kSwScreens][8 quads][4]: e, s, i, tnc|ovf
-  int32_t *sDv = reinterpret_cast<int32_t *>(part + 4 * kSwPairs * kSwScreens * 8);  // [kTD][kMaxVars]
-
-  if (threadIdx.x < 2 * kSwPairs * kSwSlots) sw_mbar_init(bars + threadIdx.x, 32);
-  // ---- a2: stage the tile (D values, data monomials, data polynomials), all warps ---------------
-  const int nDE = pg.nDE, ndp = a.tab.nde_pad;
-  for (int i = threadIdx.x; i < kTD * d; i += blockDim.x) {
-    const int t = i / d, k = i % d;
-    const int64_t src = (t < tmax) ? (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t) : 0;
-    sDv[t * kMaxVars + k] = (t < tmax) ? a.D[src * d + k] : 1;
-  }
-  const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
-  for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) {
-    sRSM[i] = gRSM[i];
-    sRSM32[i] = (float)gRSM[i];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kTD * ndp; i += blockDim.x) {
-    const int t = i / ndp, de = i % ndp;
-    double m = 0.0;
-    if (de < nDE) {
-      m = 1.0;
-      for (int k = 0; k < d; ++k) {
-        const double u = ((double)sDv[t * kMaxVars + k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
-        for (int e = 0; e < pg.de_exp[de][k]; ++e) m *= u;
-      }
+    if (SECOND) {
+      a.secondE[o] = st.s;
+      if (a.idx2) a.idx2[o] = st.s < kInf ? st.j : -1;
     }
-    sMD[t * nde + de] = m;
-  }
-  __syncthreads();
-  {
-    const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
-    constexpr int MT = NPOLY * NPE / 8;
-    constexpr int NT = kTD / 8;
-    for (int tile = wid; tile < MT * NT; tile += kSwThreads / 32) {
-      const int mt = tile / NT, nt = tile % NT;
-      double c0 = 0.0, c1 = 0.0;
-      for (int ks = 0; ks < ndp / 4; ++ks) {
-        const double av = __ldg(Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3));
-        const double bv = sMD[(nt * 8 + (lane >> 2)) * nde + ks * 4 + (lane & 3)];
-        dmma(c0, c1, av, bv);
-      }
-      const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
-      sC[t * CS + row] = c0;
-      sC[(t + 1) * CS + row] = c1;
-    }
-  }
-  __syncthreads();
-
-  const int o = wid & (kSwPairs - 1);         // this warp's tuple octet
-  const bool mma_role = wid < kSwPairs;       // warps o, o + 4, o + 8, o + 12 share a sub-partition
-  const int sub = (wid >> 2) - 1;             // screen warps: 0 .. kSwScreens - 1
-  const int t = o * 8 + (lane >> 2);
-  const bool tok = t < tmax;
-  const int nFc = a.tab.nFc[2 * g];
-  const bool sorted = a.tab.nFc[2 * g + 1] != 0;
-  const int nFp = a.tab.nFp;
-  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
-  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
-  const double *arow = sC + t * CS + (lane & 3);
-  const int32_t *Dt = sDv + t * kMaxVars;
-  const int64_t D1 = Dt[0];
-  const int64_t D1sq = D1 * D1;
-  int64_t maxD1sq = tok ? D1sq : 0;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const int64_t x = __shfl_xor_sync(0xffffffffu, maxD1sq, off);
-    maxD1sq = x > maxD1sq ? x : maxD1sq;
-  }
-  const int nOctF = (nFc + 7) >> 3;
-  int nEff = (o * 8 < tmax) ? nOctF : 0;  // a3 early exit (configurations sorted by P1 P2)
-  if (sorted && nEff > 0)
-    for (int b0 = 0; b0 < nOctF; b0 += 32) {
-      const int oc = b0 + lane;
-      const unsigned stop = __ballot_sync(0xffffffffu, oc < nOctF && __ldg(&rec[oc * 8].P01) > maxD1sq);
-      if (stop) {
-        nEff = b0 + __ffs(stop) - 1;
-        break;
-      }
-    }
-  uint64_t *full = bars + o * kSwSlots * 2, *empty = full + 1;  // slot s: full[2 s], empty[2 s]
-  double *myring = ring + (size_t)o * kSwSlots * NPOLY * 64;
-
-  auto mma_tile = [&](int oc, double (&acc)[NPOLY][2], const double (&afr)[NPOLY][KS]) {
-    double bfr[KS];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
-#pragma unroll
-    for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], afr[k][ks], bfr[ks]);
-  };
-
-  if (mma_role) {
-    // ---- MMA warp: a4 tiles into the ring (B fragments of the next tile prefetched) ----------
-    double afr[NPOLY][KS];
-#pragma unroll
-    for (int k = 0; k < NPOLY; ++k)
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
-    double bnext[KS];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-      bnext[ks] = nEff > 0 ? __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + (lane >> 2)) : 0.0;
-    for (int oc = 0; oc < nEff; ++oc) {
-      const int sl = oc % kSwSlots, use = oc / kSwSlots;
-      double bfr[KS];
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) bfr[ks] = bnext[ks];
-      if (oc + 1 < nEff)
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
-          bnext[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + (oc + 1) * 8 + (lane >> 2));
-      double acc[NPOLY][2];
-#pragma unroll
-      for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-        for (int k = 0; k < NPOLY; ++k) dmma(acc[k][0], acc[k][1], afr[k][ks], bfr[ks]);
-      if (use > 0) sw_mbar_wait(empty + 2 * sl, (use - 1) & 1);
-      double *dst = myring + sl * NPOLY * 64 + 2 * lane;
-#pragma unroll
-      for (int k = 0; k < NPOLY; ++k) *reinterpret_cast<double2 *>(dst + k * 64) = make_double2(acc[k][0], acc[k][1]);
-      sw_mbar_arrive(full + 2 * sl);
-    }
-    return;
-  }
-
-  // ---- screen warp ---------------------------------------------------------------------------
-  const EConst kc = make_econst(pg);
-  const EConst32 kc32 = to_econst32(kc);
-  const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1,
-            map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
-  const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
-  // a6: #Blocks = prod ceil(D / P), exact integers.  A grid dimension with no
-  // data parameter has D = 1, whose factor ceil(1 / P) is 1: all three are multiplied (branch-free)
-  auto grid_blocks = [&](const longlong2 &h0, const int4 &h1, const int4 &h2) -> int64_t {
-    const uint32_t s012 = (uint32_t)h2.y;
-    return ceil_div_magic(Da, (int32_t)(h0.y >> 32), (uint32_t)h1.z, s012 & 255) *
-           ceil_div_magic(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) *
-           ceil_div_magic(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
-  };
-  // the exact FP64 evaluation of one pair (a3, a6, a7): E, +inf when masked
-  auto pair_E64 = [&](const CfgRec *cr, const double *pk, int32_t &orig) -> double {
-    const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
-    const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
-    const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
-    const double2 h3 = __ldg(reinterpret_cast<const double2 *>(cr) + 3);
-    orig = (int32_t)(h0.y & 0xffffffff);
-    const bool ok = tok && h0.x <= D1sq;  // a3
-    const int64_t blocks = grid_blocks(h0, h1, h2);
-    const int64_t smact = blocks < n_sm ? blocks : n_sm;
-    const double rSM = sRSM[smact];
-    const double Rep = (double)blocks * h3.x * rSM;  // line 15
-    const double E = mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], __hiloint2double(h2.w, h2.z), Rep, rSM,
-                              (double)smact, kc);
-    return (ok && pos_finite(E)) ? E : kInf;  // line 19, R17
-  };
-  auto take = [](Best &b, double E, int32_t orig) {  // a8: exact key (E, original index)
-    const long long eb = __double_as_longlong(E), sb = __double_as_longlong(b.e);
-    const bool better = eb < sb || (eb == sb && orig < b.i);
-    if (SECOND) b.s = better ? b.e : fmin(b.s, E);
-    b.i = better ? orig : b.i;
-    b.e = better ? E : b.e;
-  };
-
-  float ck[KC];
-  int cp[KC];
-#pragma unroll
-  for (int i = 0; i < KC; ++i) {
-    ck[i] = __int_as_float(0x7f800000);
-    cp[i] = 0x7fffffff;
-  }
-  float tnc = __int_as_float(0x7f800000);  // smallest screened key not kept
-  bool ovf = false;                        // an untrusted pair (key -1) fell off the list
-  for (int oc = sub; oc < nEff; oc += kSwScreens) {
-    const int sl = oc % kSwSlots, use = oc / kSwSlots;
-    sw_mbar_wait(full + 2 * sl, use & 1);
-    const double *src = myring + sl * NPOLY * 64 + 2 * lane;
-    double2 pv[NPOLY];
-#pragma unroll
-    for (int k = 0; k < NPOLY; ++k) pv[k] = *reinterpret_cast<const double2 *>(src + k * 64);
-    sw_mbar_arrive(empty + 2 * sl);
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int pos = oc * 8 + 2 * (lane & 3) + v;
-      const CfgRec *cr = rec + pos;
-      const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
-      const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
-      const int4 h2 = __ldg(reinterpret_cast<const int4 *>(cr) + 2);
-      const int2 h3 = __ldg(reinterpret_cast<const int2 *>(cr) + 7);  // W32, rB32
-      const bool ok = tok && h0.x <= D1sq;                               // a3
-      const int64_t blocks = grid_blocks(h0, h1, h2);
-      const int smact = (int)(blocks < n_sm ? blocks : n_sm);
-      const float rSMf = sRSM32[smact];
-      const float Rep = (float)blocks * __int_as_float(h3.y) * rSMf;
-      double p[NPOLY];
-#pragma unroll
-      for (int k = 0; k < NPOLY; ++k) p[k] = v ? pv[k].y : pv[k].x;
-      bool unc;
-      const float E32 = mwpcwp_E32((float)p[0], (float)p[1], (float)p[2], (float)p[3], (float)p[4], (float)p[5],
-                                   __int_as_float(h3.x), Rep, rSMf, (float)smact, kc32, unc);
-      // masked pairs enter as +inf: never kept, never counted (branch-free insertion)
-      float k = ok ? (unc ? -1.0f : E32) : __int_as_float(0x7f800000);
-      int q = pos;
-#pragma unroll
-      for (int i = 0; i < KC; ++i) {  // positions grow along the stream: ties keep the earlier
-        const bool lt = k < ck[i];
-        const float tk = ck[i];
-        const int tq = cp[i];
-        ck[i] = lt ? k : tk;
-        cp[i] = lt ? q : tq;
-        k = lt ? tk : k;
-        q = lt ? tq : q;
-      }
-      ovf = ovf | (k < 0.f);  // (k, q) fell off the list (or was never kept)
-      tnc = fminf(tnc, k);
-    }
-  }
-  // the lane's candidates in FP64: scalar dot products over the staged data polynomials and the
-  // configuration's monomials, then the exact pair evaluation; the quad's exact argmin
-  Best st;
-  st.e = kInf;
-  st.i = 0x7fffffff;
-  st.s = kInf;
-#pragma unroll
-  for (int i = 0; i < KC; ++i) {
-    if (cp[i] != 0x7fffffff) {
-      const int pos = cp[i];
-      double mv[NPE];
-#pragma unroll
-      for (int pe = 0; pe < NPE; ++pe) mv[pe] = __ldg(mP + (int64_t)pe * nFp + pos);
-      const double *crow = sC + t * CS;
-      double pk[NPOLY];
-#pragma unroll
-      for (int k = 0; k < NPOLY; ++k) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int pe = 0; pe < NPE; ++pe) sacc = fma(crow[k * NPE + pe], mv[pe], sacc);
-        pk[k] = sacc;
-      }
-      int32_t orig;
-      const double E = pair_E64(rec + pos, pk, orig);
-      take(st, E, orig);
-    }
-  }
-  st = merge(st, shfl_xor(st, 1));
-  st = merge(st, shfl_xor(st, 2));
-  tnc = fminf(tnc, __shfl_xor_sync(0xffffffffu, tnc, 1));
-  tnc = fminf(tnc, __shfl_xor_sync(0xffffffffu, tnc, 2));
-  {
-    int ov = ovf ? 1 : 0;
-    ov |= __shfl_xor_sync(0xffffffffu, ov, 1);
-    ov |= __shfl_xor_sync(0xffffffffu, ov, 2);
-    ovf = ov != 0;
-  }
-  // the octet's screen warps saw disjoint tiles: their quad results merged in sub order
-  {
-    double *pq = part + ((size_t)(o * kSwScreens + sub) * 8 + (lane >> 2)) * 4;
-    if ((lane & 3) == 0) {
-      pq[0] = st.e;
-      pq[1] = st.s;
-      pq[2] = __longlong_as_double((long long)st.i);
-      pq[3] = ovf ? -1.0 : (double)tnc;
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kSwPairs * kSwScreens) : "memory");  // screen warps only
-    if (sub != 0) return;
-    for (int j = 1; j < kSwScreens; ++j) {
-      const double *pj = part + ((size_t)(o * kSwScreens + j) * 8 + (lane >> 2)) * 4;
-      Best bj;
-      bj.e = pj[0];
-      bj.s = pj[1];
-      bj.i = (int32_t)__double_as_longlong(pj[2]);
-      st = merge(st, bj);
-      if (pj[3] < 0.0) ovf = true;
-      else tnc = fminf(tnc, (float)pj[3]);
-    }
-  }
-  // exact unless a key that was not kept could reach the winner (or the runner-up)
-  const double lim = (double)tnc * (1.0 - kScreenEta);
-  const bool fb = tok && (ovf || (tnc < __int_as_float(0x7f800000) && (!(st.e < lim) || (SECOND && !(st.s < lim)))));
-  if (__any_sync(0xffffffffu, fb)) {  // rare: the tuple redone by the full FP64 sweep (DMMA here)
-    Best sf;
-    sf.e = kInf;
-    sf.i = 0x7fffffff;
-    sf.s = kInf;
-    double afr[NPOLY][KS];
-#pragma unroll
-    for (int k = 0; k < NPOLY; ++k)
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) afr[k][ks] = arow[k * NPE + ks * 4];
-    for (int oc = 0; oc < nEff; ++oc) {
-      double acc[NPOLY][2];
-      mma_tile(oc, acc, afr);
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        double pk[NPOLY];
-#pragma unroll
-        for (int k = 0; k < NPOLY; ++k) pk[k] = acc[k][v];
-        int32_t orig;
-        const double E = pair_E64(rec + oc * 8 + 2 * (lane & 3) + v, pk, orig);
-        take(sf, E, orig);
-      }
-    }
-    sf = merge(sf, shfl_xor(sf, 1));
-    sf = merge(sf, shfl_xor(sf, 2));
-    if (fb) st = sf;
-  }
-  if ((lane & 3) == 0 && tok) {
-    const int64_t out = (int64_t)g * a.nD + (a.perm ? (int64_t)a.perm[d0 + t] : d0 + t);
-    a.idx[out] = (st.e < kInf) ? st.i : -1;
-    a.bestE[out] = st.e;
-    if (SECOND) a.secondE[out] = st.s;
   }
 }
 
@@ -1206,9 +828,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     const int t = (wid & 3) * 32 + lane;  // TMEM lane = tuple
     const bool tok = t < tmax;
     const int32_t *Dt = sDv + t * kMaxVars;
-    const int64_t D1sq = (int64_t)Dt[0] * Dt[0];
+    bool dpos = true;  // reading R32: data parameters are sizes >= 1
+    for (int k = 0; k < d; ++k) dpos = dpos && Dt[k] >= 1;
+    // a tuple with some D_k < 1 has no candidate: its D1^2 is taken as 0 (no P1 P2 <= 0)
+    const int64_t D1sq = dpos ? (int64_t)Dt[0] * Dt[0] : -1;
     const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
-    const int32_t Da = map0 >= 0 ? Dt[map0] : 1, Db = map1 >= 0 ? Dt[map1] : 1, Dc = map2 >= 0 ? Dt[map2] : 1;
+    const int32_t Da = map0 >= 0 && dpos ? Dt[map0] : 1, Db = map1 >= 0 && dpos ? Dt[map1] : 1,
+                  Dc = map2 >= 0 && dpos ? Dt[map2] : 1;
     const EConst32 kc32 = to_econst32(make_econst(pg));
     const float rNSM32 = sRSM32[n_sm];
     float rcn[NPOLY];  // 1 / ||C_k(D)||: rho = ||m|| / min_k (|p_k| / ||C_k||), one reciprocal per pair
@@ -1326,8 +952,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     const EConst kc = make_econst(pg);
     auto pair_E64 = [&](int tt, int pos, const double *pk, int32_t &orig) -> double {
       const int32_t *Dq = sDv + tt * kMaxVars;
-      const int64_t D1q = (int64_t)Dq[0] * Dq[0];
-      const int32_t qa = map0 >= 0 ? Dq[map0] : 1, qb = map1 >= 0 ? Dq[map1] : 1, qc = map2 >= 0 ? Dq[map2] : 1;
+      bool dq = true;  // reading R32
+      for (int k = 0; k < d; ++k) dq = dq && Dq[k] >= 1;
+      const int64_t D1q = dq ? (int64_t)Dq[0] * Dq[0] : -1;
+      const int32_t qa = map0 >= 0 && dq ? Dq[map0] : 1, qb = map1 >= 0 && dq ? Dq[map1] : 1,
+                    qc = map2 >= 0 && dq ? Dq[map2] : 1;
       const CfgRec *cr = rec + pos;
       const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));
       const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);
@@ -1369,6 +998,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
     st.e = kInf;
     st.i = 0x7fffffff;
     st.s = kInf;
+    st.j = 0x7fffffff;
 #pragma unroll 1
     for (int j = 0; j < kTcKC; ++j) {
       if (cp[j] != 0x7fffffff && !(ck[j] > ubt)) {
@@ -1413,6 +1043,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sweep_tc(SweepArgs a) {
       sf.e = kInf;
       sf.i = 0x7fffffff;
       sf.s = kInf;
+      sf.j = 0x7fffffff;
       for (int pos = lane; pos < nEff * kTcN && pos < nFc; pos += 32) {
         double pk[NPOLY];
         exact_pk(tt, pos, pk);
@@ -1497,17 +1128,6 @@ static cudaError_t launch_tc(SweepArgs a, int n_prog, cudaStream_t s) {
   return e;
 }
 
-template <int NPE, bool SECOND>
-static cudaError_t launch_ws(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
-  const size_t smem = sweep_ws_smem_bytes<6, NPE>(a.nde_stride, n_sm_max);
-  const int64_t tiles = (a.nD + kTD - 1) / kTD;
-  if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_ws<NPE, SECOND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_sweep_ws<NPE, SECOND><<<dim3((unsigned)tiles, (unsigned)n_prog), kSwThreads, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 template <int NPE, bool MWP, bool SECOND>
 static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
   const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_stride, n_sm_max);
@@ -1529,8 +1149,6 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
   if (NPE == kTcNPE && mwp && !second && kern && strcmp(kern, "tc") == 0 && a.tab.nde_pad <= kTcMaxNdp &&
       num_sms() <= kTcMaxSM)
     return launch_tc(a, n_prog, s);
-  if (mwp && kern && strcmp(kern, "ws") == 0)
-    return second ? launch_ws<NPE, true>(a, n_prog, n_sm_max, s) : launch_ws<NPE, false>(a, n_prog, n_sm_max, s);
   if (mwp)
     return second ? launch3<NPE, true, true>(a, n_prog, n_sm_max, s)
                   : launch3<NPE, true, false>(a, n_prog, n_sm_max, s);
@@ -1539,108 +1157,299 @@ static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm
 }
 
 // ============================================================================================
-// Winner refinement (RP_SWEEP_REFINE=1, opt-in; reading R31).  A program fitted to
-// noisy samples has polynomials whose terms cancel (condition numbers to 1e6), so the FP64 sweep's
-// E can differ from the exact value by up to ~1e-9 relative.  This pass re-evaluates, per tuple,
-// the winner the sweep chose with the staged contraction in double-double (error-free products by
-// FMA, compensated sums): p_k to ~2^-100 relative to sum |terms|, then Appendix A in FP64.  The
-// winner index is unchanged; E becomes accurate to the formula's own rounding.
+// Winner refinement (default on; RP_SWEEP_REFINE=0 disables it).  A program fitted to noisy
+// samples has polynomials whose terms cancel (kappa = sum |c m| / |p| up to ~1e7 on the bench's
+// program, reading R31), so the FP64 sweep's E can be ~1e-9 off the exact value of
+// the chosen pair.  k_refine re-evaluates, per tuple, the sweep's winner (and with a runner-up
+// output also the runner-up, re-ranking the two) with every p_k accurate to ~u + n^2 u^2 kappa:
+//   * monomials m = m_de(u_D) m_pe(u_P) in double-double (error-free products by FMA);
+//   * each p_k = sum c m accumulated by error-free extraction against a power of two
+//     sigma_k >= 4 sum |c m| (a bound from the plan: A_k = sum |c|, times max(1, |u|)^maxdeg):
+//     x = fma(c, m_hi, sigma) rounds c m_hi to a multiple of ulp(sigma)/2, t = x - sigma is exact
+//     (Sterbenz), the t are summed exactly in hi (multiples of ulp(sigma)/2 below sigma), and
+//     the remainders fma(c, m_hi, -t) (one rounding of a value below ulp(sigma)) and c m_lo
+//     go to lo -- 6 FP64 operations per term and polynomial instead of the ~11 of a TwoSum
+//     chain;
+//   * then a6 and Appendix A exactly as the sweep evaluates them.
+// The plan keeps the union of the polynomials' (de, pe) terms with one coefficient per
+// polynomial (zero where a polynomial lacks the term), so the monomial product is shared by the
+// 2l polynomials.  One thread per tuple; the tuple's data monomials and the chosen configurations'
+// program monomials sit in shared memory (thread-private columns, no barrier).
 // ============================================================================================
-struct DD {
-  double hi, lo;
-};
-__device__ __forceinline__ DD dd_two_prod(double a, double b) {
-  const double p = a * b;
-  return DD{p, fma(a, b, -p)};
-}
-__device__ __forceinline__ DD dd_add(DD x, DD y) {  // Knuth two-sum on the high parts, then renormalise
-  const double s = x.hi + y.hi, bb = s - x.hi;
-  const double e = (x.hi - (s - bb)) + (y.hi - bb) + x.lo + y.lo;
-  const double h = s + e;
-  return DD{h, e - (h - s)};
-}
-__device__ __forceinline__ DD dd_mul(DD x, DD y) {
-  DD p = dd_two_prod(x.hi, y.hi);
-  p.lo = fma(x.hi, y.lo, fma(x.lo, y.hi, p.lo));
-  const double h = p.hi + p.lo;
-  return DD{h, p.lo - (h - p.hi)};
+constexpr int kRefThreads = 128;
+
+// the union term list of program g's polynomials (rterm, rcoef) and its bounds (rinfo), from the
+// staging matrix Cmat; called by every thread of a plan kernel after Cmat is written
+__device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab, int npe_pad) {
+  __shared__ int rt_warp[32];
+  __shared__ int rt_base;
+  const int ndp = tab.nde_pad, ncell = npe_pad * ndp;
+  const double *Cm = tab.Cmat + (int64_t)g * kMaxPolys * npe_pad * ndp;
+  double *rc = tab.rcoef + (int64_t)g * ncell * kMaxPolys;
+  int32_t *rt = tab.rterm + (int64_t)g * ncell;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) rt_base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < ncell; c0 += blockDim.x) {
+    const int cell = c0 + threadIdx.x, pe = cell / ndp, de = cell % ndp;
+    bool nz = false;
+    if (cell < ncell && pe < pg.nPE && de < pg.nDE)
+      for (int k = 0; k < pg.npoly; ++k) nz = nz || Cm[(int64_t)(k * npe_pad + pe) * ndp + de] != 0.0;
+    const unsigned ball = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) rt_warp[wid] = __popc(ball);
+    __syncthreads();
+    if (wid == 0) {
+      const int v = lane < (int)(blockDim.x >> 5) ? rt_warp[lane] : 0;
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      rt_warp[lane] = incl - v;
+    }
+    __syncthreads();
+    const int pos = rt_base + rt_warp[wid] + __popc(ball & ((1u << lane) - 1u));
+    if (nz) {
+      rt[pos] = de | (pe << 16);
+      for (int k = 0; k < kMaxPolys; ++k)
+        rc[(int64_t)pos * kMaxPolys + k] = k < pg.npoly ? Cm[(int64_t)(k * npe_pad + pe) * ndp + de] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) rt_base = pos + nz;
+    __syncthreads();
+  }
+  const int nrt = rt_base;
+  double *ri = tab.rinfo + (int64_t)g * 8;
+  if (threadIdx.x < kMaxPolys) {  // A_k = sum |c| over the terms of polynomial k (fixed order)
+    double A = 0.0;
+    for (int j = 0; j < nrt; ++j) A += fabs(rc[(int64_t)j * kMaxPolys + threadIdx.x]);
+    ri[threadIdx.x] = A;
+  } else if (threadIdx.x == kMaxPolys) {
+    int md = 0;
+    for (int j = 0; j < nrt; ++j) {
+      const int de = rt[j] & 0xffff, pe = rt[j] >> 16;
+      int dg = 0;
+      for (int k = 0; k < pg.d; ++k) dg += pg.de_exp[de][k];
+      for (int k = 0; k < pg.p; ++k) dg += pg.pe_exp[pe][k];
+      md = dg > md ? dg : md;
+    }
+    ri[6] = (double)md;
+    ri[7] = (double)nrt;
+  }
 }
 
-__global__ void k_refine_winners(SweepArgs a) {
+// m = prod u_k^{e_k} as a double-double (hi exact product chain by FMA, lo the running error)
+__device__ __forceinline__ double2 dd_monomial(const int8_t *e, int n, const double *u) {
+  double h = 1.0, l = 0.0;
+  for (int k = 0; k < n; ++k)
+    for (int t = 0; t < e[k]; ++t) {
+      const double nh = h * u[k];
+      l = fma(l, u[k], fma(h, u[k], -nh));
+      h = nh;
+    }
+  return make_double2(h, l);
+}
+
+// the smallest power of two > 4 B (B >= 0 finite); 1 for B = 0; 0 if it would overflow
+__device__ __forceinline__ double extract_sigma(double B) {
+  if (!(B > 0.0)) return B == 0.0 ? 1.0 : 0.0;
+  const long long ex = ((__double_as_longlong(B) >> 52) & 0x7ff) - 1023;  // B in [2^ex, 2^(ex+1))
+  if (ex + 3 > 1023) return 0.0;
+  return __longlong_as_double((ex + 3 + 1023) << 52);
+}
+
+// a6 + Appendix A for one pair from its polynomial values (as k_sweep evaluates them)
+template <int NPOLY>
+__device__ __forceinline__ double pair_E(const DevProg &pg, const CfgTable &tab, int g, const int32_t *Dt,
+                                         const CfgRec &r, const double *pk) {
+  if (NPOLY != 6) return pk[0] * frcp(pk[1]);  // template g1
+  const int P[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+  int64_t blocks = 1;
+  for (int k = 0; k < pg.p && k < 3; ++k)
+    if (pg.grid_map[k] >= 0) blocks *= ((int64_t)Dt[pg.grid_map[k]] + P[k] - 1) / P[k];
+  const int64_t smact = blocks < pg.n_sm ? blocks : pg.n_sm;
+  const double rSM = tab.rSM[(int64_t)g * kRSMTab + smact];
+  const double Rep = (double)blocks * r.rB * rSM;
+  return mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], r.W, Rep, rSM, (double)smact, make_econst(pg));
+}
+
+// shared memory of k_refine: the term list (int32, padded to 16 B), its coefficients
+// [nrt][kMaxPolys] and the tuples' data monomials [nDE][T] (double-double)
+__host__ __device__ inline size_t refine_smem_bytes(int nrt, int nDE, int T) {
+  return (size_t)((nrt + 3) & ~3) * 4 + (size_t)nrt * kMaxPolys * 8 + (size_t)nDE * T * 16;
+}
+
+template <int NPOLY, bool SECOND>
+__global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
   const int g = blockIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const DevProg &pg = a.progs[g];
+  const double *ri = a.tab.rinfo + (int64_t)g * 8;
+  const int maxdeg = (int)ri[6], nrt = (int)ri[7];
+  const int d = a.d, nDE = pg.nDE;
+  // stage the term list and its coefficients (read by every thread in the same order: broadcast)
+  extern __shared__ __align__(16) unsigned char rsh[];
+  int32_t *sT = reinterpret_cast<int32_t *>(rsh);
+  double2 *sCf = reinterpret_cast<double2 *>(rsh + (size_t)((nrt + 3) & ~3) * 4);  // [nrt][kMaxPolys / 2]
+  double2 *sMD = sCf + (size_t)nrt * (kMaxPolys / 2);                              // [nDE][T]
+  {
+    const int32_t *rt = a.tab.rterm + (int64_t)g * a.npe_pad * a.tab.nde_pad;
+    const double2 *rc = reinterpret_cast<const double2 *>(a.tab.rcoef + (int64_t)g * a.npe_pad * a.tab.nde_pad * kMaxPolys);
+    for (int i = tid; i < nrt; i += T) sT[i] = rt[i];
+    for (int i = tid; i < nrt * (kMaxPolys / 2); i += T) sCf[i] = rc[i];
+  }
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * T + tid;
   if (t >= a.nD) return;
   const int64_t o = (int64_t)g * a.nD + t;
   const int32_t win = a.idx[o];
   if (win < 0) return;
-  const DevProg &pg = a.progs[g];
-  const int d = a.d, nFp = a.tab.nFp, nFc = a.tab.nFc[2 * g], npe = a.npe_pad, ndp = a.tab.nde_pad;
-  // the winner's record: compacted configurations in ascending original index (binary search)
-  const CfgRec *sr = a.tab.srec + (int64_t)g * nFp;
-  int lo = 0, hi = nFc - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sr[mid].orig < win) lo = mid + 1;
-    else hi = mid;
-  }
-  const CfgRec r = sr[lo];
-  if (r.orig != win) return;
+  const CfgRec *sr = a.tab.srec + (int64_t)g * a.tab.nFp;
+  const int32_t *inv = a.tab.inv + (int64_t)g * a.tab.nFp;
+  const int p1 = __ldg(inv + win);
+  if (p1 < 0) return;
+  const CfgRec *r1 = sr + p1;
+  const int32_t run = SECOND ? a.idx2[o] : -1;
+  const int p2 = (SECOND && run >= 0) ? __ldg(inv + run) : -1;
+  const CfgRec *r2 = p2 >= 0 ? sr + p2 : nullptr;
+  const bool two = SECOND && r2 != nullptr;
   const int32_t *Dt = a.D + t * d;
-  // data monomials in double-double (u exact in FP64: integer minus the box centre, times 2^-e)
-  DD md[kMaxDE];
-  for (int de = 0; de < pg.nDE; ++de) {
-    DD m{1.0, 0.0};
-    for (int k = 0; k < d; ++k) {
-      const double u = ((double)Dt[k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
-      for (int e = 0; e < pg.de_exp[de][k]; ++e) m = dd_mul(m, DD{u, 0.0});
-    }
-    md[de] = m;
+
+  double u[kMaxVars];
+  double R = 1.0;  // max(1, |u_k|) over the variables of both pairs
+  for (int k = 0; k < d; ++k) {
+    u[k] = ((double)Dt[k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
+    R = fmax(R, fabs(u[k]));
   }
-  const int P[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
-  const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * npe * ndp;
-  double pk[kMaxPolys];
-  for (int k = 0; k < pg.npoly; ++k) {
-    DD acc{0.0, 0.0};
-    for (int pe = 0; pe < pg.nPE; ++pe) {
-      DD mp{1.0, 0.0};
-      for (int q = 0; q < pg.p; ++q) {
-        const double u = ((double)P[q] - pg.xc[d + q]) * ldexp(1.0, -pg.xe[d + q]);
-        for (int e = 0; e < pg.pe_exp[pe][q]; ++e) mp = dd_mul(mp, DD{u, 0.0});
-      }
-      DD c{0.0, 0.0};
-      const double *row = Cm + (int64_t)(k * npe + pe) * ndp;
-      for (int de = 0; de < pg.nDE; ++de) {
-        if (row[de] == 0.0) continue;
-        c = dd_add(c, dd_mul(md[de], DD{row[de], 0.0}));
-      }
-      acc = dd_add(acc, dd_mul(c, mp));
+  for (int de = 0; de < nDE; ++de) sMD[(size_t)de * T + tid] = dd_monomial(pg.de_exp[de], d, u);
+  double uP[3] = {0.0, 0.0, 0.0}, uP2[3] = {0.0, 0.0, 0.0};
+  {
+    const int P1[3] = {r1->Pm1_0 + 1, r1->Pm1_1 + 1, r1->Pm1_2 + 1};
+    for (int k = 0; k < pg.p; ++k) {
+      uP[k] = ((double)P1[k] - pg.xc[d + k]) * ldexp(1.0, -pg.xe[d + k]);
+      R = fmax(R, fabs(uP[k]));
     }
-    pk[k] = acc.hi + acc.lo;
   }
-  // a6 and Appendix A exactly as the sweep does them, on the refined polynomial values
-  const int map0 = pg.grid_map[0], map1 = pg.p >= 2 ? pg.grid_map[1] : -1, map2 = pg.p >= 3 ? pg.grid_map[2] : -1;
-  int64_t blocks = 1;
-  if (map0 >= 0) blocks *= ((int64_t)Dt[map0] + P[0] - 1) / P[0];
-  if (map1 >= 0) blocks *= ((int64_t)Dt[map1] + P[1] - 1) / P[1];
-  if (map2 >= 0) blocks *= ((int64_t)Dt[map2] + P[2] - 1) / P[2];
-  const int n_sm = pg.n_sm;
-  const int64_t smact = blocks < n_sm ? blocks : n_sm;
-  const double rSM = a.tab.rSM[(int64_t)g * kRSMTab + smact];
-  const double Rep = (double)blocks * r.rB * rSM;
-  double E;
-  if (pg.npoly == 6) E = mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], r.W, Rep, rSM, (double)smact, make_econst(pg));
-  else E = pk[0] * frcp(pk[1]);
-  if (pos_finite(E)) a.bestE[o] = E;
+  if (two) {
+    const int P2[3] = {r2->Pm1_0 + 1, r2->Pm1_1 + 1, r2->Pm1_2 + 1};
+    for (int k = 0; k < pg.p; ++k) {
+      uP2[k] = ((double)P2[k] - pg.xc[d + k]) * ldexp(1.0, -pg.xe[d + k]);
+      R = fmax(R, fabs(uP2[k]));
+    }
+  }
+  double Rp = 1.0;
+  for (int i = 0; i < maxdeg; ++i) Rp *= R;
+  double sg[NPOLY];
+  bool okb = true;
+#pragma unroll
+  for (int k = 0; k < NPOLY; ++k) {
+    sg[k] = extract_sigma(ri[k] * Rp * 1.0000000001);  // |c m| <= |c| R^maxdeg (+ rounding)
+    okb = okb && sg[k] > 0.0;
+  }
+  if (!okb) return;  // bounds overflow: keep the sweep's values
+  double h1[NPOLY], l1[NPOLY], h2[NPOLY], l2[NPOLY];
+#pragma unroll
+  for (int k = 0; k < NPOLY; ++k) h1[k] = l1[k] = h2[k] = l2[k] = 0.0;
+  // terms in (pe, de) order: the program monomial m_pe(u_P) changes ~nPE times per tuple and is
+  // recomputed then (uniform across the warp), the data monomial comes from shared memory
+  int cur_pe = -1;
+  double2 mp1 = make_double2(0.0, 0.0), mp2 = make_double2(0.0, 0.0);
+  for (int j = 0; j < nrt; ++j) {
+    const int32_t tt = sT[j];
+    const int pe = tt >> 16;
+    if (pe != cur_pe) {
+      cur_pe = pe;
+      mp1 = dd_monomial(pg.pe_exp[pe], pg.p, uP);
+      if (two) mp2 = dd_monomial(pg.pe_exp[pe], pg.p, uP2);
+    }
+    const double2 md = sMD[(size_t)(tt & 0xffff) * T + tid];
+    double c[NPOLY];
+#pragma unroll
+    for (int k = 0; k < NPOLY; k += 2) {
+      const double2 cc = sCf[(size_t)j * (kMaxPolys / 2) + k / 2];
+      c[k] = cc.x;
+      c[k + 1] = cc.y;
+    }
+    {
+      const double mh = md.x * mp1.x;
+      const double ml = fma(md.x, mp1.y, fma(md.y, mp1.x, fma(md.x, mp1.x, -mh)));
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) {
+        const double tq = fma(c[k], mh, sg[k]) - sg[k];
+        h1[k] += tq;
+        l1[k] = fma(c[k], ml, l1[k] + fma(c[k], mh, -tq));
+      }
+    }
+    if (two) {
+      const double mh = md.x * mp2.x;
+      const double ml = fma(md.x, mp2.y, fma(md.y, mp2.x, fma(md.x, mp2.x, -mh)));
+#pragma unroll
+      for (int k = 0; k < NPOLY; ++k) {
+        const double tq = fma(c[k], mh, sg[k]) - sg[k];
+        h2[k] += tq;
+        l2[k] = fma(c[k], ml, l2[k] + fma(c[k], mh, -tq));
+      }
+    }
+  }
+  double pk[NPOLY];
+#pragma unroll
+  for (int k = 0; k < NPOLY; ++k) pk[k] = h1[k] + l1[k];
+  double E1 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r1, pk);
+  if (!pos_finite(E1)) E1 = a.bestE[o];  // exact evaluation masks the pair: keep the sweep's value
+  if (!SECOND) {
+    a.bestE[o] = E1;
+    return;
+  }
+  double E2 = a.secondE[o];
+  if (two) {
+#pragma unroll
+    for (int k = 0; k < NPOLY; ++k) pk[k] = h2[k] + l2[k];
+    const double e2 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r2, pk);
+    if (pos_finite(e2)) E2 = e2;
+  }
+  // re-rank the two on the exact key (E, original index)
+  if (two && key_less(E2, run, E1, win)) {
+    a.idx[o] = run;
+    a.bestE[o] = E2;
+    a.secondE[o] = E1;
+    a.idx2[o] = win;
+  } else {
+    a.bestE[o] = E1;
+    a.secondE[o] = E2;
+  }
+}
+
+static bool refine_enabled() {
+  const char *v = getenv("RP_SWEEP_REFINE");
+  return !(v && v[0] == '0');
+}
+
+template <int NPOLY, bool SECOND>
+static cudaError_t launch_refine_t(const SweepArgs &a, int n_prog, int nDE, int nPE, cudaStream_t s) {
+  (void)nPE;
+  // union terms <= npe_pad * nde_pad (the plan's bound; the kernel reads the actual count)
+  const int nrt_max = a.tab.nrt_max;
+  int T = kRefThreads;
+  auto bytes = [&](int th) { return refine_smem_bytes(nrt_max, nDE, th); };
+  while (T > 32 && bytes(T) > 200 * 1024) T >>= 1;
+  const size_t smem = bytes(T);
+  cudaError_t e = cudaFuncSetAttribute(k_refine<NPOLY, SECOND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (a.nD + T - 1) / T;
+  if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
+  k_refine<NPOLY, SECOND><<<dim3((unsigned)blocks, (unsigned)n_prog), T, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable tab, int npe_pad,
                          int nde_max, int n_sm_max, int d, const int32_t *d_D, int64_t nD,
                          int32_t *idx, double *bestE, double *secondE, const int32_t *perm,
-                         cudaStream_t s) {
+                         int32_t *idx2, cudaEvent_t *ev, cudaStream_t s) {
   if (nD == 0) return cudaSuccess;
+  if (ev) cudaEventRecord(ev[1], s);
   // n_sm < kRSMTab for every program (compile_program): the 1/SM_act tables always exist
-  (void)nde_max;
   SweepArgs a{d_progs, tab, npe_pad, d, md_stride(tab.nde_pad), d_D, nD, idx, bestE, secondE, perm};
+  a.idx2 = refine_enabled() ? idx2 : nullptr;
   cudaError_t e;
   switch (npe_pad) {
     case 4: e = launch_npe<4>(a, n_prog, mwp, n_sm_max, s); break;
@@ -1651,12 +1460,15 @@ cudaError_t launch_sweep(const DevProg *d_progs, int n_prog, bool mwp, CfgTable 
     case 36: e = launch_npe<36>(a, n_prog, mwp, n_sm_max, s); break;
     default: return cudaErrorInvalidValue;
   }
-  const char *refine = getenv("RP_SWEEP_REFINE");
-  if (e == cudaSuccess && refine && refine[0] == '1') {  // opt-in: the winners' E in double-double
-    const int64_t blocks = (nD + 127) / 128;
-    if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
-    k_refine_winners<<<dim3((unsigned)blocks, (unsigned)n_prog), 128, 0, s>>>(a);
-    e = cudaGetLastError();
+  if (ev) cudaEventRecord(ev[2], s);
+  if (e == cudaSuccess && refine_enabled()) {  // the winners' E (and runner-ups') accurate
+    const bool second = secondE != nullptr && a.idx2 != nullptr;
+    if (mwp)
+      e = second ? launch_refine_t<6, true>(a, n_prog, nde_max, npe_pad, s)
+                 : launch_refine_t<6, false>(a, n_prog, nde_max, npe_pad, s);
+    else
+      e = second ? launch_refine_t<2, true>(a, n_prog, nde_max, npe_pad, s)
+                 : launch_refine_t<2, false>(a, n_prog, nde_max, npe_pad, s);
   }
   return e;
 }

@@ -1,0 +1,176 @@
+"""Full-size gates of the bench's own workload (SURVEY 8(c) #25, 8(d) run matrix).
+
+bench.py times: fit of the 3 metrics on the `fitheavy` sample set (K = 10^6 rows, 1% noise)
+followed by the sweep of the fitted program over `large` (10^6 D x 1,024 F) with argmin.  Here,
+at exactly those sizes and in the bench's launch configuration (a Plan, second=False):
+
+* test_bench_workload_noisy_fit_sweep -- the fitted program of 1%-noise samples (the diagnostic
+  class of SURVEY 8(d): its polynomials cancel, kappa up to ~1e7).  Both sides sweep the
+  ORACLE's fit (class-L rule of SURVEY 8(c): sweep parity decoupled from fit conditioning; the
+  GPU fit itself is gated against the oracle's at 1e-9).  Gates, on the standard subsample
+  (every 100th D + first/last 100):
+    - SURVEY 8(c) #25 against the long double oracle where its kappa <= 1e3 at the winner and
+      the runner-up: idx bit-exact where the margin exceeds 1e-9, E within 1e-12; the covered
+      fraction is reported;
+    - everywhere against the binary128 oracle (orc_sweep_q, accurate to ~1e-28 kappa): E within
+      1e-12 of the exact value at the GPU's winner; idx bit-exact where the exact margin
+      exceeds 1e-9; otherwise the GPU's winner lies in the exact 1e-9 tie set.
+* test_end_to_end_noise_free_chain_full_size -- the gated class-F chain: noise-free fitheavy
+  fit -> sweep, GPU fit -> GPU sweep against oracle fit -> oracle sweep (exact data determine
+  g_i), all 10^6 D on the GPU, compared on the subsample.
+
+A JSON summary goes to gpurun_out/ (committed under profiles/ as r02_parity_*.json) and is
+embedded in the bench line's `parity` field.
+"""
+import copy
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1911_02373_b200 as rp  # noqa: E402
+from conftest import oracle_fitheavy_fit  # noqa: E402
+
+DEV = torch.device("cuda:0")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NT = len(os.sched_getaffinity(0))
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _report(name, data):
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, name), "w") as f:
+        json.dump(data, f, indent=1, sort_keys=True)
+
+
+def _program(truth, res):
+    spec = copy.deepcopy(truth)
+    spec.coef = [np.asarray(r["coef"], dtype=np.float64) for r in res]
+    spec.xform_c, spec.xform_e = list(res[0]["c"]), list(res[0]["e"])
+    return spec
+
+
+def _margin(ref):
+    with np.errstate(invalid="ignore", divide="ignore"):
+        return (ref["second"] - ref["best"]) / ref["best"]
+
+
+def test_bench_workload_noisy_fit_sweep():
+    fc, V, ores = oracle_fitheavy_fit(0.01)
+    # the GPU fit of the same sample set against the oracle's (north star: 1e-9 after beta_0 = 1)
+    coef, (c, e), _ = rp.fit(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp, raise_on_degenerate=False)
+    fit_gap = [float(np.max(np.abs(coef[i] - ores[i]["coef"])) / np.max(np.abs(ores[i]["coef"]))) for i in range(3)]
+    assert max(fit_gap) <= 1e-9, fit_gap
+    spec = _program(fc.truths[0], ores)
+    D = synth.large_D(1_000_000)
+    F = synth.F_large()
+    plan = rp.Plan([spec], _cuda(F))
+    idx, E, _ = plan.eval(_cuda(D), second=False)  # the bench's launch
+    idx2, E2, S2 = plan.eval(_cuda(D), second=True)
+    sub = synth.large_subsample_index(len(D))
+    gi = idx.cpu().numpy().ravel()[sub]
+    gE = E.cpu().numpy().ravel()[sub]
+    assert np.array_equal(idx2.cpu().numpy().ravel()[sub], gi)
+    assert np.array_equal(E2.cpu().numpy().ravel()[sub], gE)
+    Ds = D[sub]
+    ref = oracle.sweep(spec, Ds, F, nthreads=NT)
+    refq = oracle.sweep(spec, Ds, F, nthreads=NT, quad=True)
+    feas = refq["idx"] >= 0
+    assert np.array_equal(gi >= 0, feas)
+    # (1) everywhere, against binary128
+    mq = _margin(refq)
+    strict = feas & (mq > 1e-9)
+    idx_ok = gi == refq["idx"]
+    assert np.all(idx_ok[strict]), np.nonzero(~idx_ok & strict)[0][:10]
+    Eq = refq["best"].copy()
+    tie_gap = np.zeros(len(sub))
+    for t in np.nonzero(feas & ~idx_ok)[0]:  # near ties: exact E of the GPU's pick
+        tr = oracle.eval_pair(spec, Ds[t], F[gi[t]], quad=True)
+        assert tr["feasible"]
+        Eq[t] = float(tr["E"])
+        tie_gap[t] = (Eq[t] - refq["best"][t]) / refq["best"][t]
+    assert np.all(tie_gap <= 1e-9), tie_gap.max()
+    relq = np.abs(gE[feas] - Eq[feas]) / Eq[feas]
+    assert relq.max() <= 1e-12, relq.max()
+    # (2) SURVEY 8(c) #25 literally: long double oracle where kappa <= 1e3 at winner and runner-up
+    cov = feas & (ref["kappa"] <= 1e3) & ((ref["kappa2"] <= 1e3) | (ref["idx2"] < 0))
+    ml = _margin(ref)
+    s2 = cov & (ml > 1e-9)
+    assert np.array_equal(gi[s2], ref["idx"][s2])
+    rel2 = np.abs(gE[cov] - ref["best"][cov]) / ref["best"][cov]
+    assert rel2.max(initial=0) <= 1e-12, rel2.max()
+    # long double vs binary128 oracle where kappa > 1e3 (why the gate uses binary128 there)
+    big = feas & ~cov
+    ld_gap = np.abs(ref["best"][big] - refq["best"][big]) / refq["best"][big]
+    _report("parity_bench_workload.json", {
+        "workload": "bench: fitheavy 1% noise fit (K=1e6) -> large sweep (1e6 D x 1024 F), Plan, second=False",
+        "program": "oracle's fit of the bench's sample set (both sides sweep it); GPU fit gated separately",
+        "fit_coef_gap_inf_norm": fit_gap, "fit_gate": 1e-9,
+        "subsample": int(len(sub)), "feasible": int(feas.sum()),
+        "vs_binary128": {"idx_exact_where_margin_gt_1e-9": int(strict.sum()),
+                         "idx_mismatch_total": int((feas & ~idx_ok).sum()),
+                         "near_tie_max_gap": float(tie_gap.max(initial=0)),
+                         "E_max_rel_err": float(relq.max()), "E_p99_rel_err": float(np.quantile(relq, 0.99)),
+                         "gate": "E <= 1e-12 at the GPU's pick; idx exact where exact margin > 1e-9, else in the 1e-9 tie set"},
+        "survey_8c_25": {"covered_fraction": float(cov.sum() / max(feas.sum(), 1)),
+                         "idx_exact": int(s2.sum()), "E_max_rel_err": float(rel2.max(initial=0)),
+                         "gate": "long double oracle where kappa <= 1e3 at winner and runner-up"},
+        "kappa_winner": {"median": float(np.median(ref["kappa"][feas])), "max": float(ref["kappa"][feas].max())},
+        "long_double_vs_binary128_where_kappa_gt_1e3": float(ld_gap.max(initial=0)),
+        "passed": True})
+    plan.close()
+
+
+def test_end_to_end_noise_free_chain_full_size():
+    fc, V, ores = oracle_fitheavy_fit(0.0)
+    coef, (c, e), _ = rp.fit(_cuda(fc.X), _cuda(V), fc.num_exp, fc.den_exp)
+    assert np.array_equal(ores[0]["c"], c) and np.array_equal(ores[0]["e"], e)
+    fit_gap = max(float(np.max(np.abs(coef[i] - ores[i]["coef"])) / np.max(np.abs(ores[i]["coef"]))) for i in range(3))
+    assert fit_gap <= 1e-9, fit_gap
+    # the two chains sweep two programs whose coefficients differ by fit_gap (gated above); E moves
+    # by at most ~kappa_g (<= 3 for class-F truths) x the E amplification (<= ~20) times that
+    # (reading R33), so the chain's E gate is max(1e-12, 60 fit_gap)
+    e_tol = max(1e-12, 60 * fit_gap)
+    gpu_prog = copy.deepcopy(fc.truths[0])
+    gpu_prog.coef = [coef[i] for i in range(3)]
+    gpu_prog.xform_c, gpu_prog.xform_e = list(c), list(e)
+    orc_prog = _program(fc.truths[0], ores)
+    D = synth.large_D(1_000_000)
+    F = synth.F_large()
+    plan = rp.Plan([gpu_prog], _cuda(F))
+    idx, E, _ = plan.eval(_cuda(D), second=False)
+    sub = synth.large_subsample_index(len(D))
+    gi = idx.cpu().numpy().ravel()[sub]
+    gE = E.cpu().numpy().ravel()[sub]
+    ref = oracle.sweep(orc_prog, D[sub], F, nthreads=NT)
+    feas = ref["idx"] >= 0
+    assert np.array_equal(gi >= 0, feas)
+    m = _margin(ref)
+    strict = feas & (m > 1e-9)
+    assert np.array_equal(gi[strict], ref["idx"][strict])
+    rel = np.abs(gE[feas] - ref["best"][feas]) / ref["best"][feas]
+    assert rel.max() <= e_tol, (rel.max(), e_tol)
+    for t in np.nonzero(feas & (gi != ref["idx"]))[0]:
+        tr = oracle.eval_pair(orc_prog, D[sub][t], F[gi[t]])
+        assert abs(float(tr["E"]) - ref["best"][t]) <= 1e-9 * ref["best"][t]
+    _report("parity_e2e_noise_free.json", {
+        "workload": "noise-free fitheavy fit (K=1e6) -> large sweep (1e6 D x 1024 F): GPU chain vs oracle chain",
+        "subsample": int(len(sub)), "feasible": int(feas.sum()), "idx_exact_where_margin_gt_1e-9": int(strict.sum()),
+        "E_max_rel_err": float(rel.max()), "E_gate": e_tol, "fit_coef_gap_inf_norm": fit_gap,
+        "kappa_winner_max": float(ref["kappa"][feas].max()),
+        "case_counters": ref["counters"], "passed": True})
+    plan.close()
