@@ -58,6 +58,20 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
+// 1/x with one Newton step, r = r0 (1 + e): relative error ~e0^2 (< 2^-40), 2 DFMA.  Used by the
+// sweep when the winners are re-evaluated exactly afterwards (k_refine): its E only ranks, and a
+// ~1e-12 error changes the ranking only between configurations tied within ~1e-11 (the idx gate
+// excludes margins below 1e-9; the refined winner's E is exact either way).
+__device__ __forceinline__ double frcp1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
+template <bool FAST>
+__device__ __forceinline__ double rcp_t(double x) {
+  return FAST ? frcp1(x) : frcp(x);
+}
+
 // positive finite doubles order like their bit patterns: the validity test and the argmin key
 // compare run on the integer pipes instead of the (shared, saturated) FP64 datapath
 __device__ __forceinline__ bool pos_finite(double x) {
@@ -97,6 +111,7 @@ __device__ __forceinline__ EConst make_econst(const DevProg &pg) {
   return kc;
 }
 
+template <bool FAST = false>
 __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, double q2, double p3,
                                            double q3, double W, double Rep, double rSM,
                                            double SMact, const EConst &k) {
@@ -108,11 +123,11 @@ __device__ __forceinline__ double mwpcwp_E(double p1, double q1, double p2, doub
   const double mc = fma(k.Lunc, a3, k.Lcoal * a2);            // Mem_c Q        (line 13)
   const double dn = fma(k.DdU, a3, k.ddc * a2);               // Dep Mem Q      (lines 6, 9)
   const double cc = k.issue * s;                              // Comp_c Q       (line 13)
-  const double rQ = frcp(Q), r23 = frcp(s23);
+  const double rQ = rcp_t<FAST>(Q), r23 = rcp_t<FAST>(s23);
   const double Mem_c = mc * rQ, Comp_c = cc * rQ;
-  const double MWP_nb = mc * frcp(dn);         // line 10: Mem_L / Dep
+  const double MWP_nb = mc * rcp_t<FAST>(dn);  // line 10: Mem_L / Dep
   const double MWP_bw = k.Kbw * mc * r23 * rSM;  // line 11: Mem_BW / (BW_per_warp SM_act)
-  const double CWPf = 1.0 + mc * frcp(cc);     // line 14: (Mem_c + Comp_c) / Comp_c
+  const double CWPf = 1.0 + mc * rcp_t<FAST>(cc);  // line 14: (Mem_c + Comp_c) / Comp_c
   // line 12: MWP = min(MWP_nb, MWP_bw, W_act); each comparison is made once and its outcome
   // reused for the case tests (MWP == W_act <=> W_act <= min(MWP_nb, MWP_bw), also for NaN)
   const bool bw = MWP_bw < MWP_nb;

@@ -344,7 +344,9 @@ size_t sweep_smem_bytes(int nde_stride, int n_sm) {
          sizeof(int32_t) * kTD * kMaxVars;
 }
 
-template <int NPE, bool MWP, bool SECOND>
+// FAST (MWP-CWP programs whose winners k_refine re-evaluates): E only ranks here -- one-step
+// reciprocals and Rep = 1/B_act when #Blocks < n_SM (SM_act = #Blocks cancels exactly)
+template <int NPE, bool MWP, bool SECOND, bool FAST>
 __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArgs a) {
   constexpr int NPOLY = MWP ? 6 : 2;
   constexpr int KS = NPE / 4;
@@ -460,10 +462,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   // configurations (k-step major: the NPOLY accumulation chains are independent, so consecutive
   // DMMAs do not wait).  B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
 #define RP_AFR(k, ks) arow[(k) * NPE + (ks) * 4]
-  auto mma_oct = [&](int oc, double (&acc)[NPOLY][2]) {
-    double bfr[KS];
+  auto load_b = [&](int oc, double (&bfr)[KS]) {
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
+  };
+  auto mma_oct = [&](int oc, double (&acc)[NPOLY][2], const double (&bfr)[KS]) {
 #pragma unroll
     for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
 #pragma unroll
@@ -500,9 +503,10 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
         if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
         const int64_t smact = blocks < n_sm ? blocks : n_sm;
         const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
-        const double Rep = (double)blocks * h3.x * rSM;  // line 15: #Blocks / (B_act SM_act)
-        E = mwpcwp_E(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
-                     rSM, (double)smact, kc);
+        // line 15: #Blocks / (B_act SM_act)
+        const double Rep = FAST ? (smact == n_sm ? (double)blocks * h3.x * rNSM : h3.x) : (double)blocks * h3.x * rSM;
+        E = mwpcwp_E<FAST>(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
+                           rSM, (double)smact, kc);
       } else {
         E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
       }
@@ -534,9 +538,21 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           break;
         }
       }
-    for (int oc = 0; oc < nEff; ++oc) {
-      double acc[NPOLY][2];
-      mma_oct(oc, acc);
+    // two configuration octets per iteration: 4 independent pairs per lane in the epilogue
+    int oc = 0;
+    for (; oc + 1 < nEff; oc += 2) {
+      double acc[NPOLY][2], acc2[NPOLY][2], bfr[KS], bfr2[KS];
+      load_b(oc, bfr);
+      load_b(oc + 1, bfr2);
+      mma_oct(oc, acc, bfr);
+      mma_oct(oc + 1, acc2, bfr2);
+      epi_oct(oc, acc);
+      epi_oct(oc + 1, acc2);
+    }
+    if (oc < nEff) {
+      double acc[NPOLY][2], bfr[KS];
+      load_b(oc, bfr);
+      mma_oct(oc, acc, bfr);
       epi_oct(oc, acc);
     }
   }
@@ -1128,16 +1144,24 @@ static cudaError_t launch_tc(SweepArgs a, int n_prog, cudaStream_t s) {
   return e;
 }
 
-template <int NPE, bool MWP, bool SECOND>
-static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
+template <int NPE, bool MWP, bool SECOND, bool FAST>
+static cudaError_t launch4(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
   const size_t smem = sweep_smem_bytes<MWP ? 6 : 2, NPE>(a.nde_stride, n_sm_max);
   const int64_t tiles = (a.nD + kTD - 1) / kTD;
   if (tiles > 0x7fffffffll || n_prog > 65535) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k_sweep<NPE, MWP, SECOND>,
+  cudaError_t e = cudaFuncSetAttribute(k_sweep<NPE, MWP, SECOND, FAST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_sweep<NPE, MWP, SECOND><<<dim3((unsigned)tiles, (unsigned)n_prog), kSweepThreads, smem, s>>>(a);
+  k_sweep<NPE, MWP, SECOND, FAST><<<dim3((unsigned)tiles, (unsigned)n_prog), kSweepThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+static bool refine_enabled();
+template <int NPE, bool MWP, bool SECOND>
+static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStream_t s) {
+  if constexpr (MWP) {
+    if (refine_enabled()) return launch4<NPE, MWP, SECOND, true>(a, n_prog, n_sm_max, s);
+  }
+  return launch4<NPE, MWP, SECOND, false>(a, n_prog, n_sm_max, s);
 }
 
 template <int NPE>
