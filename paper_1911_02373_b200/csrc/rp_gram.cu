@@ -221,8 +221,13 @@ __host__ __device__ inline int gram_stride(int nb) {  // smem row stride (double
   return s;
 }
 
+#ifdef RP_GRAM_DMMA_NV  // a pure function of its operands: the scheduler may move it
+#define RP_GRAM_ASM asm
+#else
+#define RP_GRAM_ASM asm volatile
+#endif
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  RP_GRAM_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -245,6 +250,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP), completes on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
@@ -540,6 +548,7 @@ struct FusedArgs {
   const double *S;  // [K] row scales (NV = 1, weighted refit) or null
   int64_t K;
   double *part;     // [gridDim.x][NT][64]  canonical (pair, upper tile) order
+  int tma = 0;      // k_gram_ws: inputs of full tiles by bulk copy (16-byte aligned X, V rows, S)
 };
 
 template <int NB, int NV>
@@ -670,6 +679,15 @@ constexpr int kWsNS = RP_WS_NS;  // stages
 constexpr int kWsUnroll = RP_WS_UNROLL;  // k-steps per MMA loop body (code size: instruction cache)
 constexpr int kWsFlush = 32;   // tiles between flushes of the register accumulators (1024 rows)
 constexpr int kWsThreads = 32 * (kWsMW + kWsPW);
+constexpr int kWsIS = 4;       // input stages (raw X / V / S of a tile, filled by the TMA engine)
+// registers per thread after setmaxnreg: 12 x 32 x CREG + 4 x 32 x PREG <= 64K
+#ifndef RP_WS_PREG
+#define RP_WS_PREG 72
+#endif
+#ifndef RP_WS_CREG
+#define RP_WS_CREG 144
+#endif
+static_assert(kWsMW * 32 * RP_WS_CREG + kWsPW * 32 * RP_WS_PREG <= 65536, "register file");
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -681,13 +699,28 @@ struct WsL {
   static constexpr int XB = kWsRT * S + kWsRT * SCS;   // doubles per stage: X_0 | scales
 };
 
+// doubles before the input ring: stages | producers' power tables | exponent / tree tables
+template <int NB, int NV>
+__host__ __device__ constexpr size_t ws_in_off(int n, int pw) {
+  // rounded up to an even count: bulk-copy destinations are 16-byte aligned
+  return ((size_t)kWsNS * WsL<NB, NV>::XB + (size_t)kWsPW * (8 * n * pw + 16) +
+          ((size_t)kWsPW * 3 * FL<NB, NV>::M8 + 1) / 2 + 2) & ~(size_t)1;
+}
+
+// tile id of slot j of consumer warp WID: contiguous ranges of SLOTS tiles (measured faster than
+// spreading them so that every sub-partition holds NT / 4: 1.464 vs 1.509 ms at K = 10^6)
+template <int NT, int SLOTS>
+__host__ __device__ constexpr int ws_tile_id(int wid, int j) {
+  return wid * SLOTS + j < NT ? wid * SLOTS + j : -1;
+}
+
 // slot j of consumer warp WID: A = X_0 block bi scaled by sc (0: 1, 1 + v: V_v, 1 + NV + v: V_v^2),
 // B = X_0 block bj; packed as A offset | B offset << 12 | sc << 24
 template <int NB, int NV, int WID, int SLOTS>
 __host__ __device__ constexpr uint32_t ws_slot(int j) {
   constexpr int NT = (1 + 2 * NV) * NB * (NB + 1) / 2;
-  const int id = WID * SLOTS + j;
-  if (id >= NT) return kNoTile;
+  const int id = ws_tile_id<NT, SLOTS>(WID, j);
+  if (id < 0) return kNoTile;
   int pa = 0, pb = 0, pair = 0, bi = 0, bj = 0;
   fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
   return (uint32_t)(8 * bi) | ((uint32_t)(8 * bj) << 12) | ((uint32_t)pair << 24);
@@ -728,17 +761,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *sX = fsm;  // [kWsNS][W::XB]
 
-  const int64_t r_begin = a.K * blockIdx.x / gridDim.x;
-  const int64_t r_end = a.K * (blockIdx.x + 1) / gridDim.x;
+  // slabs of whole 32-row tiles (tile starts are 16-byte aligned in X, V and S)
+  const int64_t ntiles = (a.K + kWsRT - 1) / kWsRT;
+  const int64_t r_begin = kWsRT * (ntiles * blockIdx.x / gridDim.x);
+  const int64_t r_end_t = kWsRT * (ntiles * (blockIdx.x + 1) / gridDim.x);
+  const int64_t r_end = r_end_t < a.K ? r_end_t : a.K;
   const int ntr = (int)((r_end - r_begin + kWsRT - 1) / kWsRT);
+  // input ring after the producers' scratch: [kWsIS][INB] doubles + 2 kWsIS mbarriers
+  const int INB = kWsRT * (B.n + NV + 1);
+  double *sIn = fsm + ws_in_off<NB, NV>(B.n, B.maxdeg + 1);
+  uint64_t *inFull = reinterpret_cast<uint64_t *>(sIn + kWsIS * INB), *inEmpty = inFull + kWsIS;
   for (int i = threadIdx.x; i < kWsNS * W::XB; i += blockDim.x) sX[i] = 0.0;  // pads stay zero
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsIS; ++i) {
+      mbar_init(inFull + i, 1);        // the issuing thread's expect_tx arrival (+ the bytes)
+      mbar_init(inEmpty + i, kWsPW);   // every producer warp has read its inputs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
   if (wid >= kWsMW) {
     // ---- producers: 8 rows per warp per tile --------------------------------------------------
     // The inputs of the warp's 8 rows, [X (8 n) | V (8 NV) | S (8)], are loaded into registers one
     // tile ahead (2 values per lane), so the HBM latency is off the staging path.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RP_WS_PREG));
     const int pw = wid - kWsMW;
     const int n = B.n, m = B.n_num, pwr = B.maxdeg + 1;
     const int nXv = 8 * n, nVv = 8 * NV, nIn = nXv + nVv + (a.S ? 8 : 0);
@@ -765,7 +812,34 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
       i -= nVv;
       return r0 + i < r_end ? a.S[r0 + i] : 0.0;
     };
-    double v0 = fetch(0, lane), v1 = fetch(0, lane + 32);
+    // TMA path: tile tr's raw inputs [X (32 n) | V (NV x 32) | S (32)] land in input stage
+    // tr % kWsIS by bulk copies that one thread issues kWsIS - 1 tiles ahead; a partial tail
+    // tile (and any launch whose rows are not 16-byte aligned) takes the register path below.
+    const bool tma = a.tma != 0;
+    auto full_tile = [&](int tr) { return r_begin + (int64_t)(tr + 1) * kWsRT <= r_end; };
+    auto issue = [&](int tr) {  // one thread: the bulk copies of tile tr into its input stage
+      const int st = tr % kWsIS;
+      double *dst = sIn + st * INB;
+      const int64_t r0 = r_begin + (int64_t)tr * kWsRT;
+      const unsigned bx = kWsRT * n * 8, bv = kWsRT * 8;
+      mbar_expect_tx(inFull + st, bx + NV * bv + (a.S ? bv : 0));
+      bulk_g2s(dst, a.X + r0 * n, bx, inFull + st);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) bulk_g2s(dst + kWsRT * n + v * kWsRT, a.V + (int64_t)v * a.K + r0, bv, inFull + st);
+      if (a.S) bulk_g2s(dst + kWsRT * (n + NV), a.S + r0, bv, inFull + st);
+    };
+    auto from_stage = [&](const double *src, int i) -> double {  // input i of the warp's rows
+      if (i >= nIn) return 0.0;
+      if (i < nXv) return src[8 * pw * n + i];
+      i -= nXv;
+      if (i < nVv) return src[kWsRT * n + (i / 8) * kWsRT + 8 * pw + i % 8];
+      i -= nVv;
+      return src[kWsRT * (n + NV) + 8 * pw + i];
+    };
+    if (tma && pw == 0 && lane == 0)
+      for (int t = 0; t < kWsIS - 1 && t < ntr; ++t)
+        if (full_tile(t)) issue(t);
+    double v0 = tma ? 0.0 : fetch(0, lane), v1 = tma ? 0.0 : fetch(0, lane + 32);
     __syncwarp();
     for (int tr = 0; tr < ntr; ++tr) {
       const int b = tr % kWsNS;
@@ -773,9 +847,32 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
       double *scb = buf + kWsRT * W::S + 8 * pw * W::SCS;  // scales of the warp's 8 rows
       const int64_t r0 = r_begin + (int64_t)tr * kWsRT + 8 * pw;
       const int nvalid = (int)((r_end - r0) < 8 ? (r_end - r0) : 8);  // rows of the warp in the slab
-      const double cv0 = v0, cv1 = v1;
-      v0 = fetch(tr + 1, lane);  // the next tile's inputs: in flight while this one is built
-      v1 = fetch(tr + 1, lane + 32);
+      double cv0, cv1;
+      if (tma) {
+        if (full_tile(tr)) {
+          const int st = tr % kWsIS;
+          mbar_wait(inFull + st, (tr / kWsIS) & 1);
+          const double *src = sIn + st * INB;
+          cv0 = from_stage(src, lane);
+          cv1 = from_stage(src, lane + 32);
+          __syncwarp();
+          if (lane == 0) mbar_arrive1(inEmpty + st);
+        } else {
+          cv0 = fetch(tr, lane);
+          cv1 = fetch(tr, lane + 32);
+        }
+        // refill the stage of tile tr - 1 with tile tr + kWsIS - 1 once every producer read it
+        const int tn = tr + kWsIS - 1;
+        if (pw == 0 && lane == 0 && tn < ntr && full_tile(tn)) {
+          if (tn >= kWsIS) mbar_wait(inEmpty + tn % kWsIS, ((tn / kWsIS) - 1) & 1);
+          issue(tn);
+        }
+      } else {
+        cv0 = v0;
+        cv1 = v1;
+        v0 = fetch(tr + 1, lane);  // the next tile's inputs: in flight while this one is built
+        v1 = fetch(tr + 1, lane + 32);
+      }
       {  // row scales S
         const int i0 = lane - nXv - nVv, i1 = lane + 32 - nXv - nVv;
         if (i0 >= 0 && i0 < 8) sSw[i0] = cv0;
@@ -856,7 +953,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
   }
 
   // ---- consumers: the upper tiles of the 1 + 2 NV blocks ----------------------------------------
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RP_WS_CREG));
   double acc[SLOTS][2];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j) acc[j][0] = acc[j][1] = 0.0;
@@ -876,8 +973,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
     if (((tr + 1) % kWsFlush) == 0 || tr + 1 == ntr) {
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j) {
-        const int id = wid * SLOTS + j;
-        if (id < L::NT) {
+        const int id = ws_tile_id<L::NT, SLOTS>(wid, j);
+        if (id >= 0) {
           int pa, pb, pair, bi, bj;
           fused_tile<NB, NV>(id, pa, pb, pair, bi, bj);
           double *dst = part + (int64_t)(pair * L::T + upper_index(NB, bi, bj)) * 64 + lane * 2;
@@ -900,10 +997,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
 
 template <int NB, int NV>
 static size_t ws_smem(int n, int pw) {
-  using L = FL<NB, NV>;
-  using W = WsL<NB, NV>;
-  return sizeof(double) * ((size_t)kWsNS * W::XB + (size_t)kWsPW * (8 * n * pw + 16)) +
-         sizeof(uint32_t) * kWsPW * 3 * L::M8;
+  return sizeof(double) * (ws_in_off<NB, NV>(n, pw) + (size_t)kWsIS * kWsRT * (n + NV + 1)) +
+         sizeof(uint64_t) * 2 * kWsIS;
 }
 
 // The per-CTA partials summed over CTAs in a fixed order: 4 quarter sums per element (CTAs
@@ -968,6 +1063,11 @@ static cudaError_t launch_fused_t(const GramBasis *d_basis, const GramBasis &h, 
   const int gx = fused_grid_x(K);
   if ((size_t)(gx + 1) * L::NT * 64 > part_elems) return cudaErrorInvalidValue;
   FusedArgs fa{d_basis, X, V, S, K, d_part};
+  // bulk copies need 16-byte aligned sources: X rows and V / S tile starts (K even)
+  fa.tma = ((uintptr_t)X % 16 == 0) && ((uintptr_t)V % 16 == 0) && (!S || (uintptr_t)S % 16 == 0) && (K % 2 == 0);
+#ifdef RP_WS_NOTMA  // measurement: the register-prefetch path only
+  fa.tma = 0;
+#endif
   cudaError_t e;
   const char *gk = getenv("RP_GRAM_KERNEL");  // "fused": the single-role kernel (tests, measurements)
   const bool ws = !(gk && strcmp(gk, "fused") == 0);
