@@ -390,14 +390,17 @@ def main():
     gram_ms = g0.elapsed_time(g1) / 3
 
     # ---- e2e: the same step fed from pinned host buffers --------------------------------------
-    # (1) pipelined (the headline e2e): FitSweepPipeline streams step i+1's inputs in and step
-    #     i-1's winners out while step i computes; every step's copies are inside the timed
-    #     region, and the L2 is flushed before every step's fit (on the compute stream, timed).
+    # (1) pipelined (the headline e2e): at N = 1 the C ABI's rp_pipeline (rp_pipeline.cu, through
+    #     pipeline.StepPipeline): step i+1's X, V, D stream in on one copy stream and step i-1's
+    #     winners stream out on another while step i fits, refreshes the plan and sweeps; timed by
+    #     librp's device events from the first H2D to the last D2H (rp_pipeline_timer_*), every
+    #     step's copies inside.  At N > 1 the sharded fit needs torch.distributed between the Gram
+    #     and the solve, so pipeline.FitSweepPipeline runs the same schedule on torch streams.
     # (2) call by call: rp_fit / rp_plan_create / rp_plan_eval_argmin with host pointers, the
     #     library staging the copies synchronously (no overlap) -- reported as e2e.sync.
     e2e = None
     if not args.no_e2e:
-        from paper_1911_02373_b200.pipeline import FitSweepPipeline
+        from paper_1911_02373_b200.pipeline import FitSweepPipeline, StepPipeline
         Xh = torch.from_numpy(inp["X"][klo:khi]).pin_memory()
         Vh = V_dev.cpu().pin_memory()
         Dh = torch.from_numpy(inp["D"][dlo:dhi]).pin_memory()
@@ -405,36 +408,55 @@ def main():
         n_out = nD if world > 1 else dhi - dlo
         oi = torch.empty((1, n_out), dtype=torch.int32).pin_memory()
         oE = torch.empty((1, n_out), dtype=torch.float64).pin_memory()
-        fit_fn = None
-        gather_fn = None
-        if world > 1:
-            def fit_fn(X, V):
-                return rdist.sharded_fit_dev(X, V, inp["num"], inp["den"], ops, n_vars=4)[:2]
-
-            def gather_fn(i, E):
-                return rdist.gather_winners(i, E, nD)
-        pipe = FitSweepPipeline(inp["truth"], F_dev, inp["num"], inp["den"], khi - klo, 4, 3, dhi - dlo, 2,
-                                device=dev, fit_fn=fit_fn, gather_fn=gather_fn)
-
-        def fed_step():
-            with torch.cuda.stream(pipe.compute):
-                flush.zero_()
-            return pipe.submit(Xh, Vh, Dh, oi, oE)
-
-        for _ in range(3):
-            fed_step()
-        barrier()
         n_e = max(4, args.steps)
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(pipe.h2d)
-        for _ in range(n_e):
-            done = fed_step()
-        pipe.d2h.wait_event(done)
-        t1.record(pipe.d2h)
-        barrier()
-        e_ms = t0.elapsed_time(t1) / n_e
+        if world == 1:
+            cpipe = StepPipeline(inp["truth"], F_dev, inp["num"], inp["den"], khi - klo, 3, dhi - dlo, 2, depth=2)
+            oi1, oE1 = oi.reshape(-1), oE.reshape(-1)
+            for _ in range(3):
+                cpipe.submit(Xh, Vh, Dh, oi1, oE1)
+            cpipe.sync()
+            barrier()
+            cpipe.timer_start()
+            for _ in range(n_e):
+                cpipe.submit(Xh, Vh, Dh, oi1, oE1)
+            e_ms = cpipe.timer_stop() / n_e
+            cpipe.sync()
+            cpipe.close()
+            e2e_path = ("rp_pipeline (C ABI, rp_pipeline.cu): pinned X, V, D in and winners out on two copy streams "
+                        "inside librp, overlapped with the neighbouring steps' fit -> plan update -> sweep; device "
+                        "events from the first H2D to the last D2H")
+        else:
+            fit_fn = None
+            gather_fn = None
+            if world > 1:
+                def fit_fn(X, V):
+                    return rdist.sharded_fit_dev(X, V, inp["num"], inp["den"], ops, n_vars=4)[:2]
+
+                def gather_fn(i, E):
+                    return rdist.gather_winners(i, E, nD)
+            pipe = FitSweepPipeline(inp["truth"], F_dev, inp["num"], inp["den"], khi - klo, 4, 3, dhi - dlo, 2,
+                                    device=dev, fit_fn=fit_fn, gather_fn=gather_fn)
+
+            def fed_step():
+                with torch.cuda.stream(pipe.compute):
+                    flush.zero_()
+                return pipe.submit(Xh, Vh, Dh, oi, oE)
+
+            for _ in range(3):
+                fed_step()
+            barrier()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(pipe.h2d)
+            for _ in range(n_e):
+                done = fed_step()
+            pipe.d2h.wait_event(done)
+            t1.record(pipe.d2h)
+            barrier()
+            e_ms = t0.elapsed_time(t1) / n_e
+            pipe.close()
+            e2e_path = ("FitSweepPipeline (pipeline.py): pinned X, V, D in and winners out on two copy streams, "
+                        "overlapped with the neighbouring steps' sharded fit -> plan update -> sweep -> gather")
         ok_e2e = bool(torch.equal(oi.reshape(-1), i_dev.reshape(-1).cpu()))
-        pipe.close()
         # call by call (no overlap)
         Xn, Vn, Dn = Xh.numpy(), Vh.numpy(), Dh.numpy()
         oin = torch.empty((1, dhi - dlo), dtype=torch.int32).pin_memory().numpy()
@@ -462,10 +484,8 @@ def main():
         d2h = oi.nbytes + oE.nbytes
         e2e = {"value": nD * nF / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": n_e, "winners_match_device_step": ok_e2e,
-               "path": "FitSweepPipeline (pipeline.py): pinned X, V, D in and winners out on two copy streams, "
-                       "overlapped with the neighbouring steps' fit -> plan update -> sweep (librp device forms); "
-                       "L2 flushed before every step",
+               "steps": n_e, "winners_match_device_step": ok_e2e, "path": e2e_path,
+               "l2": "not flushed: every step's 72 MB of inputs arrive by H2D while the previous step computes",
                "sync": {"value": nD * nF / (s_ms * 1e-3), "ms_per_step": s_ms,
                         "path": "rp_fit + rp_plan_create + rp_plan_eval_argmin with pinned host buffers, "
                                 "library-staged copies, no overlap"}}

@@ -362,6 +362,32 @@ rp_status rp_decider_create(rp_plan plan, int32_t prog, double margin, rp_decide
 rp_status rp_decider_decide(rp_decider dc, const int32_t *D, rp_decision *out);
 rp_status rp_decider_destroy(rp_decider dc);
 
+/* ---- host-fed steps, pipelined (the e2e use: batches arrive in host memory) -------------------
+ * One step = the whole path for one batch: fit of n_v metrics on the samples X (host float64
+ * [K][n]) with measured V (host float64 [n_v][K]) -> rp_plan_update_program of program 0 of
+ * `plan` (a single-program plan created for the program's bases, F, H and resources) -> sweep of
+ * the data tuples D (host int32 [nD][d]) -> per-D winners into best_idx (host int32 [nD]) and
+ * best_E (host float64 [nD]).  rp_pipeline_submit enqueues a step and returns at once: the H2D
+ * copies of the step's inputs run on a copy stream while the previous step computes, and its
+ * winners come back on another copy stream while the next step computes (up to `depth` steps in
+ * flight, depth in [1, 4]; device buffers allocated once per slot at creation).  Host buffers must
+ * stay valid and unmodified until rp_pipeline_sync returns (pinned memory makes the copies truly
+ * asynchronous; pageable memory is still correct but the copies then block the submitting thread).
+ * PAPER.md:2094-2099 (evaluate before each launch), 2222-2235 (re-estimate from samples).
+ * Errors: INVALID_ARG (shapes, a multi-program plan), CUDA.  Not thread-safe per pipeline. */
+typedef struct rp_pipeline_s *rp_pipeline;
+rp_status rp_pipeline_create(rp_plan plan, int32_t prog, const rp_basis *basis, int32_t n_v, int64_t K,
+                             int32_t d, int64_t nD, int32_t depth, rp_pipeline *out);
+rp_status rp_pipeline_submit(rp_pipeline p, const double *X, const double *V, const int32_t *D, int32_t *best_idx,
+                             double *best_E);
+rp_status rp_pipeline_sync(rp_pipeline p);
+/* Device time of a run of steps: timer_start records an event on the copy-in stream ahead of the
+ * next submitted step's H2D (call rp_pipeline_sync first so no earlier step overlaps); timer_stop
+ * records one after the last submitted step's D2H, waits for it and writes the elapsed ms.      */
+rp_status rp_pipeline_timer_start(rp_pipeline p);
+rp_status rp_pipeline_timer_stop(rp_pipeline p, float *ms);
+rp_status rp_pipeline_destroy(rp_pipeline p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,12 @@ _SIGS = {
     "rp_plan_history_clear": [_vp, _vp],
     "rp_plan_enable_timing": [_vp, _i32],
     "rp_plan_last_timing": [_vp, _vp],
+    "rp_pipeline_create": [_vp, _i32, C.POINTER(rp_basis), _i32, _i64, _i32, _i64, _i32, C.POINTER(_vp)],
+    "rp_pipeline_submit": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "rp_pipeline_sync": [_vp],
+    "rp_pipeline_timer_start": [_vp],
+    "rp_pipeline_timer_stop": [_vp, _vp],
+    "rp_pipeline_destroy": [_vp],
 }
 for _name, _args in _SIGS.items():
     getattr(_lib, _name).argtypes = _args

@@ -362,6 +362,16 @@ struct rp_plan_s {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, sweep, refine, end
 };
 
+namespace rp {
+int plan_num_programs(rp_plan plan) { return plan ? plan->n_prog : 0; }
+int plan_num_data_params(rp_plan plan) { return plan ? plan->d : 0; }
+// a stream the plan was last used on is about to be destroyed: later stream-ordered frees of the
+// plan go to the legacy default stream instead
+void plan_forget_stream(rp_plan plan, cudaStream_t s) {
+  if (plan && plan->stream == s) plan->stream = nullptr;
+}
+}  // namespace rp
+
 static void plan_free(rp_plan pl) {
   if (!pl) return;
   // stream-ordered frees on the stream the plan was last used on (rp.h: rp_plan_destroy)

@@ -162,5 +162,8 @@ cudaError_t launch_jit(rp_jit jit, const int32_t *D, int64_t nD, const int32_t *
                        double *bestE, double *secondE, cudaStream_t s);
 
 int num_sms();
+int plan_num_programs(rp_plan plan);     // rp_pipeline: shape checks against the plan
+int plan_num_data_params(rp_plan plan);
+void plan_forget_stream(rp_plan plan, cudaStream_t s);
 
 }  // namespace rp

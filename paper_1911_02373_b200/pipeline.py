@@ -1,5 +1,9 @@
 """Host-fed fit -> plan update -> sweep, pipelined over steps (plumbing only).
 
+`StepPipeline` is the C ABI's rp_pipeline (rp_pipeline.cu): the copies and the event ordering run
+inside librp.  `FitSweepPipeline` below is the same schedule written with torch streams, for the
+multi-rank case, whose fit needs the torch.distributed all-reduce between the Gram and the solve.
+
 A user who tunes many launches feeds batches from host memory: sampled points X, measured metrics
 V and data tuples D in, the per-D winners out.  `FitSweepPipeline` overlaps those copies with the
 computation of the neighbouring steps: the inputs of step i+1 stream in on one copy stream and the
@@ -17,7 +21,51 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import Plan, fit_dev
+import ctypes as C
+
+from . import Basis, Plan, _check, _lib, _ptr, fit_dev
+
+
+class StepPipeline:
+    """rp_pipeline: submit(X, V, D, idx_out, E_out) with host arrays (pinned for overlap) enqueues
+    one fit -> plan update -> sweep step and returns at once; sync() waits for every step."""
+
+    def __init__(self, program, F, num_exp, den_exp, K: int, n_v: int, nD: int, d: int, depth: int = 2):
+        self.plan = Plan([program], F)
+        self.basis = Basis(num_exp, den_exp)
+        self.h = C.c_void_p()
+        _check(_lib.rp_pipeline_create(self.plan.handle, 0, C.byref(self.basis.c), n_v, K, d, nD, depth,
+                                       C.byref(self.h)))
+        self.keep = []  # host buffers of steps in flight
+
+    def submit(self, X, V, D, idx_out, E_out):
+        self.keep.append((X, V, D, idx_out, E_out))
+        _check(_lib.rp_pipeline_submit(self.h, _ptr(X), _ptr(V), _ptr(D), _ptr(idx_out), _ptr(E_out)))
+
+    def sync(self):
+        _check(_lib.rp_pipeline_sync(self.h))
+        self.keep.clear()
+
+    def timer_start(self):
+        _check(_lib.rp_pipeline_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        """ms from timer_start to the D2H of the last submitted step (device events)."""
+        ms = C.c_float()
+        _check(_lib.rp_pipeline_timer_stop(self.h, C.byref(ms)))
+        return float(ms.value)
+
+    def close(self):
+        if self.h:
+            _lib.rp_pipeline_destroy(self.h)
+            self.h = C.c_void_p()
+            self.plan.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class FitSweepPipeline:
