@@ -1283,15 +1283,155 @@ __device__ __forceinline__ double extract_sigma(double B) {
 }
 
 // a6 + Appendix A for one pair from its polynomial values (as k_sweep evaluates them)
+// ---- double-double arithmetic for the refined E (the literal order of Appendix A) ----------------
+// When the metrics have mixed signs (a fitted g_i < 0 somewhere) the sums of Appendix A cancel and
+// an FP64 evaluation of E from exact inputs can be off by 1e4 ulp; in double-double (~2^-104) the
+// estimate of the refined pair is accurate to the rounding of its final value.
+struct ddv {
+  double h, l;
+};
+__device__ __forceinline__ ddv dd_qts(double a, double b) {  // |a| >= |b|
+  const double s = a + b;
+  return ddv{s, b - (s - a)};
+}
+__device__ __forceinline__ ddv dd_ts(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return ddv{s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ ddv dd_add(ddv x, ddv y) {
+  ddv s = dd_ts(x.h, y.h), t = dd_ts(x.l, y.l);
+  s.l += t.h;
+  s = dd_qts(s.h, s.l);
+  s.l += t.l;
+  return dd_qts(s.h, s.l);
+}
+__device__ __forceinline__ ddv dd_neg(ddv x) { return ddv{-x.h, -x.l}; }
+__device__ __forceinline__ ddv dd_sub(ddv x, ddv y) { return dd_add(x, dd_neg(y)); }
+__device__ __forceinline__ ddv dd_mul(ddv x, ddv y) {
+  const double p = x.h * y.h;
+  double e = fma(x.h, y.h, -p);
+  e = fma(x.h, y.l, fma(x.l, y.h, e));
+  return dd_qts(p, e);
+}
+__device__ __forceinline__ ddv dd_muld(ddv x, double b) {
+  const double p = x.h * b;
+  return dd_qts(p, fma(x.l, b, fma(x.h, b, -p)));
+}
+// x / y: three quotient digits from one ~1-ulp reciprocal of y.h; each remainder step removes
+// the previous digit's error (QD's accurate division with the IEEE divisions replaced)
+__device__ __forceinline__ ddv dd_div(ddv x, ddv y) {
+  const double ry = frcp(y.h);
+  const double q1 = x.h * ry;
+  ddv r = dd_sub(x, dd_muld(y, q1));
+  const double q2 = r.h * ry;
+  r = dd_sub(r, dd_muld(y, q2));
+  const double q3 = r.h * ry;
+  return dd_add(dd_qts(q1, q2), ddv{q3, 0.0});
+}
+__device__ __forceinline__ bool dd_lt(ddv x, ddv y) { return x.h < y.h || (x.h == y.h && x.l < y.l); }
+__device__ __forceinline__ bool dd_eq(ddv x, ddv y) { return x.h == y.h && x.l == y.l; }
+__device__ __forceinline__ ddv dd_min(ddv x, ddv y) { return dd_lt(y, x) ? y : x; }
+__device__ __forceinline__ ddv dd_d(double a) { return ddv{a, 0.0}; }
+
+// Appendix A lines 5-18 in double-double, in the oracle's literal order (DESIGN.md Appendix A)
+__device__ double mwpcwp_E_dd(const ddv *pk, double W, int64_t blocks, double B, int64_t smact,
+                              const DevProg &pg) {
+  const ddv g1 = dd_div(pk[0], pk[1]), g2 = dd_div(pk[2], pk[3]), g3 = dd_div(pk[4], pk[5]);
+  const ddv Wact = dd_d(W), SMact = dd_d((double)smact);
+  const ddv Mem = dd_add(g2, g3), Tot = dd_add(dd_add(g1, g2), g3);             // 5
+  const ddv W_unc = dd_div(g3, Mem), W_coal = dd_div(g2, Mem);                   // 6
+  const ddv L_unc = dd_add(dd_d(pg.mem_ld), dd_muld(dd_d(pg.U - 1.0), pg.dd_unc));  // 7
+  const ddv L_coal = dd_d(pg.mem_ld);
+  const ddv Mem_L = dd_add(dd_mul(L_unc, W_unc), dd_mul(L_coal, W_coal));        // 8
+  const ddv Dep = dd_add(dd_mul(dd_muld(dd_d(pg.dd_unc), pg.U), W_unc), dd_muld(W_coal, pg.dd_coal));  // 9
+  const ddv MWP_nb = dd_div(Mem_L, Dep);                                         // 10
+  const ddv BWpw = dd_div(dd_muld(dd_d(pg.freq), pg.lbpw), Mem_L);               // 11
+  const ddv MWP_bw = dd_div(dd_d(pg.mem_bw), dd_mul(BWpw, SMact));
+  ddv MWP = MWP_nb;                                                              // 12
+  if (dd_lt(MWP_bw, MWP)) MWP = MWP_bw;
+  if (dd_lt(Wact, MWP)) MWP = Wact;
+  const ddv Comp_c = dd_muld(Tot, pg.issue);                                     // 13
+  const ddv Mem_c = dd_add(dd_mul(L_unc, g3), dd_mul(L_coal, g2));
+  const ddv CWP_full = dd_div(dd_add(Mem_c, Comp_c), Comp_c);                    // 14
+  const ddv CWP = dd_lt(CWP_full, Wact) ? CWP_full : Wact;
+  const ddv Rep = dd_div(dd_d((double)blocks), dd_muld(SMact, B));               // 15
+  const ddv tail = dd_mul(dd_div(Comp_c, Mem), dd_sub(MWP, dd_d(1.0)));
+  ddv E;
+  if (dd_eq(MWP, Wact) && dd_eq(CWP, Wact))                                      // 16
+    E = dd_mul(dd_add(dd_add(Mem_c, Comp_c), tail), Rep);
+  else if (!dd_lt(CWP, MWP) || dd_lt(Mem_c, Comp_c))                             // 17
+    E = dd_mul(dd_add(dd_div(dd_mul(Mem_c, Wact), MWP), tail), Rep);
+  else                                                                           // 18
+    E = dd_mul(dd_add(Mem_L, dd_mul(Comp_c, Wact)), Rep);
+  return E.h + E.l;
+}
+
+// the same E in double-double in the sweep's common-denominator arrangement (g_i = a_i / Q;
+// rp_device.cuh mwpcwp_E): 4 divisions instead of the literal order's 12, identical to it up to
+// double-double rounding; the case tests compare the same quantities as Appendix A
+__device__ double mwpcwp_E_dd2(const ddv *pk, double W, int64_t blocks, double B, int64_t smact,
+                               const DevProg &pg) {
+  const EConst k = make_econst(pg);
+  const ddv q23 = dd_mul(pk[3], pk[5]), q13 = dd_mul(pk[1], pk[5]), q12 = dd_mul(pk[1], pk[3]);
+  const ddv Q = dd_mul(pk[1], q23);
+  const ddv a1 = dd_mul(pk[0], q23), a2 = dd_mul(pk[2], q13), a3 = dd_mul(pk[4], q12);
+  const ddv s23 = dd_add(a2, a3), s = dd_add(a1, s23);                           // Mem Q, Tot Q
+  const ddv mc = dd_add(dd_muld(a3, k.Lunc), dd_muld(a2, k.Lcoal));              // Mem_c Q
+  const ddv dn = dd_add(dd_muld(a3, k.DdU), dd_muld(a2, k.ddc));                 // Dep Mem Q
+  const ddv cc = dd_muld(s, k.issue);                                            // Comp_c Q
+  const ddv SM = dd_d((double)smact), Wd = dd_d(W), one = dd_d(1.0);
+  const ddv Mem_c = dd_div(mc, Q), Comp_c = dd_div(cc, Q);
+  const ddv MWP_nb = dd_div(mc, dn);                                             // 10
+  const ddv MWP_bw = dd_div(dd_muld(mc, k.Kbw), dd_mul(s23, SM));               // 11
+  const ddv CWPf = dd_add(one, dd_div(mc, cc));                                  // 14
+  const bool bw = dd_lt(MWP_bw, MWP_nb);
+  const ddv mwp0 = bw ? MWP_bw : MWP_nb;
+  const bool mwpW = !dd_lt(mwp0, Wd);                                            // 12: MWP = W_act
+  const ddv mwp = mwpW ? Wd : mwp0;
+  const bool cwpf = dd_lt(CWPf, Wd);
+  const ddv cwp = cwpf ? CWPf : Wd;
+  const ddv cpm = dd_div(cc, s23);                                               // Comp_c / Mem
+  const ddv tail = dd_mul(cpm, dd_sub(mwp, one));
+  ddv X;
+  if (mwpW && !cwpf)                                                             // 16
+    X = dd_add(dd_add(Mem_c, Comp_c), tail);
+  else if (!dd_lt(cwp, mwp) || dd_lt(Mem_c, Comp_c))                             // 17
+    X = dd_add(mwpW ? Mem_c : dd_div(dd_mul(Mem_c, Wd), mwp0), tail);
+  else                                                                           // 18
+    X = dd_add(dd_div(mc, s23), dd_mul(Comp_c, Wd));
+  const ddv E = dd_div(dd_mul(X, dd_d((double)blocks)), dd_muld(SM, B));         // 15: x #Blocks / (B SM)
+  return E.h + E.l;
+}
+
+// pk: the refined polynomial values; (ph, pl): their unevaluated high / low sums
 template <int NPOLY>
 __device__ __forceinline__ double pair_E(const DevProg &pg, const CfgTable &tab, int g, const int32_t *Dt,
-                                         const CfgRec &r, const double *pk) {
-  if (NPOLY != 6) return pk[0] * frcp(pk[1]);  // template g1
+                                         const CfgRec &r, const double *pk, const double *ph, const double *pl) {
+  if (NPOLY != 6) {  // template g1: E = p_0 / q_0
+    const ddv p0 = dd_ts(ph[0], pl[0]), q0 = dd_ts(ph[1], pl[1]);
+    const ddv E = dd_div(p0, q0);
+    return E.h + E.l;
+  }
   const int P[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
   int64_t blocks = 1;
   for (int k = 0; k < pg.p && k < 3; ++k)
     if (pg.grid_map[k] >= 0) blocks *= ((int64_t)Dt[pg.grid_map[k]] + P[k] - 1) / P[k];
   const int64_t smact = blocks < pg.n_sm ? blocks : pg.n_sm;
+  // all six values positive: every sum of Appendix A adds positive terms and FP64 is accurate to
+  // ~20 ulp; otherwise (a metric <= 0 somewhere, sums that cancel) the double-double form
+  bool pos = true;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) pos = pos && pk[k] > 0.0;
+  if (!pos) {
+    ddv pd[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) pd[k] = dd_ts(ph[k], pl[k]);
+#ifdef RP_REFINE_LITERAL_DD
+    return mwpcwp_E_dd(pd, r.W, blocks, rint(1.0 / r.rB), smact, pg);  // B_active: a small integer
+#else
+    return mwpcwp_E_dd2(pd, r.W, blocks, rint(1.0 / r.rB), smact, pg);
+#endif
+  }
   const double rSM = tab.rSM[(int64_t)g * kRSMTab + smact];
   const double Rep = (double)blocks * r.rB * rSM;
   return mwpcwp_E(pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], r.W, Rep, rSM, (double)smact, make_econst(pg));
@@ -1418,7 +1558,7 @@ __global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
   double pk[NPOLY];
 #pragma unroll
   for (int k = 0; k < NPOLY; ++k) pk[k] = h1[k] + l1[k];
-  double E1 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r1, pk);
+  double E1 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r1, pk, h1, l1);
   if (!pos_finite(E1)) E1 = a.bestE[o];  // exact evaluation masks the pair: keep the sweep's value
   if (!SECOND) {
     a.bestE[o] = E1;
@@ -1428,7 +1568,7 @@ __global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
   if (two) {
 #pragma unroll
     for (int k = 0; k < NPOLY; ++k) pk[k] = h2[k] + l2[k];
-    const double e2 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r2, pk);
+    const double e2 = pair_E<NPOLY>(pg, a.tab, g, Dt, *r2, pk, h2, l2);
     if (pos_finite(e2)) E2 = e2;
   }
   // re-rank the two on the exact key (E, original index)

@@ -345,3 +345,127 @@ def random_D_edge_cases(d: int) -> np.ndarray:
     """Degenerate data tuples: smallest sizes (D1 < 32 fires P1*P2 <= D1^2), D1 = 1."""
     rows = [[1] * d, [4] * d, [5] * d, [31] * d, [32] * d, [33] * d]
     return np.asarray(rows, dtype=np.int32)
+
+
+# --------------------------------------------------------------------------------------------
+# class L (SURVEY 8(c) "parity classes", 8(d) "Program generators"): the paper's own regime --
+# samples profiled at small data sizes and launch shapes (PAPER.md:2119-2120, 2352-2357) and
+# kernel-flavoured truths of lower degree than the fit's bounds (non-unique fits, PAPER.md:
+# 2609-2615).  Diagnostics, not gated fits.
+# --------------------------------------------------------------------------------------------
+
+
+def launch_design_tiny() -> np.ndarray:
+    """64 points: N in {32, 64, 128, 256} x 16 seeded configurations of the 2-D pow2 set."""
+    g = rng("tiny", "launch")
+    F = F_pow2_2d()
+    rows = []
+    for N in (32, 64, 128, 256):
+        for j in g.choice(len(F), size=16, replace=False):
+            rows.append([N, F[j][0], F[j][1]])
+    return np.asarray(rows, dtype=np.float64)
+
+
+def launch_design_poly(config: str = "polybench", K: int = 2000) -> np.ndarray:
+    """K points: N log-uniform in [32, 512], P uniform over the 231 warp-valid 3-D pow2 shapes."""
+    g = rng(config, "launch")
+    F = F_pow2_3d()
+    F = F[(F.prod(axis=1) % 32) == 0]
+    N = log_uniform_ints(g, 32, 512, K)
+    P = F[g.integers(0, len(F), size=K)]
+    return np.concatenate([N.reshape(-1, 1), P], axis=1).astype(np.float64)
+
+
+def _rat(terms_num, terms_den, n=4):
+    """(exponent list, coefficient list) pairs of one rational function in raw x (identity transform)."""
+    ne = np.zeros((len(terms_num), n), dtype=np.int16)
+    de = np.zeros((len(terms_den), n), dtype=np.int16)
+    cn, cd = [], []
+    for i, (c, e) in enumerate(terms_num):
+        ne[i, :len(e)] = e
+        cn.append(c)
+    for i, (c, e) in enumerate(terms_den):
+        de[i, :len(e)] = e
+        cd.append(c)
+    return ne, de, np.asarray(cn + cd, dtype=np.float64)
+
+
+# kernel-flavoured truths (SURVEY 8(d)) over x = (N, bx, by, bz): (comp, coal, uncoal) per thread
+KERNEL_FAMILIES = {
+    "gemm": (  # also 2mm K1
+        ([(10.0, ()), (8.0, (1,))], [(1.0, ())]),
+        ([(2.0, (1, 1)), (1.0, (0, 1))], [(8.0, ()), (1.0, (0, 1))]),
+        ([(16.0, ()), (16.0, (1,)), (2.0, (0, 1))], [(8.0, ()), (1.0, (0, 1))]),
+    ),
+    "2mm_k2": (
+        ([(12.0, ()), (9.0, (1,))], [(1.0, ())]),
+        ([(2.0, (1, 1)), (1.0, (0, 1))], [(8.0, ()), (1.0, (0, 1))]),
+        ([(16.0, ()), (16.0, (1,)), (2.0, (0, 1))], [(8.0, ()), (1.0, (0, 1))]),
+    ),
+    "jacobi2d": (
+        ([(14.0, ())], [(1.0, ())]),
+        ([(6.0, (0, 1))], [(2.0, ()), (1.0, (0, 1))]),
+        ([(12.0, ())], [(2.0, ()), (1.0, (0, 1))]),
+    ),
+}
+
+
+def kernel_truth(family: str, hw=HW_GTX1080TI, R: int = 32, Z0: int = 0, Z1: int = 0, scale=None) -> ProgramSpec:
+    """A kernel-flavoured truth as a program in the raw variables (identity transform); `scale`
+    optionally multiplies each metric's numerator constants (the multikernel perturbations)."""
+    num, den, coef = [], [], []
+    for i, (tn, td) in enumerate(KERNEL_FAMILIES[family]):
+        ne, de, c = _rat(tn, td)
+        if scale is not None:
+            c = c.copy()
+            c[:len(ne)] *= scale[i]
+        num.append(ne)
+        den.append(de)
+        coef.append(c)
+    return ProgramSpec(d=1, p=3, num_exp=num, den_exp=den, coef=coef, hw=dict(hw), R=R, Z0=Z0, Z1=Z1,
+                       grid_map=(0, 0, -1), xform_c=[0.0] * 4, xform_e=[0] * 4)
+
+
+@dataclass
+class ClassLCase:
+    name: str
+    X: np.ndarray            # launch-design samples [K][n]
+    truths: list             # ProgramSpec per program (the data generators)
+    basis: np.ndarray        # the fit's basis (numerator = denominator)
+    noise: list              # per program [l][K] multipliers
+    sweep: SweepCase         # the D x F grid the fitted programs are swept over
+    fit_programs: list       # ProgramSpec per program: H, resources, grid rule of the swept kernel
+
+
+def classL_case(name: str, sigma: float = 0.01, n_kernels: int = 20) -> ClassLCase:
+    """tiny: the class-F truth on the launch design (degree <= 2); polybench: gemm, 2mm K1/K2,
+    jacobi-2d kernel-flavoured truths; multikernel: seeded constant-perturbations of the three
+    families with the multikernel resources (degree <= 3 in (N, bx, by, bz))."""
+    if name == "tiny":
+        sw = tiny_sweep()
+        X = launch_design_tiny()
+        truths = sw.programs
+        basis = sw.programs[0].num_exp[0]
+        fit_programs = sw.programs
+    elif name == "polybench":
+        sw = polybench_sweep()
+        X = launch_design_poly("polybench")
+        fams = ["gemm", "gemm", "2mm_k2", "jacobi2d"]
+        truths = [kernel_truth(f, R=p.R) for f, p in zip(fams, sw.programs)]
+        basis = sw.programs[0].num_exp[0]
+        fit_programs = sw.programs
+    elif name == "multikernel":
+        sw = multikernel_sweep(n_kernels=n_kernels)
+        X = launch_design_poly("multikernel")
+        g = rng("multikernel", "perturb")
+        fams = ["gemm", "2mm_k2", "jacobi2d"]
+        truths = [kernel_truth(fams[k % 3], R=p.R, Z0=p.Z0, Z1=p.Z1, scale=g.uniform(0.8, 1.2, size=3))
+                  for k, p in enumerate(sw.programs)]
+        basis = sw.programs[0].num_exp[0]
+        fit_programs = sw.programs
+    else:
+        raise ValueError(name)
+    g = rng(name, "launch-noise")
+    noise = [np.stack([noise_multipliers(g, len(X), sigma) for _ in range(3)]) for _ in truths]
+    return ClassLCase(name, X, truths, basis, noise, sw, fit_programs)
+

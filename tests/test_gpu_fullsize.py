@@ -107,7 +107,11 @@ def test_bench_workload_noisy_fit_sweep():
     relq = np.abs(gE[feas] - Eq[feas]) / Eq[feas]
     assert relq.max() <= 1e-12, relq.max()
     # (2) SURVEY 8(c) #25 literally: long double oracle where kappa <= 1e3 at winner and runner-up
-    cov = feas & (ref["kappa"] <= 1e3) & ((ref["kappa2"] <= 1e3) | (ref["idx2"] < 0))
+    # (where the long double oracle is itself accurate: kappa <= 1e3 and its E within 1e-13 of the
+    # binary128 value -- mixed-sign metrics make Appendix A's sums cancel, R31)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        ld_ok = np.abs(ref["best"] - refq["best"]) <= 1e-13 * np.abs(refq["best"])
+    cov = feas & ld_ok & (ref["kappa"] <= 1e3) & ((ref["kappa2"] <= 1e3) | (ref["idx2"] < 0))
     ml = _margin(ref)
     s2 = cov & (ml > 1e-9)
     assert np.array_equal(gi[s2], ref["idx"][s2])
@@ -128,7 +132,8 @@ def test_bench_workload_noisy_fit_sweep():
                          "gate": "E <= 1e-12 at the GPU's pick; idx exact where exact margin > 1e-9, else in the 1e-9 tie set"},
         "survey_8c_25": {"covered_fraction": float(cov.sum() / max(feas.sum(), 1)),
                          "idx_exact": int(s2.sum()), "E_max_rel_err": float(rel2.max(initial=0)),
-                         "gate": "long double oracle where kappa <= 1e3 at winner and runner-up"},
+                         "gate": "long double oracle where kappa <= 1e3 at winner and runner-up and its E "
+                                 "within 1e-13 of the binary128 value"},
         "kappa_winner": {"median": float(np.median(ref["kappa"][feas])), "max": float(ref["kappa"][feas].max())},
         "long_double_vs_binary128_where_kappa_gt_1e3": float(ld_gap.max(initial=0)),
         "passed": True})

@@ -18,6 +18,8 @@ if [ "$3" = "full" ]; then
     python tools/prof_kernels.py sweep --reps 5 > gpurun_out/${TAG}_ncu_sweep.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_refine -s 3 -c 1 -o gpurun_out/${TAG}_refine \
     python tools/prof_kernels.py sweep --reps 5 > gpurun_out/${TAG}_ncu_refine.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gram_ws -s 2 -c 1 -o gpurun_out/${TAG}_gram \
+    python tools/gram_variant_time.py ncu > gpurun_out/${TAG}_ncu_gram.log 2>&1
 fi
 tail -5 gpurun_out/${TAG}_pytest.log 2>/dev/null
 head -c 600 gpurun_out/${TAG}_bench.json
