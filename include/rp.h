@@ -345,6 +345,34 @@ rp_status rp_plan_history_enable(rp_plan plan, int32_t prog, int32_t log2_capaci
 rp_status rp_plan_history_stats(rp_plan plan, int64_t *hits, int64_t *misses, int64_t *entries);
 rp_status rp_plan_history_clear(rp_plan plan, rp_stream s);
 
+/* ---- persistence --------------------------------------------------------------------------
+ * The paper keeps two artefacts across runs: the rational program built at compile time (step 3,
+ * PAPER.md:2243-2258) and the runtime history that "instantly provide[s] results for future
+ * kernel launches".  Both are saved as self-describing little-endian byte
+ * blobs with a magic, a version and an FNV-1a 64 checksum; coefficients keep their IEEE bits
+ * (a load reproduces the program exactly).  Writers: buf may be null to query *size; a non-null
+ * buf shorter than the blob is INVALID_ARG (with *size set).  Readers: INVALID_ARG on a wrong
+ * magic, a checksum mismatch, truncation or content that rp_plan_create would reject.
+ *   rp_program_save     -- rp_program (host) -> bytes (validated like rp_plan_create).
+ *   rp_program_load     -- bytes -> an owned rp_program_blob; rp_program_blob_program returns
+ *                          the rp_program inside (valid until rp_program_blob_free).
+ *   rp_plan_history_save -- the ready entries of the plan's runtime history (in slot order), its
+ *                          program index and margin, and a fingerprint of the device program
+ *                          (its coefficients and transform as they are now) and of F.
+ *                          INVALID_ARG if the history is not enabled.  Synchronises.
+ *   rp_plan_history_load -- inserts the saved entries into the plan's enabled history through the
+ *                          decision kernel's own hashing (rp_plan_decide then serves them as
+ *                          hits).  INVALID_ARG unless the data arity, program index, margin and
+ *                          fingerprint match: a history never outlives the program and
+ *                          configuration set that made it.  Synchronises.                      */
+typedef struct rp_program_blob_s *rp_program_blob;
+rp_status rp_program_save(const rp_program *prog, void *buf, int64_t cap, int64_t *size);
+rp_status rp_program_load(const void *buf, int64_t size, rp_program_blob *out);
+const rp_program *rp_program_blob_program(rp_program_blob blob);
+rp_status rp_program_blob_free(rp_program_blob blob);
+rp_status rp_plan_history_save(rp_plan plan, void *buf, int64_t cap, int64_t *size);
+rp_status rp_plan_history_load(rp_plan plan, const void *buf, int64_t size);
+
 /* Single-launch decider (the per-launch use of PAPER.md:2094-2099, "immediately preceding the
  * launch of a kernel", with the lowest host-visible latency the library offers): one data tuple
  * in, one rp_decision out, through host-mapped pinned memory (no copy nodes) and a CUDA graph of

@@ -123,12 +123,19 @@ _SIGS = {
     "rp_pipeline_timer_start": [_vp],
     "rp_pipeline_timer_stop": [_vp, _vp],
     "rp_pipeline_destroy": [_vp],
+    "rp_program_save": [C.POINTER(rp_program), _vp, _i64, C.POINTER(_i64)],
+    "rp_program_load": [_vp, _i64, C.POINTER(_vp)],
+    "rp_program_blob_free": [_vp],
+    "rp_plan_history_save": [_vp, _vp, _i64, C.POINTER(_i64)],
+    "rp_plan_history_load": [_vp, _vp, _i64],
 }
 for _name, _args in _SIGS.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
 
-EXPORTED = ["rp_abi_version", "rp_last_error", "rp_device_count"] + list(_SIGS)
+_lib.rp_program_blob_program.argtypes = [_vp]
+_lib.rp_program_blob_program.restype = C.POINTER(rp_program)
+EXPORTED = ["rp_abi_version", "rp_last_error", "rp_device_count", "rp_program_blob_program"] + list(_SIGS)
 
 
 def lib():
@@ -273,6 +280,53 @@ class Program:
     @property
     def n_metrics(self):
         return self.c.n_metrics
+
+
+class LoadedProgram:
+    """A program read back by :func:`load_program`, with the attributes :class:`Program`
+    accepts (copies of the blob's arrays; the transform is explicit)."""
+
+    def __init__(self, pr):
+        inv = {v: k for k, v in TEMPLATES.items()}
+        self.d, self.p = pr.d, pr.p
+        self.template = inv[pr.e_template]
+        n = pr.d + pr.p
+        self.num_exp, self.den_exp, self.coef = [], [], []
+        for i in range(pr.n_metrics):
+            b = pr.basis[i]
+            num = np.ctypeslib.as_array(C.cast(b.num_exp, C.POINTER(C.c_int16)), (b.n_num * b.n_vars,))
+            den = np.ctypeslib.as_array(C.cast(b.den_exp, C.POINTER(C.c_int16)), (b.n_den * b.n_vars,))
+            cf = np.ctypeslib.as_array(C.cast(pr.coef[i], C.POINTER(C.c_double)), (b.n_num + b.n_den,))
+            self.num_exp.append(num.reshape(b.n_num, b.n_vars).copy())
+            self.den_exp.append(den.reshape(b.n_den, b.n_vars).copy())
+            self.coef.append(cf.copy())
+        self.hw = {k: getattr(pr.hw, k) for k, _ in rp_hw._fields_}
+        self.R = pr.regs_per_thread
+        self.Z0, self.Z1 = pr.smem_words_base, pr.smem_words_per_thread
+        self.grid_map = tuple(pr.grid_map[k] for k in range(3))
+        self.xform_c = [pr.xform.c[k] for k in range(n)]
+        self.xform_e = [pr.xform.e[k] for k in range(n)]
+        self.box_lo = self.box_hi = None
+
+
+def save_program(prog) -> bytes:
+    """rp_program_save: the rational program as bytes (exact coefficients)."""
+    prog = prog if isinstance(prog, Program) else Program(prog)
+    n = _i64()
+    _check(_lib.rp_program_save(C.byref(prog.c), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(_lib.rp_program_save(C.byref(prog.c), buf, n.value, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def load_program(blob: bytes) -> LoadedProgram:
+    """rp_program_load: a program saved by :func:`save_program`."""
+    h = _vp()
+    _check(_lib.rp_program_load(blob, len(blob), C.byref(h)))
+    try:
+        return LoadedProgram(_lib.rp_program_blob_program(h).contents)
+    finally:
+        _lib.rp_program_blob_free(h)
 
 
 def _programs(progs):
@@ -426,6 +480,18 @@ class Plan:
 
     def clear_history(self):
         _check(_lib.rp_plan_history_clear(self.handle, C.c_void_p(0)))
+
+    def save_history(self) -> bytes:
+        """rp_plan_history_save: the runtime history as bytes (bound to the program and F)."""
+        n = _i64()
+        _check(_lib.rp_plan_history_save(self.handle, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(_lib.rp_plan_history_save(self.handle, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def load_history(self, blob: bytes):
+        """rp_plan_history_load: insert a saved history into this plan's enabled history."""
+        _check(_lib.rp_plan_history_load(self.handle, blob, len(blob)))
 
     def enable_timing(self, on: bool = True):
         """Per-phase CUDA events in every later eval (rp_plan_enable_timing)."""

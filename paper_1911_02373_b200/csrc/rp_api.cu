@@ -351,6 +351,7 @@ struct rp_plan_s {
   DevProg *d_progs = nullptr;
   int32_t *buf_i = nullptr;
   double *buf_d = nullptr;
+  unsigned char *buf_g = nullptr;  // the sweep's tile schedule (CfgTable grec, gmP, ghv, gdesc, gcnt)
   int32_t *d_F = nullptr;  // F kept on the device (rp_plan_update_program re-runs a1 / a5)
   std::vector<int> nc_of;  // per program: max n_c over its metrics (coefficient row stride check)
   CfgTable tab{};
@@ -378,6 +379,7 @@ static void plan_free(rp_plan pl) {
   if (pl->d_progs) cudaFreeAsync(pl->d_progs, pl->stream);
   if (pl->buf_i) cudaFreeAsync(pl->buf_i, pl->stream);
   if (pl->buf_d) cudaFreeAsync(pl->buf_d, pl->stream);
+  if (pl->buf_g) cudaFreeAsync(pl->buf_g, pl->stream);
   if (pl->d_F) cudaFreeAsync(pl->d_F, pl->stream);
   if (pl->hist.slots) {
     cudaStreamSynchronize(pl->stream);
@@ -461,6 +463,21 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   pl->tab.rterm = pl->tab.nFc + 2 * n_prog + 4;
   pl->tab.inv = pl->tab.rterm + nrt;
   pl->tab.nrt_max = 1;
+  {  // tile schedule: factored tiles are full, the dense part pads once (slots <= nFc + 7)
+    const int nGp = nFp + 8;
+    const size_t b_rec = (size_t)n_prog * nGp * sizeof(CfgRec), b_mp = (size_t)n_prog * npe_pad * nGp * 8,
+                 b_hv = (size_t)n_prog * nGp * 4, b_gd = (size_t)n_prog * kMaxGroups * sizeof(GroupDesc),
+                 b_cnt = (size_t)n_prog * 16;
+    const size_t nb = b_rec + b_mp + b_hv + b_gd + b_cnt;
+    if ((e = cudaMallocAsync((void **)&pl->buf_g, nb, s)) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMemsetAsync(pl->buf_g, 0, nb, s)) != cudaSuccess) return fail(e, "memset");
+    pl->tab.nGp = nGp;
+    pl->tab.grec = reinterpret_cast<CfgRec *>(pl->buf_g);
+    pl->tab.gmP = reinterpret_cast<double *>(pl->buf_g + b_rec);
+    pl->tab.gdesc = reinterpret_cast<GroupDesc *>(pl->buf_g + b_rec + b_mp);
+    pl->tab.ghv = reinterpret_cast<int32_t *>(pl->buf_g + b_rec + b_mp + b_gd);
+    pl->tab.gcnt = pl->tab.ghv + (size_t)n_prog * nGp;
+  }
   for (int g = 0; g < n_prog; ++g) {  // distinct (pe, de) pairs over the polynomials' terms
     std::vector<char> seen((size_t)npe_pad * nde_pad, 0);
     int cnt = 0;
@@ -1364,6 +1381,268 @@ rp_status rp_eval_argmin_batched(const rp_program *progs, int32_t n_prog, const 
 rp_status rp_eval_argmin(const rp_program *prog, const int32_t *D, int64_t nD, const int32_t *F,
                          int32_t nF, int32_t *best_idx, double *best_E, double *second_E, rp_stream s) {
   return rp_eval_argmin_batched(prog, 1, D, nD, F, nF, best_idx, best_E, second_E, s);
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// persistence: the rational program and the runtime history (byte layout only; no arithmetic)
+// =============================================================================================
+namespace {
+struct Writer {
+  std::vector<unsigned char> b;
+  template <class T>
+  void put(const T &v) {
+    const unsigned char *p = reinterpret_cast<const unsigned char *>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+  void put_bytes(const void *p, size_t n) {
+    const unsigned char *c = reinterpret_cast<const unsigned char *>(p);
+    b.insert(b.end(), c, c + n);
+  }
+};
+struct Reader {
+  const unsigned char *p;
+  size_t n, off = 0;
+  bool ok = true;
+  template <class T>
+  T get() {
+    T v{};
+    if (off + sizeof(T) > n) {
+      ok = false;
+      return v;
+    }
+    memcpy(&v, p + off, sizeof(T));
+    off += sizeof(T);
+    return v;
+  }
+  bool get_bytes(void *dst, size_t k) {
+    if (off + k > n) return ok = false;
+    memcpy(dst, p + off, k);
+    off += k;
+    return true;
+  }
+};
+uint64_t fnv64(const unsigned char *b, size_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+const char kProgMagic[8] = {'R', 'P', 'P', 'R', 'O', 'G', '0', '1'};
+const char kHistMagic[8] = {'R', 'P', 'H', 'I', 'S', 'T', '0', '1'};
+// hand the bytes out: buf null -> size only; too small -> INVALID_ARG (size still written)
+rp_status emit(const Writer &w, void *buf, int64_t cap, int64_t *size) {
+  *size = (int64_t)w.b.size();
+  if (!buf) return RP_OK;
+  RP_REQUIRE(cap >= (int64_t)w.b.size(), RP_ERR_INVALID_ARG, "buffer of %lld bytes < %lld", (long long)cap,
+             (long long)w.b.size());
+  memcpy(buf, w.b.data(), w.b.size());
+  return RP_OK;
+}
+}  // namespace
+
+struct rp_program_blob_s {
+  rp_program prog{};
+  std::vector<int16_t> exps[RP_MAX_METRICS][2];
+  std::vector<double> coef[RP_MAX_METRICS];
+};
+
+extern "C" {
+
+rp_status rp_program_save(const rp_program *prog, void *buf, int64_t cap, int64_t *size) {
+  RP_REQUIRE(prog && size, RP_ERR_INVALID_ARG, "null argument");
+  DevProg scratch;  // validates the program exactly as rp_plan_create would
+  rp_status st = compile_program(prog, &scratch);
+  if (st != RP_OK) return st;
+  Writer w;
+  w.put_bytes(kProgMagic, 8);
+  w.put(prog->d);
+  w.put(prog->p);
+  w.put(prog->n_metrics);
+  w.put(prog->e_template);
+  w.put(prog->regs_per_thread);
+  for (int k = 0; k < 3; ++k) w.put(prog->grid_map[k]);
+  w.put(prog->smem_words_base);
+  w.put(prog->smem_words_per_thread);
+  w.put(prog->hw);
+  w.put(prog->xform);
+  for (int i = 0; i < prog->n_metrics; ++i) {
+    const rp_basis &b = prog->basis[i];
+    w.put(b.n_vars);
+    w.put(b.n_num);
+    w.put(b.n_den);
+    w.put_bytes(b.num_exp, sizeof(int16_t) * b.n_num * b.n_vars);
+    w.put_bytes(b.den_exp, sizeof(int16_t) * b.n_den * b.n_vars);
+    w.put_bytes(prog->coef[i], sizeof(double) * (b.n_num + b.n_den));  // IEEE bits: exact
+  }
+  w.put(fnv64(w.b.data(), w.b.size()));
+  return emit(w, buf, cap, size);
+}
+
+rp_status rp_program_load(const void *buf, int64_t size, rp_program_blob *out) {
+  RP_REQUIRE(buf && out && size >= 16, RP_ERR_INVALID_ARG, "null argument or short buffer");
+  *out = nullptr;
+  const unsigned char *b = reinterpret_cast<const unsigned char *>(buf);
+  uint64_t want;
+  memcpy(&want, b + size - 8, 8);
+  RP_REQUIRE(memcmp(b, kProgMagic, 8) == 0, RP_ERR_INVALID_ARG, "not a saved rp_program (magic)");
+  RP_REQUIRE(fnv64(b, (size_t)size - 8) == want, RP_ERR_INVALID_ARG, "saved rp_program: checksum mismatch");
+  Reader r{b + 8, (size_t)size - 16};
+  rp_program_blob o = new rp_program_blob_s;
+  rp_program &p = o->prog;
+  p.d = r.get<int32_t>();
+  p.p = r.get<int32_t>();
+  p.n_metrics = r.get<int32_t>();
+  p.e_template = r.get<int32_t>();
+  p.regs_per_thread = r.get<int32_t>();
+  for (int k = 0; k < 3; ++k) p.grid_map[k] = r.get<int32_t>();
+  p.smem_words_base = r.get<int64_t>();
+  p.smem_words_per_thread = r.get<int64_t>();
+  p.hw = r.get<rp_hw>();
+  p.xform = r.get<rp_xform>();
+  bool ok = r.ok && p.n_metrics >= 1 && p.n_metrics <= RP_MAX_METRICS;
+  for (int i = 0; ok && i < p.n_metrics; ++i) {
+    rp_basis &bs = p.basis[i];
+    bs.n_vars = r.get<int32_t>();
+    bs.n_num = r.get<int32_t>();
+    bs.n_den = r.get<int32_t>();
+    ok = r.ok && bs.n_vars >= 1 && bs.n_vars <= RP_MAX_VARS && bs.n_num >= 0 && bs.n_den >= 1 &&
+         bs.n_num + bs.n_den < kMaxSrc;
+    if (!ok) break;
+    o->exps[i][0].resize((size_t)bs.n_num * bs.n_vars);
+    o->exps[i][1].resize((size_t)bs.n_den * bs.n_vars);
+    o->coef[i].resize((size_t)bs.n_num + bs.n_den);
+    ok = r.get_bytes(o->exps[i][0].data(), o->exps[i][0].size() * 2) &&
+         r.get_bytes(o->exps[i][1].data(), o->exps[i][1].size() * 2) &&
+         r.get_bytes(o->coef[i].data(), o->coef[i].size() * 8);
+    bs.num_exp = o->exps[i][0].data();
+    bs.den_exp = o->exps[i][1].data();
+    p.coef[i] = o->coef[i].data();
+  }
+  ok = ok && r.off == r.n;
+  if (!ok) {
+    delete o;
+    RP_REQUIRE(false, RP_ERR_INVALID_ARG, "saved rp_program: truncated or malformed");
+  }
+  DevProg scratch;
+  const rp_status st = compile_program(&p, &scratch);
+  if (st != RP_OK) {
+    delete o;
+    return st;
+  }
+  *out = o;
+  return RP_OK;
+}
+
+const rp_program *rp_program_blob_program(rp_program_blob blob) { return blob ? &blob->prog : nullptr; }
+
+rp_status rp_program_blob_free(rp_program_blob blob) {
+  delete blob;
+  return RP_OK;
+}
+
+// fingerprint of program `prog` of a plan as the device holds it now, and of the plan's F
+static rp_status plan_fingerprint(rp_plan plan, int32_t prog, uint64_t *fp) {
+  Tmp t;
+  RP_CUDA(t.alloc(sizeof(unsigned long long), plan->stream));
+  RP_CUDA(launch_fingerprint(plan->d_progs + prog, plan->d_F, (size_t)plan->nF * plan->p * sizeof(int32_t),
+                             (unsigned long long *)t.p, plan->stream));
+  RP_CUDA(cudaMemcpy(fp, t.p, 8, cudaMemcpyDeviceToHost));
+  return RP_OK;
+}
+
+rp_status rp_plan_history_save(rp_plan plan, void *buf, int64_t cap, int64_t *size) {
+  RP_REQUIRE(plan && size, RP_ERR_INVALID_ARG, "null argument");
+  RP_REQUIRE(plan->hist.enabled, RP_ERR_INVALID_ARG, "the plan's runtime history is not enabled");
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  const int d = plan->d;
+  const int64_t cap_slots = (int64_t)plan->hist.mask + 1;
+  uint64_t fp = 0;
+  rp_status st = plan_fingerprint(plan, plan->hist.prog, &fp);
+  if (st != RP_OK) return st;
+  Tmp t;
+  const size_t kb = (size_t)cap_slots * d * 4, vb = (size_t)cap_slots * sizeof(rp_decision), sb = (size_t)cap_slots * 4;
+  RP_CUDA(t.alloc(kb + vb + sb + 16, plan->stream));
+  unsigned char *base = (unsigned char *)t.p;
+  rp_decision *dv = (rp_decision *)base;  // 48-byte records first (alignment)
+  int32_t *dk = (int32_t *)(base + vb);
+  int32_t *ds = (int32_t *)(base + vb + kb);
+  unsigned *dc = (unsigned *)(base + vb + kb + sb);
+  RP_CUDA(launch_hist_export(plan->hist, d, dk, dv, ds, dc, plan->stream));
+  unsigned n = 0;
+  RP_CUDA(cudaMemcpyAsync(&n, dc, 4, cudaMemcpyDeviceToHost, plan->stream));
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  std::vector<int32_t> hk((size_t)n * d), hs(n);
+  std::vector<rp_decision> hv(n);
+  if (n) {
+    RP_CUDA(cudaMemcpy(hk.data(), dk, (size_t)n * d * 4, cudaMemcpyDeviceToHost));
+    RP_CUDA(cudaMemcpy(hv.data(), dv, (size_t)n * sizeof(rp_decision), cudaMemcpyDeviceToHost));
+    RP_CUDA(cudaMemcpy(hs.data(), ds, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  }
+  std::vector<unsigned> order(n);
+  for (unsigned i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](unsigned a, unsigned b) { return hs[a] < hs[b]; });  // slot order
+  Writer w;
+  w.put_bytes(kHistMagic, 8);
+  w.put((int32_t)d);
+  w.put((int32_t)plan->hist.prog);
+  w.put(plan->hist.margin);
+  w.put(fp);
+  w.put((int64_t)n);
+  for (unsigned i : order) {
+    w.put_bytes(hk.data() + (size_t)i * d, (size_t)d * 4);
+    hv[i].from_history = 0;
+    w.put(hv[i]);
+  }
+  w.put(fnv64(w.b.data(), w.b.size()));
+  return emit(w, buf, cap, size);
+}
+
+rp_status rp_plan_history_load(rp_plan plan, const void *buf, int64_t size) {
+  RP_REQUIRE(plan && buf && size >= 16, RP_ERR_INVALID_ARG, "null argument or short buffer");
+  RP_REQUIRE(plan->hist.enabled, RP_ERR_INVALID_ARG, "enable the plan's runtime history before loading one");
+  const unsigned char *b = reinterpret_cast<const unsigned char *>(buf);
+  uint64_t want;
+  memcpy(&want, b + size - 8, 8);
+  RP_REQUIRE(memcmp(b, kHistMagic, 8) == 0, RP_ERR_INVALID_ARG, "not a saved runtime history (magic)");
+  RP_REQUIRE(fnv64(b, (size_t)size - 8) == want, RP_ERR_INVALID_ARG, "saved runtime history: checksum mismatch");
+  Reader r{b + 8, (size_t)size - 16};
+  const int32_t d = r.get<int32_t>(), prog = r.get<int32_t>();
+  const double margin = r.get<double>();
+  const uint64_t fp = r.get<uint64_t>();
+  const int64_t n = r.get<int64_t>();
+  RP_REQUIRE(r.ok && d == plan->d && n >= 0 && r.n - r.off == (size_t)n * ((size_t)d * 4 + sizeof(rp_decision)),
+             RP_ERR_INVALID_ARG, "saved runtime history: malformed or of another data arity");
+  RP_REQUIRE(prog == plan->hist.prog && margin == plan->hist.margin, RP_ERR_INVALID_ARG,
+             "saved runtime history of program %d, margin %g; the plan's is program %d, margin %g", prog, margin,
+             plan->hist.prog, plan->hist.margin);
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  uint64_t mine = 0;
+  rp_status st = plan_fingerprint(plan, prog, &mine);
+  if (st != RP_OK) return st;
+  RP_REQUIRE(mine == fp, RP_ERR_INVALID_ARG,
+             "saved runtime history belongs to another program or configuration set (fingerprint)");
+  if (n == 0) return RP_OK;
+  std::vector<int32_t> hk((size_t)n * d);
+  std::vector<rp_decision> hv(n);
+  for (int64_t i = 0; i < n; ++i) {
+    r.get_bytes(hk.data() + (size_t)i * d, (size_t)d * 4);
+    hv[i] = r.get<rp_decision>();
+  }
+  Tmp t;
+  const size_t vb = (size_t)n * sizeof(rp_decision), kb = (size_t)n * d * 4;
+  RP_CUDA(t.alloc(vb + kb, plan->stream));
+  RP_CUDA(cudaStreamSynchronize(plan->stream));  // the synchronous copies below use the allocation
+  rp_decision *dv = (rp_decision *)t.p;
+  int32_t *dk = (int32_t *)((unsigned char *)t.p + vb);
+  RP_CUDA(cudaMemcpy(dv, hv.data(), vb, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(dk, hk.data(), kb, cudaMemcpyHostToDevice));
+  RP_CUDA(launch_hist_import(plan->hist, d, dk, dv, n, plan->stream));
+  RP_CUDA(cudaStreamSynchronize(plan->stream));
+  return RP_OK;
 }
 
 }  // extern "C"

@@ -285,6 +285,74 @@ static cudaError_t launch_decide_npe(const DecideArgs &a, bool mwp, int nFp, cud
   return cudaGetLastError();
 }
 
+// ---- persistence of the runtime history (rp_plan_history_save / _load) ------------------------
+// Export: the ready slots, compacted with their slot index (the host sorts by it: deterministic).
+__global__ void k_hist_export(HistTable H, int d, int32_t *keys, rp_decision *vals, int32_t *slot_of,
+                              unsigned *count) {
+  const int64_t n = (int64_t)H.mask + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const HistSlot &sl = H.slots[i];
+    if (sl.state != 2) continue;
+    const unsigned j = atomicAdd(count, 1u);
+    for (int k = 0; k < d; ++k) keys[(int64_t)j * d + k] = sl.key[k];
+    vals[j] = sl.val;
+    slot_of[j] = (int32_t)i;
+  }
+}
+
+// Import: every entry goes through the decision kernel's own insertion (same hash, same probes),
+// so rp_plan_decide finds it exactly where it would have put it
+__global__ void k_hist_import(HistTable H, int d, const int32_t *keys, const rp_decision *vals, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    rp_decision v = vals[i];
+    v.from_history = 0;
+    hist_insert(H, keys + i * d, d, v);
+  }
+}
+
+// FNV-1a 64 over device bytes, chained through *h (compile_program zeroes the device program
+// first, and the refit kernel rewrites coefficients and transform in place): a saved history is
+// bound to the program and the configuration set that made its decisions
+__global__ void k_fnv64(const unsigned char *b, size_t n, unsigned long long *h) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long x = *h;
+  for (size_t i = 0; i < n; ++i) {
+    x ^= b[i];
+    x *= 1099511628211ull;
+  }
+  *h = x;
+}
+
+cudaError_t launch_hist_export(const HistTable &H, int d, int32_t *keys, rp_decision *vals, int32_t *slot_of,
+                               unsigned *count, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  const int64_t n = (int64_t)H.mask + 1;
+  const int grid = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  k_hist_export<<<grid, 256, 0, s>>>(H, d, keys, vals, slot_of, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_import(const HistTable &H, int d, const int32_t *keys, const rp_decision *vals, int64_t n,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = (int)((n + 127) / 128 < 1024 ? (n + 127) / 128 : 1024);
+  k_hist_import<<<grid, 128, 0, s>>>(H, d, keys, vals, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fingerprint(const DevProg *pg, const int32_t *F, size_t f_bytes, unsigned long long *out,
+                               cudaStream_t s) {
+  const unsigned long long basis = 1469598103934665603ull;
+  cudaError_t e = cudaMemcpyAsync(out, &basis, sizeof basis, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  k_fnv64<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned char *>(pg), sizeof(DevProg), out);
+  k_fnv64<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned char *>(F), f_bytes, out);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);  // (the pageable source of the async copy must outlive it)
+}
+
 cudaError_t launch_decide(const DecideArgs &a, bool mwp, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
   if (a.n > 0x7fffffffll) return cudaErrorInvalidValue;

@@ -38,5 +38,11 @@ struct DecideArgs {
 };
 
 cudaError_t launch_decide(const DecideArgs &a, bool mwp, cudaStream_t s);
+cudaError_t launch_hist_export(const HistTable &H, int d, int32_t *keys, rp_decision *vals, int32_t *slot_of,
+                               unsigned *count, cudaStream_t s);
+cudaError_t launch_hist_import(const HistTable &H, int d, const int32_t *keys, const rp_decision *vals, int64_t n,
+                               cudaStream_t s);
+cudaError_t launch_fingerprint(const DevProg *pg, const int32_t *F, size_t f_bytes, unsigned long long *out,
+                               cudaStream_t s);
 
 }  // namespace rp

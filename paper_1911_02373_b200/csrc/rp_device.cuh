@@ -47,6 +47,13 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
               : "d"(a), "d"(b));
 }
 
+// D = A B + C with C given separately (the factored tiles start from w_{k,0})
+__device__ __forceinline__ void dmma_c(double &d0, double &d1, double a, double b, double c0, double c1) {
+  RP_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+              : "=d"(d0), "=d"(d1)
+              : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
 // 1/x: MUFU.RCP64H seed r0 (relative error e0 < 2^-20) and one cubically convergent step
 // r = r0 (1 + e + e^2), e = 1 - x r0 (exact 1/x = r0 / (1 - e)): relative error e^3 + rounding,
 // ~1 ulp, in 3 DFMA instead of the 4 of two Newton steps.  0 and +-inf give NaN (e = NaN),

@@ -70,6 +70,26 @@ struct CfgRec {      // one statically feasible configuration, 64 B (4 x 16-byte
 };
 static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
 
+// Factored contraction of the sweep (k_plan_groups).  A group is a
+// set of feasible configurations that share every P_k except P_hv (the Horner variable).  With
+// x = u_hv(P_hv) and i_pe the exponent of u_hv in m_pe, every polynomial factors as
+//   p_k(D, P) = sum_i x^i w_{k,i}(D),   w_{k,i}(D) = sum_{pe: i_pe = i} C_{k,pe}(D) Y_pe,
+// Y_pe = prod_{j != hv} u_j(P_j)^{e_pe,j} (one value per group), so a tile of 8 configurations of
+// one group is two DMMA.8x8x4 per polynomial instead of ceil(nPE / 4): A = the shares of w_{k,0},
+// B = 1 (w_{k,0} in every column), then A = w_{k,1..4} of 8 tuples (lane q of a quad holds
+// w_{k,1+q}), B = x^{1..4} of the 8 configurations.
+// Lane q of a quad evaluates w_{k,1+q} from kGS1 terms and its share of w_{k,0} (terms q, q + 4 of
+// the i = 0 list) from kGW0 terms; a DMMA with B = 1 sums the four shares.
+constexpr int kGS1 = 4, kGW0 = 2, kGS = kGS1 + kGW0;
+constexpr int kMaxGroups = 128;      // groups per program
+constexpr int kGroupMaxPlan = 4096;  // plans with more feasible configurations stay dense
+struct GroupDesc {
+  int32_t tile_begin, tile_end, hv, nmem;  // tiles [tile_begin, tile_end) of the schedule
+  int32_t P[3], pad;                       // the members' P (P[hv] unused)
+  int32_t off[4][kGS];                     // lane q, term s: pe (s < kGS1: of w_{1+q}; else of w_0's share)
+  double y[4][kGS];                        // Y_pe of that term (0 for padding)
+};
+
 struct CfgTable {
   int32_t nFp;     // padded stride (multiple of 8)
   CfgRec *rec;     // [n_prog][nFp]  sorted by (P1 P2, original index)
@@ -87,6 +107,14 @@ struct CfgTable {
   double *rinfo;   // [n_prog][8]: A_k = sum_j |rcoef[j][k]| (k < 6), max total degree, nRT
   int32_t *inv;    // [n_prog][nFp]: original index -> position in srec (-1: statically infeasible)
   int32_t nrt_max; // host bound on the union term count of any program (shared-memory sizing)
+  // the sweep's tile schedule (k_plan_groups): factored tiles of the groups, then dense tiles of
+  // the remaining configurations in (P1 P2, index) order; every tile is 8 slots
+  int32_t nGp;        // slots per program (multiple of 8, >= nFp + 8)
+  CfgRec *grec;       // [n_prog][nGp]: records of the slots (zero record, orig INT_MAX: padding)
+  double *gmP;        // [n_prog][npe_pad][nGp]: B operands (factored: x^{1+q} in rows q < 4)
+  int32_t *ghv;       // [n_prog][nGp]: slot's Horner variable, -1 dense, -2 padding
+  GroupDesc *gdesc;   // [n_prog][kMaxGroups]
+  int32_t *gcnt;      // [n_prog][4]: groups, factored tiles, tiles, -
 };
 constexpr int kRSMTab = 1024;  // n_sm <= 1023 uses the table
 

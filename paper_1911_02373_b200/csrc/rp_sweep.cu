@@ -39,6 +39,7 @@ __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_
 }
 
 __device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab, int npe_pad);
+__device__ void refresh_schedule(const DevProg &pg, int g, int npe_pad, const CfgTable &tab);
 
 // ---- a1 + a5 + P-monomials, compaction in index order --------------------------------------
 __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, const int32_t *F,
@@ -219,8 +220,264 @@ __global__ void __launch_bounds__(1024) k_plan_refresh(DevProg *pgp, int g, cons
     for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
       Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
   }
+  refresh_schedule(pg, g, npe_pad, tab);
   __syncthreads();
   build_refine_terms(g, pg, tab, npe_pad);
+}
+
+// ---- the sweep's tile schedule: factored tiles of configuration groups, then dense tiles ----------
+// u_k of program variable k (the transform of k_plan_configs)
+__device__ __forceinline__ double prog_u(const DevProg &pg, int k, int32_t P) {
+  return ((double)P - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
+}
+
+// B operands of one schedule slot: a factored slot holds x^{1+q} (x = u_hv(P_hv)) in rows q < 4,
+// a dense slot the program-part monomials m_pe(u_P) (as k_plan_configs computes them)
+__device__ void schedule_slot_mp(const DevProg &pg, const CfgRec &r, int hv, int npe_pad, double *col, int nGp) {
+  const int32_t Pk[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+  if (hv == -2) {  // padding
+    for (int pe = 0; pe < npe_pad; ++pe) col[(int64_t)pe * nGp] = 0.0;
+    return;
+  }
+  if (hv >= 0) {
+    const double x = prog_u(pg, hv, Pk[hv]);
+    double m = 1.0;
+    for (int q = 0; q < npe_pad; ++q) {
+      m = q < 4 ? m * x : 0.0;
+      col[(int64_t)q * nGp] = m;
+    }
+    return;
+  }
+  double u[3];
+  for (int k = 0; k < pg.p; ++k) u[k] = prog_u(pg, k, Pk[k]);
+  for (int pe = 0; pe < npe_pad; ++pe) {
+    double m = 0.0;
+    if (pe < pg.nPE) {
+      m = 1.0;
+      for (int k = 0; k < pg.p; ++k)
+        for (int t = 0; t < pg.pe_exp[pe][k]; ++t) m *= u[k];
+    }
+    col[(int64_t)pe * nGp] = m;
+  }
+}
+
+// the term lists of Horner variable hv: lane q sums w_{1+q} over off[q][0..kGS1) and its share of
+// w_0 over off[q][kGS1..kGS) (entries q, q + 4 of the i = 0 list); false when the program's
+// monomials do not fit them (then no groups on hv)
+__device__ bool group_lists(const DevProg &pg, int hv, int32_t (*off)[kGS]) {
+  int cnt[5] = {0, 0, 0, 0, 0};
+  for (int q = 0; q < 4; ++q)
+    for (int s = 0; s < kGS; ++s) off[q][s] = -1;  // padding terms (Y = 0)
+  for (int pe = 0; pe < pg.nPE; ++pe) {
+    const int i = pg.pe_exp[pe][hv];
+    if (i > 4) return false;
+    if (i == 0) {
+      if (cnt[0] >= 4 * kGW0) return false;
+      off[cnt[0] % 4][kGS1 + cnt[0] / 4] = pe;
+    } else {
+      if (cnt[i] >= kGS1) return false;
+      off[i - 1][cnt[i]] = pe;
+    }
+    ++cnt[i];
+  }
+  return true;
+}
+
+// Y_pe of a group's terms (they depend on the transform: recomputed by k_plan_refresh)
+__device__ void group_y(const DevProg &pg, GroupDesc &gd) {
+  double u[3] = {1.0, 1.0, 1.0};
+  for (int k = 0; k < pg.p; ++k) u[k] = prog_u(pg, k, gd.P[k]);
+  for (int q = 0; q < 4; ++q)
+    for (int s = 0; s < kGS; ++s) {
+      const int pe = gd.off[q][s];
+      double y = 0.0;
+      if (pe >= 0) {
+        y = 1.0;
+        for (int k = 0; k < pg.p; ++k)
+          if (k != gd.hv)
+            for (int t = 0; t < pg.pe_exp[pe][k]; ++t) y *= u[k];
+      }
+      gd.y[q][s] = y;
+    }
+  for (int q = 0; q < 4; ++q)  // padding terms read a valid column with Y = 0
+    for (int s = 0; s < kGS; ++s) gd.off[q][s] = gd.off[q][s] < 0 ? 0 : gd.off[q][s];
+}
+
+// One CTA per program, after k_plan_configs.  Candidate groups: for every Horner variable whose
+// term lists fit, the sets of feasible configurations with equal P_k (k != hv) and >= 8 members.
+// Greedy, largest first (ties: lower hv, then lower position): a group takes the floor(n / 8) * 8
+// lowest-P1P2 members nobody took yet (full tiles only).  The rest is dense, in (P1 P2, index) order.
+// Which tile evaluates a pair changes only the rounding of p_k (the exact key (E, index) decides).
+__global__ void __launch_bounds__(1024) k_plan_groups(const DevProg *progs, int npe_pad, CfgTable tab, int enable) {
+  const int g = blockIdx.x;
+  const DevProg &pg = progs[g];
+  const int nFp = tab.nFp, nGp = tab.nGp;
+  const int nFc = tab.nFc[2 * g];
+  const bool sorted = tab.nFc[2 * g + 1] != 0;
+  const CfgRec *rec = tab.rec + (int64_t)g * nFp;
+  const double *mP = tab.mP + (int64_t)g * npe_pad * nFp;
+  CfgRec *grec = tab.grec + (int64_t)g * nGp;
+  double *gmP = tab.gmP + (int64_t)g * npe_pad * nGp;
+  int32_t *ghv = tab.ghv + (int64_t)g * nGp;
+  GroupDesc *gdesc = tab.gdesc + (int64_t)g * kMaxGroups;
+
+  __shared__ int32_t s_slot[kGroupMaxPlan + 8];   // schedule slot -> position in rec (-1: padding)
+  __shared__ int8_t s_hv[kGroupMaxPlan + 8];      // slot's Horner variable (-1 dense)
+  __shared__ uint8_t s_taken[kGroupMaxPlan];
+  // candidates: a key has >= 8 members, so at most 3 nFc / 8 of them
+  constexpr int kMaxCand = 3 * kGroupMaxPlan / 8;
+  __shared__ int32_t s_cand[kMaxCand];   // hv << 16 | first member position
+  __shared__ int32_t s_csize[kMaxCand];
+  __shared__ int32_t s_corder[kMaxCand];
+  __shared__ int32_t s_off[3][4][kGS];
+  __shared__ int s_hvok[3], s_ncand, s_ngroups, s_ntiles, s_ngt;
+  const bool grouping = enable && sorted && pg.p >= 2 && nFc <= kGroupMaxPlan;
+  if (threadIdx.x == 0) {
+    for (int hv = 0; hv < 3; ++hv) s_hvok[hv] = grouping && hv < pg.p && group_lists(pg, hv, s_off[hv]);
+    s_ncand = 0;
+  }
+  for (int i = threadIdx.x; i < kGroupMaxPlan; i += blockDim.x) s_taken[i] = 0;
+  __syncthreads();
+  auto same_key = [&](const CfgRec &a, const CfgRec &b, int hv) {
+    return (hv == 0 || a.Pm1_0 == b.Pm1_0) && (hv == 1 || a.Pm1_1 == b.Pm1_1) && (hv == 2 || a.Pm1_2 == b.Pm1_2);
+  };
+  if (grouping) {
+    for (int hv = 0; hv < 3; ++hv) {
+      if (!s_hvok[hv]) continue;
+      for (int c = threadIdx.x; c < nFc; c += blockDim.x) {
+        const CfgRec rc = rec[c];
+        int n = 0;
+        bool first = true;
+        for (int j = 0; j < nFc; ++j) {
+          const bool m = same_key(rec[j], rc, hv);
+          n += m;
+          first = first && !(m && j < c);
+        }
+        if (first && n >= 8) {
+          const int k = atomicAdd(&s_ncand, 1);
+          s_cand[k] = hv << 16 | c;
+          s_csize[k] = n;
+        }
+      }
+      __syncthreads();
+    }
+    // order: size descending, then (hv, position) ascending -- a rank sort, deterministic
+    const int nc = s_ncand;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      int rank = 0;
+      for (int j = 0; j < nc; ++j)
+        rank += s_csize[j] > s_csize[i] || (s_csize[j] == s_csize[i] && s_cand[j] < s_cand[i]);
+      s_corder[rank] = i;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // greedy assignment and the slot list (serial: n <= kGroupMaxPlan)
+    int ns = 0, ngroups = 0;
+    const int nc = grouping ? s_ncand : 0;
+    for (int r = 0; r < nc && ngroups < kMaxGroups; ++r) {
+      const int cd = s_cand[s_corder[r]], hv = cd >> 16, c0 = cd & 0xffff;
+      const CfgRec rc = rec[c0];
+      int n = 0;
+      for (int j = c0; j < nFc; ++j) n += !s_taken[j] && same_key(rec[j], rc, hv);
+      const int take = n / 8 * 8;
+      if (take == 0) continue;
+      GroupDesc &gd = gdesc[ngroups];
+      gd.tile_begin = ns / 8;
+      gd.hv = hv;
+      gd.nmem = take;
+      gd.P[0] = rc.Pm1_0 + 1;
+      gd.P[1] = rc.Pm1_1 + 1;
+      gd.P[2] = rc.Pm1_2 + 1;
+      gd.pad = 0;
+      for (int q = 0; q < 4; ++q)
+        for (int s = 0; s < kGS; ++s) gd.off[q][s] = s_off[hv][q][s];
+      int got = 0;
+      for (int j = c0; j < nFc && got < take; ++j)
+        if (!s_taken[j] && same_key(rec[j], rc, hv)) {
+          s_taken[j] = 1;
+          s_slot[ns] = j;
+          s_hv[ns] = (int8_t)hv;
+          ++ns;
+          ++got;
+        }
+      gd.tile_end = ns / 8;
+      group_y(pg, gd);
+      ++ngroups;
+    }
+    s_ngt = ns / 8;
+    if (!grouping) {  // dense only: the slots are the sorted table (the sweep reads grec/gmP)
+      for (int j = 0; j < nFc && nFc <= kGroupMaxPlan; ++j) {
+        s_slot[j] = j;
+        s_hv[j] = -1;
+      }
+      ns = nFc;
+    } else {
+      for (int j = 0; j < nFc; ++j)
+        if (!s_taken[j]) {
+          s_slot[ns] = j;
+          s_hv[ns] = -1;
+          ++ns;
+        }
+    }
+    while (ns % 8 && nFc <= kGroupMaxPlan) {
+      s_slot[ns] = -1;
+      s_hv[ns] = -2;
+      ++ns;
+    }
+    s_ngroups = ngroups;
+    s_ntiles = ns / 8;
+  }
+  __syncthreads();
+  const int nslots = s_ntiles * 8;
+  // nFc > kGroupMaxPlan: the slots are the table itself, 1:1 (no shared list)
+  const bool big = nFc > kGroupMaxPlan;
+  const int nsl = big ? ((nFc + 7) & ~7) : nslots;
+  for (int s = threadIdx.x; s < nGp; s += blockDim.x) {
+    int pos = -1, hv = -2;
+    if (s < nsl) {
+      pos = big ? (s < nFc ? s : -1) : s_slot[s];
+      hv = big ? (s < nFc ? -1 : -2) : s_hv[s];
+    }
+    CfgRec r;
+    if (pos >= 0) {
+      r = rec[pos];
+    } else {
+      memset(&r, 0, sizeof(r));
+      r.orig = 0x7fffffff;  // zero record: W = 0, 1/B_act = 0, so its E is never a candidate
+    }
+    grec[s] = r;
+    ghv[s] = hv;
+    if (hv == -1 && pos >= 0) {  // dense: the table's monomials, bit for bit
+      for (int pe = 0; pe < npe_pad; ++pe) gmP[(int64_t)pe * nGp + s] = mP[(int64_t)pe * nFp + pos];
+    } else {
+      schedule_slot_mp(pg, r, hv, npe_pad, gmP + s, nGp);
+    }
+  }
+  if (threadIdx.x == 0) {
+    tab.gcnt[4 * g + 0] = big ? 0 : s_ngroups;
+    tab.gcnt[4 * g + 1] = big ? 0 : s_ngt;
+    tab.gcnt[4 * g + 2] = big ? nsl / 8 : s_ntiles;
+    tab.gcnt[4 * g + 3] = 0;
+  }
+}
+
+// refit: the factored slots' powers and the groups' Y values follow the new transform
+__device__ void refresh_schedule(const DevProg &pg, int g, int npe_pad, const CfgTable &tab) {
+  const int nGp = tab.nGp, ntile = tab.gcnt[4 * g + 2], ngr = tab.gcnt[4 * g + 0];
+  const CfgRec *grec = tab.grec + (int64_t)g * nGp;
+  double *gmP = tab.gmP + (int64_t)g * npe_pad * nGp;
+  const int32_t *ghv = tab.ghv + (int64_t)g * nGp;
+  for (int s = threadIdx.x; s < ntile * 8; s += blockDim.x) schedule_slot_mp(pg, grec[s], ghv[s], npe_pad, gmP + s, nGp);
+  GroupDesc *gdesc = tab.gdesc + (int64_t)g * kMaxGroups;
+  for (int i = threadIdx.x; i < ngr; i += blockDim.x) {
+    GroupDesc &gd = gdesc[i];
+    // off[][] holds 0 for padding terms now: rebuild the lists (Y = 0 marks them)
+    int32_t off[4][kGS];
+    group_lists(pg, gd.hv, off);
+    for (int q = 0; q < 4; ++q)
+      for (int s = 0; s < kGS; ++s) gd.off[q][s] = off[q][s];
+    group_y(pg, gd);
+  }
 }
 
 cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, int stride, const double *d_xf,
@@ -232,6 +489,10 @@ cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, in
 cudaError_t launch_plan_configs(const DevProg *d_progs, int n_prog, const int32_t *d_F, int nF,
                                 int npe_pad, CfgTable tab, cudaStream_t s) {
   k_plan_configs<<<n_prog, 1024, 0, s>>>(d_progs, d_F, nF, npe_pad, tab);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const char *ge = getenv("RP_SWEEP_GROUPS");  // 0: dense tiles only (A/B measurements)
+  k_plan_groups<<<n_prog, 1024, 0, s>>>(d_progs, npe_pad, tab, !(ge && ge[0] == '0'));
   return cudaGetLastError();
 }
 
@@ -320,6 +581,18 @@ struct SweepArgs {
 #ifndef RP_SWEEP_MINB
 #define RP_SWEEP_MINB 4
 #endif
+#ifndef RP_GPAIR
+#define RP_GPAIR 0
+#endif
+#ifndef RP_GRID_LEAN
+#define RP_GRID_LEAN 0
+#endif
+#ifndef RP_KEY_F64
+#define RP_KEY_F64 0
+#endif
+#ifndef RP_PREF
+#define RP_PREF 0
+#endif
 constexpr int kSweepWarps = 4;
 constexpr int kSweepThreads = 32 * kSweepWarps;
 constexpr int kTD = 8 * kSweepWarps;  // tuples per CTA: one octet (the DMMA M side) per warp
@@ -374,9 +647,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     sDv[t * kMaxVars + k] = (t < tmax) ? a.D[src * d + k] : 1;
   }
   const double *gRSM = a.tab.rSM + (int64_t)g * kRSMTab;
-  const bool rsm_tab = n_sm < kRSMTab;
-  if (rsm_tab)
-    for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) sRSM[i] = gRSM[i];
+  for (int i = threadIdx.x; i <= n_sm; i += blockDim.x) sRSM[i] = gRSM[i];
   __syncthreads();
   // data monomials m_de(u_D), u = (D - c) 2^-e, zero for the padding de >= nDE
   for (int i = threadIdx.x; i < kTD * ndp; i += blockDim.x) {
@@ -422,11 +693,13 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   const double rNSM = 1.0 / (double)n_sm;
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nFc = a.tab.nFc[2 * g];
   const bool sorted = a.tab.nFc[2 * g + 1] != 0;
-  const int nFp = a.tab.nFp;
-  const CfgRec *rec = a.tab.rec + (int64_t)g * nFp;
-  const double *mP = a.tab.mP + (int64_t)g * a.npe_pad * nFp;
+  // the tile schedule (k_plan_groups): factored tiles [0, ngt) in groups, dense tiles [ngt, ntile)
+  const int nGp = a.tab.nGp;
+  const int ngr = a.tab.gcnt[4 * g], ngt = a.tab.gcnt[4 * g + 1], ntile = a.tab.gcnt[4 * g + 2];
+  const CfgRec *grec = a.tab.grec + (int64_t)g * nGp;
+  const double *gmP = a.tab.gmP + (int64_t)g * a.npe_pad * nGp;
+  const GroupDesc *gdesc = a.tab.gdesc + (int64_t)g * kMaxGroups;
 
   // this warp's octet of tuples: row lane/4 of the DMMA tiles
   const int t = wid * 8 + (lane >> 2);
@@ -457,16 +730,15 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     const int64_t x = __shfl_xor_sync(0xffffffffu, maxD1sq, o);
     maxD1sq = x > maxD1sq ? x : maxD1sq;
   }
-  const int nOctF = (nFc + 7) >> 3;
-  // a4 for one octet of configurations: p_k(D_t, P_c) for the octet of tuples x the octet of
+  // a4 for one dense tile of configurations: p_k(D_t, P_c) for the octet of tuples x the octet of
   // configurations (k-step major: the NPOLY accumulation chains are independent, so consecutive
   // DMMAs do not wait).  B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
 #define RP_AFR(k, ks) arow[(k) * NPE + (ks) * 4]
   auto load_b = [&](int oc, double (&bfr)[KS]) {
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(mP + (int64_t)(ks * 4 + (lane & 3)) * nFp + oc * 8 + (lane >> 2));
+    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(gmP + (int64_t)(ks * 4 + (lane & 3)) * nGp + oc * 8 + (lane >> 2));
   };
-  auto mma_oct = [&](int oc, double (&acc)[NPOLY][2], const double (&bfr)[KS]) {
+  auto mma_oct = [&](double (&acc)[NPOLY][2], const double (&bfr)[KS]) {
 #pragma unroll
     for (int k = 0; k < NPOLY; ++k) acc[k][0] = acc[k][1] = 0.0;
 #pragma unroll
@@ -476,13 +748,13 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     }
   };
 #undef RP_AFR
-  // a3, a6, a7, a8 for the 2 pairs of this lane in one octet
-  auto epi_oct = [&](int oc, const double (&acc)[NPOLY][2]) {
+  // a3, a6, a7, a8 for the 2 pairs of this lane in one tile
+  auto epi_oct = [&](const CfgRec *trec, const double (&acc)[NPOLY][2]) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-      // output column 2 (lane % 4) + v; padded configurations (c >= nFc) have zero records
-      // and zero monomials, so their E is NaN and they are masked below
-      const CfgRec *cr = rec + oc * 8 + 2 * (lane & 3) + v;
+      // output column 2 (lane % 4) + v; padding slots have zero records (W = 0, 1/B_act = 0),
+      // so their E is 0 or NaN and they are masked below
+      const CfgRec *cr = trec + 2 * (lane & 3) + v;
       const longlong2 h0 = __ldg(reinterpret_cast<const longlong2 *>(cr));      // P01 | orig, Pm1_0
       const int4 h1 = __ldg(reinterpret_cast<const int4 *>(cr) + 1);             // Pm1_1, Pm1_2, M0, M1
       const int32_t orig = (int32_t)(h0.y & 0xffffffff);
@@ -499,25 +771,48 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
         // (each factor is < 2^32: 32-bit factors, 64-bit products only where needed)
         const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, Pm1_0, (uint32_t)h1.z, s012 & 255) : 1u;
         const uint32_t f1 = map1 >= 0 ? ceil_div32(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) : 1u;
+#if RP_GRID_LEAN
+        const uint32_t f2 = map2 >= 0 ? ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255) : 1u;
+        // SM_act in 32 bits: a factor >= 1023 >= n_SM already saturates it, and the product of
+        // three factors below 1023 is < 2^30
+        const uint32_t bc = min(f0, 1023u) * min(f1, 1023u) * min(f2, 1023u);
+        const int smact = (int)min(bc, (uint32_t)n_sm);
+        const bool full = smact == n_sm;
+        double rSM = rNSM;
+        if (!full) rSM = sRSM[smact];  // n_SM < kRSMTab for every program (compile_program)
+        uint64_t blocks = (uint64_t)f0 * f1;
+        if (map2 >= 0) blocks *= f2;
+        const double Rep = FAST ? (full ? (double)blocks * h3.x * rNSM : h3.x) : (double)blocks * h3.x * rSM;
+#else
         int64_t blocks = (int64_t)((uint64_t)f0 * f1);
         if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
         const int64_t smact = blocks < n_sm ? blocks : n_sm;
-        const double rSM = smact == n_sm ? rNSM : (rsm_tab ? sRSM[smact] : 1.0 / (double)smact);
+        // (n_SM < kRSMTab for every program, compile_program: the 1/SM_act table exists)
+        const double rSM = smact == n_sm ? rNSM : sRSM[smact];
         // line 15: #Blocks / (B_act SM_act)
         const double Rep = FAST ? (smact == n_sm ? (double)blocks * h3.x * rNSM : h3.x) : (double)blocks * h3.x * rSM;
+#endif
         E = mwpcwp_E<FAST>(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
                            rSM, (double)smact, kc);
       } else {
         E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
       }
       // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
+#if RP_KEY_F64
+      // a8 on the FP64 pipe: a masked, non-finite or non-positive E never beats the running best
+      // (+inf or a finite positive value); ties go to the lowest index
+      const bool okE = ok && E > 0.0 && E < kInf;
+      const bool better = okE && (E < st.e || (E == st.e && orig < st.i));
+#else
       E = (ok && pos_finite(E)) ? E : kInf;
       // a8: exact lexicographic key (E, original index): ties go to the lowest index (E and the
       // running best are positive or +inf, so their bit patterns compare as integers)
       const long long eb = __double_as_longlong(E), sb = __double_as_longlong(st.e);
       const bool better = eb < sb || (eb == sb && orig < st.i);
+      const bool okE = true;  // (an invalid E is +inf here)
+#endif
       if (SECOND) {  // runner-up on the same exact key
-        const bool sec = !better && key_less(E, orig, st.s, st.j);
+        const bool sec = !better && okE && key_less(E, orig, st.s, st.j);
         st.s = better ? st.e : (sec ? E : st.s);
         st.j = better ? st.i : (sec ? orig : st.j);
       }
@@ -526,34 +821,118 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     }
   };
   if (wid * 8 < tmax) {
-    // a3 early exit: configurations are sorted by P1 P2, so every octet from the first one whose
+    // factored tiles (k_plan_groups): per group, lane q of a quad forms w_{k,1+q} and its share of
+    // w_{k,0} for its tuple from the staged C (kGS terms per polynomial); each tile of the group is
+    // then two DMMAs per polynomial: (shares, B = 1), then A = w_{k,1+q}, B = x^{1+q} of
+    // configuration lane / 4
+    const int q = lane & 3;
+    const double *crow = sC + t * CS;
+    for (int gi = 0; gi < ngr; ++gi) {
+      const GroupDesc *gd = gdesc + gi;
+      const int tb = __ldg(&gd->tile_begin), te = __ldg(&gd->tile_end);
+      if (sorted && __ldg(&grec[tb * 8].P01) > maxD1sq) continue;  // a3: every member fails
+      // lane q: w_{k,1+q} (kGS1 terms) and its share of w_{k,0} (its K slot of the DMMA with B = 1,
+      // which sums the four shares into every column)
+      double w1[NPOLY], a0[NPOLY];
+      {
+        int off[kGS];
+        double y[kGS];
+#pragma unroll
+        for (int s = 0; s < kGS; ++s) {
+          off[s] = __ldg(&gd->off[q][s]);
+          y[s] = __ldg(&gd->y[q][s]);
+        }
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) {
+          const double *ck = crow + k * NPE;
+          double s1 = ck[off[0]] * y[0];
+#pragma unroll
+          for (int s = 1; s < kGS1; ++s) s1 = fma(ck[off[s]], y[s], s1);
+          double s0 = ck[off[kGS1]] * y[kGS1];
+#pragma unroll
+          for (int s = kGS1 + 1; s < kGS; ++s) s0 = fma(ck[off[s]], y[s], s0);
+          w1[k] = s1;
+          a0[k] = s0;
+        }
+      }
+      int tend = te;  // members in P1 P2 order: stop at the first tile that fails a3 everywhere
+      if (sorted)
+        for (int tile = tb + 1; tile < te; ++tile)
+          if (__ldg(&grec[tile * 8].P01) > maxD1sq) {
+            tend = tile;
+            break;
+          }
+      int tile = tb;
+#if RP_GPAIR
+      for (; tile + 1 < tend; tile += 2) {  // two tiles per iteration: 4 independent pairs per lane
+        const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
+        const double b2 = __ldg(gmP + (int64_t)q * nGp + tile * 8 + 8 + (lane >> 2));
+        double acc[NPOLY][2], acc2[NPOLY][2];
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) {
+          dmma_c(acc[k][0], acc[k][1], a0[k], 1.0, 0.0, 0.0);
+          dmma(acc[k][0], acc[k][1], w1[k], b);
+        }
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) {
+          dmma_c(acc2[k][0], acc2[k][1], a0[k], 1.0, 0.0, 0.0);
+          dmma(acc2[k][0], acc2[k][1], w1[k], b2);
+        }
+        epi_oct(grec + tile * 8, acc);
+        epi_oct(grec + tile * 8 + 8, acc2);
+      }
+#endif
+#if RP_PREF
+      const double *bp = gmP + (int64_t)q * nGp + (lane >> 2);
+      double bn = tile < tend ? __ldg(bp + tile * 8) : 0.0;
+#endif
+      for (; tile < tend; ++tile) {
+#if RP_PREF
+        const double b = bn;
+        if (tile + 1 < tend) bn = __ldg(bp + tile * 8 + 8);
+#else
+        const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
+#endif
+        double acc[NPOLY][2];
+#pragma unroll
+        for (int k = 0; k < NPOLY; ++k) {
+          dmma_c(acc[k][0], acc[k][1], a0[k], 1.0, 0.0, 0.0);  // w_{k,0} in both columns
+          dmma(acc[k][0], acc[k][1], w1[k], b);
+        }
+        epi_oct(grec + tile * 8, acc);
+      }
+    }
+    // dense tiles; a3 early exit: they are sorted by P1 P2, so every tile from the first one whose
     // smallest P1 P2 exceeds the largest D1^2 of the warp's tuples fails the D rule
+    const int nOctF = ntile - ngt;
+    const CfgRec *drec = grec + ngt * 8;
     int nEff = nOctF;
     if (sorted)
       for (int b0 = 0; b0 < nOctF; b0 += 32) {
         const int oc = b0 + lane;
-        const unsigned stop = __ballot_sync(0xffffffffu, oc < nOctF && __ldg(&rec[oc * 8].P01) > maxD1sq);
+        const unsigned stop = __ballot_sync(0xffffffffu, oc < nOctF && __ldg(&drec[oc * 8].P01) > maxD1sq);
         if (stop) {
           nEff = b0 + __ffs(stop) - 1;
           break;
         }
       }
     // two configuration octets per iteration: 4 independent pairs per lane in the epilogue
-    int oc = 0;
+    int oc = ngt;
+    nEff += ngt;
     for (; oc + 1 < nEff; oc += 2) {
       double acc[NPOLY][2], acc2[NPOLY][2], bfr[KS], bfr2[KS];
       load_b(oc, bfr);
       load_b(oc + 1, bfr2);
-      mma_oct(oc, acc, bfr);
-      mma_oct(oc + 1, acc2, bfr2);
-      epi_oct(oc, acc);
-      epi_oct(oc + 1, acc2);
+      mma_oct(acc, bfr);
+      mma_oct(acc2, bfr2);
+      epi_oct(grec + oc * 8, acc);
+      epi_oct(grec + (oc + 1) * 8, acc2);
     }
     if (oc < nEff) {
       double acc[NPOLY][2], bfr[KS];
       load_b(oc, bfr);
-      mma_oct(oc, acc, bfr);
-      epi_oct(oc, acc);
+      mma_oct(acc, bfr);
+      epi_oct(grec + oc * 8, acc);
     }
   }
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------

@@ -181,3 +181,53 @@ def test_decision_service_memo_invalidated_by_update():
     assert after["idx"] == ref[0]["idx"] and after["E"] == ref[0]["E"]
     assert len(svc.memo) == 1 and svc.memo[tuple(int(v) for v in d)]["E"] == ref[0]["E"]
     assert before["E"] != after["E"]
+
+
+def test_history_save_load_across_plans():
+    """rp_plan_history_save / _load: a saved runtime history serves the next run's decisions as
+    hits and is refused by a plan whose program or F differs."""
+    case = synth.polybench_sweep(nD=200)
+    D = case.D
+    plan = rp.Plan(case.programs, _cuda(case.F))
+    plan.enable_history(prog=1, log2_capacity=12, margin=0.01)
+    first = plan.decide(D, prog=1, margin=0.01)
+    blob = plan.save_history()
+    assert blob == plan.save_history()  # deterministic (slot order)
+    n_entries = plan.history_stats()["entries"]
+    assert n_entries == len(np.unique(D, axis=0))
+
+    plan2 = rp.Plan(case.programs, _cuda(case.F))
+    plan2.enable_history(prog=1, log2_capacity=12, margin=0.01)
+    plan2.load_history(blob)
+    assert plan2.history_stats()["entries"] == n_entries
+    again = plan2.decide(D, prog=1, margin=0.01)
+    assert np.all(again["from_history"] == 1)
+    for f in ("idx", "E", "launch"):
+        assert np.array_equal(again[f], first[f])
+    # another capacity: the entries re-hash into the new table
+    plan3 = rp.Plan(case.programs, _cuda(case.F))
+    plan3.enable_history(prog=1, log2_capacity=9, margin=0.01)
+    plan3.load_history(blob)
+    assert np.all(plan3.decide(D, prog=1, margin=0.01)["from_history"] == 1)
+    # refused: other margin, other program index, other coefficients, other F, refit, tampering
+    plan4 = rp.Plan(case.programs, _cuda(case.F))
+    plan4.enable_history(prog=1, log2_capacity=12, margin=0.02)
+    with pytest.raises(rp.RPError):
+        plan4.load_history(blob)
+    other = copy.deepcopy(case.programs)
+    other[1].coef[0] = other[1].coef[0] * (1 + 2.0 ** -40)
+    plan5 = rp.Plan(other, _cuda(case.F))
+    plan5.enable_history(prog=1, log2_capacity=12, margin=0.01)
+    with pytest.raises(rp.RPError):
+        plan5.load_history(blob)
+    plan6 = rp.Plan(case.programs, _cuda(case.F[:-1]))
+    plan6.enable_history(prog=1, log2_capacity=12, margin=0.01)
+    with pytest.raises(rp.RPError):
+        plan6.load_history(blob)
+    coef = _cuda(np.stack([np.asarray(c, dtype=np.float64) for c in case.programs[1].coef]))
+    plan2.update(coef, prog=1)  # same values, but a refit clears the history
+    assert plan2.history_stats()["entries"] == 0
+    bad = bytearray(blob)
+    bad[40] ^= 1
+    with pytest.raises(rp.RPError):
+        plan3.load_history(bytes(bad))

@@ -674,3 +674,53 @@ def test_sweep_nonpositive_data_and_huge_blocks():
     jit = rp.Jit(spec)
     ji, jE, _ = jit.eval(_cuda(D), _cuda(F))
     assert np.array_equal(ji.cpu().numpy().ravel(), ref["idx"])
+
+
+def test_factored_tiles_match_dense_and_oracle():
+    """The factored contraction (k_plan_groups: configurations sharing every P_k but one, one
+    DMMA pair per polynomial and tile) against the dense one (RP_SWEEP_GROUPS=0) and the
+    oracle: `large` truth program on a 20,000-tuple slice plus edge tuples (small D1 exercises
+    the a3 exit inside groups), and a p = 3 program whose groups fall back to dense."""
+    import os
+    for name, spec, F, D in (
+            ("large", synth.large_program(), synth.F_large(),
+             np.concatenate([synth.random_D_edge_cases(2), synth.large_D(20_000)])),
+            ("polybench", synth.polybench_sweep(nD=8).programs[0], synth.F_pow2_3d(),
+             synth.polybench_sweep(nD=3000).D)):
+        outs = []
+        for groups in ("1", "0"):
+            os.environ["RP_SWEEP_GROUPS"] = groups
+            try:
+                plan = rp.Plan([spec], _cuda(F))
+            finally:
+                os.environ.pop("RP_SWEEP_GROUPS", None)
+            outs.append([t.cpu().numpy() for t in plan.eval(_cuda(D), second=True)])
+        (i1, e1, s1), (i0, e0, s0) = outs
+        assert np.array_equal(i1, i0), name
+        fin = np.isfinite(e0)
+        assert np.array_equal(fin, np.isfinite(e1)), name
+        assert np.max(np.abs(e1[fin] - e0[fin]) / e0[fin], initial=0) <= 1e-12, name
+        sel = np.arange(0, len(D), 7)
+        ref = oracle.sweep(spec, D[sel], F)
+        check_sweep(i1[0][sel], e1[0][sel], s1[0][sel], ref, spec, D[sel], F, name)
+
+
+def test_sweep_beyond_sort_limit():
+    """A plan with more than 8,192 statically feasible configurations keeps index order (no
+    P1 P2 sort, no a3 early exit, no groups): parity with the oracle, and rp_plan_decide
+    refuses it (its per-CTA candidate limit)."""
+    hw = dict(synth.HW_GTX1080TI)
+    hw.update(t_max=16384, w_max=1024, b_max=32, r_max=1 << 40, z_max=1 << 40)
+    spec = synth.classf_program("bigF", 1, 3, 2, [8, 1, 1, 1], [4096, 64, 64, 64], hw, R=16, Z0=0, Z1=0,
+                                grid_map=(0, 0, 0), stream="bigF")
+    F = np.array([(a, b, c) for a in range(1, 65) for b in range(1, 65) for c in range(1, 65)
+                  if (a * b * c) % 32 == 0], dtype=np.int32)
+    plan = rp.Plan([spec], _cuda(F))
+    assert plan.static_feasible() > 8192
+    D = np.concatenate([synth.random_D_edge_cases(1),
+                        synth.log_uniform_ints(np.random.default_rng(5), 1, 4096, (120, 1))]).astype(np.int32)
+    idx, E, S = plan.eval(_cuda(D), second=True)
+    ref = oracle.sweep(spec, D, F)
+    check_sweep(idx[0], E[0], S[0], ref, spec, D, F, "bigF")
+    with pytest.raises(rp.RPError):
+        plan.decide(D[:2])

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "rp.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:rp_status|int32_t|const char \*)\s*(rp_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:rp_status|int32_t|const char \*|const rp_program \*)\s*(rp_\w+)\s*\(", src, re.M)))
 
 
 def test_header_symbols_exported():
@@ -100,3 +100,31 @@ def test_program_limits_rejected_without_gpu():
     ok = copy.deepcopy(spec)
     ok.hw = dict(spec.hw, n_sm=1023)
     rp.codegen(ok)
+
+
+def test_program_save_load_roundtrip():
+    """rp_program_save / rp_program_load (host only): exact round trip of every field, stable
+    bytes, and loud failures on tampering, truncation and a foreign blob."""
+    import copy
+    import oracle  # (test infrastructure: the box transform, so no device call is needed)
+    import paper_1911_02373_b200 as rp
+    import synth
+    for spec in (synth.large_program(), synth.polybench_sweep(nD=8).programs[2], synth.tiny_sweep().programs[0]):
+        spec = copy.deepcopy(spec)
+        c, e = oracle.xform_from_box(spec.box_lo, spec.box_hi)
+        spec.xform_c, spec.xform_e = list(c), list(e)
+        blob = rp.save_program(spec)
+        back = rp.load_program(blob)
+        ref = rp.Program(spec)
+        assert (back.d, back.p, back.template) == (spec.d, spec.p, spec.template)
+        for i in range(len(spec.coef)):
+            assert np.array_equal(back.num_exp[i], np.asarray(spec.num_exp[i], dtype=np.int16))
+            assert np.array_equal(back.den_exp[i], np.asarray(spec.den_exp[i], dtype=np.int16))
+            assert np.asarray(spec.coef[i], dtype=np.float64).tobytes() == back.coef[i].tobytes()
+        assert back.hw == {k: getattr(ref.c.hw, k) for k, _ in rp.rp_hw._fields_}
+        assert (back.R, back.Z0, back.Z1) == (spec.R, spec.Z0, spec.Z1)
+        assert list(back.xform_c) == list(ref.xform[0]) and list(back.xform_e) == list(ref.xform[1])
+        assert rp.save_program(back) == blob  # the loaded program saves to the same bytes
+        for bad in (blob[:-1], blob[:20], b"XX" + blob[2:], blob[:30] + bytes([blob[30] ^ 1]) + blob[31:]):
+            with pytest.raises(rp.RPError):
+                rp.load_program(bad)

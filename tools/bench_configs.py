@@ -84,10 +84,27 @@ t0 = time.perf_counter()
 for d in case.D[50:1050]:
     dc(d)
 nohist_us = 1e6 * (time.perf_counter() - t0) / 1000
+# the paper's own placement of the decision (host CPU, one D at a time):
+# the oracle's orc_decide on one core, program marshalled once, the same 1,000 tuples
+import ctypes as C
+import numpy as np
+import oracle
+h = oracle._ProgramHolder(case.programs[0])
+Fa = np.ascontiguousarray(case.F, dtype=np.int32)
+Eh, six, gap = np.zeros(1), np.zeros(6, dtype=np.int32), np.zeros(1)
+Ds = [np.ascontiguousarray(d, dtype=np.int32).ravel() for d in case.D[50:1050]]
+t0 = time.perf_counter()
+for d in Ds:
+    oracle.lib().orc_decide(C.byref(h.pr), oracle._p(d), oracle._p(Fa), len(Fa), 0.01, oracle._p(Eh), oracle._p(six),
+                            oracle._p(gap))
+host_us = 1e6 * (time.perf_counter() - t0) / len(Ds)
 out["decision_service"] = {"program": "polybench gemm, 266 configs", "path": "rp_decider (mapped memory + graph)",
                            "fresh_decision_us": fresh_us, "device_history_hit_us": hit_us,
                            "host_memo_hit_us": memo_us, "no_history_decision_us": nohist_us,
-                           "history": stats}
+                           "history": stats,
+                           "host_oracle_decision_us": host_us,
+                           "host_oracle_note": "orc_decide (x87 long double, 1 core, the same 1,000 tuples and margin): "
+                                               "the paper's host-side placement of the decision, as a reference point"}
 
 for name, case in (("polybench", synth.polybench_sweep()), ("multikernel", synth.multikernel_sweep())):
     D, F = torch.from_numpy(case.D).to(dev), torch.from_numpy(case.F).to(dev)
