@@ -174,6 +174,12 @@ rp_status rp_fit(const double *X, const double *V, int64_t K, int32_t n_v, const
  *   resid2, min_pivot, cond_est as doubles; nullable).  A degenerate system leaves NaN
  *   coefficients and status 3 in info (no error is returned: nothing is read back).
  * rp_fit_dev: the four above in order; xf_out [n][2] nullable.                               */
+/* rp_gram_sum_ordered: a13 in its deterministic form -- out[e] = ((parts[0][e] + parts[1][e]) +
+ * parts[2][e]) + ... for the n_parts partial Grams of the K shards, stacked in rank order (device
+ * float64 [n_parts][elems], e.g. an all_gather's output); out device float64 [elems] (may not
+ * alias parts).  Bit-reproducible, unlike an all_reduce whose summation order is NCCL's.
+ * INVALID_ARG for n_parts < 1 or host pointers.  Stream-ordered.                           */
+rp_status rp_gram_sum_ordered(const double *parts, int32_t n_parts, int64_t elems, double *out, rp_stream s);
 rp_status rp_minmax_dev(const double *X, int64_t K, int32_t n, double *lohi, rp_stream s);
 rp_status rp_xform_dev(const double *lohi, int32_t n, double *xf, rp_stream s);
 rp_status rp_gram_accumulate_dev(const double *X, const double *V, int64_t K, int32_t n_v,

@@ -123,6 +123,7 @@ _SIGS = {
     "rp_pipeline_timer_start": [_vp],
     "rp_pipeline_timer_stop": [_vp, _vp],
     "rp_pipeline_destroy": [_vp],
+    "rp_gram_sum_ordered": [_vp, _i32, _i64, _vp, _vp],
     "rp_program_save": [C.POINTER(rp_program), _vp, _i64, C.POINTER(_i64)],
     "rp_program_load": [_vp, _i64, C.POINTER(_vp)],
     "rp_program_blob_free": [_vp],
@@ -625,6 +626,14 @@ def fit(X, V, num_exp, den_exp, raise_on_degenerate: bool = True):
 
 def _dev_empty(ref, shape):
     return _torch().empty(shape, dtype=_torch().float64, device=ref.device)
+
+
+def gram_sum_ordered(parts, out=None):
+    """rp_gram_sum_ordered: the rank-ordered sum of stacked partial Grams [n_parts][...] (device)."""
+    parts = parts.contiguous()
+    out = out if out is not None else _dev_empty(parts, tuple(parts.shape[1:]))
+    _check(_lib.rp_gram_sum_ordered(_ptr(parts), parts.shape[0], parts[0].numel(), _ptr(out), _stream_of(parts)))
+    return out
 
 
 def minmax_dev(X, out=None):

@@ -819,6 +819,17 @@ rp_status rp_xform_dev(const double *lohi, int32_t n, double *xf, rp_stream sv) 
   return RP_OK;
 }
 
+rp_status rp_gram_sum_ordered(const double *parts, int32_t n_parts, int64_t elems, double *out, rp_stream sv) {
+  cudaStream_t s = (cudaStream_t)sv;
+  RP_REQUIRE(n_parts >= 1 && elems >= 0, RP_ERR_INVALID_ARG, "n_parts %d, elems %lld", n_parts, (long long)elems);
+  rp_status st = ensure_device();
+  if (st != RP_OK) return st;
+  if (elems == 0) return RP_OK;
+  if ((st = require_dev(parts, "parts")) != RP_OK || (st = require_dev(out, "out")) != RP_OK) return st;
+  RP_CUDA(launch_sum_ordered(parts, n_parts, elems, out, s));
+  return RP_OK;
+}
+
 rp_status rp_gram_accumulate_dev(const double *X, const double *V, int64_t K, int32_t n_v, const rp_basis *basis,
                                  const double *xf, double *G, rp_stream sv) {
   cudaStream_t s = (cudaStream_t)sv;

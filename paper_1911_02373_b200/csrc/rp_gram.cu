@@ -1195,6 +1195,24 @@ __global__ void k_den_weights(const GramBasis *gb, const double *X, int64_t K, i
   }
 }
 
+// a13, deterministic form: out = ((p_0 + p_1) + p_2) + ... elementwise, partials in rank order
+// (the all_gather'ed partial Grams of the K shards; bit-reproducible whatever the collective)
+__global__ void k_sum_ordered(const double *parts, int n_parts, int64_t elems, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = parts[i];
+    for (int r = 1; r < n_parts; ++r) acc += parts[(int64_t)r * elems + i];
+    out[i] = acc;
+  }
+}
+
+cudaError_t launch_sum_ordered(const double *parts, int n_parts, int64_t elems, double *out, cudaStream_t s) {
+  if (elems == 0) return cudaSuccess;
+  const int64_t b = (elems + 255) / 256;
+  const int grid = (int)(b < 4 * num_sms() ? b : 4 * num_sms());
+  k_sum_ordered<<<grid, 256, 0, s>>>(parts, n_parts, elems, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_den_weights(const GramBasis *d_basis, const double *X, int64_t K, int n_v,
                                const double *d_coef, double *S, cudaStream_t s) {
   if (K == 0) return cudaSuccess;

@@ -163,6 +163,7 @@ cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, cons
                         const double *V, const double *S, int64_t K, int n_v, double *G,
                         double *d_part, size_t part_elems, cudaStream_t s);
 size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_sms, bool weighted);
+cudaError_t launch_sum_ordered(const double *parts, int n_parts, int64_t elems, double *out, cudaStream_t s);
 cudaError_t launch_den_weights(const GramBasis *d_basis, const double *X, int64_t K, int n_v,
                                const double *d_coef, double *S, cudaStream_t s);
 

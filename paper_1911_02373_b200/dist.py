@@ -59,6 +59,9 @@ class LibOps:
     def solve_dev(self, G, num, den):
         return self.rp.solve_dev(G, num, den)
 
+    def gram_sum(self, parts):
+        return self.rp.gram_sum_ordered(parts)
+
     def tsqr(self, X, V, num, den, c, e):
         return self.rp.tsqr(X, V, num, den, c, e)
 
@@ -94,12 +97,11 @@ def sharded_fit(X_local, V_local, num, den, ops, n_vars: int, group=None, determ
     G = ops.gram(X_local, V_local, num, den, c, e)
     G = G if isinstance(G, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(G, dtype=np.float64))
     G = G.to(dev)
-    if deterministic:
-        parts = [torch.empty_like(G) for _ in range(dist.get_world_size(group))]
-        dist.all_gather(parts, G, group=group)
-        G = parts[0].clone()
-        for p in parts[1:]:
-            G += p
+    if deterministic:  # all_gather, then the rank-ordered sum on the device (ops.gram_sum)
+        world = dist.get_world_size(group)
+        parts = torch.empty((world * G.shape[0],) + tuple(G.shape[1:]), dtype=G.dtype, device=G.device)
+        dist.all_gather_into_tensor(parts, G.contiguous(), group=group)
+        G = ops.gram_sum(parts.view((world,) + tuple(G.shape)))
     else:
         dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
     coef, infos = ops.solve(G, num, den)

@@ -54,6 +54,13 @@ class OracleOps:
         coef, out = self.solve(G, num, den)
         return torch.from_numpy(coef), out
 
+    def gram_sum(self, parts):
+        """Rank-ordered sum of the gathered partials (what rp_gram_sum_ordered computes)."""
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        return acc
+
     def tsqr(self, X, V, num, den, c, e):
         """Any B with B^T B = A^T A serves: the shard's design rows themselves."""
         X = np.asarray(X)

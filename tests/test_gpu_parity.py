@@ -724,3 +724,15 @@ def test_sweep_beyond_sort_limit():
     check_sweep(idx[0], E[0], S[0], ref, spec, D, F, "bigF")
     with pytest.raises(rp.RPError):
         plan.decide(D[:2])
+
+
+def test_gram_sum_ordered_bitwise():
+    """rp_gram_sum_ordered (a13, deterministic form) equals the rank-ordered sum bit for bit."""
+    g = np.random.default_rng(11)
+    for n_parts in (1, 2, 3, 8):
+        parts = g.standard_normal((n_parts, 3, 140, 140)) * 10.0 ** g.integers(-3, 8, (n_parts, 1, 1, 1))
+        want = parts[0].copy()
+        for p in parts[1:]:
+            want = want + p
+        got = rp.gram_sum_ordered(_cuda(parts)).cpu().numpy()
+        assert got.tobytes() == want.tobytes(), n_parts
