@@ -39,7 +39,9 @@ __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_
 }
 
 __device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab, int npe_pad);
-__device__ void refresh_schedule(const DevProg &pg, int g, int npe_pad, const CfgTable &tab);
+__device__ void schedule_slot_mp(const DevProg &pg, const CfgRec &r, int hv, int npe_pad, double *col, int nGp);
+__device__ bool group_lists(const DevProg &pg, int hv, int32_t (*off)[kGS]);
+__device__ void group_y(const DevProg &pg, GroupDesc &gd);
 
 // ---- a1 + a5 + P-monomials, compaction in index order --------------------------------------
 __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, const int32_t *F,
@@ -180,12 +182,14 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
   build_refine_terms(g, pg, tab, npe_pad);
 }
 
-// rp_plan_update_program in one launch: the configuration table (a1 masks, a5 occupancy, the
-// P1 P2 order) depends on F, the hardware and the kernel's resources only, so a refit changes
-// just the coefficients (the dense staging matrix Cmat) and the transform (the program-part
-// monomials mP of the sorted feasible configurations).
-__global__ void __launch_bounds__(1024) k_plan_refresh(DevProg *pgp, int g, const double *coef, int stride,
-                                                       const double *xf, int npe_pad, CfgTable tab) {
+// rp_plan_update_program: the configuration table (a1 masks, a5 occupancy, the P1 P2 order, the
+// tile schedule) depends on F, the hardware and the kernel's resources only, so a refit changes
+// just the coefficients (the dense staging matrix Cmat and the refinement's term table) and the
+// transform (the program-part monomials of the configurations, the factored tiles' powers and
+// the groups' Y values).  Three launches: the new values into the program (one CTA), the tables
+// that depend on them (grid-stride over every entry), the refinement terms (one CTA: a compaction).
+__global__ void __launch_bounds__(1024) k_plan_refresh_prog(DevProg *pgp, const double *coef, int stride,
+                                                            const double *xf) {
   DevProg &pg = *pgp;
   const int nterm = pg.nterm;
   for (int j = threadIdx.x; j < nterm; j += blockDim.x) {
@@ -196,33 +200,57 @@ __global__ void __launch_bounds__(1024) k_plan_refresh(DevProg *pgp, int g, cons
     pg.xc[threadIdx.x] = xf[2 * threadIdx.x];
     pg.xe[threadIdx.x] = (int32_t)xf[2 * threadIdx.x + 1];
   }
-  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_plan_refresh_tables(const DevProg *pgp, int g, int npe_pad, CfgTable tab) {
+  const DevProg &pg = *pgp;
   const int nFp = tab.nFp, nFc = tab.nFc[2 * g];
+  const int nGp = tab.nGp, nslot = tab.gcnt[4 * g + 2] * 8, ngr = tab.gcnt[4 * g + 0];
+  const int nrow = pg.npoly * pg.nPE;
   const CfgRec *rec = tab.rec + (int64_t)g * nFp;
   double *mP = tab.mP + (int64_t)g * npe_pad * nFp;
-  for (int t = threadIdx.x; t < nFc * npe_pad; t += blockDim.x) {
-    const int pos = t / npe_pad, pe = t % npe_pad;
-    double m = 0.0;
-    if (pe < pg.nPE) {
-      const CfgRec &r = rec[pos];
-      const int32_t Pk[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
-      m = 1.0;
-      for (int k = 0; k < pg.p; ++k) {
-        const double u = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
-        for (int e = 0; e < pg.pe_exp[pe][k]; ++e) m *= u;
-      }
-    }
-    mP[(int64_t)pe * nFp + pos] = m;
-  }
+  const CfgRec *grec = tab.grec + (int64_t)g * nGp;
+  double *gmP = tab.gmP + (int64_t)g * npe_pad * nGp;
+  const int32_t *ghv = tab.ghv + (int64_t)g * nGp;
+  GroupDesc *gdesc = tab.gdesc + (int64_t)g * kMaxGroups;
   double *Cm = tab.Cmat + (int64_t)g * kMaxPolys * npe_pad * tab.nde_pad;
-  for (int r = threadIdx.x; r < pg.npoly * pg.nPE; r += blockDim.x) {
-    const int k = r / pg.nPE, pe = r % pg.nPE;
-    for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
-      Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
+  // work items: [configuration monomials | schedule slots | staging rows | groups]
+  const int n0 = nFc * npe_pad, n1 = n0 + nslot, n2 = n1 + nrow, n3 = n2 + ngr;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n3; t += gridDim.x * blockDim.x) {
+    if (t < n0) {
+      const int pos = t / npe_pad, pe = t % npe_pad;
+      double m = 0.0;
+      if (pe < pg.nPE) {
+        const CfgRec &r = rec[pos];
+        const int32_t Pk[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+        m = 1.0;
+        for (int k = 0; k < pg.p; ++k) {
+          const double u = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
+          for (int e = 0; e < pg.pe_exp[pe][k]; ++e) m *= u;
+        }
+      }
+      mP[(int64_t)pe * nFp + pos] = m;
+    } else if (t < n1) {
+      const int sl = t - n0;
+      schedule_slot_mp(pg, grec[sl], ghv[sl], npe_pad, gmP + sl, nGp);
+    } else if (t < n2) {
+      const int r = t - n1, k = r / pg.nPE, pe = r % pg.nPE;
+      for (int j = pg.row_start[r]; j < pg.row_start[r + 1]; ++j)
+        Cm[(int64_t)(k * npe_pad + pe) * tab.nde_pad + pg.term_de[j]] = pg.term_coef[j];
+    } else {
+      GroupDesc &gd = gdesc[t - n2];
+      // off[][] holds 0 for padding terms now: rebuild the lists (Y = 0 marks them)
+      int32_t off[4][kGS];
+      group_lists(pg, gd.hv, off);
+      for (int q = 0; q < 4; ++q)
+        for (int s = 0; s < kGS; ++s) gd.off[q][s] = off[q][s];
+      group_y(pg, gd);
+    }
   }
-  refresh_schedule(pg, g, npe_pad, tab);
-  __syncthreads();
-  build_refine_terms(g, pg, tab, npe_pad);
+}
+
+__global__ void __launch_bounds__(1024) k_plan_refresh_terms(const DevProg *pgp, int g, int npe_pad, CfgTable tab) {
+  build_refine_terms(g, *pgp, tab, npe_pad);
 }
 
 // ---- the sweep's tile schedule: factored tiles of configuration groups, then dense tiles ----------
@@ -283,7 +311,7 @@ __device__ bool group_lists(const DevProg &pg, int hv, int32_t (*off)[kGS]) {
   return true;
 }
 
-// Y_pe of a group's terms (they depend on the transform: recomputed by k_plan_refresh)
+// Y_pe of a group's terms (they depend on the transform: recomputed at every refit)
 __device__ void group_y(const DevProg &pg, GroupDesc &gd) {
   double u[3] = {1.0, 1.0, 1.0};
   for (int k = 0; k < pg.p; ++k) u[k] = prog_u(pg, k, gd.P[k]);
@@ -461,28 +489,11 @@ __global__ void __launch_bounds__(1024) k_plan_groups(const DevProg *progs, int 
   }
 }
 
-// refit: the factored slots' powers and the groups' Y values follow the new transform
-__device__ void refresh_schedule(const DevProg &pg, int g, int npe_pad, const CfgTable &tab) {
-  const int nGp = tab.nGp, ntile = tab.gcnt[4 * g + 2], ngr = tab.gcnt[4 * g + 0];
-  const CfgRec *grec = tab.grec + (int64_t)g * nGp;
-  double *gmP = tab.gmP + (int64_t)g * npe_pad * nGp;
-  const int32_t *ghv = tab.ghv + (int64_t)g * nGp;
-  for (int s = threadIdx.x; s < ntile * 8; s += blockDim.x) schedule_slot_mp(pg, grec[s], ghv[s], npe_pad, gmP + s, nGp);
-  GroupDesc *gdesc = tab.gdesc + (int64_t)g * kMaxGroups;
-  for (int i = threadIdx.x; i < ngr; i += blockDim.x) {
-    GroupDesc &gd = gdesc[i];
-    // off[][] holds 0 for padding terms now: rebuild the lists (Y = 0 marks them)
-    int32_t off[4][kGS];
-    group_lists(pg, gd.hv, off);
-    for (int q = 0; q < 4; ++q)
-      for (int s = 0; s < kGS; ++s) gd.off[q][s] = off[q][s];
-    group_y(pg, gd);
-  }
-}
-
 cudaError_t launch_plan_refresh(DevProg *d_prog, int g, const double *d_coef, int stride, const double *d_xf,
                                 int npe_pad, CfgTable tab, cudaStream_t s) {
-  k_plan_refresh<<<1, 1024, 0, s>>>(d_prog, g, d_coef, stride, d_xf, npe_pad, tab);
+  k_plan_refresh_prog<<<1, 1024, 0, s>>>(d_prog, d_coef, stride, d_xf);
+  k_plan_refresh_tables<<<4 * num_sms() < 64 ? 4 * num_sms() : 64, 256, 0, s>>>(d_prog, g, npe_pad, tab);
+  k_plan_refresh_terms<<<1, 1024, 0, s>>>(d_prog, g, npe_pad, tab);
   return cudaGetLastError();
 }
 
@@ -1623,21 +1634,32 @@ __device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab
   }
   const int nrt = rt_base;
   double *ri = tab.rinfo + (int64_t)g * 8;
-  if (threadIdx.x < kMaxPolys) {  // A_k = sum |c| over the terms of polynomial k (fixed order)
+  // A_k = sum |c| over the terms of polynomial k (warp k: lane-strided partial sums, then a fixed
+  // butterfly: deterministic); warp kMaxPolys: the largest total degree and the term count
+  if (wid < kMaxPolys) {
     double A = 0.0;
-    for (int j = 0; j < nrt; ++j) A += fabs(rc[(int64_t)j * kMaxPolys + threadIdx.x]);
-    ri[threadIdx.x] = A;
-  } else if (threadIdx.x == kMaxPolys) {
+    for (int j = lane; j < nrt; j += 32) A += fabs(rc[(int64_t)j * kMaxPolys + wid]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) A += __shfl_xor_sync(0xffffffffu, A, o);
+    if (lane == 0) ri[wid] = A;
+  } else if (wid == kMaxPolys) {
     int md = 0;
-    for (int j = 0; j < nrt; ++j) {
+    for (int j = lane; j < nrt; j += 32) {
       const int de = rt[j] & 0xffff, pe = rt[j] >> 16;
       int dg = 0;
       for (int k = 0; k < pg.d; ++k) dg += pg.de_exp[de][k];
       for (int k = 0; k < pg.p; ++k) dg += pg.pe_exp[pe][k];
       md = dg > md ? dg : md;
     }
-    ri[6] = (double)md;
-    ri[7] = (double)nrt;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const int x = __shfl_xor_sync(0xffffffffu, md, o);
+      md = x > md ? x : md;
+    }
+    if (lane == 0) {
+      ri[6] = (double)md;
+      ri[7] = (double)nrt;
+    }
   }
 }
 
