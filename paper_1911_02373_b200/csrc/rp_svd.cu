@@ -15,12 +15,18 @@
 //      factors are merged by a binary tree inside the same launch: the second CTA to reach a
 //      tree node stacks [R_left; R_right] (fixed order: deterministic) and re-triangularises;
 //      the root writes R.
-//   2. k_svd_jacobi -- one-sided (Hestenes) Jacobi SVD of R, one CTA per metric: R lives in
-//      shared memory (column-major, 157 KB at n_c = 140), the accumulated rotations V in L2;
-//      each round of the round-robin ordering (all pairs disjoint) gives one pair per warp,
-//      whose V columns are fetched before the dot products so that their latency overlaps.
-//      Singular values are the final column norms.
+//   2. k_svd_gk (default) -- the SVD of R by Householder bidiagonalisation, bisection on the
+//      Golub-Kahan tridiagonal for every singular value and inverse iteration for the vector of
+//      the smallest (one CTA per metric, R in shared memory; below).  k_svd_jacobi
+//      (RP_SVD_SOLVER=jacobi) -- one-sided (Hestenes) Jacobi SVD of R, R in shared memory
+//      (column-major, 157 KB at n_c = 140), the accumulated rotations V in L2; each round of the
+//      round-robin ordering (all pairs disjoint) gives one pair per warp.  Singular values are the
+//      final column norms.
+#include <cstdlib>
+#include <cstring>
+
 #include "rp_internal.cuh"
+#include "rp_umma.cuh"
 
 namespace rp {
 
@@ -31,6 +37,7 @@ constexpr int kSD = 36;               // staging stride (32 rows + pad, = 4 mod 
 constexpr int kTsqrMaxThreads = 576;
 constexpr int kJacThreads = 1024;
 constexpr int kJacMaxSweeps = 40;
+constexpr int kGkThreads = 512;  // k_svd_gk
 
 __host__ __device__ inline int64_t packed_off(int i, int nc) {  // start of row i of packed R
   return (int64_t)i * nc - (int64_t)i * (i - 1) / 2;
@@ -59,15 +66,32 @@ struct TsqrArgs {
 __device__ __forceinline__ void householder_params(double a, double sub, double &tau, double &beta,
                                                    double &s) {
   // H = I - tau v v^T with v = (1, s * x_sub): H (a, x_sub) = (beta, 0)
+  // (on the wavefront's critical path: MUFU seeds with Newton steps instead of IEEE sqrt and
+  // division, ~1 ulp; the reflector stays exactly orthogonal in exact arithmetic for any s)
   if (sub == 0.0) {
     tau = 0.0;
     beta = a;
     s = 0.0;
   } else {
-    const double nrm = sqrt(fma(a, a, sub));
+    const double x = fma(a, a, sub);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-0.5 * x * y, y, 0.5), y);  // y <- y (3 - x y^2) / 2, twice
+    y = fma(y, fma(-0.5 * x * y, y, 0.5), y);
+    double nrm = x * y;
+    nrm = fma(0.5 * y, fma(-nrm, nrm, x), nrm);  // one Newton step on the root itself
     beta = a >= 0.0 ? -nrm : nrm;
-    s = 1.0 / (a - beta);
-    tau = (beta - a) / beta;
+    const double den = a - beta;  // |den| = |a| + nrm > 0
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    double ee = fma(-den, r, 1.0);
+    r = fma(r, fma(ee, ee, ee), r);
+    s = r;
+    double rb;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rb) : "d"(beta));
+    ee = fma(-beta, rb, 1.0);
+    rb = fma(rb, fma(ee, ee, ee), rb);
+    tau = (beta - a) * rb;
   }
 }
 
@@ -534,9 +558,20 @@ cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double 
   return cudaGetLastError();
 }
 
+__global__ void k_svd_gk(JacArgs a);
+static bool svd_use_jacobi();
+
 cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, double *V_ws, double *coef,
                               double *sigma, double *info, cudaStream_t s) {
   if (nc < 2 || nc > kSvdMaxCols) return cudaErrorInvalidValue;
+  if (!svd_use_jacobi()) {
+    const size_t smem = ((size_t)nc * (nc | 1) + 20 * (size_t)nc + 16) * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_svd_gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    JacArgs a{R, nc, n_num, V_ws, coef, sigma, info};
+    k_svd_gk<<<n_v, kGkThreads, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   const int np = (nc + 1) & ~1;
   const size_t smem = (size_t)nc * (nc | 1) * 8 + (size_t)(((np - 1) * (np / 2) + 3) & ~3) * 2 +
                       kSvdMaxCols * 8 + 16;
@@ -545,6 +580,274 @@ cudaError_t launch_svd_jacobi(const double *R, int nc, int n_num, int n_v, doubl
   JacArgs a{R, nc, n_num, V_ws, coef, sigma, info};
   k_svd_jacobi<<<n_v, kJacThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// ============================================================================================
+// k_svd_gk -- the SVD of R by Householder bidiagonalisation, bisection on the Golub-Kahan
+// tridiagonal and inverse iteration (default; RP_SVD_SOLVER=jacobi keeps k_svd_jacobi).
+//
+//   1. R = U B V^T, B upper bidiagonal (d, e): left and right Householder reflectors alternately,
+//      A in shared memory (column-major, odd stride); the right reflectors stay in A's rows.
+//   2. All singular values by bisection on T_GK, the 2n x 2n symmetric tridiagonal with zero
+//      diagonal and off-diagonal (d0, e0, d1, e1, ..., d_{n-1}), whose eigenvalues are
+//      +-sigma_i: sigma_i is where the Sturm count (eigenvalues < x) passes n + i.  Four threads
+//      per value (quadrisection), 30 rounds: absolute accuracy ~ u ||B||.
+//   3. The vector of sigma_min by inverse iteration on T_GK - sigma_min I (tridiagonal LU with
+//      partial pivoting): the even entries of the eigenvector are B's right singular vector (the
+//      +-sigma_min pair shares them, so a tiny sigma_min does not matter), then V applies the right
+//      reflectors in reverse.  Clustered sigma_min: any vector of the cluster (reading R30).
+// Same outputs as k_svd_jacobi: coef = v / v[n_num], sigma ascending, info[6] (sweeps = 0).
+// ============================================================================================
+
+__device__ __forceinline__ double gk_rcp(double x) {  // ~1 ulp reciprocal (MUFU seed + cubic step)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// number of eigenvalues of T_GK below x (a2[j] = a_j^2, j < 2n - 1)
+__device__ int gk_count(const double *a2, int m2, double x, double pivmin) {
+  int cnt = 0;
+  double q = -x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int j = 1; j < m2; ++j) {
+    q = -x - a2[j - 1] * gk_rcp(q);
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(kGkThreads, 1) k_svd_gk(JacArgs a) {
+  extern __shared__ __align__(16) double sg[];
+  const int n = a.nc, ld = n | 1, m2 = 2 * n;
+  double *A = sg;                     // [n][ld] column-major: A[c * ld + r]
+  double *d = A + (int64_t)n * ld;    // [n]    diagonal of B
+  double *e = d + n;                  // [n]    superdiagonal of B (e[n-1] = 0)
+  double *tauR = e + n;               // [n]    right reflectors
+  double *a2 = tauR + n;              // [2n]   squared off-diagonal of T_GK
+  double *sig = a2 + m2;              // [n]    singular values, ascending
+  double *z = sig + n;                // [2n]   inverse iteration vector
+  double *w = z + m2;                 // [n]    the singular vector
+  double *Ud = w + n;                 // [2n]   inverse iteration: U's diagonal,
+  double *Uo1 = Ud + m2;              // [2n]   first and
+  double *Uo2 = Uo1 + m2;             // [2n]   second superdiagonals,
+  double *Lm = Uo2 + m2;              // [2n]   multipliers,
+  int *piv = (int *)(Lm + m2);        // [2n]   row interchanges
+  __shared__ double s_par[4];
+  const int metric = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double *R = a.R + (int64_t)metric * n * n;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) A[(i % n) * ld + i / n] = R[i];
+  __syncthreads();
+
+  // ---- 1. bidiagonalisation ------------------------------------------------------------------
+  for (int k = 0; k < n; ++k) {
+    // left reflector of column k (rows k..n-1): one warp forms it
+    if (wid == 0) {
+      double s2 = 0.0;
+      for (int r = k + 1 + lane; r < n; r += 32) s2 = fma(A[k * ld + r], A[k * ld + r], s2);
+      s2 = warp_sum(s2);
+      const double al = A[k * ld + k];
+      double tau = 0.0, beta = al, sc = 0.0;
+      if (s2 != 0.0) {
+        const double nrm = sqrt(fma(al, al, s2));
+        beta = al >= 0.0 ? -nrm : nrm;
+        sc = 1.0 / (al - beta);
+        tau = (beta - al) / beta;
+      }
+      for (int r = k + 1 + lane; r < n; r += 32) A[k * ld + r] *= sc;  // v (v_k = 1 implicit)
+      if (lane == 0) {
+        d[k] = beta;
+        s_par[0] = tau;
+      }
+    }
+    __syncthreads();
+    const double tl = s_par[0];
+    if (tl != 0.0)
+      for (int j = k + 1 + wid; j < n; j += nw) {  // columns j > k: A_j -= tau (v^T A_j) v
+        double t = lane == 0 ? A[j * ld + k] : 0.0;
+        for (int r = k + 1 + lane; r < n; r += 32) t = fma(A[k * ld + r], A[j * ld + r], t);
+        t = tl * warp_sum(t);
+        if (lane == 0) A[j * ld + k] -= t;
+        for (int r = k + 1 + lane; r < n; r += 32) A[j * ld + r] = fma(-t, A[k * ld + r], A[j * ld + r]);
+      }
+    __syncthreads();
+    if (k + 1 >= n) break;
+    // right reflector of row k (columns k+1..n-1)
+    if (wid == 0) {
+      double s2 = 0.0;
+      for (int c = k + 2 + lane; c < n; c += 32) s2 = fma(A[c * ld + k], A[c * ld + k], s2);
+      s2 = warp_sum(s2);
+      const double al = A[(k + 1) * ld + k];
+      double tau = 0.0, beta = al, sc = 0.0;
+      if (s2 != 0.0) {
+        const double nrm = sqrt(fma(al, al, s2));
+        beta = al >= 0.0 ? -nrm : nrm;
+        sc = 1.0 / (al - beta);
+        tau = (beta - al) / beta;
+      }
+      for (int c = k + 2 + lane; c < n; c += 32) A[c * ld + k] *= sc;  // v (v_{k+1} = 1 implicit)
+      if (lane == 0) {
+        e[k] = beta;
+        tauR[k] = tau;
+        s_par[1] = tau;
+      }
+    }
+    __syncthreads();
+    const double tr = s_par[1];
+    if (tr != 0.0)
+      for (int i = k + 1 + wid; i < n; i += nw) {  // rows i > k: A^i -= tau (A^i v) v^T
+        double t = lane == 0 ? A[(k + 1) * ld + i] : 0.0;
+        for (int c = k + 2 + lane; c < n; c += 32) t = fma(A[c * ld + i], A[c * ld + k], t);
+        t = tr * warp_sum(t);
+        if (lane == 0) A[(k + 1) * ld + i] -= t;
+        for (int c = k + 2 + lane; c < n; c += 32) A[c * ld + i] = fma(-t, A[c * ld + k], A[c * ld + i]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    e[n - 1] = 0.0;
+    tauR[n - 1] = 0.0;
+    if (n >= 2) tauR[n - 2] = 0.0;  // row n-2 has a single entry right of the diagonal: no reflector
+  }
+  __syncthreads();
+
+  // ---- 2. singular values: bisection on T_GK --------------------------------------------------
+  for (int j = threadIdx.x; j < m2 - 1; j += blockDim.x) {
+    const double v = (j & 1) ? e[j >> 1] : d[j >> 1];
+    a2[j] = v * v;
+  }
+  if (threadIdx.x == 0) {  // Gershgorin bound of T_GK and the pivot floor
+    double b = 0.0, amax = 0.0;
+    for (int j = 0; j < m2; ++j) {
+      const double lo = j > 0 ? fabs((j - 1) & 1 ? e[(j - 1) >> 1] : d[(j - 1) >> 1]) : 0.0;
+      const double hi = j < m2 - 1 ? fabs(j & 1 ? e[j >> 1] : d[j >> 1]) : 0.0;
+      b = fmax(b, lo + hi);
+      amax = fmax(amax, hi);
+    }
+    s_par[2] = b * (1.0 + 1e-14) + 1e-300;
+    s_par[3] = fmax(amax * amax * 1e-300, 1e-300);  // LAPACK-style safe minimum pivot
+  }
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x >> 2) {
+    const double bound = s_par[2], pivmin = s_par[3];
+    const int i = base + (threadIdx.x >> 2), q = threadIdx.x & 3;  // value i, quadrisection point q
+    double lo = 0.0, hi = bound;
+    for (int it = 0; it < 30; ++it) {  // 5^30 > 2^69: the interval ends below u ||B||
+      const double h = (hi - lo) * 0.2;
+      const double x = lo + h * (q + 1);
+      // sigma_i >= x  <=>  at most n + i eigenvalues of T_GK lie below x
+      const int below = i < n ? gk_count(a2, m2, x, pivmin) <= n + i : 0;
+      // the quad's answers form a prefix: sigma_i lies in sub-interval nb
+      const unsigned b = __ballot_sync(0xffffffffu, below);
+      const int nb = __popc((b >> (lane & 28)) & 0xFu);
+      const double nlo = lo + h * nb;
+      hi = nb < 4 ? lo + h * (nb + 1) : hi;
+      lo = nlo;
+    }
+    if (i < n && q == 0) sig[i] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+
+  // ---- 3. the right singular vector of sigma_min --------------------------------------------
+  if (threadIdx.x == 0) {
+    // inverse iteration on M = T - lam I by Gaussian elimination with row interchanges (the
+    // factor U has two superdiagonals); a zero pivot is replaced by eps ||T||
+    const double lam = sig[0];
+    const double eps = 2.220446049250313e-16 * fmax(s_par[2], 1e-300);
+    auto aj = [&](int j) { return (j & 1) ? e[j >> 1] : d[j >> 1]; };  // off-diagonal j of T_GK
+    double D = -lam, U1 = m2 > 1 ? aj(0) : 0.0, U2 = 0.0;
+    for (int j = 0; j < m2; ++j) {
+      if (j + 1 < m2) {
+        const double L = aj(j), nd = -lam, nu = j + 2 < m2 ? aj(j + 1) : 0.0;
+        if (fabs(D) >= fabs(L)) {  // keep row j
+          const double dv = fabs(D) > 0.0 ? D : eps;
+          const double mlt = L / dv;
+          Ud[j] = dv; Uo1[j] = U1; Uo2[j] = U2; Lm[j] = mlt; piv[j] = 0;
+          D = nd - mlt * U1;
+          U1 = nu - mlt * U2;
+        } else {                   // row j + 1 becomes the pivot row
+          const double mlt = D / L;
+          Ud[j] = L; Uo1[j] = nd; Uo2[j] = nu; Lm[j] = mlt; piv[j] = 1;
+          D = U1 - mlt * nd;
+          U1 = U2 - mlt * nu;
+        }
+        U2 = 0.0;
+      } else {
+        Ud[j] = fabs(D) >= eps ? D : (D < 0.0 ? -eps : eps);
+        Uo1[j] = 0.0;
+        Uo2[j] = 0.0;
+      }
+    }
+    for (int j = 0; j < m2; ++j) z[j] = 1.0 + 0.01 * (double)(j % 7);  // fixed start: deterministic
+    for (int iter = 0; iter < 3; ++iter) {
+      for (int j = 0; j + 1 < m2; ++j) {
+        if (piv[j]) {
+          const double t = z[j];
+          z[j] = z[j + 1];
+          z[j + 1] = t - Lm[j] * z[j];
+        } else {
+          z[j + 1] -= Lm[j] * z[j];
+        }
+      }
+      for (int j = m2 - 1; j >= 0; --j) {
+        double t = z[j];
+        if (j + 1 < m2) t -= Uo1[j] * z[j + 1];
+        if (j + 2 < m2) t -= Uo2[j] * z[j + 2];
+        z[j] = t / Ud[j];
+      }
+      double mx = 0.0;
+      for (int j = 0; j < m2; ++j) mx = fmax(mx, fabs(z[j]));
+      const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+      for (int j = 0; j < m2; ++j) z[j] *= sc;
+    }
+    // B's right singular vector: the even entries, normalised, into w
+    double nv = 0.0;
+    for (int i = 0; i < n; ++i) nv = fma(z[2 * i], z[2 * i], nv);
+    nv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;
+    for (int i = 0; i < n; ++i) w[i] = z[2 * i] * nv;
+  }
+  __syncthreads();
+  // v = H_0 H_1 ... H_{n-3} v_B: the right reflectors in reverse (the reflector of row k acts on
+  // entries k+1..n-1 with vector (1, A[k][k+2..n-1]))
+  for (int k = n - 3; k >= 0; --k) {
+    const double tr = tauR[k];
+    if (tr != 0.0 && wid == 0) {
+      double t = lane == 0 ? w[k + 1] : 0.0;
+      for (int c = k + 2 + lane; c < n; c += 32) t = fma(A[c * ld + k], w[c], t);
+      t = tr * warp_sum(t);
+      if (lane == 0) w[k + 1] -= t;
+      for (int c = k + 2 + lane; c < n; c += 32) w[c] = fma(-t, A[c * ld + k], w[c]);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  double *so = a.sigma + (int64_t)metric * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) so[i] = sig[i];
+  const double b0 = w[a.n_num];
+  const bool bad = !(fabs(b0) > 1e-300);
+  for (int r = threadIdx.x; r < n; r += blockDim.x)
+    a.coef[(int64_t)metric * n + r] = bad ? __longlong_as_double(0x7ff8000000000000ll) : w[r] / b0;
+  if (threadIdx.x == 0) {
+    const double smin = sig[0], smax = sig[n - 1];
+    int rank = 0;
+    for (int o = 0; o < n; ++o) rank += sig[o] > 1e-13 * smax;
+    double *inf = a.info + metric * 6;
+    inf[0] = bad ? (double)RP_ERR_DEGENERATE : 0.0;
+    inf[1] = rank;
+    inf[2] = (smin / b0) * (smin / b0);
+    inf[3] = smin;
+    inf[4] = smax / smin;
+    inf[5] = 0;
+  }
+}
+
+static bool svd_use_jacobi() {
+  const char *v = getenv("RP_SVD_SOLVER");
+  return v && strcmp(v, "jacobi") == 0;
 }
 
 }  // namespace rp
