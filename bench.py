@@ -212,6 +212,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the informational k_sweep_tc timing (ncu launch lists)")
     ap.add_argument("--nD", type=int, default=1_000_000)
     ap.add_argument("--K", type=int, default=1_000_000)
     args = ap.parse_args()
@@ -356,6 +357,8 @@ def main():
     loc_idx, loc_E = idx_out.clone(), E_out.clone()
     os.environ["RP_SWEEP_KERNEL"] = "tc"
     try:
+        if args.no_alt:
+            raise RuntimeError("skipped (--no-alt)")
         ti, tE = torch.empty_like(idx_out), torch.empty_like(E_out)
         plan_dev.eval(D_dev, out=(ti, tE, None), second=False)
         tc_ms = []

@@ -656,18 +656,21 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_gram_fused(FusedArgs a) {
 // ============================================================================================
 // Warp-specialised fused Gram (default).  In k_gram_fused every warp stages, then every warp
 // multiplies, so the FP64 tensor pipe idles during staging (~30% of a tile, measured with
-// -DRP_GRAM_TS).  Here warpgroup 3 (warps 12-15, one per SM sub-partition) only builds design
-// rows and warpgroups 0-2 (12 warps, 27 accumulator slots each) only multiply.  A stage holds
+// -DRP_GRAM_TS).  Here the last warpgroup (kWsPW = 4 warps, one per SM sub-partition) only builds
+// design rows and the first kWsMW warps (16: 20 accumulator slots each; 12: 27) only multiply.  A stage holds
 // X_0 = M(u) of 32 rows and, per row, the scales V_v and V_v^2: since
 //   X_0^T diag(V_v) X_0  and  X_0^T diag(V_v^2) X_0
 // are the (0, 1+v) and (1+v, 1+v) blocks, the consumers scale their A fragment (one row per lane)
 // instead of the producers writing X_{1+v} = V_v X_0 (4x less staging and shared memory).  Stages
 // are handed over with named barriers (FULL[b]: producers arrive, consumers wait; EMPTY[b]:
-// consumers arrive, producers wait); setmaxnreg moves 72 registers per producer thread to the
-// consumers (56 / 152 of the 128 at launch).
+// consumers arrive, producers wait); setmaxnreg gives the producers RP_WS_PREG registers and the
+// consumers RP_WS_CREG (56 / 104 with 16 consumer warps).
 // ============================================================================================
 constexpr int kWsRT = 32;      // rows per tile
-constexpr int kWsMW = 12;      // MMA (consumer) warps
+#ifndef RP_WS_MW
+#define RP_WS_MW 16
+#endif
+constexpr int kWsMW = RP_WS_MW;  // MMA (consumer) warps: 16 (4 per sub-partition), 12 measured 1.5% slower
 constexpr int kWsPW = 4;       // staging (producer) warps
 #ifndef RP_WS_NS
 #define RP_WS_NS 3
@@ -681,11 +684,20 @@ constexpr int kWsFlush = 32;   // tiles between flushes of the register accumula
 constexpr int kWsThreads = 32 * (kWsMW + kWsPW);
 constexpr int kWsIS = 4;       // input stages (raw X / V / S of a tile, filled by the TMA engine)
 // registers per thread after setmaxnreg: 12 x 32 x CREG + 4 x 32 x PREG <= 64K
+#if RP_WS_MW > 12
+#ifndef RP_WS_PREG
+#define RP_WS_PREG 56
+#endif
+#ifndef RP_WS_CREG
+#define RP_WS_CREG 104
+#endif
+#else
 #ifndef RP_WS_PREG
 #define RP_WS_PREG 72
 #endif
 #ifndef RP_WS_CREG
 #define RP_WS_CREG 144
+#endif
 #endif
 static_assert(kWsMW * 32 * RP_WS_CREG + kWsPW * 32 * RP_WS_PREG <= 65536, "register file");
 
@@ -967,6 +979,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gram_ws(FusedArgs a) {
 #define RP_W(w) \
   case w: ws_mma_warp<NB, NV, w, SLOTS>(cur, lane, acc); break;
       RP_W(0) RP_W(1) RP_W(2) RP_W(3) RP_W(4) RP_W(5) RP_W(6) RP_W(7) RP_W(8) RP_W(9) RP_W(10) RP_W(11)
+#if RP_WS_MW > 12
+      RP_W(12) RP_W(13) RP_W(14) RP_W(15)
+#endif
 #undef RP_W
     }
     named_arrive(1 + kWsNS + b, kWsThreads);  // EMPTY[b]

@@ -82,7 +82,7 @@ static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
 // the i = 0 list) from kGW0 terms; a DMMA with B = 1 sums the four shares.
 constexpr int kGS1 = 4, kGW0 = 2, kGS = kGS1 + kGW0;
 constexpr int kMaxGroups = 128;      // groups per program
-constexpr int kGroupMaxPlan = 4096;  // plans with more feasible configurations stay dense
+constexpr int kGroupMaxPlan = 2048;  // plans with more feasible configurations stay dense
 struct GroupDesc {
   int32_t tile_begin, tile_end, hv, nmem;  // tiles [tile_begin, tile_end) of the schedule
   int32_t P[3], pad;                       // the members' P (P[hv] unused)

@@ -352,32 +352,70 @@ __global__ void __launch_bounds__(1024) k_plan_groups(const DevProg *progs, int 
   __shared__ int32_t s_slot[kGroupMaxPlan + 8];   // schedule slot -> position in rec (-1: padding)
   __shared__ int8_t s_hv[kGroupMaxPlan + 8];      // slot's Horner variable (-1 dense)
   __shared__ uint8_t s_taken[kGroupMaxPlan];
+  __shared__ int32_t s_P[3][kGroupMaxPlan];       // P_k - 1 of the sorted configurations
   // candidates: a key has >= 8 members, so at most 3 nFc / 8 of them
   constexpr int kMaxCand = 3 * kGroupMaxPlan / 8;
   __shared__ int32_t s_cand[kMaxCand];   // hv << 16 | first member position
   __shared__ int32_t s_csize[kMaxCand];
   __shared__ int32_t s_corder[kMaxCand];
   __shared__ int32_t s_off[3][4][kGS];
-  __shared__ int s_hvok[3], s_ncand, s_ngroups, s_ntiles, s_ngt;
+  __shared__ int32_t s_wsum[32];
+  __shared__ int s_hvok[3], s_ncand, s_ngroups, s_ntiles, s_ngt, s_ns, s_cnt;
   const bool grouping = enable && sorted && pg.p >= 2 && nFc <= kGroupMaxPlan;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   if (threadIdx.x == 0) {
     for (int hv = 0; hv < 3; ++hv) s_hvok[hv] = grouping && hv < pg.p && group_lists(pg, hv, s_off[hv]);
     s_ncand = 0;
+    s_ns = 0;
   }
-  for (int i = threadIdx.x; i < kGroupMaxPlan; i += blockDim.x) s_taken[i] = 0;
+  for (int i = threadIdx.x; i < kGroupMaxPlan; i += blockDim.x) {
+    s_taken[i] = 0;
+    if (grouping && i < nFc) {
+      s_P[0][i] = rec[i].Pm1_0;
+      s_P[1][i] = rec[i].Pm1_1;
+      s_P[2][i] = rec[i].Pm1_2;
+    }
+  }
   __syncthreads();
-  auto same_key = [&](const CfgRec &a, const CfgRec &b, int hv) {
-    return (hv == 0 || a.Pm1_0 == b.Pm1_0) && (hv == 1 || a.Pm1_1 == b.Pm1_1) && (hv == 2 || a.Pm1_2 == b.Pm1_2);
+  auto same_key = [&](int a, int b, int hv) {  // configurations a, b share every P_k, k != hv
+    return (hv == 0 || s_P[0][a] == s_P[0][b]) && (hv == 1 || s_P[1][a] == s_P[1][b]) &&
+           (hv == 2 || s_P[2][a] == s_P[2][b]);
+  };
+  // block-wide exclusive prefix of one count per thread (deterministic; all threads call it)
+  auto block_scan = [&](int v, int &total) {
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int w = lane < nwarp ? s_wsum[lane] : 0;
+      int wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      s_wsum[lane] = wi - w;  // exclusive prefix of the warps
+      if (lane == 31) s_cnt = wi;
+    }
+    __syncthreads();
+    const int ex = s_wsum[wid] + incl - v;
+    total = s_cnt;
+    __syncthreads();
+    return ex;
   };
   if (grouping) {
     for (int hv = 0; hv < 3; ++hv) {
       if (!s_hvok[hv]) continue;
       for (int c = threadIdx.x; c < nFc; c += blockDim.x) {
-        const CfgRec rc = rec[c];
         int n = 0;
         bool first = true;
         for (int j = 0; j < nFc; ++j) {
-          const bool m = same_key(rec[j], rc, hv);
+          const bool m = same_key(j, c, hv);
           n += m;
           first = first && !(m && j < c);
         }
@@ -399,61 +437,69 @@ __global__ void __launch_bounds__(1024) k_plan_groups(const DevProg *progs, int 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {  // greedy assignment and the slot list (serial: n <= kGroupMaxPlan)
-    int ns = 0, ngroups = 0;
-    const int nc = grouping ? s_ncand : 0;
-    for (int r = 0; r < nc && ngroups < kMaxGroups; ++r) {
-      const int cd = s_cand[s_corder[r]], hv = cd >> 16, c0 = cd & 0xffff;
-      const CfgRec rc = rec[c0];
-      int n = 0;
-      for (int j = c0; j < nFc; ++j) n += !s_taken[j] && same_key(rec[j], rc, hv);
-      const int take = n / 8 * 8;
-      if (take == 0) continue;
+  // greedy assignment, one candidate at a time; each thread owns the contiguous positions
+  // [per t, per (t + 1)) so member ranks follow the position order
+  const int per = (nFc + blockDim.x - 1) / blockDim.x;
+  const int p0 = threadIdx.x * per, p1 = min(nFc, p0 + per);
+  int ngroups = 0;
+  const int ncand = grouping ? s_ncand : 0;
+  for (int r = 0; r < ncand && ngroups < kMaxGroups; ++r) {
+    const int cd = s_cand[s_corder[r]], hv = cd >> 16, c0 = cd & 0xffff;
+    int mine = 0;
+    for (int q = p0; q < p1; ++q) mine += q >= c0 && !s_taken[q] && same_key(q, c0, hv);
+    int n;
+    int rank = block_scan(mine, n);
+    const int take = n / 8 * 8;
+    if (take == 0) continue;  // (uniform)
+    const int ns = s_ns;
+    for (int q = p0; q < p1 && rank < take; ++q)
+      if (q >= c0 && !s_taken[q] && same_key(q, c0, hv)) {
+        s_taken[q] = 1;
+        s_slot[ns + rank] = q;
+        s_hv[ns + rank] = (int8_t)hv;
+        ++rank;
+      }
+    if (threadIdx.x == 0) {
       GroupDesc &gd = gdesc[ngroups];
       gd.tile_begin = ns / 8;
+      gd.tile_end = (ns + take) / 8;
       gd.hv = hv;
       gd.nmem = take;
-      gd.P[0] = rc.Pm1_0 + 1;
-      gd.P[1] = rc.Pm1_1 + 1;
-      gd.P[2] = rc.Pm1_2 + 1;
+      gd.P[0] = s_P[0][c0] + 1;
+      gd.P[1] = s_P[1][c0] + 1;
+      gd.P[2] = s_P[2][c0] + 1;
       gd.pad = 0;
       for (int q = 0; q < 4; ++q)
-        for (int s = 0; s < kGS; ++s) gd.off[q][s] = s_off[hv][q][s];
-      int got = 0;
-      for (int j = c0; j < nFc && got < take; ++j)
-        if (!s_taken[j] && same_key(rec[j], rc, hv)) {
-          s_taken[j] = 1;
-          s_slot[ns] = j;
-          s_hv[ns] = (int8_t)hv;
-          ++ns;
-          ++got;
-        }
-      gd.tile_end = ns / 8;
+        for (int t = 0; t < kGS; ++t) gd.off[q][t] = s_off[hv][q][t];
       group_y(pg, gd);
-      ++ngroups;
+      s_ns = ns + take;
     }
-    s_ngt = ns / 8;
-    if (!grouping) {  // dense only: the slots are the sorted table (the sweep reads grec/gmP)
-      for (int j = 0; j < nFc && nFc <= kGroupMaxPlan; ++j) {
-        s_slot[j] = j;
-        s_hv[j] = -1;
+    ++ngroups;
+    __syncthreads();
+  }
+  // the dense remainder in (P1 P2, index) order, then padding to a whole tile
+  if (nFc <= kGroupMaxPlan) {
+    int mine = 0;
+    for (int q = p0; q < p1; ++q) mine += !s_taken[q];
+    int tot;
+    int rank = block_scan(mine, tot);
+    const int ns = s_ns;
+    if (threadIdx.x == 0) s_ngt = ns / 8;
+    for (int q = p0; q < p1; ++q)
+      if (!s_taken[q]) {
+        s_slot[ns + rank] = q;
+        s_hv[ns + rank] = -1;
+        ++rank;
       }
-      ns = nFc;
-    } else {
-      for (int j = 0; j < nFc; ++j)
-        if (!s_taken[j]) {
-          s_slot[ns] = j;
-          s_hv[ns] = -1;
-          ++ns;
-        }
+    int end = ns + tot;
+    for (int t = end + threadIdx.x; t < ((end + 7) & ~7); t += blockDim.x) {
+      s_slot[t] = -1;
+      s_hv[t] = -2;
     }
-    while (ns % 8 && nFc <= kGroupMaxPlan) {
-      s_slot[ns] = -1;
-      s_hv[ns] = -2;
-      ++ns;
+    if (threadIdx.x == 0) {
+      s_ngroups = ngroups;
+      s_ntiles = ((end + 7) & ~7) / 8;
     }
-    s_ngroups = ngroups;
-    s_ntiles = ns / 8;
   }
   __syncthreads();
   const int nslots = s_ntiles * 8;
