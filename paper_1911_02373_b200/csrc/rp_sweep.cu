@@ -267,8 +267,8 @@ __device__ void schedule_slot_mp(const DevProg &pg, const CfgRec &r, int hv, int
     for (int pe = 0; pe < npe_pad; ++pe) col[(int64_t)pe * nGp] = 0.0;
     return;
   }
-  if (hv >= 0) {
-    const double x = prog_u(pg, hv, Pk[hv]);
+  if (hv >= 0) {  // factored slots are hv-major (k_plan_groups): P_hv at position 0
+    const double x = prog_u(pg, hv, Pk[0]);
     double m = 1.0;
     for (int q = 0; q < npe_pad; ++q) {
       m = q < 4 ? m * x : 0.0;
@@ -515,6 +515,22 @@ __global__ void __launch_bounds__(1024) k_plan_groups(const DevProg *progs, int 
     CfgRec r;
     if (pos >= 0) {
       r = rec[pos];
+      if (hv > 0) {  // factored slot, hv-major: P_hv's (P - 1, M, s) at position 0 for the sweep
+        const int32_t Ph = hv == 1 ? r.Pm1_1 : r.Pm1_2;
+        const uint32_t Mh = hv == 1 ? r.M1 : r.M2;
+        const uint32_t sh = (r.s012 >> (8 * hv)) & 255u;
+        if (hv == 1) {
+          r.Pm1_1 = r.Pm1_0;
+          r.M1 = r.M0;
+        } else {
+          r.Pm1_2 = r.Pm1_0;
+          r.M2 = r.M0;
+        }
+        const uint32_t s0 = r.s012 & 255u;
+        r.s012 = (r.s012 & ~(255u | (255u << (8 * hv)))) | sh | (s0 << (8 * hv));
+        r.Pm1_0 = Ph;
+        r.M0 = Mh;
+      }
     } else {
       memset(&r, 0, sizeof(r));
       r.orig = 0x7fffffff;  // zero record: W = 0, 1/B_act = 0, so its E is never a candidate
@@ -640,12 +656,6 @@ struct SweepArgs {
 #endif
 #ifndef RP_GPAIR
 #define RP_GPAIR 0
-#endif
-#ifndef RP_GRID_LEAN
-#define RP_GRID_LEAN 0
-#endif
-#ifndef RP_KEY_F64
-#define RP_KEY_F64 0
 #endif
 #ifndef RP_PREF
 #define RP_PREF 0
@@ -806,7 +816,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   };
 #undef RP_AFR
   // a3, a6, a7, a8 for the 2 pairs of this lane in one tile
-  auto epi_oct = [&](const CfgRec *trec, const double (&acc)[NPOLY][2]) {
+  // fact: a factored tile (grid factors other than P_hv's are the group's fcon; Dv = D_{map[hv]})
+  auto epi_oct = [&](const CfgRec *trec, const double (&acc)[NPOLY][2], bool fact, uint64_t fcon, int32_t Dv) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       // output column 2 (lane % 4) + v; padding slots have zero records (W = 0, 1/B_act = 0),
@@ -826,50 +837,33 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
         const double W = __hiloint2double(h2.w, h2.z);
         // a6: #Blocks = prod ceil(D / P); SM_act = min(#Blocks, n_SM)
         // (each factor is < 2^32: 32-bit factors, 64-bit products only where needed)
-        const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, Pm1_0, (uint32_t)h1.z, s012 & 255) : 1u;
-        const uint32_t f1 = map1 >= 0 ? ceil_div32(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) : 1u;
-#if RP_GRID_LEAN
-        const uint32_t f2 = map2 >= 0 ? ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255) : 1u;
-        // SM_act in 32 bits: a factor >= 1023 >= n_SM already saturates it, and the product of
-        // three factors below 1023 is < 2^30
-        const uint32_t bc = min(f0, 1023u) * min(f1, 1023u) * min(f2, 1023u);
-        const int smact = (int)min(bc, (uint32_t)n_sm);
-        const bool full = smact == n_sm;
-        double rSM = rNSM;
-        if (!full) rSM = sRSM[smact];  // n_SM < kRSMTab for every program (compile_program)
-        uint64_t blocks = (uint64_t)f0 * f1;
-        if (map2 >= 0) blocks *= f2;
-        const double Rep = FAST ? (full ? (double)blocks * h3.x * rNSM : h3.x) : (double)blocks * h3.x * rSM;
-#else
-        int64_t blocks = (int64_t)((uint64_t)f0 * f1);
-        if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+        int64_t blocks;
+        if (fact) {  // factored slot: position 0 holds P_hv; the other factors are the group's
+          blocks = (int64_t)(fcon * ceil_div32(Dv, Pm1_0, (uint32_t)h1.z, s012 & 255));
+        } else {
+          const uint32_t f0 = map0 >= 0 ? ceil_div32(Da, Pm1_0, (uint32_t)h1.z, s012 & 255) : 1u;
+          const uint32_t f1 = map1 >= 0 ? ceil_div32(Db, h1.x, (uint32_t)h1.w, (s012 >> 8) & 255) : 1u;
+          blocks = (int64_t)((uint64_t)f0 * f1);
+          if (map2 >= 0) blocks *= ceil_div32(Dc, h1.y, (uint32_t)h2.x, (s012 >> 16) & 255);
+        }
         const int64_t smact = blocks < n_sm ? blocks : n_sm;
         // (n_SM < kRSMTab for every program, compile_program: the 1/SM_act table exists)
         const double rSM = smact == n_sm ? rNSM : sRSM[smact];
         // line 15: #Blocks / (B_act SM_act)
         const double Rep = FAST ? (smact == n_sm ? (double)blocks * h3.x * rNSM : h3.x) : (double)blocks * h3.x * rSM;
-#endif
         E = mwpcwp_E<FAST>(acc[0][v], acc[1][v], acc[2][v], acc[3][v], acc[4][v], acc[5][v], W, Rep,
                            rSM, (double)smact, kc);
       } else {
         E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
       }
       // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
-#if RP_KEY_F64
-      // a8 on the FP64 pipe: a masked, non-finite or non-positive E never beats the running best
-      // (+inf or a finite positive value); ties go to the lowest index
-      const bool okE = ok && E > 0.0 && E < kInf;
-      const bool better = okE && (E < st.e || (E == st.e && orig < st.i));
-#else
       E = (ok && pos_finite(E)) ? E : kInf;
       // a8: exact lexicographic key (E, original index): ties go to the lowest index (E and the
       // running best are positive or +inf, so their bit patterns compare as integers)
       const long long eb = __double_as_longlong(E), sb = __double_as_longlong(st.e);
       const bool better = eb < sb || (eb == sb && orig < st.i);
-      const bool okE = true;  // (an invalid E is +inf here)
-#endif
       if (SECOND) {  // runner-up on the same exact key
-        const bool sec = !better && okE && key_less(E, orig, st.s, st.j);
+        const bool sec = !better && key_less(E, orig, st.s, st.j);
         st.s = better ? st.e : (sec ? E : st.s);
         st.j = better ? st.i : (sec ? orig : st.j);
       }
@@ -912,6 +906,24 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           a0[k] = s0;
         }
       }
+      // a6 per group: every grid factor but P_hv's is the group's (exact, once per group)
+      uint64_t fcon = 1;
+      int32_t Dv = 1;
+      {
+        const int hv = __ldg(&gd->hv);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int mk = k == 0 ? map0 : (k == 1 ? map1 : map2);
+          if (mk < 0) continue;
+          const int32_t Dk = k == 0 ? Da : (k == 1 ? Db : Dc);
+          if (k == hv) {
+            Dv = Dk;
+          } else {
+            const int64_t Pk = __ldg(&gd->P[k]);
+            fcon *= (uint64_t)(((int64_t)Dk + Pk - 1) / Pk);
+          }
+        }
+      }
       int tend = te;  // members in P1 P2 order: stop at the first tile that fails a3 everywhere
       if (sorted)
         for (int tile = tb + 1; tile < te; ++tile)
@@ -935,8 +947,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           dmma_c(acc2[k][0], acc2[k][1], a0[k], 1.0, 0.0, 0.0);
           dmma(acc2[k][0], acc2[k][1], w1[k], b2);
         }
-        epi_oct(grec + tile * 8, acc);
-        epi_oct(grec + tile * 8 + 8, acc2);
+        epi_oct(grec + tile * 8, acc, true, fcon, Dv);
+        epi_oct(grec + tile * 8 + 8, acc2, true, fcon, Dv);
       }
 #endif
 #if RP_PREF
@@ -956,7 +968,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           dmma_c(acc[k][0], acc[k][1], a0[k], 1.0, 0.0, 0.0);  // w_{k,0} in both columns
           dmma(acc[k][0], acc[k][1], w1[k], b);
         }
-        epi_oct(grec + tile * 8, acc);
+        epi_oct(grec + tile * 8, acc, true, fcon, Dv);
       }
     }
     // dense tiles; a3 early exit: they are sorted by P1 P2, so every tile from the first one whose
@@ -982,14 +994,14 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       load_b(oc + 1, bfr2);
       mma_oct(acc, bfr);
       mma_oct(acc2, bfr2);
-      epi_oct(grec + oc * 8, acc);
-      epi_oct(grec + (oc + 1) * 8, acc2);
+      epi_oct(grec + oc * 8, acc, false, 1ull, 1);
+      epi_oct(grec + (oc + 1) * 8, acc2, false, 1ull, 1);
     }
     if (oc < nEff) {
       double acc[NPOLY][2], bfr[KS];
       load_b(oc, bfr);
       mma_oct(acc, bfr);
-      epi_oct(grec + oc * 8, acc);
+      epi_oct(grec + oc * 8, acc, false, 1ull, 1);
     }
   }
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
