@@ -510,6 +510,266 @@ static int pow2_ceil(int x) {
   return p;
 }
 
+// ============================================================================================
+// k_tsqr_b -- the blocked form of k_tsqr (RP_TSQR_KERNEL=blocked; work in progress: 77.8 ms with
+// the scalar trailing update below, which is shared-memory bound, against 34.2 for the wavefront).
+// Same slabs, chunks and tree as k_tsqr, but each chunk C (96 design rows, row-major in shared
+// memory) is absorbed into [R; C] panel by panel (8 columns): one warp factors the panel with
+// its 96 x 8 entries in registers (the column chain runs inside the warp: shuffle reductions,
+// no cross-warp hand-off), forms the compact-WY factor T (H_0 ... H_7 = I - V T V^T, the unit
+// parts of the reflectors on R's rows c0 .. c0 + 7, their C parts in V), and then every thread
+// applies the block reflector to the trailing columns: Y = V^T [R; C], Z = T^T Y,
+// [R; C] -= V Z (LAPACK's dlarft / dlarfb, forward columnwise).
+// ============================================================================================
+constexpr int kTbThreads = 512;
+constexpr int kTbPW = 8;                 // panel width
+constexpr int kTbLdC = kSvdMaxCols | 1;  // C row stride (odd)
+
+__host__ __device__ inline size_t tsqr_b_smem(int nc) {
+  return (size_t)((packed_size(nc) + 1) & ~1ll) * 8 + (size_t)kChunk * kTbLdC * 8 + (size_t)kChunk * kTbPW * 8 +
+         (kTbPW * kTbPW + kTbPW) * 8 + 64;
+}
+
+// batched sum over the warp of NV values (xor butterfly: every lane gets every sum)
+template <int NV>
+__device__ __forceinline__ void warp_sum_n(double (&x)[NV]) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], o);
+}
+
+// absorb C (rows 0 .. kChunk-1 of sC; zero rows beyond the data) into the packed R
+__device__ void absorb_chunk_b(double *Rp, double *sC, double *sV, double *sT, double *sTau, int nc) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < nc; c0 += kTbPW) {
+    const int w = min(kTbPW, nc - c0), c1 = c0 + w;
+    if (wid == 0) {
+      // ---- panel: columns c0 .. c1-1 of [R; C], in registers (lane: rows lane + 32 t) --------
+      double pc[3][kTbPW];
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int j = 0; j < kTbPW; ++j) pc[t][j] = j < w ? sC[(lane + 32 * t) * kTbLdC + c0 + j] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kTbPW; ++j) {
+        if (j >= w) break;
+        double s2[1] = {0.0};
+#pragma unroll
+        for (int t = 0; t < 3; ++t) s2[0] = fma(pc[t][j], pc[t][j], s2[0]);
+        warp_sum_n<1>(s2);
+        double *rjj = Rp + packed_off(c0 + j, nc);
+        double tau, beta, sc;
+        householder_params(*rjj, s2[0], tau, beta, sc);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          pc[t][j] *= sc;
+          sV[(lane + 32 * t) * kTbPW + j] = pc[t][j];
+        }
+        // reflector j on the panel's columns k > j: dot_k = R[c0+j][c0+k] + v^T C[:, c0+k]
+        double d[kTbPW];
+#pragma unroll
+        for (int k = 0; k < kTbPW; ++k) {
+          d[k] = 0.0;
+          if (k > j)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) d[k] = fma(pc[t][j], pc[t][k], d[k]);
+        }
+        warp_sum_n<kTbPW>(d);
+#pragma unroll
+        for (int k = 0; k < kTbPW; ++k) {
+          if (k > j && k < w) {
+            double *rjk = rjj + (k - j);  // R[c0+j][c0+k] (packed row c0+j starts at its diagonal)
+            const double tw = tau * (*rjk + d[k]);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) pc[t][k] = fma(-tw, pc[t][j], pc[t][k]);
+            __syncwarp();
+            if (lane == 0) *rjk -= tw;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          *rjj = beta;
+          sTau[j] = tau;
+        }
+      }
+      // ---- T (dlarft, forward columnwise): G[m][i] = v_m^T v_i (C parts; the unit parts sit
+      // on distinct rows of R), T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i] ----
+      double g[kTbPW * (kTbPW - 1) / 2];
+      {
+        int q = 0;
+#pragma unroll
+        for (int i = 1; i < kTbPW; ++i)
+#pragma unroll
+          for (int m = 0; m < i; ++m, ++q) {
+            g[q] = 0.0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) g[q] = fma(pc[t][m], pc[t][i], g[q]);
+          }
+      }
+      warp_sum_n<kTbPW * (kTbPW - 1) / 2>(g);
+      __syncwarp();
+      if (lane == 0) {
+        for (int i = 0; i < kTbPW; ++i)
+          for (int j = 0; j < kTbPW; ++j) sT[j * kTbPW + i] = 0.0;
+        int q = 0;
+        for (int i = 0; i < w; ++i) {
+          const double ti = sTau[i];
+          sT[i * kTbPW + i] = ti;
+          // column i above the diagonal: -tau_i T[0:i,0:i] G[0:i,i]  (G[0:i,i] = g[q .. q+i-1])
+          for (int jr = 0; jr < i; ++jr) {
+            double acc = 0.0;
+            for (int m = jr; m < i; ++m) acc = fma(sT[jr * kTbPW + m], g[q + m], acc);
+            sT[jr * kTbPW + i] = -ti * acc;
+          }
+          q += i;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- trailing columns c1 .. nc-1: four threads per column (rows q, q + 4, ...) ---------
+    for (int cbase = c1; cbase < nc; cbase += kTbThreads / 4) {
+      const int col = cbase + (threadIdx.x >> 2), q = threadIdx.x & 3;
+      const bool on = col < nc;  // (whole quads are on or off: the shuffles stay in the quad)
+      double y[kTbPW];
+#pragma unroll
+      for (int j = 0; j < kTbPW; ++j) y[j] = 0.0;
+      if (on)
+        for (int r = q; r < kChunk; r += 4) {
+          const double cv = sC[r * kTbLdC + col];
+#pragma unroll
+          for (int j = 0; j < kTbPW; ++j) y[j] = fma(sV[r * kTbPW + j], cv, y[j]);
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < kTbPW; ++j) y[j] += __shfl_xor_sync(0xffffffffu, y[j], o);
+      double z[kTbPW];
+      if (on) {
+#pragma unroll
+        for (int j = 0; j < kTbPW; ++j) y[j] = j < w ? y[j] + Rp[packed_off(c0 + j, nc) + (col - c0 - j)] : 0.0;
+        // Z = T^T Y (T upper triangular: Z[i] = sum_{j <= i} T[j][i] Y[j])
+#pragma unroll
+        for (int i = 0; i < kTbPW; ++i) {
+          double a = 0.0;
+#pragma unroll
+          for (int j = 0; j <= i; ++j) a = fma(sT[j * kTbPW + i], y[j], a);
+          z[i] = a;
+        }
+        if (q == 0)
+#pragma unroll
+          for (int j = 0; j < kTbPW; ++j)
+            if (j < w) Rp[packed_off(c0 + j, nc) + (col - c0 - j)] -= z[j];
+        for (int r = q; r < kChunk; r += 4) {
+          double a = sC[r * kTbLdC + col];
+#pragma unroll
+          for (int j = 0; j < kTbPW; ++j) a = fma(-sV[r * kTbPW + j], z[j], a);
+          sC[r * kTbLdC + col] = a;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kTbThreads, 1) k_tsqr_b(TsqrArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nc = a.nc, n = a.n;
+  const int64_t psz = packed_size(nc);
+  double *Rp = sm;
+  double *sC = Rp + ((psz + 1) & ~1ll);
+  double *sV = sC + (size_t)kChunk * kTbLdC;
+  double *sT = sV + (size_t)kChunk * kTbPW;
+  double *sTau = sT + kTbPW * kTbPW;
+  int *flag = (int *)(sTau + kTbPW);
+  const int metric = blockIdx.y;
+  const int leaf = blockIdx.x;
+
+  for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) Rp[i] = 0.0;
+  __syncthreads();
+  const int64_t r_begin = a.K * leaf / a.leaves, r_end = a.K * (leaf + 1) / a.leaves;
+  const double *V = a.V ? a.V + (int64_t)metric * a.K : nullptr;
+  const double *S = a.S ? a.S + (int64_t)metric * a.K : nullptr;
+  const double *rows = a.rows ? a.rows + (int64_t)metric * a.K * nc : nullptr;
+  const GramBasis *B = a.basis;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kChunk) {
+    const int cnt = (int)((r_end - r0) < kChunk ? (r_end - r0) : kChunk);
+    // a10 + a11: the chunk's design rows (one thread per entry; rows beyond cnt are zero)
+    for (int idx = threadIdx.x; idx < kChunk * nc; idx += blockDim.x) {
+      const int r = idx / nc, col = idx % nc;
+      double m = 0.0;
+      if (r < cnt) {
+        const int64_t row = r0 + r;
+        if (rows) {
+          m = rows[row * nc + col];
+        } else {
+          m = 1.0;
+          for (int t = 0; t < n; ++t) {
+            const int e = B->exp[col][t];
+            if (e) {
+              const double u = (a.X[row * n + t] - B->xc[t]) * ldexp(1.0, -B->xe[t]);
+              for (int q = 0; q < e; ++q) m *= u;
+            }
+          }
+          if (col >= B->n_num) m *= -V[row];
+          if (S) m *= S[row];
+        }
+      }
+      sC[r * kTbLdC + col] = m;
+    }
+    __syncthreads();
+    absorb_chunk_b(Rp, sC, sV, sT, sTau, nc);
+  }
+  // ---- tree merge (as k_tsqr) ---------------------------------------------------------------
+  double *slots = a.slots + (int64_t)metric * 2 * a.P * psz;
+  unsigned *cntr = a.counters + (int64_t)metric * 2 * a.P;
+  int node = a.P + leaf, h = 0;
+  while (node > 1) {
+    const int sib = node ^ 1;
+    if ((int64_t)(sib << h) - a.P >= a.leaves) {  // no leaf under the sibling: pass through
+      node >>= 1;
+      ++h;
+      continue;
+    }
+    double *mine = slots + (int64_t)node * psz;
+    for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) mine[i] = Rp[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned old = atomicAdd(&cntr[node >> 1], 1u);
+      if (old == 1u) {
+        cntr[node >> 1] = 0u;  // both children arrived: reset for the next call
+        __threadfence();
+      }
+      *flag = (int)old;
+    }
+    __syncthreads();
+    if (*flag == 0) return;  // first to arrive: the sibling's CTA continues
+    const double *other = slots + (int64_t)sib * psz;
+    const double *R2 = other;
+    if (node & 1) {  // right child: R := R_left, then absorb my own rows
+      for (int64_t i = threadIdx.x; i < psz; i += blockDim.x) Rp[i] = __ldcg(other + i);
+      R2 = mine;
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < nc; r0 += kChunk) {  // R2's rows as chunks
+      for (int idx = threadIdx.x; idx < kChunk * nc; idx += blockDim.x) {
+        const int r = idx / nc, col = idx % nc, rho = r0 + r;
+        sC[r * kTbLdC + col] = (rho < nc && col >= rho) ? __ldcg(R2 + packed_off(rho, nc) + (col - rho)) : 0.0;
+      }
+      __syncthreads();
+      absorb_chunk_b(Rp, sC, sV, sT, sTau, nc);
+    }
+    node >>= 1;
+    ++h;
+  }
+  double *Ro = a.R_out + (int64_t)metric * nc * nc;
+  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
+    const int r = i / nc, col = i % nc;
+    Ro[i] = col >= r ? Rp[packed_off(r, nc) + (col - r)] : 0.0;
+  }
+}
+
 int tsqr_leaves(int64_t K, int n_v) {
   const int64_t want = (K + kChunk - 1) / kChunk;
   int cap = num_sms() / (n_v > 0 ? n_v : 1);
@@ -550,6 +810,14 @@ cudaError_t launch_tsqr(const GramBasis *d_basis, const double *X, const double 
   a.R_out = R_out;
   cudaError_t e = cudaMemsetAsync(a.counters, 0, (size_t)n_v * 2 * P * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
+  const char *kv = getenv("RP_TSQR_KERNEL");
+  if (kv && strcmp(kv, "blocked") == 0) {
+    const size_t smb = tsqr_b_smem(nc);
+    e = cudaFuncSetAttribute(k_tsqr_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+    if (e != cudaSuccess) return e;
+    k_tsqr_b<<<dim3(leaves, n_v), kTbThreads, smb, s>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = tsqr_smem(nc);
   e = cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
