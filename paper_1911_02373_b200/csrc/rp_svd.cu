@@ -27,6 +27,7 @@
 
 #include "rp_internal.cuh"
 #include "rp_umma.cuh"
+#include "rp_device.cuh"
 
 namespace rp {
 
@@ -511,23 +512,24 @@ static int pow2_ceil(int x) {
 }
 
 // ============================================================================================
-// k_tsqr_b -- the blocked form of k_tsqr (RP_TSQR_KERNEL=blocked; work in progress: 77.8 ms with
-// the scalar trailing update below, which is shared-memory bound, against 34.2 for the wavefront).
+// k_tsqr_b -- the blocked form of k_tsqr (RP_TSQR_KERNEL=blocked; measured 44.2 ms for fit_svd
+// against 34.2 with the wavefront k_tsqr: the one-warp panel factorisation, ~6-8k cycles per
+// 8 columns, is the critical path and the other warps wait at the panel barrier).
 // Same slabs, chunks and tree as k_tsqr, but each chunk C (96 design rows, row-major in shared
 // memory) is absorbed into [R; C] panel by panel (8 columns): one warp factors the panel with
 // its 96 x 8 entries in registers (the column chain runs inside the warp: shuffle reductions,
 // no cross-warp hand-off), forms the compact-WY factor T (H_0 ... H_7 = I - V T V^T, the unit
-// parts of the reflectors on R's rows c0 .. c0 + 7, their C parts in V), and then every thread
-// applies the block reflector to the trailing columns: Y = V^T [R; C], Z = T^T Y,
-// [R; C] -= V Z (LAPACK's dlarft / dlarfb, forward columnwise).
+// parts of the reflectors on R's rows c0 .. c0 + 7, their C parts in V), and the block reflector
+// goes to the trailing columns on DMMA, one 8-column tile per warp: Y = V^T [R; C], Z = T^T Y,
+// [R; C] -= V Z (LAPACK's dlarft / dlarfb, forward columnwise), with a one-panel look-ahead.
 // ============================================================================================
 constexpr int kTbThreads = 512;
 constexpr int kTbPW = 8;                 // panel width
-constexpr int kTbLdC = kSvdMaxCols | 1;  // C row stride (odd)
+constexpr int kTbLdC = (kSvdMaxCols + 8) | 1;  // C row stride (odd; room for a last column tile)
 
 __host__ __device__ inline size_t tsqr_b_smem(int nc) {
-  return (size_t)((packed_size(nc) + 1) & ~1ll) * 8 + (size_t)kChunk * kTbLdC * 8 + (size_t)kChunk * kTbPW * 8 +
-         (kTbPW * kTbPW + kTbPW) * 8 + 64;
+  return (size_t)((packed_size(nc) + 1) & ~1ll) * 8 + (size_t)kChunk * kTbLdC * 8 + 2 * (size_t)kChunk * kTbPW * 8 +
+         2 * kTbPW * kTbPW * 8 + 64;
 }
 
 // batched sum over the warp of NV values (xor butterfly: every lane gets every sum)
@@ -539,134 +541,174 @@ __device__ __forceinline__ void warp_sum_n(double (&x)[NV]) {
     for (int i = 0; i < NV; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], o);
 }
 
-// absorb C (rows 0 .. kChunk-1 of sC; zero rows beyond the data) into the packed R
-__device__ void absorb_chunk_b(double *Rp, double *sC, double *sV, double *sT, double *sTau, int nc) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c0 = 0; c0 < nc; c0 += kTbPW) {
-    const int w = min(kTbPW, nc - c0), c1 = c0 + w;
-    if (wid == 0) {
-      // ---- panel: columns c0 .. c1-1 of [R; C], in registers (lane: rows lane + 32 t) --------
-      double pc[3][kTbPW];
+// Panel factorisation by one warp: columns c0 .. c0 + w - 1 of [R; C] (lane: C rows lane + 32 t
+// in registers).  Writes V (the reflectors' C parts, zero beyond w), tau, T (compact WY,
+// row-major 8 x 8) and R's panel rows at the panel's columns.
+__device__ void tb_panel(double *Rp, const double *sC, double *sV, double *sT, int nc, int c0, int w) {
+  const int lane = threadIdx.x & 31;
+  double pc[3][kTbPW];
 #pragma unroll
-      for (int t = 0; t < 3; ++t)
+  for (int t = 0; t < 3; ++t)
 #pragma unroll
-        for (int j = 0; j < kTbPW; ++j) pc[t][j] = j < w ? sC[(lane + 32 * t) * kTbLdC + c0 + j] : 0.0;
+    for (int j = 0; j < kTbPW; ++j) pc[t][j] = j < w ? sC[(lane + 32 * t) * kTbLdC + c0 + j] : 0.0;
+  double tauv[kTbPW];
 #pragma unroll
-      for (int j = 0; j < kTbPW; ++j) {
-        if (j >= w) break;
-        double s2[1] = {0.0};
+  for (int j = 0; j < kTbPW; ++j) {
+    tauv[j] = 0.0;
+    if (j >= w) continue;
+    double *rr = Rp + packed_off(c0 + j, nc) - (c0 + j);  // rr[c] = R[c0 + j][c]
+    double rk[kTbPW];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) s2[0] = fma(pc[t][j], pc[t][j], s2[0]);
-        warp_sum_n<1>(s2);
-        double *rjj = Rp + packed_off(c0 + j, nc);
-        double tau, beta, sc;
-        householder_params(*rjj, s2[0], tau, beta, sc);
+    for (int k = 0; k < kTbPW; ++k) rk[k] = (k >= j && k < w) ? rr[c0 + k] : 0.0;  // (issued early)
+    double s2[1] = {0.0};
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          pc[t][j] *= sc;
-          sV[(lane + 32 * t) * kTbPW + j] = pc[t][j];
-        }
-        // reflector j on the panel's columns k > j: dot_k = R[c0+j][c0+k] + v^T C[:, c0+k]
-        double d[kTbPW];
+    for (int t = 0; t < 3; ++t) s2[0] = fma(pc[t][j], pc[t][j], s2[0]);
+    warp_sum_n<1>(s2);
+    double tau, beta, sc;
+    householder_params(rk[j], s2[0], tau, beta, sc);
+    tauv[j] = tau;
 #pragma unroll
-        for (int k = 0; k < kTbPW; ++k) {
-          d[k] = 0.0;
-          if (k > j)
+    for (int t = 0; t < 3; ++t) pc[t][j] *= sc;
+    // reflector j on the panel's columns k > j: dot_k = R[c0+j][c0+k] + v^T C[:, c0+k]
+    double d[kTbPW];
 #pragma unroll
-            for (int t = 0; t < 3; ++t) d[k] = fma(pc[t][j], pc[t][k], d[k]);
-        }
-        warp_sum_n<kTbPW>(d);
+    for (int k = 0; k < kTbPW; ++k) {
+      d[k] = 0.0;
+      if (k > j)
 #pragma unroll
-        for (int k = 0; k < kTbPW; ++k) {
-          if (k > j && k < w) {
-            double *rjk = rjj + (k - j);  // R[c0+j][c0+k] (packed row c0+j starts at its diagonal)
-            const double tw = tau * (*rjk + d[k]);
-#pragma unroll
-            for (int t = 0; t < 3; ++t) pc[t][k] = fma(-tw, pc[t][j], pc[t][k]);
-            __syncwarp();
-            if (lane == 0) *rjk -= tw;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          *rjj = beta;
-          sTau[j] = tau;
-        }
-      }
-      // ---- T (dlarft, forward columnwise): G[m][i] = v_m^T v_i (C parts; the unit parts sit
-      // on distinct rows of R), T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i] ----
-      double g[kTbPW * (kTbPW - 1) / 2];
-      {
-        int q = 0;
-#pragma unroll
-        for (int i = 1; i < kTbPW; ++i)
-#pragma unroll
-          for (int m = 0; m < i; ++m, ++q) {
-            g[q] = 0.0;
-#pragma unroll
-            for (int t = 0; t < 3; ++t) g[q] = fma(pc[t][m], pc[t][i], g[q]);
-          }
-      }
-      warp_sum_n<kTbPW * (kTbPW - 1) / 2>(g);
-      __syncwarp();
-      if (lane == 0) {
-        for (int i = 0; i < kTbPW; ++i)
-          for (int j = 0; j < kTbPW; ++j) sT[j * kTbPW + i] = 0.0;
-        int q = 0;
-        for (int i = 0; i < w; ++i) {
-          const double ti = sTau[i];
-          sT[i * kTbPW + i] = ti;
-          // column i above the diagonal: -tau_i T[0:i,0:i] G[0:i,i]  (G[0:i,i] = g[q .. q+i-1])
-          for (int jr = 0; jr < i; ++jr) {
-            double acc = 0.0;
-            for (int m = jr; m < i; ++m) acc = fma(sT[jr * kTbPW + m], g[q + m], acc);
-            sT[jr * kTbPW + i] = -ti * acc;
-          }
-          q += i;
-        }
-      }
+        for (int t = 0; t < 3; ++t) d[k] = fma(pc[t][j], pc[t][k], d[k]);
     }
-    __syncthreads();
-    // ---- trailing columns c1 .. nc-1: four threads per column (rows q, q + 4, ...) ---------
-    for (int cbase = c1; cbase < nc; cbase += kTbThreads / 4) {
-      const int col = cbase + (threadIdx.x >> 2), q = threadIdx.x & 3;
-      const bool on = col < nc;  // (whole quads are on or off: the shuffles stay in the quad)
-      double y[kTbPW];
+    warp_sum_n<kTbPW>(d);
+    double tw[kTbPW];
 #pragma unroll
-      for (int j = 0; j < kTbPW; ++j) y[j] = 0.0;
-      if (on)
-        for (int r = q; r < kChunk; r += 4) {
-          const double cv = sC[r * kTbLdC + col];
+    for (int k = 0; k < kTbPW; ++k) {
+      tw[k] = (k > j && k < w) ? tau * (rk[k] + d[k]) : 0.0;
 #pragma unroll
-          for (int j = 0; j < kTbPW; ++j) y[j] = fma(sV[r * kTbPW + j], cv, y[j]);
-        }
+      for (int t = 0; t < 3; ++t) pc[t][k] = fma(-tw[k], pc[t][j], pc[t][k]);
+    }
+    __syncwarp();  // every lane has read R[c0 + j][.]
+    if (lane == j) rr[c0 + j] = beta;
 #pragma unroll
-      for (int o = 1; o <= 2; o <<= 1)
+    for (int k = 0; k < kTbPW; ++k)
+      if (lane == k && k > j && k < w) rr[c0 + k] = rk[k] - tw[k];
+  }
 #pragma unroll
-        for (int j = 0; j < kTbPW; ++j) y[j] += __shfl_xor_sync(0xffffffffu, y[j], o);
-      double z[kTbPW];
-      if (on) {
+  for (int t = 0; t < 3; ++t)
 #pragma unroll
-        for (int j = 0; j < kTbPW; ++j) y[j] = j < w ? y[j] + Rp[packed_off(c0 + j, nc) + (col - c0 - j)] : 0.0;
-        // Z = T^T Y (T upper triangular: Z[i] = sum_{j <= i} T[j][i] Y[j])
+    for (int j = 0; j < kTbPW; ++j) sV[(lane + 32 * t) * kTbPW + j] = j < w ? pc[t][j] : 0.0;
+  // T (dlarft, forward columnwise): G[m][i] = v_m^T v_i (the unit parts sit on distinct R rows),
+  // T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i]; lane jr keeps row jr of T
+  double g[kTbPW * (kTbPW - 1) / 2];
+  {
+    int q = 0;
 #pragma unroll
-        for (int i = 0; i < kTbPW; ++i) {
-          double a = 0.0;
+    for (int i = 1; i < kTbPW; ++i)
 #pragma unroll
-          for (int j = 0; j <= i; ++j) a = fma(sT[j * kTbPW + i], y[j], a);
-          z[i] = a;
-        }
-        if (q == 0)
+      for (int m = 0; m < i; ++m, ++q) {
+        g[q] = 0.0;
 #pragma unroll
-          for (int j = 0; j < kTbPW; ++j)
-            if (j < w) Rp[packed_off(c0 + j, nc) + (col - c0 - j)] -= z[j];
-        for (int r = q; r < kChunk; r += 4) {
-          double a = sC[r * kTbLdC + col];
-#pragma unroll
-          for (int j = 0; j < kTbPW; ++j) a = fma(-sV[r * kTbPW + j], z[j], a);
-          sC[r * kTbLdC + col] = a;
-        }
+        for (int t = 0; t < 3; ++t) g[q] = fma(pc[t][m], pc[t][i], g[q]);
       }
+  }
+  warp_sum_n<kTbPW * (kTbPW - 1) / 2>(g);
+  double trow[kTbPW];
+#pragma unroll
+  for (int i = 0; i < kTbPW; ++i) trow[i] = 0.0;
+  {
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < kTbPW; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < kTbPW; ++m)
+        if (m < i) acc = fma(lane <= m ? trow[m] : 0.0, g[q + m], acc);  // T[jr][m] = 0 for m < jr
+      trow[i] = lane == i ? tauv[i] : (lane < i ? -tauv[i] * acc : 0.0);
+      q += i;
+    }
+  }
+  if (lane < kTbPW)
+#pragma unroll
+    for (int i = 0; i < kTbPW; ++i) sT[lane * kTbPW + i] = trow[i];
+}
+
+// One 8-column trailing tile (columns col0 .. col0 + 7) by one warp, with the panel's V and T:
+// Y = V^T C + R_panel (DMMA, two chains), Z = T^T Y (shuffles), R_panel -= Z, C -= V Z (DMMA).
+__device__ void tb_tile(double *Rp, double *sC, const double *sV, const double *sT, int nc, int c0, int w, int col0) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, q = lane & 3;
+  const int ca = col0 + 2 * q, cb = ca + 1;  // this lane's accumulator columns
+  double y0 = 0.0, y1 = 0.0, u0 = 0.0, u1 = 0.0;
+  if (r < w) {
+    const double *rr = Rp + packed_off(c0 + r, nc) - (c0 + r);
+    if (ca < nc) y0 = rr[ca];
+    if (cb < nc) y1 = rr[cb];
+  }
+#pragma unroll 4
+  for (int ks = 0; ks < kChunk / 4; ks += 2) {
+    const double a0 = sV[(ks * 4 + q) * kTbPW + r], b0 = sC[(ks * 4 + q) * kTbLdC + col0 + r];
+    const double a1 = sV[(ks * 4 + 4 + q) * kTbPW + r], b1 = sC[(ks * 4 + 4 + q) * kTbLdC + col0 + r];
+    dmma(y0, y1, a0, b0);
+    dmma(u0, u1, a1, b1);
+  }
+  y0 += u0;
+  y1 += u1;
+  // Z[r][c] = sum_{j <= r} T[j][r] Y[j][c]: Y[j][2q..2q+1] sits in lane 4 j + q
+  double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < kTbPW; ++jj) {
+    const double yj0 = __shfl_sync(0xffffffffu, y0, 4 * jj + q);
+    const double yj1 = __shfl_sync(0xffffffffu, y1, 4 * jj + q);
+    if (jj <= r) {
+      const double t = sT[jj * kTbPW + r];
+      z0 = fma(t, yj0, z0);
+      z1 = fma(t, yj1, z1);
+    }
+  }
+  if (r < w) {
+    double *rr = Rp + packed_off(c0 + r, nc) - (c0 + r);
+    if (ca < nc) rr[ca] -= z0;
+    if (cb < nc) rr[cb] -= z1;
+  }
+  // B fragments of Z for C -= V Z: lane (r, q) needs Z[4 h + q][r], held by lane
+  // 4 (4 h + q) + r / 2 in slot r % 2
+  double bz[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int src = 4 * (4 * h + q) + (r >> 1);
+    const double s0 = __shfl_sync(0xffffffffu, z0, src), s1 = __shfl_sync(0xffffffffu, z1, src);
+    bz[h] = (r & 1) ? s1 : s0;
+  }
+#pragma unroll 2
+  for (int mt = 0; mt < kChunk / 8; ++mt) {
+    double *cr = sC + (mt * 8 + r) * kTbLdC + col0 + 2 * q;
+    double d0 = cr[0], d1 = cr[1];
+    const double va = -sV[(mt * 8 + r) * kTbPW + q], vb = -sV[(mt * 8 + r) * kTbPW + 4 + q];
+    dmma(d0, d1, va, bz[0]);
+    dmma(d0, d1, vb, bz[1]);
+    cr[0] = d0;
+    cr[1] = d1;
+  }
+}
+
+// absorb C (rows 0 .. kChunk-1 of sC; zero rows beyond the data) into the packed R, with a
+// look-ahead of one panel: while warps 1.. apply panel p to the trailing tiles 1.., warp 0
+// applies it to tile 0 (panel p + 1's columns) and factors panel p + 1 (V, T double-buffered)
+__device__ void absorb_chunk_b(double *Rp, double *sC, double *sV, double *sT, int nc) {
+  const int wid = threadIdx.x >> 5, nw = kTbThreads / 32;
+  if (wid == 0) tb_panel(Rp, sC, sV, sT, nc, 0, min(kTbPW, nc));
+  __syncthreads();
+  for (int p = 0, c0 = 0; c0 < nc; ++p, c0 += kTbPW) {
+    const int w = min(kTbPW, nc - c0), c1 = c0 + w;
+    const double *V = sV + (p & 1) * kChunk * kTbPW, *T = sT + (p & 1) * kTbPW * kTbPW;
+    const int ntile = (nc - c1 + 7) / 8;
+    if (wid == 0) {
+      if (ntile > 0) {
+        tb_tile(Rp, sC, V, T, nc, c0, w, c1);
+        __syncwarp();
+        tb_panel(Rp, sC, sV + ((p + 1) & 1) * kChunk * kTbPW, sT + ((p + 1) & 1) * kTbPW * kTbPW, nc, c1,
+                 min(kTbPW, nc - c1));
+      }
+    } else {
+      for (int tt = wid; tt < ntile; tt += nw - 1) tb_tile(Rp, sC, V, T, nc, c0, w, c1 + 8 * tt);
     }
     __syncthreads();
   }
@@ -678,10 +720,9 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tsqr_b(TsqrArgs a) {
   const int64_t psz = packed_size(nc);
   double *Rp = sm;
   double *sC = Rp + ((psz + 1) & ~1ll);
-  double *sV = sC + (size_t)kChunk * kTbLdC;
-  double *sT = sV + (size_t)kChunk * kTbPW;
-  double *sTau = sT + kTbPW * kTbPW;
-  int *flag = (int *)(sTau + kTbPW);
+  double *sV = sC + (size_t)kChunk * kTbLdC;      // [2][kChunk][8]  V of the current / next panel
+  double *sT = sV + 2 * (size_t)kChunk * kTbPW;   // [2][8][8]
+  int *flag = (int *)(sT + 2 * kTbPW * kTbPW);
   const int metric = blockIdx.y;
   const int leaf = blockIdx.x;
 
@@ -718,7 +759,7 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tsqr_b(TsqrArgs a) {
       sC[r * kTbLdC + col] = m;
     }
     __syncthreads();
-    absorb_chunk_b(Rp, sC, sV, sT, sTau, nc);
+    absorb_chunk_b(Rp, sC, sV, sT, nc);
   }
   // ---- tree merge (as k_tsqr) ---------------------------------------------------------------
   double *slots = a.slots + (int64_t)metric * 2 * a.P * psz;
@@ -758,7 +799,7 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tsqr_b(TsqrArgs a) {
         sC[r * kTbLdC + col] = (rho < nc && col >= rho) ? __ldcg(R2 + packed_off(rho, nc) + (col - rho)) : 0.0;
       }
       __syncthreads();
-      absorb_chunk_b(Rp, sC, sV, sT, sTau, nc);
+      absorb_chunk_b(Rp, sC, sV, sT, nc);
     }
     node >>= 1;
     ++h;
