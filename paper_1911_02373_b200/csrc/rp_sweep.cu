@@ -737,18 +737,33 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double *Cm = a.tab.Cmat + (int64_t)g * kMaxPolys * NPE * ndp;
     constexpr int MT = NPOLY * NPE / 8;  // 8-row tiles of the staging matrix
-    constexpr int NT = kTD / 8;          // 8-tuple tiles
-    for (int tile = wid; tile < MT * NT; tile += kSweepWarps) {
-      const int mt = tile / NT, nt = tile % NT;
-      double c0 = 0.0, c1 = 0.0;
-      for (int ks = 0; ks < ndp / 4; ++ks) {
-        const double av = __ldg(Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + ks * 4 + (lane & 3));
-        const double bv = sMD[(nt * 8 + (lane >> 2)) * nde + ks * 4 + (lane & 3)];
-        dmma(c0, c1, av, bv);
+    constexpr int NT = kTD / 8;          // 8-tuple tiles (= kSweepWarps)
+    // a warp takes whole row tiles: each A fragment (from the plan's matrix, L2) is loaded once
+    // and used for the NT tuple tiles, and a row tile's k-step loads are issued together
+    for (int mt = wid; mt < MT; mt += kSweepWarps) {
+      const double *ca = Cm + (int64_t)(mt * 8 + (lane >> 2)) * ndp + (lane & 3);
+      double c0[NT], c1[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) c0[nt] = c1[nt] = 0.0;
+      for (int ks0 = 0; ks0 < ndp / 4; ks0 += 4) {
+        double av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = ks0 + u < ndp / 4 ? __ldg(ca + (ks0 + u) * 4) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (ks0 + u >= ndp / 4) break;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            dmma(c0[nt], c1[nt], av[u], sMD[(nt * 8 + (lane >> 2)) * nde + (ks0 + u) * 4 + (lane & 3)]);
+        }
       }
-      const int row = mt * 8 + (lane >> 2), t = nt * 8 + 2 * (lane & 3);
-      sC[t * CS + row] = c0;
-      sC[(t + 1) * CS + row] = c1;
+      const int row = mt * 8 + (lane >> 2);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int t = nt * 8 + 2 * (lane & 3);
+        sC[t * CS + row] = c0[nt];
+        sC[(t + 1) * CS + row] = c1[nt];
+      }
     }
   }
   __syncthreads();
