@@ -1630,8 +1630,8 @@ static cudaError_t launch3(const SweepArgs &a, int n_prog, int n_sm_max, cudaStr
 template <int NPE>
 static cudaError_t launch_npe(const SweepArgs &a, int n_prog, bool mwp, int n_sm_max, cudaStream_t s) {
   const bool second = a.secondE != nullptr;
-  // RP_SWEEP_KERNEL=ws: the warp-specialised screened sweep (MWP-CWP programs; parity-tested, not
-  // yet faster: DESIGN.md "Warp-specialised screened sweep"); default: k_sweep
+  // RP_SWEEP_KERNEL=tc: the tensor-core screened sweep (MWP-CWP programs with nPE <= 16 and no
+  // runner-up); default: k_sweep
   const char *kern = getenv("RP_SWEEP_KERNEL");
   if (NPE == kTcNPE && mwp && !second && kern && strcmp(kern, "tc") == 0 && a.tab.nde_pad <= kTcMaxNdp &&
       num_sms() <= kTcMaxSM)
