@@ -654,12 +654,6 @@ struct SweepArgs {
 #ifndef RP_SWEEP_MINB
 #define RP_SWEEP_MINB 4
 #endif
-#ifndef RP_GPAIR
-#define RP_GPAIR 0
-#endif
-#ifndef RP_PREF
-#define RP_PREF 0
-#endif
 constexpr int kSweepWarps = 4;
 constexpr int kSweepThreads = 32 * kSweepWarps;
 constexpr int kTD = 8 * kSweepWarps;  // tuples per CTA: one octet (the DMMA M side) per warp
@@ -947,36 +941,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
             break;
           }
       int tile = tb;
-#if RP_GPAIR
-      for (; tile + 1 < tend; tile += 2) {  // two tiles per iteration: 4 independent pairs per lane
-        const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
-        const double b2 = __ldg(gmP + (int64_t)q * nGp + tile * 8 + 8 + (lane >> 2));
-        double acc[NPOLY][2], acc2[NPOLY][2];
-#pragma unroll
-        for (int k = 0; k < NPOLY; ++k) {
-          dmma_c(acc[k][0], acc[k][1], a0[k], 1.0, 0.0, 0.0);
-          dmma(acc[k][0], acc[k][1], w1[k], b);
-        }
-#pragma unroll
-        for (int k = 0; k < NPOLY; ++k) {
-          dmma_c(acc2[k][0], acc2[k][1], a0[k], 1.0, 0.0, 0.0);
-          dmma(acc2[k][0], acc2[k][1], w1[k], b2);
-        }
-        epi_oct(grec + tile * 8, acc, true, fcon, Dv);
-        epi_oct(grec + tile * 8 + 8, acc2, true, fcon, Dv);
-      }
-#endif
-#if RP_PREF
-      const double *bp = gmP + (int64_t)q * nGp + (lane >> 2);
-      double bn = tile < tend ? __ldg(bp + tile * 8) : 0.0;
-#endif
       for (; tile < tend; ++tile) {
-#if RP_PREF
-        const double b = bn;
-        if (tile + 1 < tend) bn = __ldg(bp + tile * 8 + 8);
-#else
         const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
-#endif
         double acc[NPOLY][2];
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) {
