@@ -7,13 +7,19 @@
 // the paper's SVD is the f1 NEXT row).  The matrix is at most 160 x 160, so one CTA per metric
 // does it on chip:
 //   1. Jacobi equilibration  S = D G_ff D, D = diag(1/sqrt(G_ii))   (conditioning, R14);
-//   2. right-looking Cholesky S = L L^T with the matrix in registers, 2-D cyclic over the 512
-//      threads, one block barrier per column (pivot <= 1e-13 -> RP_ERR_DEGENERATE);
+//   2. Cholesky S = L L^T (pivot <= 1e-13 -> RP_ERR_DEGENERATE): by default blocked (k_solve_b:
+//      8-column panels factored by one warp with a one-panel look-ahead, the rank-8 trailing
+//      updates on DMMA); RP_SOLVE_KERNEL=reg keeps the register-resident right-looking k_solve
+//      (2-D cyclic over the 512 threads, one block barrier per column);
 //   3. two triangular solves by one warp (unknowns in registers, shuffle broadcasts);
 //   4. one step of iterative refinement with the residual b - G_ff z accumulated in
 //      double-double from the unrounded Gram entries, which removes the solve's own rounding
 //      error and leaves only the Gram's.
+#include <cstdlib>
+#include <cstring>
+
 #include "rp_internal.cuh"
+#include "rp_device.cuh"
 
 namespace rp {
 
@@ -316,10 +322,264 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_solve(const double *G, int
   }
 }
 
+// ============================================================================================
+// k_solve_b -- the same solve with a blocked Cholesky (default; RP_SOLVE_KERNEL=reg keeps k_solve).
+// The equilibrated matrix S (padded to a multiple of 8 with an identity block) lives in shared
+// memory (row-major, odd stride).  Per 8-column panel: warp 0 factors the panel with its rows in
+// registers (pivots broadcast by shuffles, no block barrier inside the panel), then every warp
+// applies the rank-8 update S22 -= L21 L21^T to its lower 8 x 8 tiles on DMMA.  So the block
+// barriers drop from one per column to two per 8 columns, and the trailing update runs on the
+// tensor pipe.  Triangular solves: one warp, column-oriented forward / row-oriented backward
+// (unknowns in registers, one shuffle per step); then the same double-double refinement step.
+// ============================================================================================
+constexpr int kSbMaxM = 160;  // padded unknowns (m <= 160)
+
+__global__ void __launch_bounds__(kSolveThreads, 1) k_solve_b(const double *G, int nc, int beta0,
+                                                              double *coef_out, double *info_out) {
+  extern __shared__ __align__(16) double sm[];
+  const int m = nc - 1, M8 = (m + 7) & ~7, ld = M8 | 1;
+  double *S = sm;               // [M8][ld]  S, then L (lower)
+  double *dsc = S + M8 * ld;    // [M8]
+  double *b0 = dsc + M8;        // [M8]  -G_{f,beta0}
+  double *x = b0 + M8;          // [M8]
+  double *z = x + M8;           // [M8]
+  double *rd = z + M8;          // [M8]  1 / L_jj
+  __shared__ int s_status;
+  __shared__ double s_pmin, s_pmax;
+  const double *Gm = G + (int64_t)blockIdx.x * nc * nc;
+  auto col = [beta0](int i) { return i < beta0 ? i : i + 1; };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#ifdef RP_SOLVE_TS
+  unsigned long long tsb[8];
+  tsb[0] = clock64();
+#define RP_TSB(k) tsb[k] = clock64()
+#else
+#define RP_TSB(k)
+#endif
+  if (threadIdx.x == 0) {
+    s_status = 0;
+    s_pmin = __longlong_as_double(0x7ff0000000000000ll);
+    s_pmax = 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < M8; i += blockDim.x) {
+    if (i < m) {
+      const double di = Gm[(int64_t)col(i) * nc + col(i)];
+      if (!(di > 0.0)) s_status = RP_ERR_DEGENERATE;
+      dsc[i] = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
+      b0[i] = -Gm[(int64_t)col(i) * nc + beta0];
+    } else {
+      dsc[i] = 0.0;
+      b0[i] = 0.0;
+    }
+  }
+  __syncthreads();
+  // S = D G_ff D, lower triangle only (the factorisation never reads above the diagonal),
+  // identity padding; a warp per row, coalesced reads of G's row
+  for (int i = wid; i < M8; i += nw)
+    for (int j = lane; j <= i; j += 32) {
+      double v;
+      if (i < m && j < m) v = Gm[(int64_t)col(i) * nc + col(j)] * dsc[i] * dsc[j];
+      else v = (i == j) ? 1.0 : 0.0;
+      S[i * ld + j] = v;
+    }
+  __syncthreads();
+  RP_TSB(1);
+  // ---- blocked Cholesky with a one-panel look-ahead ------------------------------------------
+  // panel(c): warp 0 factors columns c .. c+7 (rows in registers, pivots by shuffles)
+  auto panel = [&](int c) {
+    double P[5][8];  // rows c + lane + 32 k of the panel's 8 columns
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = c + lane + 32 * k;
+        P[k][j] = r < M8 ? S[r * ld + c + j] : 0.0;
+      }
+    int st = 0;
+    double pmin = s_pmin, pmax = s_pmax;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double piv = __shfl_sync(0xffffffffu, P[0][j], j);  // S[c+j][c+j] sits in lane j
+      if (c + j < m) {
+        pmin = fmin(pmin, piv);
+        pmax = fmax(pmax, piv);
+      }
+      if (!(piv > 1e-13)) st = RP_ERR_DEGENERATE;  // (uniform)
+      const double rs = rsqrt_nr(piv > 1e-13 ? piv : 1.0);
+      if (lane == 0) rd[c + j] = rs;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) P[k][j] *= rs;  // L[., c+j] (rows below the diagonal matter)
+#pragma unroll
+      for (int kk = j + 1; kk < 8; ++kk) {
+        const double lk = __shfl_sync(0xffffffffu, P[0][j], kk);  // L[c+kk][c+j] in lane kk
+#pragma unroll
+        for (int k = 0; k < 5; ++k) P[k][kk] = fma(-P[k][j], lk, P[k][kk]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = c + lane + 32 * k;
+        if (r < M8 && r >= c + j) S[r * ld + c + j] = P[k][j];
+      }
+    if (lane == 0) {
+      s_pmin = pmin;
+      s_pmax = pmax;
+      if (st) s_status = st;
+    }
+  };
+  // tile(c, I, J): S[I block][J block] -= L[I][c..c+7] L[J][c..c+7]^T (DMMA, K = 8)
+  const int r8 = lane >> 2, q4 = lane & 3;
+  auto tile = [&](int c, int ri, int rj) {
+    double *acc = S + (ri + r8) * ld + rj + 2 * q4;
+    double d0 = acc[0], d1 = acc[1];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double a = -S[(ri + r8) * ld + c + 4 * h + q4];  // -L[ri + r][c + 4h + q]
+      const double b = S[(rj + r8) * ld + c + 4 * h + q4];   //  L[rj + r][c + 4h + q] = B[q][r]
+      dmma(d0, d1, a, b);
+    }
+    acc[0] = d0;
+    acc[1] = d1;
+  };
+  if (wid == 0) panel(0);
+  __syncthreads();
+  for (int c = 0; c < M8 && s_status == 0; c += 8) {
+    const int c1 = c + 8;
+    if (c1 >= M8) break;
+    const int nb = M8 / 8 - c1 / 8;  // block rows / columns below the panel
+    // A: the next panel's block column (J = c1 / 8), every warp
+    for (int I = wid; I < nb; I += nw) tile(c, c1 + 8 * I, c1);
+    __syncthreads();
+    // B: warp 0 factors the next panel while the others update the remaining lower tiles
+    if (wid == 0) {
+      panel(c1);
+    } else {
+      const int nrest = nb * (nb + 1) / 2 - nb;  // tiles (I, J) with I >= J >= 1 (relative)
+      for (int tt = wid - 1; tt < nrest; tt += nw - 1) {
+        // tt -> (I, J), 1 <= J <= I < nb, row-major over that triangle
+        int I = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+        while ((I + 1) * (I + 2) / 2 <= tt) ++I;
+        while (I * (I + 1) / 2 > tt) --I;
+        const int J = tt - I * (I + 1) / 2;
+        tile(c, c1 + 8 * (I + 1), c1 + 8 * (J + 1));
+      }
+    }
+    __syncthreads();
+  }
+  RP_TSB(2);
+  double *cf = coef_out + (int64_t)blockIdx.x * nc;
+  double *inf = info_out + (int64_t)blockIdx.x * 5;
+  if (s_status != 0) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) cf[i] = __longlong_as_double(0x7ff8000000000000ll);
+    if (threadIdx.x == 0) {
+      inf[0] = (double)s_status;
+      inf[1] = 0;
+      inf[2] = __longlong_as_double(0x7ff8000000000000ll);
+      inf[3] = s_pmin;
+      inf[4] = __longlong_as_double(0x7ff0000000000000ll);
+    }
+    return;
+  }
+  // ---- (L L^T) z = D b0 by warp 0, twice (the second on the double-double residual) ---------
+  // (L L^T)^{-1} in place by warp 0: the register solver of k_solve (L lower, odd stride)
+  auto chol_solve = [&](double *v) {
+    if (wid == 0) chol_solve_warp(S, rd, ld, M8, v);
+  };
+  for (int i = threadIdx.x; i < M8; i += blockDim.x) x[i] = dsc[i] * b0[i];
+  __syncthreads();
+  chol_solve(x);
+  __syncthreads();
+  RP_TSB(3);
+  for (int i = threadIdx.x; i < M8; i += blockDim.x) z[i] = dsc[i] * x[i];
+  __syncthreads();
+  // one refinement step: r = b0 - G_ff z in double-double from the original Gram
+  for (int i = wid; i < m; i += nw) {
+    const double *Gi = Gm + (int64_t)col(i) * nc;
+    double hi = 0.0, lo = 0.0;
+    double gv[kSbMaxM / 32];  // the row's entries, loaded together (one L2 round trip)
+#pragma unroll
+    for (int k = 0; k < kSbMaxM / 32; ++k) gv[k] = lane + 32 * k < m ? Gi[col(lane + 32 * k)] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kSbMaxM / 32; ++k)
+      if (lane + 32 * k < m) dd_fma(hi, lo, -gv[k], z[lane + 32 * k]);
+    dd_warp_sum(hi, lo);
+    if (lane == 0) {
+      dd_add(hi, lo, b0[i]);
+      x[i] = dsc[i] * (hi + lo);
+    }
+  }
+  for (int i = m + threadIdx.x; i < M8; i += blockDim.x) x[i] = 0.0;
+  __syncthreads();
+  RP_TSB(4);
+  chol_solve(x);
+  __syncthreads();
+  RP_TSB(5);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] += dsc[i] * x[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) cf[col(i)] = z[i];
+  if (threadIdx.x == 0) cf[beta0] = 1.0;
+  // resid2 = coef^T G coef (double-double): a warp per row, then the warp partials in order
+  __shared__ double s_rh[32], s_rl[32];
+  {
+    double wh = 0.0, wl = 0.0;
+    for (int i = wid; i < nc; i += nw) {
+      const double ci = (i == beta0) ? 1.0 : z[i < beta0 ? i : i - 1];
+      double rh = 0.0, rl = 0.0;
+      double gv[(kSbMaxM + 32) / 32];  // loaded together (one L2 round trip)
+#pragma unroll
+      for (int k = 0; k < (kSbMaxM + 32) / 32; ++k) {
+        const int j = lane + 32 * k;
+        gv[k] = j < nc ? Gm[(int64_t)i * nc + j] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < (kSbMaxM + 32) / 32; ++k) {
+        const int j = lane + 32 * k;
+        if (j < nc) dd_fma(rh, rl, gv[k], (j == beta0) ? 1.0 : z[j < beta0 ? j : j - 1]);
+      }
+      dd_warp_sum(rh, rl);
+      dd_fma(wh, wl, ci, rh);
+      dd_fma(wh, wl, ci, rl);
+    }
+    if (lane == 0) {
+      s_rh[wid] = wh;
+      s_rl[wid] = wl;
+    }
+  }
+  __syncthreads();
+  RP_TSB(6);
+  if (threadIdx.x == 0) {
+    double hi = 0.0, lo = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      dd_add(hi, lo, s_rh[w]);
+      lo += s_rl[w];
+    }
+#ifdef RP_SOLVE_TS
+    for (int k = 1; k <= 6; ++k) cf[k] = (double)(tsb[k] - tsb[k - 1]);
+#endif
+    inf[0] = 0;
+    inf[1] = (double)m;
+    inf[2] = hi + lo;
+    inf[3] = s_pmin;
+    inf[4] = s_pmax / s_pmin;
+  }
+}
+
 cudaError_t launch_solve(const double *G, int n_v, int nc, int beta0, double *coef_out,
                          double *info_out, cudaStream_t s) {
   const int m = nc - 1;
   if (m > 16 * kRA || m > 32 * kCB) return cudaErrorInvalidValue;
+  const char *kv = getenv("RP_SOLVE_KERNEL");
+  if (!(kv && strcmp(kv, "reg") == 0) && m <= kSbMaxM) {
+    const int M8 = (m + 7) & ~7;
+    const size_t smb = ((size_t)M8 * (M8 | 1) + 5 * (size_t)M8) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_solve_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+    if (e != cudaSuccess) return e;
+    k_solve_b<<<n_v, kSolveThreads, smb, s>>>(G, nc, beta0, coef_out, info_out);
+    return cudaGetLastError();
+  }
   const size_t smem = ((size_t)m * (m | 1) + 8 * (size_t)m) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
