@@ -686,7 +686,12 @@ def test_factored_tiles_match_dense_and_oracle():
             ("large", synth.large_program(), synth.F_large(),
              np.concatenate([synth.random_D_edge_cases(2), synth.large_D(20_000)])),
             ("polybench", synth.polybench_sweep(nD=8).programs[0], synth.F_pow2_3d(),
-             synth.polybench_sweep(nD=3000).D)):
+             synth.polybench_sweep(nD=3000).D),
+            # p = 3 at degree 2: every Horner variable's lists fit, so 3-D groups form
+            ("p3deg2", synth.classf_program("p3deg2", 1, 3, 2, [8, 1, 1, 1], [16384, 1024, 1024, 64],
+                                            synth.HW_GTX1080TI, R=32, Z0=0, Z1=0, grid_map=(0, 0, -1),
+                                            stream="p3deg2"),
+             synth.F_pow2_3d(), synth.polybench_sweep(nD=3000).D)):
         outs = []
         for groups in ("1", "0"):
             os.environ["RP_SWEEP_GROUPS"] = groups
