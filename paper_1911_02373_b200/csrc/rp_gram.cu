@@ -1141,8 +1141,21 @@ static int gram_grid_x(int64_t K) {
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
+// RP_GRAM_KERNEL: unset or "mom" -> the moment contraction where supported (rp_moments.cu);
+// "ws" / "fused" -> the outer-product kernels below (A/B measurements, tests)
+static bool use_moments(const GramBasis &h, int n_v, bool weighted) {
+  const char *gk = getenv("RP_GRAM_KERNEL");
+  return (!gk || strcmp(gk, "mom") == 0) && mom_supported(h, n_v, weighted);
+}
+
+static size_t gram_partial_elems_op(const GramBasis &h, int n_v, int64_t K, bool weighted);
 size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm, bool weighted) {
   (void)nsm;
+  const size_t op = gram_partial_elems_op(h, n_v, K, weighted), mo = mom_partial_elems(h, n_v, K, weighted);
+  return op > mo ? op : mo;
+}
+
+static size_t gram_partial_elems_op(const GramBasis &h, int n_v, int64_t K, bool weighted) {
   if (weighted && fused_supported(h, 1)) return fused_partial_elems(h, 1, K);
   if (!weighted && fused_supported(h, n_v)) return fused_partial_elems(h, n_v, K);
   const int nb = (h.nc + 7) / 8;
@@ -1154,6 +1167,7 @@ size_t gram_partial_elems(const GramBasis &h, int n_v, int64_t K, int nsm, bool 
 cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const double *X,
                         const double *V, const double *S, int64_t K, int n_v, double *G,
                         double *d_part, size_t part_elems, cudaStream_t s) {
+  if (use_moments(h, n_v, S != nullptr)) return launch_gram_mom(d_basis, h, X, V, S, K, n_v, G, d_part, part_elems, s);
   if (S && fused_supported(h, 1)) {  // weighted rows: one fused launch per metric
     for (int v = 0; v < n_v; ++v) {
       cudaError_t e = launch_fused(d_basis, h, X, V + (int64_t)v * K, S + (int64_t)v * K, K, 1,
@@ -1167,7 +1181,7 @@ cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h, const doub
   const int ntiles = nb * (nb + 1) / 2;
   const int groups = (ntiles + kTilesPerGroup - 1) / kTilesPerGroup;
   const int gx = gram_grid_x(K);
-  if (gram_partial_elems(h, n_v, K, 0, false) > part_elems) return cudaErrorInvalidValue;
+  if (gram_partial_elems_op(h, n_v, K, false) > part_elems) return cudaErrorInvalidValue;
   const int stride = gram_stride(nb);
   GramArgs a{d_basis, X, V, S, K, n_v, nb, ntiles, stride, d_part};
   const size_t smem = (size_t)kRT * stride * 8 + (size_t)kTilesPerGroup * 64 * 8 +

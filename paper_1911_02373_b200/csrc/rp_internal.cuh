@@ -163,6 +163,12 @@ cudaError_t launch_gram(const GramBasis *d_basis, const GramBasis &h_basis, cons
                         const double *V, const double *S, int64_t K, int n_v, double *G,
                         double *d_part, size_t part_elems, cudaStream_t s);
 size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_sms, bool weighted);
+// a12 as a moment contraction (rp_moments.cu): the default where the exponent-sum simplex is small
+bool mom_supported(const GramBasis &h_basis, int n_v, bool weighted);
+size_t mom_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, bool weighted);
+cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h_basis, const double *X, const double *V,
+                            const double *S, int64_t K, int n_v, double *G, double *d_part, size_t part_elems,
+                            cudaStream_t s);
 cudaError_t launch_sum_ordered(const double *parts, int n_parts, int64_t elems, double *out, cudaStream_t s);
 cudaError_t launch_den_weights(const GramBasis *d_basis, const double *X, int64_t K, int n_v,
                                const double *d_coef, double *S, cudaStream_t s);

@@ -1,0 +1,582 @@
+// rp_moments.cu -- a12 (the Gram A^T A of the linearised least-squares system) as a contraction
+// of MOMENTS instead of an outer product of design rows.
+//
+// PAPER.md:2578-2584 / 2601-2603: row r of the linearised system is a_r = [M(u_r) | -V_r N(u_r)]
+// with M, N monomial columns ("essentially a Vandermonde matrix").  Every entry of
+// G = sum_r s_r^2 a_r a_r^T is then a weighted moment of ONE monomial:
+//   G[num i][num j] =  sum_r s_r^2       u_r^(e_i + e_j)
+//   G[num i][den j] = -sum_r s_r^2 V_r   u_r^(e_i + f_j)
+//   G[den i][den j] =  sum_r s_r^2 V_r^2 u_r^(f_i + f_j)
+// (s_r = 1 unless the rows are weighted, f4).  So the Gram of the n_v metrics needs only the
+// moments m_w(e) = sum_r w_r(r) u_r^e for the exponents e of total degree <= D = 2 max|e_i|
+// (the simplex: 495 of them for 4 variables and degree-4 bases) and the weights
+// w in {1, V_v, V_v^2} (unweighted: 1 + 2 n_v of them) or {s_v^2, s_v^2 V_v, s_v^2 V_v^2}:
+// 2 x 8 x 496 = 7.9k flop per row instead of the 34.8k of the 7 symmetric 70 x 70 blocks that
+// k_gram_ws accumulates.  The contraction over rows is the same dense FP64
+// product, moments[w][e] += W^T[w][rows] Mon[rows][e], on DMMA.8x8x4 (A = 8 weights x 4 rows,
+// B = 4 rows x 8 exponents).
+//
+// k_gram_mom: one CTA per SM (16 warps) owns a contiguous slab of 32-row stages.  Per stage:
+//   inputs  -- X rows, V_v (and S_v) land in a 3-stage ring by cp.async.bulk (TMA engine) issued
+//              3 stages ahead; one warp turns them into u = (x - c) 2^-e and the row weights;
+//   monomials (a11) -- lane = row; warp w generates a contiguous slot range of the simplex in
+//              lexicographic order, unit by unit (a unit fixes e_0 .. e_{n-2}; its entries run
+//              over e_{n-1}, each one DMUL from the previous), into sM[slot][row] (conflict-free:
+//              a warp stores 32 consecutive rows);
+//   moments (a12) -- warp w owns a contiguous range of 8-slot tiles and accumulates them for the
+//              8 (or 16) weights over the stage's 8 k-steps.
+// Register accumulators are added into the CTA's partial every 1,024 rows (two-level
+// summation, as k_gram_ws); k_mom_sum adds the partials in a fixed order (deterministic) and
+// k_mom_assemble scatters the moments into G_v (the slot of e_i + e_j by its lexicographic rank).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "rp_internal.cuh"
+#include "rp_umma.cuh"
+
+namespace rp {
+
+constexpr int kMomWarps = 16;
+constexpr int kMomThreads = 32 * kMomWarps;
+constexpr int kMomRT = 32;          // rows per stage (lane = row in the monomial step)
+constexpr int kMomRTP = 36;         // row stride of sM / sW in doubles (= 4 mod 16: conflict-free fragments)
+constexpr int kMomMaxSlots = 640;   // simplex size limit (shared memory)
+constexpr int kMomMaxUnits = 256;
+constexpr int kMomIS = 3;           // input stages in flight
+constexpr int kMomFlush = 32;       // stages between flushes of the register accumulators (1024 rows)
+
+struct MomArgs {
+  const GramBasis *basis;  // device: the transform (xc, xe) and the column exponents (assembly)
+  const double *X;         // [K][n]
+  const double *V;         // [nv][K]
+  const double *S;         // [nv][K] row scales or null
+  int64_t K;
+  double *part;            // [gridDim.x][nT][WT][64]
+  int n, D, nslot, nT, nv, nw, tma;
+  int16_t wunit[kMomWarps + 1];  // units of warp w: [wunit[w], wunit[w + 1])
+  int16_t wslot[kMomWarps + 1];  // first slot of warp w
+  int16_t wtile[kMomWarps + 1];  // exponent tiles of warp w: [wtile[w], wtile[w + 1])
+  uint32_t uexp[kMomMaxUnits];   // unit: e_0 .. e_{n-2}, 4 bits each
+  uint8_t ulen[kMomMaxUnits];    // its entries: e_{n-1} = 0 .. ulen - 1
+};
+
+__device__ __forceinline__ void mom_dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int mom_in_doubles(int n, int nv, bool weighted) {  // one input stage, even (16-byte aligned)
+  const int d = kMomRT * (n + nv + (weighted ? nv : 0));
+  return (d + 1) & ~1;
+}
+
+static size_t mom_smem(int nT, int n, int nv, bool weighted) {
+  return sizeof(double) * ((size_t)nT * 8 * kMomRTP + 2 * 16 * kMomRTP + 2 * kMaxVars * kMomRT +
+                           (size_t)kMomIS * mom_in_doubles(n, nv, weighted)) +
+         sizeof(uint64_t) * kMomIS;
+}
+
+// ---- the simplex's units and the warps' shares (one algorithm for the host plan and the
+// compile-time specialisations) ------------------------------------------------------------------
+struct MomTab {
+  int nu, ns;
+  int8_t ex[kMomMaxUnits][kMaxVars];  // e_0 .. e_{N-2} of unit u (e_{N-1} runs over 0 .. len - 1)
+  int len[kMomMaxUnits], slot[kMomMaxUnits];
+  int wu[kMomWarps + 1];              // units of warp w: [wu[w], wu[w + 1])
+};
+// units in lexicographic order (e_0 slowest, e_{N-2} fastest); nu = 0 when the simplex is too large
+__host__ __device__ constexpr MomTab mom_tab(int N, int D) {
+  MomTab t{};
+  int e[kMaxVars] = {};
+  const int np = N - 1;
+  int slot = 0;
+  for (;;) {
+    if (t.nu >= kMomMaxUnits) {
+      t.nu = 0;
+      return t;
+    }
+    int sum = 0;
+    for (int k = 0; k < np; ++k) sum += e[k], t.ex[t.nu][k] = (int8_t)e[k];
+    t.len[t.nu] = D - sum + 1;
+    t.slot[t.nu] = slot;
+    slot += D - sum + 1;
+    ++t.nu;
+    int k = np - 1;
+    while (k >= 0) {
+      ++e[k];
+      int s2 = 0;
+      for (int i = 0; i < np; ++i) s2 += e[i];
+      if (s2 <= D) break;
+      e[k] = 0;
+      --k;
+    }
+    if (k < 0) break;
+  }
+  t.ns = slot;
+  // generation: contiguous unit ranges of ~ns / 16 entries per warp
+  int u = 0, sl = 0;
+  for (int w = 0; w < kMomWarps; ++w) {
+    t.wu[w] = u;
+    const int target = (t.ns * (w + 1) + kMomWarps / 2) / kMomWarps;
+    while (u < t.nu && (w == kMomWarps - 1 || sl + t.len[u] / 2 < target)) sl += t.len[u++];
+  }
+  t.wu[kMomWarps] = t.nu;
+  return t;
+}
+template <int N, int D>
+struct MomC {
+  static constexpr MomTab t = mom_tab(N, D);
+};
+
+// a11 for the units [UI, UE) of one warp, every index and exponent a compile-time constant:
+// the unit's prefix from the power table (or, for the next e_{N-2} of the same prefix, one DMUL
+// from the previous unit's), then e_{N-1} = 0 .. len - 1 one DMUL each; lane = row
+struct MomUnit {
+  int len, slot;
+  bool cont;               // the previous unit has the same prefix with e_{N-2} one less
+  int8_t ex[kMaxVars];
+};
+template <int N, int D>
+__host__ __device__ constexpr MomUnit mom_unit(int u) {
+  const MomTab &T = MomC<N, D>::t;
+  MomUnit x{};
+  x.len = T.len[u];
+  x.slot = T.slot[u];
+  for (int k = 0; k < kMaxVars; ++k) x.ex[k] = T.ex[u][k];
+  x.cont = u > 0 && N >= 2;
+  for (int k = 0; k + 2 < N && x.cont; ++k) x.cont = T.ex[u][k] == T.ex[u - 1][k];
+  if (x.cont) x.cont = T.ex[u][N - 2] == T.ex[u - 1][N - 2] + 1;
+  return x;
+}
+template <int N, int D>
+__host__ __device__ constexpr int mom_wu(int w) { return MomC<N, D>::t.wu[w]; }
+
+// a11 for the units [UI, UE) of one warp, every index and exponent a compile-time constant:
+// the unit's prefix from the power table (or, for the next e_{N-2} of the same prefix, one DMUL
+// from the previous unit's), then e_{N-1} = 0 .. len - 1 one DMUL each; lane = row
+template <int N, int D, int UB, int UI, int UE>
+__device__ __forceinline__ void mom_gen_units(const double (&pw)[kMaxVars][16], double *dst, double am_prev) {
+  if constexpr (UI < UE) {
+    constexpr MomUnit U = mom_unit<N, D>(UI);
+    double am;
+    if constexpr (U.cont && UI > UB) {  // (the warp's first unit always starts from the table)
+      am = am_prev * pw[N - 2][1];
+    } else {
+      am = 1.0;
+      bool one = true;
+#pragma unroll
+      for (int k = 0; k + 1 < N; ++k)
+        if (U.ex[k] > 0) {
+          am = one ? pw[k][U.ex[k]] : am * pw[k][U.ex[k]];
+          one = false;
+        }
+    }
+    double m = am;
+#pragma unroll
+    for (int j = 0; j < U.len; ++j) {
+      dst[(U.slot + j) * kMomRTP] = m;
+      if (j + 1 < U.len) m *= pw[N - 1][1];
+    }
+    mom_gen_units<N, D, UB, UI + 1, UE>(pw, dst, am);
+  }
+}
+
+template <int N, int D, int W>
+__device__ __forceinline__ void mom_gen_warp(const double *u, double *dst) {
+  // power table u_k^j (j <= D; only the entries this warp's units use survive)
+  double pw[kMaxVars][16];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    pw[k][0] = 1.0;
+    pw[k][1] = u[k * kMomRT];
+#pragma unroll
+    for (int j = 2; j <= D; ++j) pw[k][j] = pw[k][j - 1] * pw[k][1];
+  }
+  constexpr int ub = mom_wu<N, D>(W), ue = mom_wu<N, D>(W + 1);
+  mom_gen_units<N, D, ub, ub, ue>(pw, dst, 1.0);
+}
+
+// N, D > 0: the monomial step specialised for that simplex (mom_gen_warp); N = 0: generic
+template <int WT, int TPW, int N, int D>
+__global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_constant__ MomArgs a) {
+  extern __shared__ __align__(16) double msm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int n = a.n, nv = a.nv;
+  const bool wtd = a.S != nullptr;
+  const int nslotp = a.nT * 8;
+  double *sM = msm;                                   // [nslotp][RTP]
+  double *sW = sM + (size_t)nslotp * kMomRTP;         // [2][16][RTP]
+  double *sU = sW + 2 * 16 * kMomRTP;                 // [2][kMaxVars][RT]
+  double *sIn = sU + 2 * kMaxVars * kMomRT;           // [IS][INB]
+  const int INB = mom_in_doubles(n, nv, wtd);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sIn + kMomIS * INB);
+  __shared__ double sXc[kMaxVars], sXs[kMaxVars];  // the transform: c_k, 2^-e_k
+
+  // slab: whole 32-row stages, so bulk-copy sources stay 16-byte aligned
+  const int64_t nst_all = (a.K + kMomRT - 1) / kMomRT;
+  const int64_t t0 = nst_all * blockIdx.x / gridDim.x, t1 = nst_all * (blockIdx.x + 1) / gridDim.x;
+  const int64_t r_begin = kMomRT * t0;
+  const int64_t r_end = (kMomRT * t1) < a.K ? kMomRT * t1 : a.K;
+  const int ns = (int)(t1 - t0);
+  auto full_stage = [&](int s) { return a.tma && r_begin + (int64_t)(s + 1) * kMomRT <= r_end; };
+
+  // padding slots [nslot, nslotp) stay zero
+  for (int i = threadIdx.x; i < (nslotp - a.nslot) * kMomRTP; i += blockDim.x) sM[(size_t)a.nslot * kMomRTP + i] = 0.0;
+  if (threadIdx.x < kMaxVars) {
+    sXc[threadIdx.x] = threadIdx.x < n ? a.basis->xc[threadIdx.x] : 0.0;
+    sXs[threadIdx.x] = threadIdx.x < n ? ldexp(1.0, -a.basis->xe[threadIdx.x]) : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMomIS; ++i) mbar_init(smem_u32(full + i), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int s) {  // thread 0: the bulk copies of stage s into its input stage
+    const int st = s % kMomIS;
+    double *dst = sIn + st * INB;
+    const int64_t r0 = r_begin + (int64_t)s * kMomRT;
+    const uint32_t bx = kMomRT * n * 8, bv = kMomRT * 8;
+    const uint32_t bar = smem_u32(full + st);
+    mbar_expect_tx(bar, bx + nv * bv * (wtd ? 2 : 1));
+    bulk_g2s(smem_u32(dst), a.X + r0 * n, bx, bar);
+    for (int v = 0; v < nv; ++v) bulk_g2s(smem_u32(dst + kMomRT * n + v * kMomRT), a.V + (int64_t)v * a.K + r0, bv, bar);
+    if (wtd)
+      for (int v = 0; v < nv; ++v)
+        bulk_g2s(smem_u32(dst + kMomRT * (n + nv) + v * kMomRT), a.S + (int64_t)v * a.K + r0, bv, bar);
+  };
+  // the input warp (lane = row): u and the row weights of stage s into buffer s & 1
+  auto process = [&](int s) {
+    const int b = s & 1;
+    const int64_t r = r_begin + (int64_t)s * kMomRT + lane;
+    const bool valid = r < r_end;
+    const double *src = nullptr;
+    if (full_stage(s)) {
+      mbar_wait(smem_u32(full + s % kMomIS), (uint32_t)((s / kMomIS) & 1));
+      src = sIn + (s % kMomIS) * INB;
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxVars; ++k) {
+      if (k < n) {
+        const double x = src ? src[lane * n + k] : (valid ? a.X[r * n + k] : 0.0);
+        sU[(b * kMaxVars + k) * kMomRT + lane] = valid ? (x - sXc[k]) * sXs[k] : 0.0;
+      }
+    }
+    double *w = sW + b * 16 * kMomRTP + lane;
+    for (int i = 0; i < 16; ++i) w[i * kMomRTP] = 0.0;
+    if (valid) {
+      if (!wtd) w[0] = 1.0;
+      for (int v = 0; v < nv; ++v) {
+        const double vv = src ? src[kMomRT * n + v * kMomRT + lane] : a.V[(int64_t)v * a.K + r];
+        if (wtd) {
+          const double sv = src ? src[kMomRT * (n + nv) + v * kMomRT + lane] : a.S[(int64_t)v * a.K + r];
+          const double s2 = sv * sv;
+          w[(3 * v) * kMomRTP] = s2;
+          w[(3 * v + 1) * kMomRTP] = s2 * vv;
+          w[(3 * v + 2) * kMomRTP] = s2 * vv * vv;
+        } else {
+          w[(1 + v) * kMomRTP] = vv;
+          w[(1 + nv + v) * kMomRTP] = vv * vv;
+        }
+      }
+    }
+  };
+  constexpr int kInWarp = kMomWarps - 1;  // fewest tiles (the host gives the remainder to the first warps)
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kMomIS && s < ns; ++s)
+      if (full_stage(s)) issue(s);
+  if (wid == kInWarp && ns > 0) process(0);
+  __syncthreads();
+
+  const int tb = a.wtile[wid], tc = a.wtile[wid + 1] - tb;
+  double acc[TPW][WT][2];
+#pragma unroll
+  for (int q = 0; q < TPW; ++q)
+#pragma unroll
+    for (int h = 0; h < WT; ++h) acc[q][h][0] = acc[q][h][1] = 0.0;
+  double *part = a.part + (size_t)blockIdx.x * a.nT * WT * 64;
+  bool first = true;
+  const int ub = a.wunit[wid], ue = a.wunit[wid + 1];
+  const uint32_t inc = n >= 2 ? 1u << (4 * (n - 2)) : 0u;  // e_{n-2} + 1 in a unit's packed exponents
+
+  for (int s = 0; s < ns; ++s) {
+    const int b = s & 1;
+    if (threadIdx.x == 0 && s + kMomIS < ns && full_stage(s + kMomIS)) issue(s + kMomIS);  // its stage was read
+    // ---- a11: the monomials of the warp's slots for the stage's 32 rows (lane = row) ----------
+    if constexpr (N > 0) {
+      const double *u = sU + b * kMaxVars * kMomRT + lane;
+      switch (wid) {
+#define RP_MG(w) \
+  case w: mom_gen_warp<N, D, w>(u, sM + lane); break;
+        RP_MG(0) RP_MG(1) RP_MG(2) RP_MG(3) RP_MG(4) RP_MG(5) RP_MG(6) RP_MG(7) RP_MG(8) RP_MG(9) RP_MG(10)
+        RP_MG(11) RP_MG(12) RP_MG(13) RP_MG(14) RP_MG(15)
+#undef RP_MG
+      }
+    } else {
+      const double *u = sU + b * kMaxVars * kMomRT + lane;
+      const double ul = u[(n - 1) * kMomRT], us = n >= 2 ? u[(n - 2) * kMomRT] : 1.0;
+      int slot = a.wslot[wid];
+      uint32_t pex = 0;
+      double am = 1.0;
+      for (int ui = ub; ui < ue; ++ui) {
+        const uint32_t ex = a.uexp[ui];
+        const int len = a.ulen[ui];
+        if (ui > ub && n >= 2 && ex == pex + inc) {
+          am *= us;  // the next e_{n-2} of the same prefix
+        } else {     // a new prefix: u_0^e_0 ... u_{n-2}^e_{n-2} by repeated multiplication
+          am = 1.0;
+          for (int k = 0; k + 1 < n; ++k) {
+            const double uk = u[k * kMomRT];
+            for (int e = (int)((ex >> (4 * k)) & 15u); e > 0; --e) am *= uk;
+          }
+        }
+        pex = ex;
+        double m = am;
+        double *dst = sM + (size_t)slot * kMomRTP + lane;
+        for (int j = 0; j < len; ++j) {
+          dst[j * kMomRTP] = m;
+          m *= ul;
+        }
+        slot += len;
+      }
+    }
+    __syncthreads();
+    // ---- a12: moments[w][e] += W^T Mon over the stage's 8 k-steps --------------------------------
+    {
+      const double *wb = sW + b * 16 * kMomRTP + (lane >> 2) * kMomRTP + (lane & 3);
+      const double *mb = sM + (size_t)(tb * 8 + (lane >> 2)) * kMomRTP + (lane & 3);
+#pragma unroll 2
+      for (int ks = 0; ks < kMomRT / 4; ++ks) {
+        double av[WT];
+#pragma unroll
+        for (int h = 0; h < WT; ++h) av[h] = wb[h * 8 * kMomRTP + ks * 4];
+#pragma unroll
+        for (int q = 0; q < TPW; ++q) {
+          if (q < tc) {
+            const double bv = mb[(size_t)q * 8 * kMomRTP + ks * 4];
+#pragma unroll
+            for (int h = 0; h < WT; ++h) mom_dmma(acc[q][h][0], acc[q][h][1], av[h], bv);
+          }
+        }
+      }
+    }
+    if (wid == kInWarp && s + 1 < ns) process(s + 1);
+    if (((s + 1) % kMomFlush) == 0 || s + 1 == ns) {
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+        if (q < tc) {
+#pragma unroll
+          for (int h = 0; h < WT; ++h) {
+            double *dst = part + ((size_t)(tb + q) * WT + h) * 64 + lane * 2;
+            if (first) {
+              dst[0] = acc[q][h][0];
+              dst[1] = acc[q][h][1];
+            } else {
+              dst[0] += acc[q][h][0];
+              dst[1] += acc[q][h][1];
+            }
+            acc[q][h][0] = acc[q][h][1] = 0.0;
+          }
+        }
+      }
+      first = false;
+    }
+    __syncthreads();
+  }
+  if (ns == 0)  // empty slab: zero partial
+    for (int i = threadIdx.x; i < a.nT * WT * 64; i += blockDim.x) part[i] = 0.0;
+}
+
+// fixed-order sum of the per-CTA partials: 4 quarter sums per element (CTAs q, q + 4, ...),
+// added as (q0 + q1) + (q2 + q3)
+__global__ void __launch_bounds__(256) k_mom_sum(const double *part, int nblk, int n_el, double *red) {
+  __shared__ double sq[4][64];
+  const int q = threadIdx.x >> 6, l = threadIdx.x & 63;
+  const int e = blockIdx.x * 64 + l;
+  double s = 0.0;
+  if (e < n_el)
+    for (int b = q; b < nblk; b += 4) s += part[(int64_t)b * n_el + e];
+  sq[q][l] = s;
+  __syncthreads();
+  if (q == 0 && e < n_el) red[e] = (sq[0][l] + sq[1][l]) + (sq[2][l] + sq[3][l]);
+}
+
+// lexicographic rank of e (|e| <= D) in the simplex {|e| <= D} of n variables:
+// sum_k sum_{j < e_k} #{vectors of the n - k - 1 later variables with sum <= D - s_k - j}
+__device__ __forceinline__ int simplex_rank(const int8_t *e, int n, int D) {
+  int rank = 0, s = 0;
+  for (int k = 0; k < n; ++k) {
+    const int m = n - k - 1;
+    for (int j = 0; j < e[k]; ++j) {
+      const int R = D - s - j;
+      int c = 1;  // C(R + m, m)
+      for (int i = 1; i <= m; ++i) c = c * (R + i) / i;
+      rank += c;
+    }
+    s += e[k];
+  }
+  return rank;
+}
+
+// G_v[i][j] from the summed moments red [nT][WT][64] (element 8 w + slot % 8 of tile slot / 8)
+__global__ void k_mom_assemble(const GramBasis *gb, const double *red, int D, int nv, int wtd, int WT, double *G) {
+  const GramBasis &B = *gb;
+  const int n = B.n, nc = B.nc, nn = B.n_num;
+  const int64_t total = (int64_t)nv * nc * nc;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(idx / ((int64_t)nc * nc));
+    const int rc = (int)(idx % ((int64_t)nc * nc));
+    const int i = rc / nc, j = rc % nc;
+    const int q = (i >= nn) + (j >= nn);  // 0: num-num, 1: num-den, 2: den-den
+    int8_t e[kMaxVars];
+    for (int k = 0; k < n; ++k) e[k] = (int8_t)(B.exp[i][k] + B.exp[j][k]);
+    const int slot = simplex_rank(e, n, D);
+    const int w = wtd ? 3 * v + q : (q == 0 ? 0 : (q == 1 ? 1 + v : 1 + nv + v));
+    const double m = red[((int64_t)(slot >> 3) * WT + (w >> 3)) * 64 + 8 * (w & 7) + (slot & 7)];
+    G[idx] = q == 1 ? -m : m;
+  }
+}
+
+// ---- host: the moment plan -------------------------------------------------------------------
+static int64_t binom(int a, int b) {
+  if (b < 0 || b > a) return 0;
+  int64_t c = 1;
+  for (int i = 1; i <= b; ++i) c = c * (a - b + i) / i;
+  return c;
+}
+
+struct MomShape {
+  int D, nslot, nunit, nT, nw, WT, TPW;
+};
+
+static bool mom_shape(const GramBasis &h, int n_v, bool weighted, MomShape *sh) {
+  const int n = h.n;
+  if (n < 1 || n > kMaxVars) return false;
+  int dmax = 0;
+  for (int j = 0; j < h.nc; ++j) {
+    int d = 0;
+    for (int k = 0; k < n; ++k) d += h.exp[j][k];
+    dmax = d > dmax ? d : dmax;
+  }
+  sh->D = 2 * dmax;
+  if (sh->D > 15) return false;  // unit exponents are packed 4 bits per variable
+  const int64_t nslot = binom(sh->D + n, n), nunit = n >= 2 ? binom(sh->D + n - 1, n - 1) : 1;
+  if (nslot > kMomMaxSlots || nunit > kMomMaxUnits) return false;
+  sh->nslot = (int)nslot;
+  sh->nunit = (int)nunit;
+  sh->nT = (sh->nslot + 7) / 8;
+  sh->nw = weighted ? 3 * n_v : 1 + 2 * n_v;
+  if (n_v < 1 || sh->nw > 16) return false;
+  sh->WT = sh->nw <= 8 ? 1 : 2;
+  const int tpw = (sh->nT + kMomWarps - 1) / kMomWarps;
+  sh->TPW = tpw <= 1 ? 1 : (tpw <= 2 ? 2 : (tpw <= 4 ? 4 : 8));
+  if (sh->TPW * sh->WT > 8) return false;
+  return mom_smem(sh->nT, n, n_v, weighted) <= 227 * 1024;
+}
+
+static int mom_grid_x(int64_t K) {
+  const int64_t want = (K + kMomRT - 1) / kMomRT;
+  const int64_t cap = num_sms();
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+bool mom_supported(const GramBasis &h, int n_v, bool weighted) {
+  MomShape sh;
+  return mom_shape(h, n_v, weighted, &sh);
+}
+
+size_t mom_partial_elems(const GramBasis &h, int n_v, int64_t K, bool weighted) {
+  MomShape sh;
+  if (!mom_shape(h, n_v, weighted, &sh)) return 0;
+  return (size_t)(mom_grid_x(K) + 1) * sh.nT * sh.WT * 64;  // partials + their sum
+}
+
+template <int WT, int TPW, int N, int D>
+static cudaError_t launch_mom_t(const MomArgs &a, int gx, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_gram_mom<WT, TPW, N, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gram_mom<WT, TPW, N, D><<<gx, kMomThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h, const double *X, const double *V,
+                            const double *S, int64_t K, int n_v, double *G, double *d_part, size_t part_elems,
+                            cudaStream_t s) {
+  MomShape sh;
+  const bool wtd = S != nullptr;
+  if (!mom_shape(h, n_v, wtd, &sh)) return cudaErrorInvalidValue;
+  const int gx = mom_grid_x(K);
+  const int n_el = sh.nT * sh.WT * 64;
+  if ((size_t)(gx + 1) * n_el > part_elems) return cudaErrorInvalidValue;
+  MomArgs a;
+  memset(&a, 0, sizeof a);
+  a.basis = d_basis;
+  a.X = X;
+  a.V = V;
+  a.S = S;
+  a.K = K;
+  a.part = d_part;
+  a.n = h.n;
+  a.D = sh.D;
+  a.nslot = sh.nslot;
+  a.nT = sh.nT;
+  a.nv = n_v;
+  a.nw = sh.nw;
+  // bulk copies need 16-byte aligned sources: X, V and S rows of whole stages (K even)
+  a.tma = ((uintptr_t)X % 16 == 0) && ((uintptr_t)V % 16 == 0) && (!S || (uintptr_t)S % 16 == 0) && (K % 2 == 0);
+  // units in lexicographic order and the warps' contiguous shares (the same table the
+  // specialised kernels are compiled from)
+  const int n = h.n;
+  static MomTab tab;  // (host: too large for the stack)
+  tab = mom_tab(n, sh.D);
+  if (tab.nu != sh.nunit || tab.ns != sh.nslot) return cudaErrorInvalidValue;
+  for (int i = 0; i < sh.nunit; ++i) {
+    uint32_t pk = 0;
+    for (int k = 0; k + 1 < n; ++k) pk |= (uint32_t)tab.ex[i][k] << (4 * k);
+    a.uexp[i] = pk;
+    a.ulen[i] = (uint8_t)tab.len[i];
+  }
+  for (int w = 0; w <= kMomWarps; ++w) {
+    a.wunit[w] = (int16_t)tab.wu[w];
+    a.wslot[w] = (int16_t)(tab.wu[w] < tab.nu ? tab.slot[tab.wu[w]] : tab.ns);
+  }
+  // moments: nT tiles over the warps, the remainder to the first ones (the last warp also
+  // prepares the next stage's inputs)
+  {
+    const int base = sh.nT / kMomWarps, rem = sh.nT % kMomWarps;
+    int t = 0;
+    for (int w = 0; w < kMomWarps; ++w) {
+      a.wtile[w] = (int16_t)t;
+      t += base + (w < rem ? 1 : 0);
+    }
+    a.wtile[kMomWarps] = (int16_t)t;
+  }
+  const size_t smem = mom_smem(sh.nT, n, n_v, wtd);
+  cudaError_t e;
+  const char *gen = getenv("RP_MOM_GENERIC");  // measurement: the runtime monomial step only
+  const bool spec = !(gen && gen[0] == '1');
+  // the BASELINE shapes (tiny: 3 variables, degree 2; polybench: 4, degree 3; fitheavy: 4,
+  // degree 4) with their monomial step specialised at compile time; the rest generic
+#define RP_MOM_SPEC(WT_, TPW_, N_, D_) \
+  if (spec && sh.WT == WT_ && sh.TPW == TPW_ && n == N_ && sh.D == D_) e = launch_mom_t<WT_, TPW_, N_, D_>(a, gx, smem, s); else
+#define RP_MOM_CASE(WT_, TPW_) \
+  if (sh.WT == WT_ && sh.TPW == TPW_) e = launch_mom_t<WT_, TPW_, 0, 0>(a, gx, smem, s); else
+  RP_MOM_SPEC(1, 4, 4, 8) RP_MOM_SPEC(2, 4, 4, 8) RP_MOM_SPEC(1, 2, 4, 6) RP_MOM_SPEC(2, 2, 4, 6)
+  RP_MOM_SPEC(1, 1, 3, 4) RP_MOM_SPEC(2, 1, 3, 4)
+  RP_MOM_CASE(1, 1) RP_MOM_CASE(1, 2) RP_MOM_CASE(1, 4) RP_MOM_CASE(1, 8) RP_MOM_CASE(2, 1) RP_MOM_CASE(2, 2)
+  RP_MOM_CASE(2, 4) e = cudaErrorInvalidValue;
+#undef RP_MOM_CASE
+#undef RP_MOM_SPEC
+  if (e != cudaSuccess) return e;
+  double *red = d_part + (size_t)gx * n_el;
+  k_mom_sum<<<(n_el + 63) / 64, 256, 0, s>>>(d_part, gx, n_el, red);
+  const int64_t total = (int64_t)n_v * h.nc * h.nc;
+  const int rb = (int)((total + 255) / 256);
+  k_mom_assemble<<<rb < 4 * num_sms() ? rb : 4 * num_sms(), 256, 0, s>>>(d_basis, red, sh.D, n_v, wtd ? 1 : 0, sh.WT, G);
+  return cudaGetLastError();
+}
+
+}  // namespace rp

@@ -190,14 +190,16 @@ def test_fit_host_pointers_and_gram_edge_cases():
         assert np.max(np.abs(Gk - Go) / dg) <= 1e-13, K
 
 
-@pytest.mark.parametrize("kernel", ["ws", "fused"])
+@pytest.mark.parametrize("kernel", ["mom", "mom_generic", "ws", "fused"])
 @pytest.mark.parametrize("basis", ["tree", "no_tree"])
 def test_gram_fused_kernels(kernel, basis, monkeypatch):
-    """Both fused Gram kernels (warp-specialised default, single-role fallback) on a basis that
-    is closed under parents (monomial-tree staging) and on one that is not (power-table staging),
-    at ragged row counts, against the oracle's plain sum of outer products."""
-    if kernel == "fused":
-        monkeypatch.setenv("RP_GRAM_KERNEL", "fused")
+    """The Gram kernels -- the moment contraction (default), the warp-specialised and the
+    single-role outer-product kernels -- on a basis that is closed under parents (monomial-tree
+    staging) and on one that is not (power-table staging), at ragged row counts, against the
+    oracle's plain sum of outer products."""
+    monkeypatch.setenv("RP_GRAM_KERNEL", kernel.split("_")[0])
+    if kernel == "mom_generic":  # the runtime monomial step instead of the specialised one
+        monkeypatch.setenv("RP_MOM_GENERIC", "1")
     fc = synth.polybench_fit_box()
     if basis == "tree":
         num = fc.num_exp
