@@ -20,6 +20,7 @@ from __future__ import annotations
 import argparse
 import copy
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -518,10 +519,15 @@ def main():
                 "evaluated_pairs": pairs_eval, "ms_per_launch": kern_ms,
                 "timing": "CUDA events recorded by librp around k_sweep on its stream inside every timed step "
                           "(rp_plan_last_timing), median", "ncu": counters}
-    # fused algorithm: 1 + 2*3 symmetric 70x70 blocks per row,
-    # 70*71/2 unique multiply-adds each
-    gram_flop = (khi - klo) * (1 + 2 * 3) * 70 * 71
+    # moment contraction: every Gram entry is a weighted moment of one monomial,
+    # so a row costs 2 x (1 + 2 n_v) weights x C(D + n, n) monomials of degree <= D = 2 x 4 in
+    # n = 4 variables: 2 x 7 x 495 = 6,930 flop (the DMMA tiles execute 2 x 8 x 496 = 7,936);
+    # the outer-product Gram it replaces is 2 x 7 x 70 x 71 / 2 = 34,790 flop per row
+    n_mom = math.comb(2 * 4 + 4, 4)
+    gram_flop = (khi - klo) * 2 * (1 + 2 * 3) * n_mom
     gram_ach = gram_flop / (gram_ms * 1e-3) / 1e12
+    gram_exec = (khi - klo) * 2 * 8 * (8 * ((n_mom + 7) // 8)) / (gram_ms * 1e-3) / 1e12
+    gram_equiv = (khi - klo) * (1 + 2 * 3) * 70 * 71 / (gram_ms * 1e-3) / 1e12
     gtraffic, gcounters = None, None
     gprof = os.path.join(ROOT, "profiles", "gram_ncu_latest.json")
     if os.path.exists(gprof):
@@ -530,8 +536,10 @@ def main():
             gtraffic, gcounters = gj.get("dram_bytes_per_launch"), gj.get("counters")
         except (OSError, ValueError):
             gtraffic = None
-    roofline_fit = {"bound": "tensor", "kernel": "k_gram_ws (DMMA.8x8x4, warp-specialised)", "achieved": gram_ach,
+    roofline_fit = {"bound": "tensor", "kernel": "k_gram_mom (moment contraction on DMMA.8x8x4)", "achieved": gram_ach,
                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gram_ach / FP64_PEAK_TFLOPS,
+                    "flop_per_row": 2 * (1 + 2 * 3) * n_mom, "executed_tflops": gram_exec,
+                    "outer_product_equiv_tflops": gram_equiv,
                     "traffic": gtraffic, "ncu": gcounters,
                     "ms_per_call": gram_ms, "peak_source": "FP64 tensor = FP64 FMA rate on B200 "
                                                            "(measured DMMA 36.9 TF/s)"}

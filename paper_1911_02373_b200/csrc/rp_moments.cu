@@ -38,13 +38,14 @@
 
 namespace rp {
 
-constexpr int kMomWarps = 16;
-constexpr int kMomThreads = 32 * kMomWarps;
+constexpr int kMomWarps = 16;                      // consumers: monomials + moments of their own tiles
+constexpr int kMomThreads = 32 * (kMomWarps + 1);  // + one producer warp: TMA issue, row weights
 constexpr int kMomRT = 32;          // rows per stage (lane = row in the monomial step)
-constexpr int kMomRTP = 36;         // row stride of sM / sW in doubles (= 4 mod 16: conflict-free fragments)
+constexpr int kMomRTP = 36;         // row stride of sM in doubles (= 4 mod 16: conflict-free fragments)
 constexpr int kMomMaxSlots = 640;   // simplex size limit (shared memory)
 constexpr int kMomMaxUnits = 256;
-constexpr int kMomIS = 3;           // input stages in flight
+constexpr int kMomIS = 5;           // ring slots: raw inputs + row weights of a stage
+constexpr int kMomLead = 3;         // bulk copies are issued this many stages ahead
 constexpr int kMomFlush = 32;       // stages between flushes of the register accumulators (1024 rows)
 
 struct MomArgs {
@@ -55,9 +56,9 @@ struct MomArgs {
   int64_t K;
   double *part;            // [gridDim.x][nT][WT][64]
   int n, D, nslot, nT, nv, nw, tma;
-  int16_t wunit[kMomWarps + 1];  // units of warp w: [wunit[w], wunit[w + 1])
-  int16_t wslot[kMomWarps + 1];  // first slot of warp w
-  int16_t wtile[kMomWarps + 1];  // exponent tiles of warp w: [wtile[w], wtile[w + 1])
+  int16_t wtile[kMomWarps + 1];  // tiles of consumer warp w: [wtile[w], wtile[w + 1])
+  int16_t wunit[kMomWarps];      // the first unit overlapping its slots
+  int16_t wuslot[kMomWarps];     // that unit's first slot
   uint32_t uexp[kMomMaxUnits];   // unit: e_0 .. e_{n-2}, 4 bits each
   uint8_t ulen[kMomMaxUnits];    // its entries: e_{n-1} = 0 .. ulen - 1
 };
@@ -68,15 +69,23 @@ __device__ __forceinline__ void mom_dmma(double &c0, double &c1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-__host__ __device__ inline int mom_in_doubles(int n, int nv, bool weighted) {  // one input stage, even (16-byte aligned)
-  const int d = kMomRT * (n + nv + (weighted ? nv : 0));
-  return (d + 1) & ~1;
+// one ring slot: X [RT][n] | V_v rows | S_v rows (bulk copies) | a row of ones the producer
+// writes (0 past the slab).  The per-row vectors are kMomVS apart (= 8 banks: the quads of a warp
+// read up to four of them at the same row without conflicts); every vector starts 16-byte aligned
+// (bulk-copy targets).  (The consumers square V_v and s_v themselves: scalar FP64 work in the
+// producer waits behind its sub-partition's DMMAs and starves the ring -- measured 0.474 vs
+// 0.431 ms.)
+constexpr int kMomVS = kMomRT + 4;
+__host__ __device__ inline int mom_vec_off(int n) { return (kMomRT * n + 1) & ~1; }
+__host__ __device__ inline int mom_in_doubles(int n, int nv, bool weighted) {
+  return mom_vec_off(n) + kMomVS * (nv + (weighted ? nv : 0) + 1);
 }
 
-static size_t mom_smem(int nT, int n, int nv, bool weighted) {
-  return sizeof(double) * ((size_t)nT * 8 * kMomRTP + 2 * 16 * kMomRTP + 2 * kMaxVars * kMomRT +
+static size_t mom_smem(int nT, int n, int nv, bool weighted, bool generic = true) {
+  return sizeof(double) * ((size_t)nT * 8 * kMomRTP + (generic ? kMomWarps * kMaxVars * kMomRT : 0) +
+                           kMomIS * kMaxVars * kMomRT +
                            (size_t)kMomIS * mom_in_doubles(n, nv, weighted)) +
-         sizeof(uint64_t) * kMomIS;
+         sizeof(uint64_t) * 3 * kMomIS;
 }
 
 // ---- the simplex's units and the warps' shares (one algorithm for the host plan and the
@@ -85,7 +94,9 @@ struct MomTab {
   int nu, ns;
   int8_t ex[kMomMaxUnits][kMaxVars];  // e_0 .. e_{N-2} of unit u (e_{N-1} runs over 0 .. len - 1)
   int len[kMomMaxUnits], slot[kMomMaxUnits];
-  int wu[kMomWarps + 1];              // units of warp w: [wu[w], wu[w + 1])
+  int nT;                            // 8-slot tiles
+  int tb[kMomWarps + 1];              // tiles of warp w: [tb[w], tb[w + 1]) (moments and monomials)
+  int wu[kMomWarps], wue[kMomWarps];  // units overlapping warp w's slots [8 tb[w], min(8 tb[w + 1], ns))
 };
 // units in lexicographic order (e_0 slowest, e_{N-2} fastest); nu = 0 when the simplex is too large
 __host__ __device__ constexpr MomTab mom_tab(int N, int D) {
@@ -116,14 +127,20 @@ __host__ __device__ constexpr MomTab mom_tab(int N, int D) {
     if (k < 0) break;
   }
   t.ns = slot;
-  // generation: contiguous unit ranges of ~ns / 16 entries per warp
-  int u = 0, sl = 0;
+  // every warp accumulates a contiguous range of tiles (the remainder to the first warps: the
+  // last ones stay lighter) and generates the monomials of exactly those slots
+  t.nT = (t.ns + 7) / 8;
+  const int base = t.nT / kMomWarps, rem = t.nT % kMomWarps;
+  t.tb[0] = 0;
+  for (int w = 0; w < kMomWarps; ++w) t.tb[w + 1] = t.tb[w] + base + (w < rem ? 1 : 0);
   for (int w = 0; w < kMomWarps; ++w) {
+    const int s0 = 8 * t.tb[w], s1 = 8 * t.tb[w + 1] < t.ns ? 8 * t.tb[w + 1] : t.ns;
+    int u = 0;
+    while (u < t.nu && t.slot[u] + t.len[u] <= s0) ++u;
     t.wu[w] = u;
-    const int target = (t.ns * (w + 1) + kMomWarps / 2) / kMomWarps;
-    while (u < t.nu && (w == kMomWarps - 1 || sl + t.len[u] / 2 < target)) sl += t.len[u++];
+    while (u < t.nu && t.slot[u] < s1) ++u;
+    t.wue[w] = s1 > s0 ? u : t.wu[w];
   }
-  t.wu[kMomWarps] = t.nu;
   return t;
 }
 template <int N, int D>
@@ -152,12 +169,19 @@ __host__ __device__ constexpr MomUnit mom_unit(int u) {
   return x;
 }
 template <int N, int D>
-__host__ __device__ constexpr int mom_wu(int w) { return MomC<N, D>::t.wu[w]; }
+__host__ __device__ constexpr int mom_wu(int w, int which) {  // 0: first unit, 1: end unit, 2/3: slot window
+  const MomTab &T = MomC<N, D>::t;
+  if (which == 0) return T.wu[w];
+  if (which == 1) return T.wue[w];
+  if (which == 2) return 8 * T.tb[w];
+  return 8 * T.tb[w + 1] < T.ns ? 8 * T.tb[w + 1] : T.ns;
+}
 
-// a11 for the units [UI, UE) of one warp, every index and exponent a compile-time constant:
-// the unit's prefix from the power table (or, for the next e_{N-2} of the same prefix, one DMUL
-// from the previous unit's), then e_{N-1} = 0 .. len - 1 one DMUL each; lane = row
-template <int N, int D, int UB, int UI, int UE>
+// a11 for the units [UI, UE) overlapping the warp's slots [S0, S1), every index and exponent a
+// compile-time constant: the unit's prefix from the power table (or, for the next e_{N-2} of the
+// same prefix, one DMUL from the previous unit's), then its entries in the window, one DMUL each
+// (lane = row)
+template <int N, int D, int UB, int UI, int UE, int S0, int S1>
 __device__ __forceinline__ void mom_gen_units(const double (&pw)[kMaxVars][16], double *dst, double am_prev) {
   if constexpr (UI < UE) {
     constexpr MomUnit U = mom_unit<N, D>(UI);
@@ -174,29 +198,31 @@ __device__ __forceinline__ void mom_gen_units(const double (&pw)[kMaxVars][16], 
           one = false;
         }
     }
-    double m = am;
+    constexpr int jb = S0 > U.slot ? S0 - U.slot : 0;
+    constexpr int je = S1 - U.slot < U.len ? S1 - U.slot : U.len;
+    double m = jb == 0 ? am : am * pw[N - 1][jb];
 #pragma unroll
-    for (int j = 0; j < U.len; ++j) {
+    for (int j = jb; j < je; ++j) {
       dst[(U.slot + j) * kMomRTP] = m;
-      if (j + 1 < U.len) m *= pw[N - 1][1];
+      if (j + 1 < je) m *= pw[N - 1][1];
     }
-    mom_gen_units<N, D, UB, UI + 1, UE>(pw, dst, am);
+    mom_gen_units<N, D, UB, UI + 1, UE, S0, S1>(pw, dst, am);
   }
 }
 
 template <int N, int D, int W>
-__device__ __forceinline__ void mom_gen_warp(const double *u, double *dst) {
+__device__ __forceinline__ void mom_gen_warp(const double (&u)[kMaxVars], double *dst) {
   // power table u_k^j (j <= D; only the entries this warp's units use survive)
   double pw[kMaxVars][16];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     pw[k][0] = 1.0;
-    pw[k][1] = u[k * kMomRT];
+    pw[k][1] = u[k];
 #pragma unroll
     for (int j = 2; j <= D; ++j) pw[k][j] = pw[k][j - 1] * pw[k][1];
   }
-  constexpr int ub = mom_wu<N, D>(W), ue = mom_wu<N, D>(W + 1);
-  mom_gen_units<N, D, ub, ub, ue>(pw, dst, 1.0);
+  constexpr int ub = mom_wu<N, D>(W, 0), ue = mom_wu<N, D>(W, 1), s0 = mom_wu<N, D>(W, 2), s1 = mom_wu<N, D>(W, 3);
+  mom_gen_units<N, D, ub, ub, ue, s0, s1>(pw, dst, 1.0);
 }
 
 // N, D > 0: the monomial step specialised for that simplex (mom_gen_warp); N = 0: generic
@@ -207,12 +233,14 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
   const int n = a.n, nv = a.nv;
   const bool wtd = a.S != nullptr;
   const int nslotp = a.nT * 8;
-  double *sM = msm;                                   // [nslotp][RTP]
-  double *sW = sM + (size_t)nslotp * kMomRTP;         // [2][16][RTP]
-  double *sU = sW + 2 * 16 * kMomRTP;                 // [2][kMaxVars][RT]
-  double *sIn = sU + 2 * kMaxVars * kMomRT;           // [IS][INB]
+  double *sM = msm;                                   // [nslotp][RTP]  monomials (each warp its own slots)
+  double *sUg = sM + (size_t)nslotp * kMomRTP;        // [warps][kMaxVars][RT]  u (generic monomial step)
+  double *sXt = sUg + (N > 0 ? 0 : kMomWarps * kMaxVars * kMomRT);  // [IS][kMaxVars][RT]  X transposed
+  double *sIn = sXt + kMomIS * kMaxVars * kMomRT;     // [IS][INB]  raw inputs X | V | S
   const int INB = mom_in_doubles(n, nv, wtd);
-  uint64_t *full = reinterpret_cast<uint64_t *>(sIn + kMomIS * INB);
+  uint64_t *rfull = reinterpret_cast<uint64_t *>(sIn + kMomIS * INB);  // [IS] raw inputs landed
+  uint64_t *wfull = rfull + kMomIS;                                     // [IS] X transposed, ones row written
+  uint64_t *sempty = wfull + kMomIS;                                    // [IS] every consumer warp done
   __shared__ double sXc[kMaxVars], sXs[kMaxVars];  // the transform: c_k, 2^-e_k
 
   // slab: whole 32-row stages, so bulk-copy sources stay 16-byte aligned
@@ -230,67 +258,66 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
     sXs[threadIdx.x] = threadIdx.x < n ? ldexp(1.0, -a.basis->xe[threadIdx.x]) : 0.0;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kMomIS; ++i) mbar_init(smem_u32(full + i), 1);
+    for (int i = 0; i < kMomIS; ++i) {
+      mbar_init(smem_u32(rfull + i), 1);
+      mbar_init(smem_u32(wfull + i), 1);            // the producer (lane 0 after __syncwarp)
+      mbar_init(smem_u32(sempty + i), kMomWarps);   // lane 0 of every consumer warp after __syncwarp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  auto issue = [&](int s) {  // thread 0: the bulk copies of stage s into its input stage
-    const int st = s % kMomIS;
-    double *dst = sIn + st * INB;
-    const int64_t r0 = r_begin + (int64_t)s * kMomRT;
-    const uint32_t bx = kMomRT * n * 8, bv = kMomRT * 8;
-    const uint32_t bar = smem_u32(full + st);
-    mbar_expect_tx(bar, bx + nv * bv * (wtd ? 2 : 1));
-    bulk_g2s(smem_u32(dst), a.X + r0 * n, bx, bar);
-    for (int v = 0; v < nv; ++v) bulk_g2s(smem_u32(dst + kMomRT * n + v * kMomRT), a.V + (int64_t)v * a.K + r0, bv, bar);
-    if (wtd)
-      for (int v = 0; v < nv; ++v)
-        bulk_g2s(smem_u32(dst + kMomRT * (n + nv) + v * kMomRT), a.S + (int64_t)v * a.K + r0, bv, bar);
-  };
-  // the input warp (lane = row): u and the row weights of stage s into buffer s & 1
-  auto process = [&](int s) {
-    const int b = s & 1;
-    const int64_t r = r_begin + (int64_t)s * kMomRT + lane;
-    const bool valid = r < r_end;
-    const double *src = nullptr;
-    if (full_stage(s)) {
-      mbar_wait(smem_u32(full + s % kMomIS), (uint32_t)((s / kMomIS) & 1));
-      src = sIn + (s % kMomIS) * INB;
-    }
-#pragma unroll
-    for (int k = 0; k < kMaxVars; ++k) {
-      if (k < n) {
-        const double x = src ? src[lane * n + k] : (valid ? a.X[r * n + k] : 0.0);
-        sU[(b * kMaxVars + k) * kMomRT + lane] = valid ? (x - sXc[k]) * sXs[k] : 0.0;
+  if (wid == kMomWarps) {
+    // ---- producer: raw inputs of stage s into ring slot s % IS (TMA, or plain loads for a tail
+    // or unaligned stage), then the row weights of the stage --------------------------------------
+    auto issue = [&](int s) {  // lane 0
+      const int st = s % kMomIS;
+      double *dst = sIn + st * INB;
+      const int64_t r0 = r_begin + (int64_t)s * kMomRT;
+      const uint32_t bx = kMomRT * n * 8, bv = kMomRT * 8;
+      const uint32_t bar = smem_u32(rfull + st);
+      mbar_expect_tx(bar, bx + nv * bv * (wtd ? 2 : 1));
+      bulk_g2s(smem_u32(dst), a.X + r0 * n, bx, bar);
+      double *dv = dst + mom_vec_off(n);
+      for (int v = 0; v < nv; ++v) bulk_g2s(smem_u32(dv + v * kMomVS), a.V + (int64_t)v * a.K + r0, bv, bar);
+      if (wtd)
+        for (int v = 0; v < nv; ++v) bulk_g2s(smem_u32(dv + (nv + v) * kMomVS), a.S + (int64_t)v * a.K + r0, bv, bar);
+    };
+    if (lane == 0)
+      for (int s = 0; s < kMomLead && s < ns; ++s)
+        if (full_stage(s)) issue(s);
+    for (int s = 0; s < ns; ++s) {
+      const int st = s % kMomIS;
+      double *raw = sIn + st * INB;
+      {  // stage s + Lead: its slot is free once the consumers are done with stage s + Lead - IS
+        const int t = s + kMomLead, tp = t - kMomIS;
+        if (tp >= 0 && t < ns) mbar_wait(smem_u32(sempty + tp % kMomIS), (uint32_t)((tp / kMomIS) & 1));
+        if (lane == 0 && t < ns && full_stage(t)) issue(t);
       }
-    }
-    double *w = sW + b * 16 * kMomRTP + lane;
-    for (int i = 0; i < 16; ++i) w[i * kMomRTP] = 0.0;
-    if (valid) {
-      if (!wtd) w[0] = 1.0;
-      for (int v = 0; v < nv; ++v) {
-        const double vv = src ? src[kMomRT * n + v * kMomRT + lane] : a.V[(int64_t)v * a.K + r];
-        if (wtd) {
-          const double sv = src ? src[kMomRT * (n + nv) + v * kMomRT + lane] : a.S[(int64_t)v * a.K + r];
-          const double s2 = sv * sv;
-          w[(3 * v) * kMomRTP] = s2;
-          w[(3 * v + 1) * kMomRTP] = s2 * vv;
-          w[(3 * v + 2) * kMomRTP] = s2 * vv * vv;
-        } else {
-          w[(1 + v) * kMomRTP] = vv;
-          w[(1 + nv + v) * kMomRTP] = vv * vv;
+      const int64_t r = r_begin + (int64_t)s * kMomRT + lane;
+      const bool valid = r < r_end;
+      if (full_stage(s)) {
+        mbar_wait(smem_u32(rfull + st), (uint32_t)((s / kMomIS) & 1));
+      } else {  // plain loads (zeros past the slab)
+        for (int k = 0; k < n; ++k) raw[lane * n + k] = valid ? a.X[r * n + k] : 0.0;
+        for (int v = 0; v < nv; ++v) {
+          raw[mom_vec_off(n) + v * kMomVS + lane] = valid ? a.V[(int64_t)v * a.K + r] : 0.0;
+          if (wtd) raw[mom_vec_off(n) + (nv + v) * kMomVS + lane] = valid ? a.S[(int64_t)v * a.K + r] : 0.0;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(rfull + st));  // (completes the phase: count 1, no tx)
       }
+      // X transposed for the consumers' lane = row reads
+      for (int k = 0; k < n; ++k) sXt[(st * kMaxVars + k) * kMomRT + lane] = raw[lane * n + k];
+      // the row of ones (the constant weight; 0 past the slab)
+      raw[mom_vec_off(n) + (wtd ? 2 * nv : nv) * kMomVS + lane] = valid ? 1.0 : 0.0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(wfull + st));
     }
-  };
-  constexpr int kInWarp = kMomWarps - 1;  // fewest tiles (the host gives the remainder to the first warps)
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kMomIS && s < ns; ++s)
-      if (full_stage(s)) issue(s);
-  if (wid == kInWarp && ns > 0) process(0);
-  __syncthreads();
+    return;
+  }
 
+  // ---- consumers: u of the lane's row, the monomials and the moments of the warp's own tiles ----
   const int tb = a.wtile[wid], tc = a.wtile[wid + 1] - tb;
   double acc[TPW][WT][2];
 #pragma unroll
@@ -299,15 +326,52 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
     for (int h = 0; h < WT; ++h) acc[q][h][0] = acc[q][h][1] = 0.0;
   double *part = a.part + (size_t)blockIdx.x * a.nT * WT * 64;
   bool first = true;
-  const int ub = a.wunit[wid], ue = a.wunit[wid + 1];
+  const int s0w = 8 * tb, s1w = 8 * (tb + tc) < a.nslot ? 8 * (tb + tc) : a.nslot;  // the warp's slots
   const uint32_t inc = n >= 2 ? 1u << (4 * (n - 2)) : 0u;  // e_{n-2} + 1 in a unit's packed exponents
+  // this lane's weight (row lane / 4 of each weight tile of the A operand), from the slot's vectors:
+  // unweighted w = 0: 1, w = 1 + v: V_v, w = 1 + nv + v: V_v^2; weighted w = 3 v + p: s_v^2 V_v^p;
+  // other w: 0.  wv: the vector read (the ones row for 1), wsq: squared, ws: times s_v^2, wz: 0
+  int wv[WT], ws[WT];
+  bool wsq[WT], wz[WT];
+  {
+    const int v0 = mom_vec_off(n), ones = v0 + (wtd ? 2 * nv : nv) * kMomVS;
+#pragma unroll
+    for (int h = 0; h < WT; ++h) {
+      const int w = 8 * h + (lane >> 2);
+      wv[h] = ones;
+      ws[h] = -1;
+      wsq[h] = false;
+      wz[h] = false;
+      if (wtd) {
+        if (w < 3 * nv) {
+          const int v = w / 3, p = w % 3;
+          ws[h] = v0 + (nv + v) * kMomVS;
+          if (p > 0) wv[h] = v0 + v * kMomVS;
+          wsq[h] = p == 2;
+        } else {
+          wz[h] = true;
+        }
+      } else if (w >= 1 && w <= 2 * nv) {
+        wv[h] = v0 + ((w - 1) % nv) * kMomVS;
+        wsq[h] = w > nv;
+      } else if (w != 0) {
+        wz[h] = true;
+      }
+    }
+  }
 
   for (int s = 0; s < ns; ++s) {
-    const int b = s & 1;
-    if (threadIdx.x == 0 && s + kMomIS < ns && full_stage(s + kMomIS)) issue(s + kMomIS);  // its stage was read
+    const int st = s % kMomIS;
+    const uint32_t ph = (uint32_t)((s / kMomIS) & 1);
+    mbar_wait(smem_u32(rfull + st), ph);
+    mbar_wait(smem_u32(wfull + st), ph);
+    const double *xt = sXt + st * kMaxVars * kMomRT + lane;
+    // a10 for the lane's row: u = (x - c) 2^-e (rows past the slab have zero weights)
+    double u[kMaxVars];
+#pragma unroll
+    for (int k = 0; k < kMaxVars; ++k) u[k] = k < n ? (xt[k * kMomRT] - sXc[k]) * sXs[k] : 0.0;
     // ---- a11: the monomials of the warp's slots for the stage's 32 rows (lane = row) ----------
     if constexpr (N > 0) {
-      const double *u = sU + b * kMaxVars * kMomRT + lane;
       switch (wid) {
 #define RP_MG(w) \
   case w: mom_gen_warp<N, D, w>(u, sM + lane); break;
@@ -315,44 +379,56 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
         RP_MG(11) RP_MG(12) RP_MG(13) RP_MG(14) RP_MG(15)
 #undef RP_MG
       }
-    } else {
-      const double *u = sU + b * kMaxVars * kMomRT + lane;
-      const double ul = u[(n - 1) * kMomRT], us = n >= 2 ? u[(n - 2) * kMomRT] : 1.0;
-      int slot = a.wslot[wid];
+    } else if (s1w > s0w) {
+      double *uw = sUg + wid * kMaxVars * kMomRT + lane;  // u by runtime variable index
+#pragma unroll
+      for (int k = 0; k < kMaxVars; ++k) uw[k * kMomRT] = u[k];
+      const double ul = uw[(n - 1) * kMomRT], us = n >= 2 ? uw[(n - 2) * kMomRT] : 1.0;
+      int slot = a.wuslot[wid];
       uint32_t pex = 0;
       double am = 1.0;
-      for (int ui = ub; ui < ue; ++ui) {
+      for (int ui = a.wunit[wid]; slot < s1w; ++ui) {
         const uint32_t ex = a.uexp[ui];
         const int len = a.ulen[ui];
-        if (ui > ub && n >= 2 && ex == pex + inc) {
+        if (ui > a.wunit[wid] && n >= 2 && ex == pex + inc) {
           am *= us;  // the next e_{n-2} of the same prefix
         } else {     // a new prefix: u_0^e_0 ... u_{n-2}^e_{n-2} by repeated multiplication
           am = 1.0;
           for (int k = 0; k + 1 < n; ++k) {
-            const double uk = u[k * kMomRT];
+            const double uk = uw[k * kMomRT];
             for (int e = (int)((ex >> (4 * k)) & 15u); e > 0; --e) am *= uk;
           }
         }
         pex = ex;
+        const int jb = s0w > slot ? s0w - slot : 0, je = s1w - slot < len ? s1w - slot : len;
         double m = am;
+        for (int j = 0; j < jb; ++j) m *= ul;
         double *dst = sM + (size_t)slot * kMomRTP + lane;
-        for (int j = 0; j < len; ++j) {
+        for (int j = jb; j < je; ++j) {
           dst[j * kMomRTP] = m;
           m *= ul;
         }
         slot += len;
       }
     }
-    __syncthreads();
+    __syncwarp();
     // ---- a12: moments[w][e] += W^T Mon over the stage's 8 k-steps --------------------------------
     {
-      const double *wb = sW + b * 16 * kMomRTP + (lane >> 2) * kMomRTP + (lane & 3);
+      const double *raw = sIn + st * INB + (lane & 3);
       const double *mb = sM + (size_t)(tb * 8 + (lane >> 2)) * kMomRTP + (lane & 3);
 #pragma unroll 2
       for (int ks = 0; ks < kMomRT / 4; ++ks) {
         double av[WT];
 #pragma unroll
-        for (int h = 0; h < WT; ++h) av[h] = wb[h * 8 * kMomRTP + ks * 4];
+        for (int h = 0; h < WT; ++h) {
+          const double x = raw[wv[h] + ks * 4];
+          double w = wsq[h] ? x * x : x;
+          if (wtd && ws[h] >= 0) {
+            const double sv = raw[ws[h] + ks * 4];
+            w *= sv * sv;
+          }
+          av[h] = wz[h] ? 0.0 : w;
+        }
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
           if (q < tc) {
@@ -363,7 +439,8 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
         }
       }
     }
-    if (wid == kInWarp && s + 1 < ns) process(s + 1);
+    __syncwarp();  // the warp has read stage s (and its monomial rows are rewritten next stage)
+    if (lane == 0) mbar_arrive(smem_u32(sempty + st));
     if (((s + 1) % kMomFlush) == 0 || s + 1 == ns) {
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
@@ -384,10 +461,9 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
       }
       first = false;
     }
-    __syncthreads();
   }
-  if (ns == 0)  // empty slab: zero partial
-    for (int i = threadIdx.x; i < a.nT * WT * 64; i += blockDim.x) part[i] = 0.0;
+  if (ns == 0)  // empty slab: zero partial (this warp's tiles)
+    for (int i = lane; i < tc * WT * 64; i += 32) part[(size_t)tb * WT * 64 + i] = 0.0;
 }
 
 // fixed-order sum of the per-CTA partials: 4 quarter sums per element (CTAs q, q + 4, ...),
@@ -539,29 +615,19 @@ cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h, const 
     a.uexp[i] = pk;
     a.ulen[i] = (uint8_t)tab.len[i];
   }
-  for (int w = 0; w <= kMomWarps; ++w) {
+  for (int w = 0; w <= kMomWarps; ++w) a.wtile[w] = (int16_t)tab.tb[w];
+  for (int w = 0; w < kMomWarps; ++w) {
     a.wunit[w] = (int16_t)tab.wu[w];
-    a.wslot[w] = (int16_t)(tab.wu[w] < tab.nu ? tab.slot[tab.wu[w]] : tab.ns);
+    a.wuslot[w] = (int16_t)(tab.wu[w] < tab.nu ? tab.slot[tab.wu[w]] : tab.ns);
   }
-  // moments: nT tiles over the warps, the remainder to the first ones (the last warp also
-  // prepares the next stage's inputs)
-  {
-    const int base = sh.nT / kMomWarps, rem = sh.nT % kMomWarps;
-    int t = 0;
-    for (int w = 0; w < kMomWarps; ++w) {
-      a.wtile[w] = (int16_t)t;
-      t += base + (w < rem ? 1 : 0);
-    }
-    a.wtile[kMomWarps] = (int16_t)t;
-  }
-  const size_t smem = mom_smem(sh.nT, n, n_v, wtd);
+  const size_t smem = mom_smem(sh.nT, n, n_v, wtd), smem_spec = mom_smem(sh.nT, n, n_v, wtd, false);
   cudaError_t e;
   const char *gen = getenv("RP_MOM_GENERIC");  // measurement: the runtime monomial step only
   const bool spec = !(gen && gen[0] == '1');
   // the BASELINE shapes (tiny: 3 variables, degree 2; polybench: 4, degree 3; fitheavy: 4,
   // degree 4) with their monomial step specialised at compile time; the rest generic
 #define RP_MOM_SPEC(WT_, TPW_, N_, D_) \
-  if (spec && sh.WT == WT_ && sh.TPW == TPW_ && n == N_ && sh.D == D_) e = launch_mom_t<WT_, TPW_, N_, D_>(a, gx, smem, s); else
+  if (spec && sh.WT == WT_ && sh.TPW == TPW_ && n == N_ && sh.D == D_) e = launch_mom_t<WT_, TPW_, N_, D_>(a, gx, smem_spec, s); else
 #define RP_MOM_CASE(WT_, TPW_) \
   if (sh.WT == WT_ && sh.TPW == TPW_) e = launch_mom_t<WT_, TPW_, 0, 0>(a, gx, smem, s); else
   RP_MOM_SPEC(1, 4, 4, 8) RP_MOM_SPEC(2, 4, 4, 8) RP_MOM_SPEC(1, 2, 4, 6) RP_MOM_SPEC(2, 2, 4, 6)
