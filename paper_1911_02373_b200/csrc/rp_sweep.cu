@@ -939,19 +939,22 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
           const int32_t Dk = k == 0 ? Da : (k == 1 ? Db : Dc);
           if (k == hv) {
             Dv = Dk;
-          } else {
-            const int64_t Pk = __ldg(&gd->P[k]);
-            fcon *= (uint64_t)(((int64_t)Dk + Pk - 1) / Pk);
+          } else {  // (32-bit unsigned division: D + P - 1 < 2^32; a 64-bit one costs ~70 instructions)
+            const uint32_t Pk = (uint32_t)__ldg(&gd->P[k]);
+            fcon *= (uint64_t)(((uint32_t)Dk + Pk - 1u) / Pk);
           }
         }
       }
       int tend = te;  // members in P1 P2 order: stop at the first tile that fails a3 everywhere
-      if (sorted)
-        for (int tile = tb + 1; tile < te; ++tile)
-          if (__ldg(&grec[tile * 8].P01) > maxD1sq) {
-            tend = tile;
+      if (sorted)  // (the group's tiles tested by the lanes at once)
+        for (int t0 = tb + 1; t0 < te; t0 += 32) {
+          const int tile = t0 + lane;
+          const unsigned stop = __ballot_sync(0xffffffffu, tile < te && __ldg(&grec[tile * 8].P01) > maxD1sq);
+          if (stop) {
+            tend = t0 + __ffs(stop) - 1;
             break;
           }
+        }
       int tile = tb;
       for (; tile < tend; ++tile) {
         const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
