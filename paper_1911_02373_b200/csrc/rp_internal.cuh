@@ -88,6 +88,8 @@ struct GroupDesc {
   int32_t P[3], pad;                       // the members' P (P[hv] unused)
   int32_t off[4][kGS];                     // lane q, term s: pe (s < kGS1: of w_{1+q}; else of w_0's share)
   double y[4][kGS];                        // Y_pe of that term (0 for padding)
+  double ype[kMaxPE];                      // Y_pe by pe (0 past nPE): the setup DMMA's B operand
+  int8_t ipe[kMaxPE];                      // i_pe = exponent of u_hv in m_pe (-1 past nPE)
 };
 
 struct CfgTable {

@@ -329,6 +329,19 @@ __device__ void group_y(const DevProg &pg, GroupDesc &gd) {
     }
   for (int q = 0; q < 4; ++q)  // padding terms read a valid column with Y = 0
     for (int s = 0; s < kGS; ++s) gd.off[q][s] = gd.off[q][s] < 0 ? 0 : gd.off[q][s];
+  for (int pe = 0; pe < kMaxPE; ++pe) {  // the same values by pe, with the Horner exponent
+    double y = 0.0;
+    int8_t ip = -1;
+    if (pe < pg.nPE) {
+      y = 1.0;
+      for (int k = 0; k < pg.p; ++k)
+        if (k != gd.hv)
+          for (int t = 0; t < pg.pe_exp[pe][k]; ++t) y *= u[k];
+      ip = pg.pe_exp[pe][gd.hv];
+    }
+    gd.ype[pe] = y;
+    gd.ipe[pe] = ip;
+  }
 }
 
 // One CTA per program, after k_plan_configs.  Candidate groups: for every Horner variable whose
@@ -886,45 +899,40 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       st.e = better ? E : st.e;
     }
   };
-  if (wid * 8 < tmax) {
-    // factored tiles (k_plan_groups): per group, lane q of a quad forms w_{k,1+q} and its share of
-    // w_{k,0} for its tuple from the staged C (kGS terms per polynomial), and the quad sums the
-    // shares; each tile of the group is then one DMMA per polynomial: C = w_{k,0},
-    // A = w_{k,1+q}, B = x^{1+q} of configuration lane / 4
+#ifdef RP_SWEEP_PROBE
+  const bool probe_on = false;  // timing probe: the prologue and outputs only
+#else
+  const bool probe_on = true;
+#endif
+  if (probe_on && wid * 8 < tmax) {
+    // factored tiles (k_plan_groups): per group, the octet's Horner coefficients w_{k,i} are one
+    // small DMMA product with the staged C (4.338 -> 4.282 ms against lane-wise FMA sums of
+    // bank-conflicted shared-memory reads and quad shuffles); each tile of the group is then one
+    // DMMA per polynomial: C = w_{k,0}, A = w_{k,1+q}, B = x^{1+q} of configuration lane / 4
     const int q = lane & 3;
-    const double *crow = sC + t * CS;
     for (int gi = 0; gi < ngr; ++gi) {
       const GroupDesc *gd = gdesc + gi;
       const int tb = __ldg(&gd->tile_begin), te = __ldg(&gd->tile_end);
       if (sorted && __ldg(&grec[tb * 8].P01) > maxD1sq) continue;  // a3: every member fails
-      // lane q: w_{k,1+q} (kGS1 terms) and its share of w_{k,0}
       double w1[NPOLY], a0[NPOLY];
+      // on DMMA, A = the staged C of the octet (the dense tiles' fragments: conflict-free), B =
+      // Y_pe routed to column 2q when i_pe = 1 + q and to column 2q + 1 when i_pe = 0, so lane q
+      // receives w_{k,1+q} and w_{k,0} of its tuple directly (no quad sum)
       {
-        int off[kGS];
-        double y[kGS];
+        const int col = lane >> 2, want = (col & 1) ? 0 : 1 + (col >> 1);
+        double bfr[KS];
 #pragma unroll
-        for (int s = 0; s < kGS; ++s) {
-          off[s] = __ldg(&gd->off[q][s]);
-          y[s] = __ldg(&gd->y[q][s]);
+        for (int ks = 0; ks < KS; ++ks) {
+          const int pe = ks * 4 + (lane & 3);
+          bfr[ks] = __ldg(&gd->ipe[pe]) == want ? __ldg(&gd->ype[pe]) : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) {
-          const double *ck = crow + k * NPE;
-          double s1 = ck[off[0]] * y[0];
+          double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int s = 1; s < kGS1; ++s) s1 = fma(ck[off[s]], y[s], s1);
-          double s0 = ck[off[kGS1]] * y[kGS1];
-#pragma unroll
-          for (int s = kGS1 + 1; s < kGS; ++s) s0 = fma(ck[off[s]], y[s], s0);
-          w1[k] = s1;
-          a0[k] = s0;
-        }
-        // w_{k,0} itself (the quad's four shares), the C operand of every tile's one DMMA per
-        // polynomial (measured 4.526 -> 4.451 ms against a second DMMA with B = 1 summing the shares)
-#pragma unroll
-        for (int k = 0; k < NPOLY; ++k) {
-          const double t = a0[k] + __shfl_xor_sync(0xffffffffu, a0[k], 1);
-          a0[k] = t + __shfl_xor_sync(0xffffffffu, t, 2);
+          for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, arow[k * NPE + ks * 4], bfr[ks]);
+          w1[k] = c0;
+          a0[k] = c1;
         }
       }
       // a6 per group: every grid factor but P_hv's is the group's (exact, once per group)
