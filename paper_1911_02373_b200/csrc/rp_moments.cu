@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
 #pragma unroll
     for (int k = 0; k < kMaxVars; ++k) u[k] = k < n ? (xt[k * kMomRT] - sXc[k]) * sXs[k] : 0.0;
     // ---- a11: the monomials of the warp's slots for the stage's 32 rows (lane = row) ----------
+#ifndef RP_MOM_PROBE_NOGEN  // (timing probe: no monomials, results meaningless)
     if constexpr (N > 0) {
       switch (wid) {
 #define RP_MG(w) \
@@ -411,8 +412,12 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
         slot += len;
       }
     }
+#endif
     __syncwarp();
     // ---- a12: moments[w][e] += W^T Mon over the stage's 8 k-steps --------------------------------
+#ifdef RP_MOM_PROBE_NODMMA
+    if (false)
+#endif
     {
       const double *raw = sIn + st * INB + (lane & 3);
       const double *mb = sM + (size_t)(tb * 8 + (lane >> 2)) * kMomRTP + (lane & 3);
