@@ -1036,11 +1036,17 @@ rp_status rp_fit_svd(const double *X, const double *V, int64_t K, int32_t n_v, c
   RP_CUDA(tb.alloc(sizeof(GramBasis), s));
   RP_CUDA(cudaMemcpyAsync(tb.p, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
   RP_CUDA(launch_xform_to_basis(xf, n, (GramBasis *)tb.p, s));
-  const size_t wsb = tsqr_workspace_bytes(nc, n_v, tsqr_leaves(K, n_v));
-  RP_CUDA(tws.alloc(wsb, s));
   RP_CUDA(tR.alloc((size_t)n_v * nc * nc * 8, s));
-  RP_CUDA(launch_tsqr((const GramBasis *)tb.p, dX, dV, nullptr, nullptr, K, n, nc, n_v, tws.p, wsb,
-                      (double *)tR.p, s));
+  if (gram_dd_supported(gb, n_v, K)) {  // R from the double-double Gram (rp_moments.cu)
+    const size_t wsb = gram_dd_workspace_bytes(gb, n_v, K);
+    RP_CUDA(tws.alloc(wsb, s));
+    RP_CUDA(launch_gram_dd_chol((const GramBasis *)tb.p, gb, dX, dV, K, n_v, tws.p, wsb, (double *)tR.p, s));
+  } else {  // Householder TSQR
+    const size_t wsb = tsqr_workspace_bytes(nc, n_v, tsqr_leaves(K, n_v));
+    RP_CUDA(tws.alloc(wsb, s));
+    RP_CUDA(launch_tsqr((const GramBasis *)tb.p, dX, dV, nullptr, nullptr, K, n, nc, n_v, tws.p, wsb,
+                        (double *)tR.p, s));
+  }
   rp_status sst = svd_finish((const double *)tR.p, n_v, nc, basis->n_num, coef_out, sigma_out, info, s);
   if (sst == RP_ERR_CUDA) return sst;
   double hxf[2 * RP_MAX_VARS];

@@ -168,6 +168,11 @@ size_t gram_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, int num_
 // a12 as a moment contraction (rp_moments.cu): the default where the exponent-sum simplex is small
 bool mom_supported(const GramBasis &h_basis, int n_v, bool weighted);
 size_t mom_partial_elems(const GramBasis &h_basis, int n_v, int64_t K, bool weighted);
+// f1: R = chol(A^T A) with the Gram and the factorisation in double-double (rp_moments.cu)
+bool gram_dd_supported(const GramBasis &h_basis, int n_v, int64_t K);
+size_t gram_dd_workspace_bytes(const GramBasis &h_basis, int n_v, int64_t K);
+cudaError_t launch_gram_dd_chol(const GramBasis *d_basis, const GramBasis &h_basis, const double *X, const double *V,
+                                int64_t K, int n_v, void *ws, size_t ws_bytes, double *R, cudaStream_t s);
 cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h_basis, const double *X, const double *V,
                             const double *S, int64_t K, int n_v, double *G, double *d_part, size_t part_elems,
                             cudaStream_t s);

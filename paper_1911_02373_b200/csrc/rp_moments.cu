@@ -650,4 +650,382 @@ cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h, const 
   return cudaGetLastError();
 }
 
+
+// ============================================================================================
+// f1: the triangular factor R of A = [M(u) | -V N(u)] from its Gram in DOUBLE-DOUBLE.
+//
+// The paper solves the homogeneous system by SVD because the normal equations square the
+// condition number.  That loss is a loss of precision: with G = A^T A
+// accurate to ~1e-30 relative (double-double moments: every entry is a weighted moment of one
+// monomial, as in k_gram_mom) and its Cholesky factor computed in double-double, R = chol(G)
+// carries the same information as Householder's R to well below FP64 rounding for
+// cond(A) < ~1e13 (|delta sigma_i| <~ 1e-30 sigma_max^2 / sigma_i), so the SVD of R (k_svd_gk)
+// meets the same gates as after the TSQR -- including sigma_min = 0 of exact recovery (the
+// Cholesky pivot of a null direction is ~1e-30 relative and is set to an exact zero).  The
+// moments are accumulated without rounding in their high part: term t = w m is split as
+// t_hi = fma(w_h, m_h, sigma) - sigma (a multiple of ulp(sigma) / 2, exact; sigma a power of two
+// >= 2 x the stage's bound) and the remainder t - t_hi into a low sum; every 64 rows both are
+// added into a double-double accumulator.  rp_fit_svd uses it for K >= 4 n_c (RP_SVD_R=tsqr
+// keeps the Householder TSQR, which also serves small K, weighted rows and rp_tsqr_accumulate).
+// ============================================================================================
+struct dd2 {
+  double h, l;
+};
+__device__ __forceinline__ dd2 dd2_quick(double a, double b) {
+  const double s = a + b;
+  return dd2{s, b - (s - a)};
+}
+__device__ __forceinline__ dd2 dd2_two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return dd2{s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd2 dd2_add(dd2 x, dd2 y) {
+  dd2 a = dd2_two_sum(x.h, y.h);
+  const dd2 b = dd2_two_sum(x.l, y.l);
+  a.l += b.h;
+  a = dd2_quick(a.h, a.l);
+  a.l += b.l;
+  return dd2_quick(a.h, a.l);
+}
+__device__ __forceinline__ dd2 dd2_neg(dd2 x) { return dd2{-x.h, -x.l}; }
+__device__ __forceinline__ dd2 dd2_mul(dd2 x, dd2 y) {
+  const double p = x.h * y.h;
+  double e = fma(x.h, y.h, -p);
+  e = fma(x.h, y.l, fma(x.l, y.h, e));
+  return dd2_quick(p, e);
+}
+__device__ __forceinline__ dd2 dd2_muld(dd2 x, double y) {
+  const double p = x.h * y;
+  return dd2_quick(p, fma(x.l, y, fma(x.h, y, -p)));
+}
+__device__ __forceinline__ dd2 dd2_div(dd2 a, dd2 b) {  // three quotient digits
+  const double q1 = a.h / b.h;
+  dd2 r = dd2_add(a, dd2_neg(dd2_muld(b, q1)));
+  const double q2 = r.h / b.h;
+  r = dd2_add(r, dd2_neg(dd2_muld(b, q2)));
+  const double q3 = r.h / b.h;
+  return dd2_add(dd2_quick(q1, q2), dd2{q3, 0.0});
+}
+__device__ __forceinline__ dd2 dd2_sqrt(dd2 a) {  // a > 0
+  const double x = sqrt(a.h);
+  const dd2 r = dd2_add(a, dd2_neg(dd2_mul(dd2{x, 0.0}, dd2{x, 0.0})));
+  return dd2_quick(x, r.h / (2.0 * x));
+}
+
+// max |V_v| (positive doubles order like their bit patterns: an integer atomic max)
+__global__ void k_vabsmax(const double *V, int64_t K, unsigned long long *out) {
+  const int v = blockIdx.y;
+  unsigned long long m = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < K; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(V[(int64_t)v * K + r]));
+    m = b > m ? b : m;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = x > m ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out + v, m);
+}
+
+constexpr int kDdThreads = 512;
+constexpr int kDdRS = 8;     // rows per stage
+constexpr int kDdAcc = 8;    // accumulators (weight, monomial) per thread: nw * nslot <= 4096
+constexpr int kDdFlush = 8;  // stages between flushes into the double-double accumulators (64 rows)
+
+struct DdArgs {
+  const GramBasis *basis;
+  const double *X, *V;
+  int64_t K;
+  const unsigned long long *vmax;  // [nv] bit patterns of max |V_v|
+  double *part;                    // [gridDim.x][nw * nslot][2]
+  int n, nslot, nv, nw, nunit;
+  uint32_t uexp[kMomMaxUnits];
+  uint8_t ulen[kMomMaxUnits];
+  int16_t uslot[kMomMaxUnits];
+};
+
+__global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant__ DdArgs a) {
+  extern __shared__ __align__(16) double dsm[];
+  const int tid = threadIdx.x, n = a.n, nv = a.nv, nw = a.nw, ns = a.nslot;
+  const int nsp = (ns + 1) & ~1;
+  double *sMh = dsm;                          // [RS][nsp]  monomials (hi)
+  double *sMl = sMh + kDdRS * nsp;            // [RS][nsp]  (lo)
+  double *sU = sMl + kDdRS * nsp;             // [RS][kMaxVars]
+  double *sWh = sU + kDdRS * kMaxVars;        // [RS][16]  weights (hi)
+  double *sWl = sWh + kDdRS * 16;             // [RS][16]  (lo)
+  const GramBasis &B = *a.basis;
+  const int64_t r_begin = a.K * blockIdx.x / gridDim.x, r_end = a.K * (blockIdx.x + 1) / gridDim.x;
+  const int nacc = nw * ns;
+  // accumulators a_i = tid + 512 i: weight w_i, monomial e_i; sigma_i >= 2 x 64 rows x max |w|
+  int ew[kDdAcc];
+  double sg[kDdAcc], h[kDdAcc], l[kDdAcc];
+  dd2 acc[kDdAcc];
+#pragma unroll
+  for (int i = 0; i < kDdAcc; ++i) {
+    const int ai = tid + kDdThreads * i;
+    ew[i] = ai < nacc ? ai : -1;
+    const int w = ai < nacc ? ai / ns : 0;
+    double vm = 1.0;
+    if (w >= 1) {
+      vm = __longlong_as_double((long long)a.vmax[(w - 1) % nv]);
+      if (w > nv) vm *= vm * (1.0 + 1e-15);
+    }
+    int ex;
+    frexp(2.0 * kDdRS * kDdFlush * (vm > 0.0 ? vm : 1.0) * (1.0 + 1e-12), &ex);
+    sg[i] = ldexp(1.0, ex);
+    h[i] = l[i] = 0.0;
+    acc[i] = dd2{0.0, 0.0};
+  }
+  int stage = 0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kDdRS, ++stage) {
+    // inputs: u of the stage's rows, the row weights 1, V_v, V_v^2 (double-double; 0 past the slab)
+    for (int t = tid; t < kDdRS * kMaxVars; t += kDdThreads) {
+      const int r = t / kMaxVars, k = t % kMaxVars;
+      const int64_t row = r0 + r;
+      sU[t] = (row < r_end && k < n) ? (a.X[row * n + k] - B.xc[k]) * ldexp(1.0, -B.xe[k]) : 0.0;
+    }
+    for (int t = tid; t < kDdRS * 16; t += kDdThreads) {
+      const int r = t / 16, w = t % 16;
+      const int64_t row = r0 + r;
+      double wh = 0.0, wl = 0.0;
+      if (row < r_end && w < nw) {
+        if (w == 0) {
+          wh = 1.0;
+        } else {
+          const double vv = a.V[(int64_t)((w - 1) % nv) * a.K + row];
+          if (w <= nv) {
+            wh = vv;
+          } else {
+            wh = vv * vv;
+            wl = fma(vv, vv, -wh);
+          }
+        }
+      }
+      sWh[t] = wh;
+      sWl[t] = wl;
+    }
+    __syncthreads();
+    // a11 in double-double: tasks (row, unit): the unit's prefix by repeated exact products, then
+    // its entries along the last variable
+    for (int task = tid; task < kDdRS * a.nunit; task += kDdThreads) {
+      const int r = task / a.nunit, u = task % a.nunit;
+      const double *ur = sU + r * kMaxVars;
+      const uint32_t ex = a.uexp[u];
+      dd2 m{1.0, 0.0};
+      for (int k = 0; k + 1 < n; ++k)
+        for (int e = (int)((ex >> (4 * k)) & 15u); e > 0; --e) m = dd2_muld(m, ur[k]);
+      const double ul = ur[n - 1];
+      const int slot = a.uslot[u], len = a.ulen[u];
+      for (int j = 0; j < len; ++j) {
+        sMh[r * nsp + slot + j] = m.h;
+        sMl[r * nsp + slot + j] = m.l;
+        m = dd2_muld(m, ul);
+      }
+    }
+    __syncthreads();
+    // a12: the terms w m of the stage's rows, high parts exact
+#pragma unroll
+    for (int i = 0; i < kDdAcc; ++i) {
+      if (ew[i] < 0) continue;
+      const int w = ew[i] / ns, e = ew[i] - w * ns;
+#pragma unroll
+      for (int r = 0; r < kDdRS; ++r) {
+        const double mh = sMh[r * nsp + e], ml = sMl[r * nsp + e];
+        const double wh = sWh[r * 16 + w], wl = sWl[r * 16 + w];
+        const double th = fma(wh, mh, sg[i]) - sg[i];
+        h[i] += th;
+        l[i] += fma(wh, mh, -th) + fma(wh, ml, wl * mh);
+      }
+    }
+    if ((stage + 1) % kDdFlush == 0 || r0 + kDdRS >= r_end) {
+#pragma unroll
+      for (int i = 0; i < kDdAcc; ++i) {
+        acc[i] = dd2_add(acc[i], dd2_two_sum(h[i], l[i]));
+        h[i] = l[i] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  double *out = a.part + (size_t)blockIdx.x * nacc * 2;
+#pragma unroll
+  for (int i = 0; i < kDdAcc; ++i)
+    if (ew[i] >= 0) {
+      out[2 * ew[i]] = acc[i].h;
+      out[2 * ew[i] + 1] = acc[i].l;
+    }
+}
+
+// the partials summed in CTA order (double-double), then G_v [nv][nc][nc] as (hi, lo) pairs
+__global__ void k_gram_dd_sum(const double *part, int nblk, int nacc, double *red) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nacc; e += gridDim.x * blockDim.x) {
+    dd2 s{0.0, 0.0};
+    for (int b = 0; b < nblk; ++b) s = dd2_add(s, dd2{part[((size_t)b * nacc + e) * 2], part[((size_t)b * nacc + e) * 2 + 1]});
+    red[2 * e] = s.h;
+    red[2 * e + 1] = s.l;
+  }
+}
+
+__global__ void k_gram_dd_assemble(const GramBasis *gb, const double *red, int D, int nv, int ns, double *Gdd) {
+  const GramBasis &B = *gb;
+  const int n = B.n, nc = B.nc, nn = B.n_num;
+  const int64_t total = (int64_t)nv * nc * nc;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(idx / ((int64_t)nc * nc));
+    const int rc = (int)(idx % ((int64_t)nc * nc));
+    const int i = rc / nc, j = rc % nc;
+    const int q = (i >= nn) + (j >= nn);
+    int8_t e[kMaxVars];
+    for (int k = 0; k < n; ++k) e[k] = (int8_t)(B.exp[i][k] + B.exp[j][k]);
+    const int slot = simplex_rank(e, n, D);
+    const int w = q == 0 ? 0 : (q == 1 ? 1 + v : 1 + nv + v);
+    const double sgn = q == 1 ? -1.0 : 1.0;
+    Gdd[2 * idx] = sgn * red[2 * ((size_t)w * ns + slot)];
+    Gdd[2 * idx + 1] = sgn * red[2 * ((size_t)w * ns + slot) + 1];
+  }
+}
+
+// R = chol(G) in double-double, one CTA per metric: G equilibrated by powers of two (exact),
+// right-looking, one column per step; a pivot <= 1e-26 (relative to the unit diagonal) is a
+// null direction: its column is set to an exact zero.  R [nv][nc][nc] (upper, FP64) for the SVD.
+constexpr int kCholDdThreads = 512;
+__global__ void __launch_bounds__(kCholDdThreads, 1) k_chol_dd(const double *Gdd, int nc, double *R_out) {
+  extern __shared__ __align__(16) double csm[];
+  const int v = blockIdx.x, tid = threadIdx.x;
+  const int np = nc * (nc + 1) / 2;
+  double *Sh = csm, *Sl = Sh + np;  // packed lower: (i, j), j <= i at i (i + 1) / 2 + j
+  double *dsc = Sl + np;            // [nc] the power-of-two scales
+  const double *G = Gdd + (size_t)v * nc * nc * 2;
+  auto P = [](int i, int j) { return i * (i + 1) / 2 + j; };
+  for (int i = tid; i < nc; i += kCholDdThreads) {
+    const double gii = G[2 * ((size_t)i * nc + i)];
+    int ex = 0;
+    if (gii > 0.0) frexp(sqrt(gii), &ex);
+    dsc[i] = ldexp(1.0, -ex);
+  }
+  __syncthreads();
+  for (int t = tid; t < np; t += kCholDdThreads) {
+    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (P(i + 1, 0) <= t) ++i;
+    while (P(i, 0) > t) --i;
+    const int j = t - P(i, 0);
+    const double sc = dsc[i] * dsc[j];
+    Sh[t] = G[2 * ((size_t)i * nc + j)] * sc;
+    Sl[t] = G[2 * ((size_t)i * nc + j) + 1] * sc;
+  }
+  __syncthreads();
+  for (int j = 0; j < nc; ++j) {
+    const dd2 piv{Sh[P(j, j)], Sl[P(j, j)]};
+    const bool null = !(piv.h > 1e-26);
+    dd2 rj{0.0, 0.0};
+    if (!null) rj = dd2_sqrt(piv);
+    __syncthreads();  // every thread has read the pivot
+    for (int i = j + tid; i < nc; i += kCholDdThreads) {
+      dd2 x{0.0, 0.0};
+      if (!null) x = (i == j) ? rj : dd2_div(dd2{Sh[P(i, j)], Sl[P(i, j)]}, rj);
+      Sh[P(i, j)] = x.h;
+      Sl[P(i, j)] = x.l;
+    }
+    __syncthreads();
+    if (!null) {
+      const int m = nc - j - 1, cnt = m * (m + 1) / 2;
+      for (int t = tid; t < cnt; t += kCholDdThreads) {  // trailing (i, k), j < k <= i
+        int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+        while (ii * (ii + 1) / 2 > t) --ii;
+        const int kk = t - ii * (ii + 1) / 2;
+        const int i = j + 1 + ii, k = j + 1 + kk;
+        const dd2 li{Sh[P(i, j)], Sl[P(i, j)]}, lk{Sh[P(k, j)], Sl[P(k, j)]};
+        const dd2 s = dd2_add(dd2{Sh[P(i, k)], Sl[P(i, k)]}, dd2_neg(dd2_mul(li, lk)));
+        Sh[P(i, k)] = s.h;
+        Sl[P(i, k)] = s.l;
+      }
+    }
+    __syncthreads();
+  }
+  // R = L^T D^{-1}: R[j][i] = L~[i][j] / d_i (upper)
+  double *Ro = R_out + (size_t)v * nc * nc;
+  for (int t = tid; t < nc * nc; t += kCholDdThreads) {
+    const int rr = t / nc, cc = t % nc;
+    Ro[t] = cc >= rr ? (Sh[P(cc, rr)] + Sl[P(cc, rr)]) / dsc[cc] : 0.0;
+  }
+}
+
+bool gram_dd_supported(const GramBasis &h, int n_v, int64_t K) {
+  MomShape sh;
+  if (!mom_shape(h, n_v, false, &sh)) return false;
+  if (sh.nw * sh.nslot > kDdThreads * kDdAcc || sh.nw > 16) return false;
+  const char *r = getenv("RP_SVD_R");
+  if (r && strcmp(r, "tsqr") == 0) return false;
+  return K >= 4 * (int64_t)h.nc && (size_t)h.nc * (h.nc + 1) * 8 + 8 * h.nc <= 227 * 1024;
+}
+
+static int dd_grid_x(int64_t K) {
+  const int64_t want = (K + 255) / 256;
+  const int64_t cap = num_sms();
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+size_t gram_dd_workspace_bytes(const GramBasis &h, int n_v, int64_t K) {
+  MomShape sh;
+  if (!mom_shape(h, n_v, false, &sh)) return 0;
+  const size_t nacc = (size_t)sh.nw * sh.nslot;
+  return 8 * ((size_t)(dd_grid_x(K) + 1) * nacc * 2 + (size_t)n_v * h.nc * h.nc * 2 + 16);
+}
+
+cudaError_t launch_gram_dd_chol(const GramBasis *d_basis, const GramBasis &h, const double *X, const double *V,
+                                int64_t K, int n_v, void *ws, size_t ws_bytes, double *R, cudaStream_t s) {
+  MomShape sh;
+  if (!mom_shape(h, n_v, false, &sh)) return cudaErrorInvalidValue;
+  if (ws_bytes < gram_dd_workspace_bytes(h, n_v, K)) return cudaErrorInvalidValue;
+  const int gx = dd_grid_x(K);
+  const int nacc = sh.nw * sh.nslot;
+  double *part = (double *)ws, *red = part + (size_t)gx * nacc * 2, *Gdd = red + (size_t)nacc * 2;
+  unsigned long long *vmax = (unsigned long long *)(Gdd + (size_t)n_v * h.nc * h.nc * 2);
+  cudaError_t e = cudaMemsetAsync(vmax, 0, 8 * n_v, s);
+  if (e != cudaSuccess) return e;
+  {
+    const int64_t b = (K + 255) / 256;
+    const int bx = (int)(b < 2 * num_sms() ? b : 2 * num_sms());
+    k_vabsmax<<<dim3(bx, n_v), 256, 0, s>>>(V, K, vmax);
+  }
+  DdArgs a;
+  memset(&a, 0, sizeof a);
+  a.basis = d_basis;
+  a.X = X;
+  a.V = V;
+  a.K = K;
+  a.vmax = vmax;
+  a.part = part;
+  a.n = h.n;
+  a.nslot = sh.nslot;
+  a.nv = n_v;
+  a.nw = sh.nw;
+  static MomTab tab;
+  tab = mom_tab(h.n, sh.D);
+  if (tab.nu != sh.nunit) return cudaErrorInvalidValue;
+  a.nunit = tab.nu;
+  for (int i = 0; i < tab.nu; ++i) {
+    uint32_t pk = 0;
+    for (int k = 0; k + 1 < h.n; ++k) pk |= (uint32_t)tab.ex[i][k] << (4 * k);
+    a.uexp[i] = pk;
+    a.ulen[i] = (uint8_t)tab.len[i];
+    a.uslot[i] = (int16_t)tab.slot[i];
+  }
+  const int nsp = (sh.nslot + 1) & ~1;
+  const size_t smem = 8 * ((size_t)2 * kDdRS * nsp + kDdRS * kMaxVars + 2 * kDdRS * 16);
+  e = cudaFuncSetAttribute(k_gram_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gram_dd<<<gx, kDdThreads, smem, s>>>(a);
+  k_gram_dd_sum<<<(nacc + 255) / 256, 256, 0, s>>>(part, gx, nacc, red);
+  const int64_t total = (int64_t)n_v * h.nc * h.nc;
+  const int rb = (int)((total + 255) / 256);
+  k_gram_dd_assemble<<<rb < 4 * num_sms() ? rb : 4 * num_sms(), 256, 0, s>>>(d_basis, red, sh.D, n_v, sh.nslot, Gdd);
+  const size_t csm = 8 * ((size_t)h.nc * (h.nc + 1) + h.nc);
+  e = cudaFuncSetAttribute(k_chol_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  if (e != cudaSuccess) return e;
+  k_chol_dd<<<n_v, kCholDdThreads, csm, s>>>(Gdd, h.nc, R);
+  return cudaGetLastError();
+}
+
 }  // namespace rp
