@@ -729,9 +729,10 @@ __global__ void k_vabsmax(const double *V, int64_t K, unsigned long long *out) {
 }
 
 constexpr int kDdThreads = 512;
-constexpr int kDdRS = 8;     // rows per stage
+constexpr int kDdRS = 16;    // rows per stage
 constexpr int kDdAcc = 8;    // accumulators (weight, monomial) per thread: nw * nslot <= 4096
-constexpr int kDdFlush = 8;  // stages between flushes into the double-double accumulators (64 rows)
+constexpr int kDdFlush = 4;  // stages between flushes into the double-double accumulators (64 rows)
+constexpr int kDdUS = kMaxVars + 1;  // row stride of sU (odd: conflict-free)
 
 struct DdArgs {
   const GramBasis *basis;
@@ -745,27 +746,30 @@ struct DdArgs {
   int16_t uslot[kMomMaxUnits];
 };
 
+__host__ __device__ inline int dd_nsp(int ns) { return ns | 1; }  // odd row stride: conflict-free stores
+
 __global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant__ DdArgs a) {
   extern __shared__ __align__(16) double dsm[];
   const int tid = threadIdx.x, n = a.n, nv = a.nv, nw = a.nw, ns = a.nslot;
-  const int nsp = (ns + 1) & ~1;
+  const int nsp = dd_nsp(ns);
   double *sMh = dsm;                          // [RS][nsp]  monomials (hi)
   double *sMl = sMh + kDdRS * nsp;            // [RS][nsp]  (lo)
-  double *sU = sMl + kDdRS * nsp;             // [RS][kMaxVars]
-  double *sWh = sU + kDdRS * kMaxVars;        // [RS][16]  weights (hi)
-  double *sWl = sWh + kDdRS * 16;             // [RS][16]  (lo)
+  double *sU = sMl + kDdRS * nsp;             // [RS][kDdUS]
+  double *sWh = sU + kDdRS * kDdUS;           // [16][RS]  weights (hi), weight-major
+  double *sWl = sWh + kDdRS * 16;             // [16][RS]  (lo)
   const GramBasis &B = *a.basis;
   const int64_t r_begin = a.K * blockIdx.x / gridDim.x, r_end = a.K * (blockIdx.x + 1) / gridDim.x;
   const int nacc = nw * ns;
   // accumulators a_i = tid + 512 i: weight w_i, monomial e_i; sigma_i >= 2 x 64 rows x max |w|
-  int ew[kDdAcc];
+  int aw[kDdAcc], ae[kDdAcc];
   double sg[kDdAcc], h[kDdAcc], l[kDdAcc];
   dd2 acc[kDdAcc];
 #pragma unroll
   for (int i = 0; i < kDdAcc; ++i) {
     const int ai = tid + kDdThreads * i;
-    ew[i] = ai < nacc ? ai : -1;
-    const int w = ai < nacc ? ai / ns : 0;
+    const int w = ai < nacc ? ai / ns : -1;
+    aw[i] = w;
+    ae[i] = ai < nacc ? ai - w * ns : 0;
     double vm = 1.0;
     if (w >= 1) {
       vm = __longlong_as_double((long long)a.vmax[(w - 1) % nv]);
@@ -777,16 +781,18 @@ __global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant
     h[i] = l[i] = 0.0;
     acc[i] = dd2{0.0, 0.0};
   }
+  const double xs0 = ldexp(1.0, -B.xe[tid % kMaxVars < n ? tid % kMaxVars : 0]);
+  const double xc0 = B.xc[tid % kMaxVars < n ? tid % kMaxVars : 0];
   int stage = 0;
   for (int64_t r0 = r_begin; r0 < r_end; r0 += kDdRS, ++stage) {
     // inputs: u of the stage's rows, the row weights 1, V_v, V_v^2 (double-double; 0 past the slab)
-    for (int t = tid; t < kDdRS * kMaxVars; t += kDdThreads) {
-      const int r = t / kMaxVars, k = t % kMaxVars;
+    if (tid < kDdRS * kMaxVars) {
+      const int r = tid / kMaxVars, k = tid % kMaxVars;
       const int64_t row = r0 + r;
-      sU[t] = (row < r_end && k < n) ? (a.X[row * n + k] - B.xc[k]) * ldexp(1.0, -B.xe[k]) : 0.0;
+      sU[r * kDdUS + k] = (row < r_end && k < n) ? (a.X[row * n + k] - xc0) * xs0 : 0.0;
     }
-    for (int t = tid; t < kDdRS * 16; t += kDdThreads) {
-      const int r = t / 16, w = t % 16;
+    if (tid < kDdRS * 16) {
+      const int w = tid / kDdRS, r = tid % kDdRS;
       const int64_t row = r0 + r;
       double wh = 0.0, wl = 0.0;
       if (row < r_end && w < nw) {
@@ -802,41 +808,62 @@ __global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant
           }
         }
       }
-      sWh[t] = wh;
-      sWl[t] = wl;
+      sWh[tid] = wh;
+      sWl[tid] = wl;
     }
     __syncthreads();
-    // a11 in double-double: tasks (row, unit): the unit's prefix by repeated exact products, then
-    // its entries along the last variable
+    // a11 in double-double: tasks (unit, row), row fastest (a warp runs two units: uniform
+    // control flow): the unit's prefix by repeated exact products, then its entries along the
+    // last variable
     for (int task = tid; task < kDdRS * a.nunit; task += kDdThreads) {
-      const int r = task / a.nunit, u = task % a.nunit;
-      const double *ur = sU + r * kMaxVars;
+      const int r = task % kDdRS, u = task / kDdRS;
+      const double *ur = sU + r * kDdUS;
       const uint32_t ex = a.uexp[u];
       dd2 m{1.0, 0.0};
-      for (int k = 0; k + 1 < n; ++k)
-        for (int e = (int)((ex >> (4 * k)) & 15u); e > 0; --e) m = dd2_muld(m, ur[k]);
+      for (int k = 0; k + 1 < n; ++k) {
+        const double uk = ur[k];
+        for (int e = (int)((ex >> (4 * k)) & 15u); e > 0; --e) m = dd2_muld(m, uk);
+      }
       const double ul = ur[n - 1];
       const int slot = a.uslot[u], len = a.ulen[u];
+      double *dh = sMh + r * nsp + slot, *dl = sMl + r * nsp + slot;
       for (int j = 0; j < len; ++j) {
-        sMh[r * nsp + slot + j] = m.h;
-        sMl[r * nsp + slot + j] = m.l;
+        dh[j] = m.h;
+        dl[j] = m.l;
         m = dd2_muld(m, ul);
       }
     }
     __syncthreads();
-    // a12: the terms w m of the stage's rows, high parts exact
+    // a12: the terms w m of the stage's rows, high parts exact (V^2 weights carry a low part)
 #pragma unroll
     for (int i = 0; i < kDdAcc; ++i) {
-      if (ew[i] < 0) continue;
-      const int w = ew[i] / ns, e = ew[i] - w * ns;
-#pragma unroll
-      for (int r = 0; r < kDdRS; ++r) {
-        const double mh = sMh[r * nsp + e], ml = sMl[r * nsp + e];
-        const double wh = sWh[r * 16 + w], wl = sWl[r * 16 + w];
-        const double th = fma(wh, mh, sg[i]) - sg[i];
-        h[i] += th;
-        l[i] += fma(wh, mh, -th) + fma(wh, ml, wl * mh);
+      if (aw[i] < 0) continue;
+      const double *mh = sMh + ae[i], *ml = sMl + ae[i];
+      const double *wh = sWh + aw[i] * kDdRS, *wl = sWl + aw[i] * kDdRS;
+      const double sgi = sg[i];
+      double hi = h[i], lo = l[i];
+      if (aw[i] > nv) {
+#pragma unroll 4
+        for (int r = 0; r < kDdRS; ++r) {
+          const double m_h = mh[r * nsp], m_l = ml[r * nsp], w_h = wh[r], w_l = wl[r];
+          const double th = fma(w_h, m_h, sgi) - sgi;
+          hi += th;
+          lo = fma(w_h, m_l, lo);
+          lo = fma(w_l, m_h, lo);
+          lo += fma(w_h, m_h, -th);
+        }
+      } else {
+#pragma unroll 4
+        for (int r = 0; r < kDdRS; ++r) {
+          const double m_h = mh[r * nsp], m_l = ml[r * nsp], w_h = wh[r];
+          const double th = fma(w_h, m_h, sgi) - sgi;
+          hi += th;
+          lo = fma(w_h, m_l, lo);
+          lo += fma(w_h, m_h, -th);
+        }
       }
+      h[i] = hi;
+      l[i] = lo;
     }
     if ((stage + 1) % kDdFlush == 0 || r0 + kDdRS >= r_end) {
 #pragma unroll
@@ -850,9 +877,10 @@ __global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant
   double *out = a.part + (size_t)blockIdx.x * nacc * 2;
 #pragma unroll
   for (int i = 0; i < kDdAcc; ++i)
-    if (ew[i] >= 0) {
-      out[2 * ew[i]] = acc[i].h;
-      out[2 * ew[i] + 1] = acc[i].l;
+    if (aw[i] >= 0) {
+      const int ai = aw[i] * ns + ae[i];
+      out[2 * ai] = acc[i].h;
+      out[2 * ai + 1] = acc[i].l;
     }
 }
 
@@ -1012,8 +1040,8 @@ cudaError_t launch_gram_dd_chol(const GramBasis *d_basis, const GramBasis &h, co
     a.ulen[i] = (uint8_t)tab.len[i];
     a.uslot[i] = (int16_t)tab.slot[i];
   }
-  const int nsp = (sh.nslot + 1) & ~1;
-  const size_t smem = 8 * ((size_t)2 * kDdRS * nsp + kDdRS * kMaxVars + 2 * kDdRS * 16);
+  const int nsp = dd_nsp(sh.nslot);
+  const size_t smem = 8 * ((size_t)2 * kDdRS * nsp + kDdRS * kDdUS + 2 * kDdRS * 16);
   e = cudaFuncSetAttribute(k_gram_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_gram_dd<<<gx, kDdThreads, smem, s>>>(a);
