@@ -158,3 +158,34 @@ def test_svd_fitheavy_full_size_exact_recovery():
         assert _coef_err(coef[i], fc.truths[0].coef[i]) <= 1e-9, i
         assert sigma[i][0] <= 1e-8 * sigma[i][1]
         assert infos[i]["rank"] == 139
+
+
+@pytest.mark.parametrize("r_path", ["dd", "tsqr"])
+def test_svd_both_r_paths_vs_oracle(r_path, monkeypatch):
+    """The SVD's R from the double-double Gram (default for K >= 4 n_c, reading R34) and from the
+    Householder TSQR (RP_SVD_R=tsqr), each against the oracle's one-sided Jacobi SVD of A on the
+    same polybench sample (K = 2,000 >= 4 n_c = 280), at the file's gates."""
+    if r_path == "tsqr":
+        monkeypatch.setenv("RP_SVD_R", "tsqr")
+    fc = synth.polybench_fit_box(sigma=0.01)
+    V = _metrics(fc)
+    _check_vs_oracle(fc, fc.X, V, range(len(V)), r_path)
+
+
+def test_svd_r_paths_agree_full_size():
+    """At K = 10^6 (fitheavy, 1% noise) the two R paths give the same singular values (within
+    1e-12 sigma_max) and coefficients (within 1e-9)."""
+    import os
+    fc = synth.fitheavy(sigma=0.01)
+    X = _cuda(fc.X)
+    V = (rp.eval_metrics(fc.truths[0], X) * _cuda(fc.noise)).contiguous()
+    c_dd, s_dd, _, _ = rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
+    os.environ["RP_SVD_R"] = "tsqr"
+    try:
+        c_ts, s_ts, _, _ = rp.fit_svd(X, V, fc.num_exp, fc.den_exp)
+    finally:
+        del os.environ["RP_SVD_R"]
+    for i in range(3):
+        s1, s2 = np.asarray(s_dd[i]), np.asarray(s_ts[i])
+        assert np.max(np.abs(s1 - s2)) <= 1e-12 * s2[-1], i
+        assert _coef_err(c_dd[i], c_ts[i]) <= 1e-9, i
