@@ -910,7 +910,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     // bank-conflicted shared-memory reads and quad shuffles); each tile of the group is then one
     // DMMA per polynomial: C = w_{k,0}, A = w_{k,1+q}, B = x^{1+q} of configuration lane / 4
     const int q = lane & 3;
+#ifdef RP_SWEEP_PROBE_NOFACT  // timing probe: dense tiles only
+    for (int gi = 0; gi < 0; ++gi) {
+#else
     for (int gi = 0; gi < ngr; ++gi) {
+#endif
       const GroupDesc *gd = gdesc + gi;
       const int tb = __ldg(&gd->tile_begin), te = __ldg(&gd->tile_end);
       if (sorted && __ldg(&grec[tb * 8].P01) > maxD1sq) continue;  // a3: every member fails
@@ -976,7 +980,11 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
     }
     // dense tiles; a3 early exit: they are sorted by P1 P2, so every tile from the first one whose
     // smallest P1 P2 exceeds the largest D1^2 of the warp's tuples fails the D rule
+#ifdef RP_SWEEP_PROBE_NODENSE  // timing probe: factored tiles only
+    const int nOctF = 0;
+#else
     const int nOctF = ntile - ngt;
+#endif
     const CfgRec *drec = grec + ngt * 8;
     int nEff = nOctF;
     if (sorted)
