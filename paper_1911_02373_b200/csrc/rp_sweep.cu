@@ -1892,6 +1892,9 @@ __device__ __forceinline__ double pair_E(const DevProg &pg, const CfgTable &tab,
   bool pos = true;
 #pragma unroll
   for (int k = 0; k < 6; ++k) pos = pos && pk[k] > 0.0;
+#ifdef RP_REFINE_PROBE_NODD  // timing probe: never the double-double Appendix A
+  pos = true;
+#endif
   if (!pos) {
     ddv pd[6];
 #pragma unroll
