@@ -611,7 +611,7 @@ cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h, const 
   // units in lexicographic order and the warps' contiguous shares (the same table the
   // specialised kernels are compiled from)
   const int n = h.n;
-  static MomTab tab;  // (host: too large for the stack)
+  MomTab tab;  // (~4 KB; per call: launches may come from several host threads)
   tab = mom_tab(n, sh.D);
   if (tab.nu != sh.nunit || tab.ns != sh.nslot) return cudaErrorInvalidValue;
   for (int i = 0; i < sh.nunit; ++i) {
@@ -1029,7 +1029,7 @@ cudaError_t launch_gram_dd_chol(const GramBasis *d_basis, const GramBasis &h, co
   a.nslot = sh.nslot;
   a.nv = n_v;
   a.nw = sh.nw;
-  static MomTab tab;
+  MomTab tab;  // (~4 KB; per call: launches may come from several host threads)
   tab = mom_tab(h.n, sh.D);
   if (tab.nu != sh.nunit) return cudaErrorInvalidValue;
   a.nunit = tab.nu;
