@@ -41,15 +41,23 @@ if want("sweep"):
 if want("gram"):
     fc = synth.polybench_fit_box(K=700)
     V = rp.eval_metrics(fc.truths[0], cu(fc.X))
-    rp.fit(cu(fc.X), V, fc.num_exp, fc.den_exp)                              # minmax, xform, k_gram_ws, solve
-    os.environ["RP_GRAM_KERNEL"] = "fused"
-    rp.fit(cu(fc.X), V, fc.num_exp, fc.den_exp)
-    os.environ.pop("RP_GRAM_KERNEL")
-    rp.fit_sk(cu(fc.X), V, fc.num_exp, fc.den_exp, iters=2, raise_on_degenerate=False)
+    rp.fit(cu(fc.X), V, fc.num_exp, fc.den_exp)                              # minmax, xform, k_gram_mom (TMA ring), solve
+    rp.fit(cu(fc.X[:699]), V[:, :699].contiguous(), fc.num_exp, fc.den_exp)  # odd K: the plain-load producer path
+    os.environ["RP_MOM_GENERIC"] = "1"
+    rp.fit(cu(fc.X), V, fc.num_exp, fc.den_exp)                              # the generic monomial step
+    os.environ.pop("RP_MOM_GENERIC")
+    for kern in ("ws", "fused"):                                             # the outer-product kernels
+        os.environ["RP_GRAM_KERNEL"] = kern
+        rp.fit(cu(fc.X), V, fc.num_exp, fc.den_exp)
+        os.environ.pop("RP_GRAM_KERNEL")
+    rp.fit_sk(cu(fc.X), V, fc.num_exp, fc.den_exp, iters=2, raise_on_degenerate=False)  # weighted moments (WT = 2)
 if want("svd"):
     fc = synth.tiny_fit_box()
     V = rp.eval_metrics(fc.truths[0], cu(fc.X))
-    rp.fit_svd(cu(fc.X), V, fc.num_exp, fc.den_exp, raise_on_degenerate=False)  # k_tsqr, k_svd_jacobi
+    rp.fit_svd(cu(fc.X), V, fc.num_exp, fc.den_exp, raise_on_degenerate=False)  # k_tsqr (K < 4 n_c), k_svd_gk
+    pf = synth.polybench_fit_box(K=700)
+    Vp = rp.eval_metrics(pf.truths[0], cu(pf.X))
+    rp.fit_svd(cu(pf.X), Vp, pf.num_exp, pf.den_exp, raise_on_degenerate=False)  # k_vabsmax, k_gram_dd, k_chol_dd
 if want("decide"):
     pb = synth.polybench_sweep(nD=20)
     plan = rp.Plan(pb.programs[:1], cu(pb.F))
