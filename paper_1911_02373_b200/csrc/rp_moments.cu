@@ -421,9 +421,10 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
     {
       const double *raw = sIn + st * INB + (lane & 3);
       const double *mb = sM + (size_t)(tb * 8 + (lane >> 2)) * kMomRTP + (lane & 3);
-#pragma unroll 2
-      for (int ks = 0; ks < kMomRT / 4; ++ks) {
-        double av[WT];
+      // every A value (the row weights) of the stage first, off the DMMA chain (0.430 -> 0.424 ms)
+      double aall[kMomRT / 4][WT];
+#pragma unroll
+      for (int ks = 0; ks < kMomRT / 4; ++ks)
 #pragma unroll
         for (int h = 0; h < WT; ++h) {
           const double x = raw[wv[h] + ks * 4];
@@ -432,8 +433,13 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
             const double sv = raw[ws[h] + ks * 4];
             w *= sv * sv;
           }
-          av[h] = wz[h] ? 0.0 : w;
+          aall[ks][h] = wz[h] ? 0.0 : w;
         }
+#pragma unroll
+      for (int ks = 0; ks < kMomRT / 4; ++ks) {
+        double av[WT];
+#pragma unroll
+        for (int h = 0; h < WT; ++h) av[h] = aall[ks][h];
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
           if (q < tc) {
