@@ -38,7 +38,10 @@
 
 namespace rp {
 
-constexpr int kMomWarps = 16;                      // consumers: monomials + moments of their own tiles
+#ifndef RP_MOM_WARPS
+#define RP_MOM_WARPS 16
+#endif
+constexpr int kMomWarps = RP_MOM_WARPS;            // consumers: monomials + moments of their own tiles
 constexpr int kMomThreads = 32 * (kMomWarps + 1);  // + one producer warp: TMA issue, row weights
 constexpr int kMomRT = 32;          // rows per stage (lane = row in the monomial step)
 constexpr int kMomRTP = 36;         // row stride of sM in doubles (= 4 mod 16: conflict-free fragments)
@@ -378,6 +381,10 @@ __global__ void __launch_bounds__(kMomThreads, 1) k_gram_mom(const __grid_consta
   case w: mom_gen_warp<N, D, w>(u, sM + lane); break;
         RP_MG(0) RP_MG(1) RP_MG(2) RP_MG(3) RP_MG(4) RP_MG(5) RP_MG(6) RP_MG(7) RP_MG(8) RP_MG(9) RP_MG(10)
         RP_MG(11) RP_MG(12) RP_MG(13) RP_MG(14) RP_MG(15)
+#if RP_MOM_WARPS > 16
+        RP_MG(16) RP_MG(17) RP_MG(18) RP_MG(19) RP_MG(20) RP_MG(21) RP_MG(22) RP_MG(23) RP_MG(24) RP_MG(25)
+        RP_MG(26) RP_MG(27) RP_MG(28) RP_MG(29) RP_MG(30)
+#endif
 #undef RP_MG
       }
     } else if (s1w > s0w) {
@@ -641,7 +648,11 @@ cudaError_t launch_gram_mom(const GramBasis *d_basis, const GramBasis &h, const 
   if (spec && sh.WT == WT_ && sh.TPW == TPW_ && n == N_ && sh.D == D_) e = launch_mom_t<WT_, TPW_, N_, D_>(a, gx, smem_spec, s); else
 #define RP_MOM_CASE(WT_, TPW_) \
   if (sh.WT == WT_ && sh.TPW == TPW_) e = launch_mom_t<WT_, TPW_, 0, 0>(a, gx, smem, s); else
+#if RP_MOM_WARPS > 16
+  RP_MOM_SPEC(1, 2, 4, 8) RP_MOM_SPEC(2, 2, 4, 8) RP_MOM_SPEC(1, 1, 4, 6) RP_MOM_SPEC(2, 1, 4, 6)
+#else
   RP_MOM_SPEC(1, 4, 4, 8) RP_MOM_SPEC(2, 4, 4, 8) RP_MOM_SPEC(1, 2, 4, 6) RP_MOM_SPEC(2, 2, 4, 6)
+#endif
   RP_MOM_SPEC(1, 1, 3, 4) RP_MOM_SPEC(2, 1, 3, 4)
   RP_MOM_CASE(1, 1) RP_MOM_CASE(1, 2) RP_MOM_CASE(1, 4) RP_MOM_CASE(1, 8) RP_MOM_CASE(2, 1) RP_MOM_CASE(2, 2)
   RP_MOM_CASE(2, 4) e = cudaErrorInvalidValue;
