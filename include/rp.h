@@ -208,11 +208,14 @@ rp_status rp_fit_sk(const double *X, const double *V, int64_t K, int32_t n_v, co
  * value decomposition" on the homogeneous system p(x) - V q(x) = 0 (draft
  * footnote PAPER.md:2595-2598): coef = the right singular vector of the smallest singular value
  * of A_m = [M(u_r) | -V_m[r] N(u_r)] (rows as in rp_gram_accumulate), scaled so that beta_0 = 1
- * (reading R12).  A is never formed in memory: a Householder TSQR builds R (A = QR) from design
- * rows generated on chip, and a one-sided Jacobi SVD of R (one CTA per metric) gives the
- * right singular vectors.  Deterministic (fixed merge tree).
+ * (reading R12).  A is never formed in memory: its triangular factor R (A^T A = R^T R) comes from
+ * design rows generated on chip -- for K >= 4 n_c (and a basis whose exponent-sum simplex fits
+ * the moment kernel) as the Cholesky factor of A^T A formed from double-double moments and
+ * factored in double-double (reading R34; RP_SVD_R=tsqr disables it), otherwise by a
+ * Householder TSQR -- and an SVD of R (one CTA per metric) gives the right singular vectors.
+ * Deterministic (fixed reduction orders, fixed merge tree).
  *
- * rp_fit_svd: transform from the sample box as rp_fit, then TSQR + SVD.  X [K][n], V [n_v][K]
+ * rp_fit_svd: transform from the sample box as rp_fit, then R + SVD.  X [K][n], V [n_v][K]
  *   device-or-host; coef_out host [n_v][n_c]; sigma_out host [n_v][n_c] ascending singular values
  *   (nullable); xform_out host (nullable); info host [n_v] (nullable) with rank = #{sigma >
  *   1e-13 sigma_max}, resid2 = ||A coef||^2, min_pivot = sigma_min, cond_est = sigma_max /
