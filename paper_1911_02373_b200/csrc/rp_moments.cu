@@ -765,10 +765,12 @@ struct DdArgs {
 
 __host__ __device__ inline int dd_nsp(int ns) { return ns | 1; }  // odd row stride: conflict-free stores
 
+// NSP > 0: the monomial row stride as a compile-time constant (immediate shared-memory offsets)
+template <int NSP>
 __global__ void __launch_bounds__(kDdThreads, 1) k_gram_dd(const __grid_constant__ DdArgs a) {
   extern __shared__ __align__(16) double dsm[];
   const int tid = threadIdx.x, n = a.n, nv = a.nv, nw = a.nw, ns = a.nslot;
-  const int nsp = dd_nsp(ns);
+  const int nsp = NSP > 0 ? NSP : dd_nsp(ns);
   double *sMh = dsm;                          // [RS][nsp]  monomials (hi)
   double *sMl = sMh + kDdRS * nsp;            // [RS][nsp]  (lo)
   double *sU = sMl + kDdRS * nsp;             // [RS][kDdUS]
@@ -1059,9 +1061,15 @@ cudaError_t launch_gram_dd_chol(const GramBasis *d_basis, const GramBasis &h, co
   }
   const int nsp = dd_nsp(sh.nslot);
   const size_t smem = 8 * ((size_t)2 * kDdRS * nsp + kDdRS * kDdUS + 2 * kDdRS * 16);
-  e = cudaFuncSetAttribute(k_gram_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_gram_dd<<<gx, kDdThreads, smem, s>>>(a);
+  if (nsp == 495) {  // fitheavy: 4 variables, degree-4 bases
+    e = cudaFuncSetAttribute(k_gram_dd<495>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gram_dd<495><<<gx, kDdThreads, smem, s>>>(a);
+  } else {
+    e = cudaFuncSetAttribute(k_gram_dd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gram_dd<0><<<gx, kDdThreads, smem, s>>>(a);
+  }
   k_gram_dd_sum<<<(nacc + 255) / 256, 256, 0, s>>>(part, gx, nacc, red);
   const int64_t total = (int64_t)n_v * h.nc * h.nc;
   const int rb = (int)((total + 255) / 256);
