@@ -891,16 +891,19 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
       } else {
         E = acc[0][v] * frcp(acc[1][v]);  // template g1: E = g_1
       }
+      if constexpr (FAST && !SECOND) {
+        // line 19 / reading R17 folded into the key: bits(E) - 1 as unsigned puts +0, negative
+        // values and NaN above every positive finite E (and +inf at the top of that range, which
+        // the "no winner" test below excludes); masked pairs get the largest key
+        const unsigned long long eb1 = (unsigned long long)__double_as_longlong(E) - 1ull;
+        const unsigned long long key = ok ? ((eb1 & ~0x1FFFull) | (unsigned long long)(uint32_t)orig) : ~0ull;
+        pkey = key < pkey ? key : pkey;
+        continue;
+      }
       // line 19 / reading R17: only finite positive estimates of meaningful pairs compete
       E = (ok && pos_finite(E)) ? E : kInf;
       // a8: exact lexicographic key (E, original index): ties go to the lowest index (E and the
       // running best are positive or +inf, so their bit patterns compare as integers)
-      if constexpr (FAST && !SECOND) {
-        const unsigned long long key =
-            ((unsigned long long)__double_as_longlong(E) & ~0x1FFFull) | (unsigned long long)(uint32_t)orig;
-        pkey = key < pkey ? key : pkey;
-        continue;
-      }
       const long long eb = __double_as_longlong(E), sb = __double_as_longlong(st.e);
       const bool better = eb < sb || (eb == sb && orig < st.i);
       if (SECOND) {  // runner-up on the same exact key
@@ -1030,8 +1033,8 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   }
   // ---- a8: the 4 lanes of a quad hold the same tuple ------------------------------------------
   if constexpr (FAST && !SECOND) {
-    if (pkey < 0x7FF0000000000000ull) {
-      st.e = __longlong_as_double((long long)(pkey & ~0x1FFFull));
+    if (pkey < (0x7FEFFFFFFFFFFFFFull & ~0x1FFFull)) {  // a positive finite E won
+      st.e = __longlong_as_double((long long)((pkey & ~0x1FFFull) + 1ull));
       st.i = (int32_t)(pkey & 0x1FFFull);
     }
   }
