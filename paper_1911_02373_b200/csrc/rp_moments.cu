@@ -47,8 +47,14 @@ constexpr int kMomRT = 32;          // rows per stage (lane = row in the monomia
 constexpr int kMomRTP = 36;         // row stride of sM in doubles (= 4 mod 16: conflict-free fragments)
 constexpr int kMomMaxSlots = 640;   // simplex size limit (shared memory)
 constexpr int kMomMaxUnits = 256;
-constexpr int kMomIS = 5;           // ring slots: raw inputs + row weights of a stage
-constexpr int kMomLead = 3;         // bulk copies are issued this many stages ahead
+#ifndef RP_MOM_IS
+#define RP_MOM_IS 5
+#endif
+#ifndef RP_MOM_LEAD
+#define RP_MOM_LEAD 3
+#endif
+constexpr int kMomIS = RP_MOM_IS;      // ring slots: raw inputs (+ X transposed, ones row) of a stage
+constexpr int kMomLead = RP_MOM_LEAD;  // bulk copies are issued this many stages ahead
 constexpr int kMomFlush = 32;       // stages between flushes of the register accumulators (1024 rows)
 
 struct MomArgs {
