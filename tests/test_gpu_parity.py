@@ -743,3 +743,37 @@ def test_gram_sum_ordered_bitwise():
             want = want + p
         got = rp.gram_sum_ordered(_cuda(parts)).cpu().numpy()
         assert got.tobytes() == want.tobytes(), n_parts
+
+
+def _total_degree_exps(n, deg):
+    out = []
+
+    def rec(prefix, left):
+        if len(prefix) == n:
+            out.append(list(prefix))
+            return
+        for e in range(left + 1):
+            rec(prefix + [e], left - e)
+    rec([], deg)
+    out.sort(key=lambda v: (sum(v), v))
+    return np.array(out, dtype=np.int16)
+
+
+@pytest.mark.parametrize("n,deg,diff_den", [(1, 3, False), (1, 7, True), (2, 2, False), (2, 4, True), (3, 3, False),
+                                            (5, 2, True), (6, 1, False)])
+def test_gram_moments_variable_counts(n, deg, diff_den):
+    """The moment Gram (generic monomial step: every (n, D) other than the BASELINE ones) for 1 to 6
+    variables, identical and differing numerator / denominator bases, 1 and 3 metrics, ragged K, on
+    the TMA and plain-load paths, against the oracle's sum of outer products."""
+    rng = np.random.default_rng(1000 + 10 * n + deg)
+    num = _total_degree_exps(n, deg)
+    den = _total_degree_exps(n, max(deg - 1, 0)) if diff_den else num
+    for K in (37, 1000):
+        X = rng.integers(1, 500, size=(K, n)).astype(np.float64)
+        V = rng.uniform(0.5, 3.0, size=(3, K))
+        c, e = rp.xform_from_box(X.min(axis=0), X.max(axis=0))
+        G = rp.gram(_cuda(X), _cuda(V), num, den, c, e).cpu().numpy()
+        for i in range(3):
+            Go = np.asarray(oracle.gram(X, V[i], num, den, c, e), dtype=np.float64)
+            dg = np.sqrt(np.outer(np.diag(Go), np.diag(Go))) + 1e-300
+            assert np.max(np.abs(G[i] - Go) / dg) <= 1e-12, (n, deg, diff_den, K, i)
