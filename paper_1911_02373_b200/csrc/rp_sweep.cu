@@ -831,9 +831,14 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
   // configurations (k-step major: the NPOLY accumulation chains are independent, so consecutive
   // DMMAs do not wait).  B fragments: m_pe(u_P), pe = 4 ks + lane % 4, configuration 8 oc + lane / 4
 #define RP_AFR(k, ks) arow[(k) * NPE + (ks) * 4]
+  // this lane's B-fragment column of the schedule's monomial table (4.160 -> 4.114 ms against
+  // recomputing the 64-bit address of every load)
+  const double *bbase = gmP + (int64_t)(lane & 3) * nGp + (lane >> 2);
+  const int64_t bks = 4 * (int64_t)nGp;
   auto load_b = [&](int oc, double (&bfr)[KS]) {
+    const double *bp = bbase + oc * 8;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(gmP + (int64_t)(ks * 4 + (lane & 3)) * nGp + oc * 8 + (lane >> 2));
+    for (int ks = 0; ks < KS; ++ks) bfr[ks] = __ldg(bp + ks * bks);
   };
   auto mma_oct = [&](double (&acc)[NPOLY][2], const double (&bfr)[KS]) {
 #pragma unroll
@@ -985,7 +990,7 @@ __global__ void __launch_bounds__(kSweepThreads, RP_SWEEP_MINB) k_sweep(SweepArg
         }
       int tile = tb;
       for (; tile < tend; ++tile) {
-        const double b = __ldg(gmP + (int64_t)q * nGp + tile * 8 + (lane >> 2));
+        const double b = __ldg(bbase + tile * 8);  // x^{1+q} of configuration lane / 4 (row q = lane & 3)
         double acc[NPOLY][2];
 #pragma unroll
         for (int k = 0; k < NPOLY; ++k) {
