@@ -440,7 +440,8 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   const size_t ncm = (size_t)n_prog * kMaxPolys * npe_pad * nde_pad;      // Cmat
   const size_t nrt = (size_t)n_prog * npe_pad * nde_pad;                  // refinement terms
   const size_t nd = 2 * (size_t)n_prog * nFp * npe_pad + (size_t)n_prog * kRSMTab + ncm +  // mP x2, rSM, Cmat,
-                    nrt * kMaxPolys + (size_t)n_prog * 8;                                   // rcoef, rinfo
+                    nrt * kMaxPolys + (size_t)n_prog * 8 +                                  // rcoef, rinfo,
+                    2 * (size_t)n_prog * nFp * npe_pad;                                     // mPdd
   const size_t ni = 2 * nrec * sizeof(CfgRec) + n_prog * 8 + 16 + nrt * 4 + nrec * 4;  // rec, srec, nFc, rterm, inv
   // stream-ordered pool allocations (a synchronous cudaMalloc/cudaFree per plan costs ms)
   if ((e = cudaMallocAsync((void **)&pl->d_progs, sizeof(DevProg) * n_prog, s)) != cudaSuccess) return fail(e, "alloc");
@@ -460,6 +461,7 @@ static rp_status plan_create(const rp_program *progs, int32_t n_prog, const int3
   pl->tab.nde_pad = nde_pad;
   pl->tab.rcoef = pl->tab.Cmat + ncm;  // even offset (ncm and kRSMTab even): 16-byte aligned
   pl->tab.rinfo = pl->tab.rcoef + nrt * kMaxPolys;
+  pl->tab.mPdd = reinterpret_cast<double2 *>(pl->tab.rinfo + (size_t)n_prog * 8);  // (16-byte aligned)
   pl->tab.rterm = pl->tab.nFc + 2 * n_prog + 4;
   pl->tab.inv = pl->tab.rterm + nrt;
   pl->tab.nrt_max = 1;

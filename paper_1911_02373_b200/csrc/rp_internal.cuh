@@ -117,6 +117,8 @@ struct CfgTable {
   int32_t *ghv;       // [n_prog][nGp]: slot's Horner variable, -1 dense, -2 padding
   GroupDesc *gdesc;   // [n_prog][kMaxGroups]
   int32_t *gcnt;      // [n_prog][4]: groups, factored tiles, tiles, -
+  // (last: the sweep kernel's code generation is sensitive to the offsets of the fields above)
+  double2 *mPdd;      // [n_prog][nFp][npe_pad]: m_pe(u_P) of srec position pos, double-double (k_refine)
 };
 constexpr int kRSMTab = 1024;  // n_sm <= 1023 uses the table
 

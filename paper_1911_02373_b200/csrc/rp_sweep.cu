@@ -38,6 +38,18 @@ __device__ __forceinline__ int64_t occupancy_blocks(int64_t T, int64_t R, int64_
   return 0;                                                                             // fail
 }
 
+// m = prod u_k^{e_k} as a double-double (hi exact product chain by FMA, lo the running error)
+__device__ __forceinline__ double2 dd_monomial(const int8_t *e, int n, const double *u) {
+  double h = 1.0, l = 0.0;
+  for (int k = 0; k < n; ++k)
+    for (int t = 0; t < e[k]; ++t) {
+      const double nh = h * u[k];
+      l = fma(l, u[k], fma(h, u[k], -nh));
+      h = nh;
+    }
+  return make_double2(h, l);
+}
+
 __device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab, int npe_pad);
 __device__ void schedule_slot_mp(const DevProg &pg, const CfgRec &r, int hv, int npe_pad, double *col, int nGp);
 __device__ bool group_lists(const DevProg &pg, int hv, int32_t (*off)[kGS]);
@@ -136,6 +148,9 @@ __global__ void __launch_bounds__(1024) k_plan_configs(const DevProg *progs, con
             for (int t = 0; t < pg.pe_exp[pe][k]; ++t) m *= u[k];
         }
         tab.smP[(int64_t)g * npe_pad * nFp + (int64_t)pe * nFp + pos] = m;
+        // the refinement's double-double copy, by srec position
+        tab.mPdd[((int64_t)g * nFp + pos) * npe_pad + pe] =
+            pe < pg.nPE ? dd_monomial(pg.pe_exp[pe], pg.p, u) : make_double2(0.0, 0.0);
       }
     }
     __syncthreads();
@@ -214,9 +229,24 @@ __global__ void __launch_bounds__(256) k_plan_refresh_tables(const DevProg *pgp,
   const int32_t *ghv = tab.ghv + (int64_t)g * nGp;
   GroupDesc *gdesc = tab.gdesc + (int64_t)g * kMaxGroups;
   double *Cm = tab.Cmat + (int64_t)g * kMaxPolys * npe_pad * tab.nde_pad;
-  // work items: [configuration monomials | schedule slots | staging rows | groups]
-  const int n0 = nFc * npe_pad, n1 = n0 + nslot, n2 = n1 + nrow, n3 = n2 + ngr;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n3; t += gridDim.x * blockDim.x) {
+  // work items: [configuration monomials | schedule slots | staging rows | groups | the
+  // refinement's double-double monomials by srec position]
+  const int n0 = nFc * npe_pad, n1 = n0 + nslot, n2 = n1 + nrow, n3 = n2 + ngr, n4 = n3 + nFc * npe_pad;
+  const CfgRec *srec = tab.srec + (int64_t)g * nFp;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += gridDim.x * blockDim.x) {
+    if (t >= n3) {
+      const int pos = (t - n3) / npe_pad, pe = (t - n3) % npe_pad;
+      double2 m = make_double2(0.0, 0.0);
+      if (pe < pg.nPE) {
+        const CfgRec &r = srec[pos];
+        const int32_t Pk[3] = {r.Pm1_0 + 1, r.Pm1_1 + 1, r.Pm1_2 + 1};
+        double u[3] = {0.0, 0.0, 0.0};
+        for (int k = 0; k < pg.p; ++k) u[k] = ((double)Pk[k] - pg.xc[pg.d + k]) * ldexp(1.0, -pg.xe[pg.d + k]);
+        m = dd_monomial(pg.pe_exp[pe], pg.p, u);
+      }
+      tab.mPdd[((int64_t)g * nFp + pos) * npe_pad + pe] = m;
+      continue;
+    }
     if (t < n0) {
       const int pos = t / npe_pad, pe = t % npe_pad;
       double m = 0.0;
@@ -1759,18 +1789,6 @@ __device__ void build_refine_terms(int g, const DevProg &pg, const CfgTable &tab
   }
 }
 
-// m = prod u_k^{e_k} as a double-double (hi exact product chain by FMA, lo the running error)
-__device__ __forceinline__ double2 dd_monomial(const int8_t *e, int n, const double *u) {
-  double h = 1.0, l = 0.0;
-  for (int k = 0; k < n; ++k)
-    for (int t = 0; t < e[k]; ++t) {
-      const double nh = h * u[k];
-      l = fma(l, u[k], fma(h, u[k], -nh));
-      h = nh;
-    }
-  return make_double2(h, l);
-}
-
 // the smallest power of two > 4 B (B >= 0 finite); 1 for B = 0; 0 if it would overflow
 __device__ __forceinline__ double extract_sigma(double B) {
   if (!(B > 0.0)) return B == 0.0 ? 1.0 : 0.0;
@@ -2018,13 +2036,16 @@ __global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
   // recomputed then (uniform across the warp), the data monomial comes from shared memory
   int cur_pe = -1;
   double2 mp1 = make_double2(0.0, 0.0), mp2 = make_double2(0.0, 0.0);
+  const double2 *mpd1 = a.tab.mPdd + ((int64_t)g * a.tab.nFp + p1) * a.npe_pad;
+  const double2 *mpd2 = a.tab.mPdd + ((int64_t)g * a.tab.nFp + (p2 >= 0 ? p2 : p1)) * a.npe_pad;
   for (int j = 0; j < nrt; ++j) {
     const int32_t tt = sT[j];
     const int pe = tt >> 16;
     if (pe != cur_pe) {
       cur_pe = pe;
-      mp1 = dd_monomial(pg.pe_exp[pe], pg.p, uP);
-      if (two) mp2 = dd_monomial(pg.pe_exp[pe], pg.p, uP2);
+      // (the plan's double-double program monomials: computing them here was 30% of the kernel)
+      mp1 = __ldg(mpd1 + pe);
+      if (two) mp2 = __ldg(mpd2 + pe);
     }
     const double2 md = sMD[(size_t)(tt & 0xffff) * T + tid];
     double c[NPOLY];
