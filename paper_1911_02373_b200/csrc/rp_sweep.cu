@@ -1980,6 +1980,8 @@ __global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
     for (int i = tid; i < nrt; i += T) sT[i] = rt[i];
     for (int i = tid; i < nrt * (kMaxPolys / 2); i += T) sCf[i] = rc[i];
   }
+  __shared__ int8_t sDE[kMaxDE][kMaxVars];  // the data-part exponents (broadcast reads)
+  for (int i = tid; i < nDE * kMaxVars; i += T) sDE[i / kMaxVars][i % kMaxVars] = pg.de_exp[i / kMaxVars][i % kMaxVars];
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * T + tid;
   if (t >= a.nD) return;
@@ -2003,7 +2005,7 @@ __global__ void __launch_bounds__(kRefThreads) k_refine(SweepArgs a) {
     u[k] = ((double)Dt[k] - pg.xc[k]) * ldexp(1.0, -pg.xe[k]);
     R = fmax(R, fabs(u[k]));
   }
-  for (int de = 0; de < nDE; ++de) sMD[(size_t)de * T + tid] = dd_monomial(pg.de_exp[de], d, u);
+  for (int de = 0; de < nDE; ++de) sMD[(size_t)de * T + tid] = dd_monomial(sDE[de], d, u);
   double uP[3] = {0.0, 0.0, 0.0}, uP2[3] = {0.0, 0.0, 0.0};
   {
     const int P1[3] = {r1->Pm1_0 + 1, r1->Pm1_1 + 1, r1->Pm1_2 + 1};
